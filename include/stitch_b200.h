@@ -1,0 +1,130 @@
+/* stitch_b200.h — the C-ABI boundary of the B200 stitched-kernel executor.
+ *
+ * The reference (arXiv 2009.10924 artifact, /root/reference/proj) is a C++
+ * library with no FFI of its own; its public entry points for this path are
+ * the C++ functions named below.  These extern "C" functions are what a
+ * binding to that path binds (ctypes in paper_2009_10924_b200/stitch.py; a
+ * cgo/JNI/N-API stub would bind the same symbols).
+ * Plain pointers and sizes only; no C++ or torch types cross this boundary.
+ *
+ * Conventions: every int-returning call returns 0 on success, nonzero on
+ * failure with a message in stc_last_error() (thread-local).  Codes:
+ * 1 = parse/config/planner error, 2 = execution fault / compare mismatch,
+ * 3 = CUDA/NVRTC error, 4 = bad argument.  Strings returned through char**
+ * are malloc'd; release them with stc_free().  Handles are owned by the
+ * caller and released with the matching *_destroy().  A stc_exec is bound to
+ * one GPU and must be driven by one host thread at a time (one process or
+ * thread per GPU for multi-GPU use).
+ */
+#ifndef STITCH_B200_H
+#define STITCH_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct stc_graph stc_graph; /* stitch::CompGraph */
+typedef struct stc_plan stc_plan;   /* FusionPlan + per-pattern KernelPlan + MachineModel */
+typedef struct stc_exec stc_exec;   /* compiled plan on one GPU: cubins, buffers, CUDA Graph */
+
+enum { STC_F32 = 0, STC_F16 = 1, STC_I32 = 2, STC_BOOL = 3 }; /* stitch::DType order */
+
+const char* stc_last_error(void);
+void stc_free(void* p);
+const char* stc_version(void);
+
+/* ---- graph IR ------------------------------------------------------------
+ * replaces stitch::parse_graph / serialize_graph
+ * (/root/reference/proj/include/stitch/parser.hpp:21-25, src/parser.cpp:162-285) */
+int stc_graph_parse(const char* text, stc_graph** out);
+void stc_graph_destroy(stc_graph* g);
+int stc_graph_serialize(const stc_graph* g, char** out);
+int stc_graph_num_nodes(const stc_graph* g);
+/* which: 0 = parameters (declaration order), 1 = graph outputs (output order).
+ * Returns the count; with i >= 0 also fills name/dtype/rank/dims[8]. */
+int stc_graph_io(const stc_graph* g, int which, int i, const char** name, int* dtype, int* rank,
+                 int64_t* dims);
+
+/* ---- planning ------------------------------------------------------------
+ * replaces stitch::explore_fusion_plan + CostModels::plan_for + plan_to_json
+ * (include/stitch/explorer.hpp:74-75, explorer.hpp:36, src/pipeline.cpp:45-78,
+ *  the body of run_pipeline src/pipeline.cpp:124-146).
+ * cfg_path NULL/"" -> $STITCH_DEVICE_CONFIG or built-in defaults; k/beam <= 0
+ * keep the cfg's values. */
+int stc_plan_create(const stc_graph* g, const char* cfg_path, int k, int beam, stc_plan** out);
+/* explicit patterns (vertex ids; pattern p = verts[offs[p] .. offs[p+1]-1]),
+ * each planned with stitch::plan_kernel (include/stitch/planner.hpp:101-103);
+ * rc 1 if a pattern is infeasible */
+int stc_plan_from_patterns(const stc_graph* g, const char* cfg_path, const int* verts,
+                           const int* offs, int n_patterns, stc_plan** out);
+void stc_plan_destroy(stc_plan* p);
+int stc_plan_json(const stc_plan* p, uint64_t seed, char** out);
+int stc_plan_num_patterns(const stc_plan* p);
+/* pattern i: vertex ids (up to cap) -> count; program text via kernel_text */
+int stc_plan_pattern(const stc_plan* p, int i, int* verts, int cap);
+int stc_plan_kernel_text(const stc_plan* p, int i, char** out);
+int stc_plan_stats(const stc_plan* p, int* stitched_kernels, int* baseline_kernels,
+                   int64_t* delta_evaluate_calls);
+/* stitch::plan_kernel on one vertex set -> program text; rc 1 = infeasible */
+int stc_plan_kernel(const stc_graph* g, const char* cfg_path, const int* verts, int n,
+                    char** program_text);
+
+/* ---- execution on B200 ---------------------------------------------------
+ * replaces stitch::eval_plan / run_program / eval_reference
+ * (include/stitch/sim.hpp:33-47, src/sim.cpp:231-514): the reference walks
+ * the plan on a CPU SIMT interpreter; here every planned pattern is one
+ * NVRTC-compiled sm_100a kernel, uncovered fusable ops are singleton kernels,
+ * opaque ops a placeholder kernel, all replayed as ONE CUDA Graph. */
+enum {
+  STC_EXEC_STITCHED = 0, /* dataflow templates (local/regional/global/independent) */
+  STC_EXEC_PROGRAM = 1,  /* translate each planned abstract program statement for statement */
+  STC_EXEC_UNFUSED = 2,  /* one kernel per op: eval_reference semantics on the GPU */
+  STC_EXEC_NO_GRAPH = 8  /* flag: plain stream launches instead of a CUDA Graph */
+};
+int stc_exec_create(const stc_plan* p, int device, int mode, stc_exec** out);
+void stc_exec_destroy(stc_exec* e);
+int stc_exec_num_kernels(const stc_exec* e);
+/* JSON array: per launched kernel {name, template, pattern, grid, block, smem, bytes} */
+int stc_exec_describe(const stc_exec* e, char** json);
+int stc_exec_source(const stc_exec* e, char** cuda_source);
+/* end to end with HOST buffers: H2D of every parameter, graph launch, D2H of
+ * every output, synchronise.  Buffers hold the tensor's dtype natively
+ * (f32 / f16 bits / i32 / u8 bool), parameters and outputs in stc_graph_io order. */
+int stc_exec_run_host(stc_exec* e, const void* const* inputs, void* const* outputs);
+int stc_exec_upload(stc_exec* e, const void* const* inputs);
+int stc_exec_launch(stc_exec* e, void* cuda_stream); /* async on the stream (NULL = exec stream) */
+int stc_exec_download(stc_exec* e, void* const* outputs);
+int stc_exec_sync(stc_exec* e);
+/* device buffer of a graph tensor (parameter/output/kernel boundary) */
+int stc_exec_tensor(const stc_exec* e, const char* name, void** dptr, size_t* bytes);
+/* Timing with CUDA events on the exec stream.  sets >= 1 independent copies
+ * of every buffer are rotated between replays so the working set exceeds L2
+ * (sets*bytes > L2) - inputs stay HBM-resident but cold.  Outputs:
+ * us_per_run = average graph replay time; kernel_us[i] (optional, length
+ * num_kernels) = average duration of kernel i measured by per-kernel events. */
+int stc_exec_time(stc_exec* e, int iters, int warmup, int sets, double* us_per_run,
+                  double* kernel_us);
+
+/* ---- low-level runtime (the CUDA layer the executor is built on) --------- */
+/* NVRTC -arch=sm_100a compile with the on-disk cubin cache; returns the
+ * cache key (hex) of the cubin so callers can reuse it */
+int stc_compile(const char* cuda_source, const char* options, char** cubin_key);
+/* directory of the cubin cache ($STITCH_CACHE_DIR or <pkg>/lib/cubin_cache) */
+const char* stc_cache_dir(void);
+
+/* ---- drop-in pipeline ------------------------------------------------------
+ * replaces stitch::run_pipeline (include/stitch/pipeline.hpp:28): writes
+ * plan.json, kernels/kNNN_<producer>.stitch, report.txt, [graph.dot];
+ * run_sim executes the plan on the GPU and compares with the unfused
+ * execution (rel 1e-4, abs 1e-5).  Returns 0 / 1 / 2 like the reference. */
+int stc_run_pipeline(const char* graph_path, const char* device_config_path, int k,
+                     int beam_width, const char* output_dir, int emit_dot, int run_sim,
+                     int run_baseline, uint64_t seed);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* STITCH_B200_H */

@@ -1,0 +1,123 @@
+"""Native build for stitch-b200 (no cmake, no setuptools; in-tree outputs).
+
+    python -m paper_2009_10924_b200.build          # or build() from __graft_entry__
+
+Compiles
+  csrc/host/*.cpp      stitch:: host library (IR, parser, planner, explorer, ...)
+  csrc/codegen/*.cpp   KernelPlan -> CUDA C++ source (stitching templates)
+  csrc/runtime/*.cpp   NVRTC compile + cubin cache, device buffers, CUDA Graph executor
+  csrc/abi/*.cpp       extern "C" boundary declared in include/stitch_b200.h
+  csrc/kernels/*.cu    fixed sm_100a kernels (nvcc -gencode arch=compute_100a,code=sm_100a)
+into paper_2009_10924_b200/lib/libstitch_b200.so, plus tools/stitchc.
+
+Incremental by mtime; the object dir is paper_2009_10924_b200/lib/obj.
+"""
+from __future__ import annotations
+
+import concurrent.futures as cf
+import glob
+import os
+import shutil
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+LIB_DIR = os.path.join(PKG, "lib")
+OBJ_DIR = os.path.join(LIB_DIR, "obj")
+LIB = os.path.join(LIB_DIR, "libstitch_b200.so")
+CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
+NVCC = os.path.join(CUDA, "bin", "nvcc")
+ARCH = "-gencode=arch=compute_100a,code=sm_100a"
+
+
+def _nlohmann_dir():
+    cands = glob.glob(os.path.join(sys.prefix, "lib", "python3*", "site-packages", "include",
+                                   "cudnn_frontend", "thirdparty", "nlohmann"))
+    cands += glob.glob("/opt/prime-rl/.venv/lib/python3*/site-packages/include/cudnn_frontend/"
+                       "thirdparty/nlohmann")
+    for c in cands:
+        if os.path.exists(os.path.join(c, "json.hpp")):
+            return c
+    raise RuntimeError("nlohmann/json.hpp (3.11.3) not found")
+
+
+CXXFLAGS = ["-std=c++20", "-O2", "-g1", "-fPIC", "-Wall", "-Wno-sign-compare",
+            "-I" + os.path.join(ROOT, "include"), "-I" + CSRC, "-I" + os.path.join(CUDA, "include")]
+NVCCFLAGS = ["-std=c++17", "-O3", ARCH, "-lineinfo", "-Xcompiler", "-fPIC",
+             "-I" + os.path.join(ROOT, "include"), "-I" + CSRC]
+LDFLAGS = ["-shared", "-static-libstdc++", "-static-libgcc", "-Wl,--exclude-libs,ALL",
+           "-Wl,-Bsymbolic", "-L" + os.path.join(CUDA, "lib64"),
+           "-L" + os.path.join(CUDA, "lib64", "stubs"), "-Wl,-rpath," + os.path.join(CUDA, "lib64"),
+           "-lnvrtc", "-lcudart", "-lcuda", "-lpthread", "-ldl"]
+
+
+def _stale(src, obj, extra=()):
+    if not os.path.exists(obj):
+        return True
+    t = os.path.getmtime(obj)
+    deps = [src] + list(extra)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def _headers():
+    return (glob.glob(os.path.join(ROOT, "include", "**", "*.h*"), recursive=True) +
+            glob.glob(os.path.join(CSRC, "**", "*.h"), recursive=True) +
+            glob.glob(os.path.join(CSRC, "**", "*.hpp"), recursive=True) +
+            glob.glob(os.path.join(CSRC, "**", "*.cuh"), recursive=True))
+
+
+def _run(cmd):
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError("build failed: %s\n%s%s" % (" ".join(cmd), r.stdout, r.stderr))
+    return r
+
+
+def build(verbose=False, jobs=None):
+    os.makedirs(OBJ_DIR, exist_ok=True)
+    nl = _nlohmann_dir()
+    hdrs = _headers()
+    jobs_list = []
+    cpp = sorted(glob.glob(os.path.join(CSRC, "*", "*.cpp")))
+    cu = sorted(glob.glob(os.path.join(CSRC, "kernels", "*.cu")))
+    objs = []
+    for s in cpp:
+        o = os.path.join(OBJ_DIR, os.path.basename(os.path.dirname(s)) + "_" +
+                         os.path.basename(s)[:-4] + ".o")
+        objs.append(o)
+        if _stale(s, o, hdrs):
+            jobs_list.append(["g++"] + CXXFLAGS + ["-I" + nl, "-c", s, "-o", o])
+    for s in cu:
+        o = os.path.join(OBJ_DIR, "cu_" + os.path.basename(s)[:-3] + ".o")
+        objs.append(o)
+        if _stale(s, o, hdrs):
+            jobs_list.append([NVCC] + NVCCFLAGS + ["-c", s, "-o", o])
+    with cf.ThreadPoolExecutor(max_workers=jobs or os.cpu_count() or 4) as ex:
+        for r in ex.map(_run, jobs_list):
+            if verbose and (r.stdout or r.stderr):
+                print(r.stdout + r.stderr)
+    if jobs_list or not os.path.exists(LIB) or any(os.path.getmtime(o) > os.path.getmtime(LIB)
+                                                    for o in objs):
+        _run(["g++", "-o", LIB + ".tmp"] + objs + LDFLAGS)
+        os.replace(LIB + ".tmp", LIB)
+    tool_src = os.path.join(ROOT, "tools", "stitchc.cpp")
+    tool = os.path.join(ROOT, "tools", "stitchc")
+    if os.path.exists(tool_src) and _stale(tool_src, tool, [LIB] + hdrs):
+        _run(["g++"] + CXXFLAGS + [tool_src, "-o", tool, "-L" + LIB_DIR, "-lstitch_b200",
+                                   "-Wl,-rpath," + LIB_DIR, "-static-libstdc++", "-static-libgcc"])
+    return LIB
+
+
+def build_oracle():
+    """oracle/_ref from /root/reference when present (build container only)."""
+    if not os.path.isdir("/root/reference/proj/src") or shutil.which("make") is None:
+        return None
+    _run(["make", "-s", "-C", os.path.join(ROOT, "oracle"), "-j8"])
+    return os.path.join(ROOT, "oracle", "_ref", "libstitch_ref.so")
+
+
+if __name__ == "__main__":
+    print(build(verbose=True))
+    print(build_oracle())
