@@ -84,6 +84,9 @@ enum {
   STC_EXEC_UNFUSED = 2,  /* one kernel per op: eval_reference semantics on the GPU */
   STC_EXEC_NO_GRAPH = 8  /* flag: plain stream launches instead of a CUDA Graph */
 };
+/* code generation only (no device needed): the plan's CUDA module source and
+ * a JSON description of its kernels */
+int stc_codegen(const stc_plan* p, int mode, char** cuda_source, char** kernels_json);
 int stc_exec_create(const stc_plan* p, int device, int mode, stc_exec** out);
 void stc_exec_destroy(stc_exec* e);
 int stc_exec_num_kernels(const stc_exec* e);
@@ -95,7 +98,13 @@ int stc_exec_source(const stc_exec* e, char** cuda_source);
  * (f32 / f16 bits / i32 / u8 bool), parameters and outputs in stc_graph_io order. */
 int stc_exec_run_host(stc_exec* e, const void* const* inputs, void* const* outputs);
 int stc_exec_upload(stc_exec* e, const void* const* inputs);
-int stc_exec_launch(stc_exec* e, void* cuda_stream); /* async on the stream (NULL = exec stream) */
+/* async graph replay on `cuda_stream` (NULL = the executor's stream) using
+ * buffer set `set` (0 = the uploaded buffers; see stc_exec_prepare_sets) */
+int stc_exec_launch(stc_exec* e, void* cuda_stream, int set);
+/* allocate `sets` independent copies of every buffer and copy set 0's
+ * parameters into them, so timed replays can rotate through more bytes than
+ * L2 holds with HBM-resident (cold) inputs */
+int stc_exec_prepare_sets(stc_exec* e, int sets);
 int stc_exec_download(stc_exec* e, void* const* outputs);
 int stc_exec_sync(stc_exec* e);
 /* device buffer of a graph tensor (parameter/output/kernel boundary) */

@@ -49,8 +49,8 @@ NVCCFLAGS = ["-std=c++17", "-O3", ARCH, "-lineinfo", "-Xcompiler", "-fPIC",
              "-I" + os.path.join(ROOT, "include"), "-I" + CSRC]
 LDFLAGS = ["-shared", "-static-libstdc++", "-static-libgcc", "-Wl,--exclude-libs,ALL",
            "-Wl,-Bsymbolic", "-L" + os.path.join(CUDA, "lib64"),
-           "-L" + os.path.join(CUDA, "lib64", "stubs"), "-Wl,-rpath," + os.path.join(CUDA, "lib64"),
-           "-lnvrtc", "-lcudart", "-lcuda", "-lpthread", "-ldl"]
+           "-Wl,-rpath," + os.path.join(CUDA, "lib64"),
+           "-lnvrtc", "-lcudart", "-lpthread", "-ldl"]
 
 
 def _stale(src, obj, extra=()):

@@ -1,0 +1,137 @@
+// extern "C" boundary, device half: code generation, NVRTC, the CUDA-Graph
+// executor (include/stitch_b200.h).
+#include <cstring>
+#include <memory>
+#include <sstream>
+
+#include "abi/abi_common.h"
+#include "runtime/executor.hpp"
+
+using namespace stitch;
+using namespace stc_abi;
+
+struct stc_exec {
+  std::unique_ptr<gpu::Executor> ex;
+};
+
+namespace {
+
+gpu::ExecMode mode_of(int mode) {
+  switch (mode & 7) {
+    case STC_EXEC_PROGRAM: return gpu::ExecMode::Program;
+    case STC_EXEC_UNFUSED: return gpu::ExecMode::Unfused;
+    default: return gpu::ExecMode::Stitched;
+  }
+}
+
+std::string specs_json(const std::vector<gpu::KernelSpec>& specs) {
+  std::ostringstream o;
+  o << "[";
+  for (size_t i = 0; i < specs.size(); ++i) {
+    const auto& k = specs[i];
+    o << (i ? "," : "") << "{\"name\":\"" << k.name << "\",\"template\":\"" << k.tmpl << "\",\"pattern\":\""
+      << k.pattern_key << "\",\"grid\":" << k.grid << ",\"block\":" << k.block << ",\"smem\":" << k.smem
+      << ",\"cooperative\":" << (k.cooperative ? "true" : "false") << ",\"bytes\":" << k.alg_bytes << "}";
+  }
+  o << "]";
+  return o.str();
+}
+
+}  // namespace
+
+extern "C" {
+
+int stc_codegen(const stc_plan* p, int mode, char** cuda_source, char** kernels_json) {
+  return guarded([&] {
+    auto pk = gpu::generate_plan_kernels(p->graph, p->plan, p->kernels, p->models.machine, mode_of(mode));
+    if (cuda_source) *cuda_source = dup_string(pk.source);
+    if (kernels_json) *kernels_json = dup_string(specs_json(pk.specs));
+  });
+}
+
+int stc_exec_create(const stc_plan* p, int device, int mode, stc_exec** out) {
+  return guarded([&] {
+    auto e = std::make_unique<stc_exec>();
+    e->ex = std::make_unique<gpu::Executor>(p->graph, p->plan, p->kernels, p->models.machine, device,
+                                            mode_of(mode), (mode & STC_EXEC_NO_GRAPH) == 0);
+    *out = e.release();
+  });
+}
+
+void stc_exec_destroy(stc_exec* e) { delete e; }
+
+int stc_exec_num_kernels(const stc_exec* e) { return static_cast<int>(e->ex->kernels().size()); }
+
+int stc_exec_describe(const stc_exec* e, char** json) {
+  return guarded([&] { *json = dup_string(e->ex->describe_json()); });
+}
+
+int stc_exec_source(const stc_exec* e, char** src) {
+  return guarded([&] { *src = dup_string(e->ex->source()); });
+}
+
+int stc_exec_run_host(stc_exec* e, const void* const* inputs, void* const* outputs) {
+  return guarded([&] { e->ex->run_host(inputs, outputs); });
+}
+
+int stc_exec_upload(stc_exec* e, const void* const* inputs) {
+  return guarded([&] { e->ex->upload(inputs, 0); });
+}
+
+int stc_exec_launch(stc_exec* e, void* stream, int set) {
+  return guarded([&] { e->ex->launch(static_cast<cudaStream_t>(stream), set); });
+}
+
+int stc_exec_prepare_sets(stc_exec* e, int sets) {
+  return guarded([&] { e->ex->prepare_sets(sets); });
+}
+
+int stc_exec_download(stc_exec* e, void* const* outputs) {
+  return guarded([&] { e->ex->download(outputs, 0); });
+}
+
+int stc_exec_sync(stc_exec* e) {
+  return guarded([&] { e->ex->sync(); });
+}
+
+int stc_exec_tensor(const stc_exec* e, const char* name, void** dptr, size_t* bytes) {
+  const auto* t = e->ex->tensor(name ? name : "");
+  if (!t) {
+    g_error = std::string("[abi] no device buffer for tensor ") + (name ? name : "(null)");
+    return 4;
+  }
+  if (dptr) *dptr = t->dptr.empty() ? nullptr : t->dptr[0];
+  if (bytes) *bytes = t->bytes;
+  return 0;
+}
+
+int stc_exec_time(stc_exec* e, int iters, int warmup, int sets, double* us_per_run, double* kernel_us) {
+  return guarded([&] {
+    std::vector<double> per;
+    const double us = e->ex->time(iters, warmup, sets, kernel_us ? &per : nullptr);
+    if (us_per_run) *us_per_run = us;
+    if (kernel_us)
+      for (size_t i = 0; i < per.size(); ++i) kernel_us[i] = per[i];
+  });
+}
+
+int stc_compile(const char* cuda_source, const char* options, char** cubin_key) {
+  return guarded([&] {
+    std::vector<std::string> opts = gpu::default_nvrtc_options();
+    if (options && *options) {
+      std::istringstream ss(options);
+      for (std::string o; ss >> o;) opts.push_back(o);
+    }
+    std::string key;
+    gpu::compile_cubin(cuda_source, opts, &key);
+    if (cubin_key) *cubin_key = dup_string(key);
+  });
+}
+
+const char* stc_cache_dir(void) {
+  static thread_local std::string d;
+  d = gpu::cubin_cache_dir();
+  return d.c_str();
+}
+
+}  // extern "C"

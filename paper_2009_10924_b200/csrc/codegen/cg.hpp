@@ -1,0 +1,79 @@
+// B200 code generator: fusion pattern (+ its KernelPlan) -> one sm_100a CUDA
+// kernel, written as CUDA C++ source for NVRTC.
+//
+// Templates, chosen per connected component of the pattern:
+//   local     no reductions: vectorised (float4) grid-stride elementwise chain,
+//             shape ops folded into index math, values kept in registers
+//   regional  row reductions over trailing axes: a team of threads owns a row,
+//             loads it once into registers, reduces with shuffles (+ smem
+//             across warps), and every consumer reads the reduced value from
+//             registers — the paper's warp/block composition
+//   global    column reductions over leading axes: per-CTA partial tiles, a
+//             cooperative grid-wide barrier, deterministic fixed-order
+//             combine, then the column consumers
+//   independent  several components (remote / kernel-packing patterns) in
+//             one launch, each on its own CTA range
+//   program   anything else: the planner's abstract stitched program
+//             translated statement for statement (always applicable)
+#pragma once
+
+#include <cstdint>
+#include <map>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "stitch/graph.hpp"
+#include "stitch/planner.hpp"
+#include "stitch/program.hpp"
+
+namespace stitch::gpu {
+
+struct KernelSpec {
+  std::string name;                  // __global__ symbol
+  std::string source;                // CUDA C++ (device code only; prelude separate)
+  std::string tmpl;                  // local | regional | global | independent | program | opaque
+  std::string pattern_key;           // FusionPattern::key() or "op:<name>"
+  int grid = 1;
+  int block = 256;
+  int64_t smem = 0;                  // dynamic shared memory bytes
+  bool cooperative = false;          // needs a grid-wide barrier (co-resident launch)
+  std::vector<std::string> inputs;   // tensor names bound to the leading pointer params
+  std::vector<std::string> outputs;  // then these
+  int64_t scratch_bytes = 0;         // trailing `void* scratch` param when > 0 (zeroed once)
+  int64_t alg_bytes = 0;             // algorithmic bytes: unique inputs read once + outputs written once
+};
+
+// Thrown when a dataflow template cannot express a component; the caller
+// falls back to the program template.
+struct TemplateMismatch : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+// Dataflow templates for a planned pattern. `outputs` = the pattern's
+// tensors that leave the kernel (graph outputs or read outside). Throws
+// TemplateMismatch if some component fits no template.
+KernelSpec generate_pattern_kernel(const CompGraph& g, const std::vector<int>& vertices,
+                                   const std::string& name, int sm_count);
+
+// Statement-for-statement translation of an abstract stitched program
+// (the reference interpreter's semantics, src/sim.cpp:256-462).
+KernelSpec generate_program_kernel(const CompGraph& g, const StitchedProgram& prog,
+                                   const std::string& name);
+
+// opaque_compute placeholder: mean of all operand elements, broadcast
+// (src/sim.cpp:215-226), one cooperative kernel.
+KernelSpec generate_opaque_kernel(const CompGraph& g, int vertex, const std::string& name,
+                                  int sm_count);
+
+// device helpers every module includes
+const std::string& device_prelude();
+
+// algorithmic bytes of a vertex set
+int64_t algorithmic_bytes(const CompGraph& g, const std::vector<int>& vertices);
+
+// small formatting helpers shared by the generators
+std::string c_float(double v);  // exact float literal of (float)v
+const char* c_type(DType d);
+
+}  // namespace stitch::gpu

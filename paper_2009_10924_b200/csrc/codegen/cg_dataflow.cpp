@@ -1,0 +1,969 @@
+// Dataflow stitching templates (local / regional / global / independent).
+//
+// A pattern is split into connected components; each component is matched to
+// a template by the shape of its reductions:
+//   no reductions                       -> local   (one body per output shape)
+//   all reductions over trailing axes,  -> regional (row-resident teams)
+//     same (outer, inner) split
+//   all reductions over leading axes,   -> global  (partials + grid barrier)
+//     same (reduced, kept) split
+// Bodies with the same domain are merged so shared inputs are read once (e.g.
+// the two column reductions of colreduce read dy once), and all bodies of a
+// pattern run in one launch on disjoint CTA ranges (independent packing).
+//
+// Values are emitted on demand with common-subexpression elimination keyed by
+// (vertex, coordinates): a tensor element requested twice at the same
+// coordinates — e.g. x in both LayerNorm reductions and in the normalisation —
+// is loaded once and stays in registers.  Coordinates are per-axis C
+// expressions; the innermost one may vary across the W (=4) lanes of a
+// 128-bit vector, which is how loads become float4 and broadcast sources
+// become single scalar loads.
+//
+// Numerics follow the reference evaluator (src/sim.cpp:111-229): every op's
+// result is rounded to its dtype (f32 arithmetic without FMA contraction is
+// exactly "compute in f64, round to f32" for + - * /), reductions accumulate
+// in f64 and round once, max/min use std::max/min argument order.
+#include <algorithm>
+#include <cmath>
+#include <functional>
+#include <map>
+#include <set>
+#include <sstream>
+
+#include "codegen/cg.hpp"
+
+namespace stitch::gpu {
+
+namespace {
+
+constexpr int kSmCount = 148;
+
+int64_t pow2ceil(int64_t x) {
+  int64_t p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+
+int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return v && *v ? std::atoi(v) : dflt;
+}
+
+struct Coord {
+  std::string base;      // C expression (index type)
+  bool vary = false;     // lane k adds k
+  bool aligned = true;   // base is a multiple of the vector width
+};
+using Coords = std::vector<Coord>;
+
+struct Val {
+  std::vector<std::string> lanes;  // 1 entry = uniform across lanes
+  const std::string& at(int k) const { return lanes.size() == 1 ? lanes[0] : lanes[static_cast<size_t>(k)]; }
+  bool uniform() const { return lanes.size() == 1; }
+};
+
+std::string coords_key(const Coords& c) {
+  std::string k;
+  for (const auto& x : c) k += x.base + (x.vary ? "~|" : "|");
+  return k;
+}
+
+// ---- per-kernel emission state ----------------------------------------------
+class Emitter {
+ public:
+  Emitter(const CompGraph& g, const std::set<int>& pattern, bool wide_index)
+      : g_(g), pattern_(pattern), ix_(wide_index ? "i64" : "int") {}
+
+  std::ostringstream out;
+  std::string ind = "  ";
+  int W = 1;
+  std::set<int> loaded;                    // external tensors read
+  std::map<std::string, Val> reduced;      // (reduction vertex, coords) -> value
+  std::set<int> cached_tensors;            // read through L1 (re-read broadcast sources)
+
+  const std::string& ix() const { return ix_; }
+  std::string fresh(const char* p) { return p + std::to_string(counter_++); }
+  void line(const std::string& s) { out << ind << s << "\n"; }
+  void open(const std::string& s) {
+    line(s + " {");
+    ind += "  ";
+    scopes_.push_back(memo_);
+  }
+  void close() {
+    ind.resize(ind.size() - 2);
+    line("}");
+    memo_ = scopes_.back();
+    scopes_.pop_back();
+  }
+  void clear_memo() { memo_.clear(); }
+
+  static std::string key(int v, const Coords& c) { return std::to_string(v) + "@" + coords_key(c); }
+
+  Val value(int v, const Coords& c) {
+    const std::string k = key(v, c);
+    if (auto it = memo_.find(k); it != memo_.end()) return it->second;
+    Val r = compute(v, c);
+    memo_[k] = r;
+    return r;
+  }
+
+  // linear element index of `c` for lane k (only varying coords shift)
+  std::string linear(int v, const Coords& c, int k) const {
+    const auto strides = g_.node(v).shape.strides();
+    std::string s;
+    for (size_t i = 0; i < c.size(); ++i) {
+      std::string term = c[i].base;
+      if (c[i].vary && k) term = "(" + term + " + " + std::to_string(k) + ")";
+      if (term == "0") continue;
+      if (strides[i] != 1) term = "(" + ix_ + ")" + term + " * " + std::to_string(strides[i]);
+      s += (s.empty() ? "" : " + ") + term;
+    }
+    return s.empty() ? "0" : s;
+  }
+
+ private:
+  Val load(int v, const Coords& c) {
+    loaded.insert(v);
+    const TensorShape& sh = g_.node(v).shape;
+    const std::string ptr = "T_" + g_.node(v).name;
+    int nvary = 0, last_vary = -1;
+    for (size_t i = 0; i < c.size(); ++i)
+      if (c[i].vary) ++nvary, last_vary = static_cast<int>(i);
+    if (nvary == 0 || W == 1) {
+      const std::string t = fresh("t");
+      line("const float " + t + " = ldv(" + ptr + ", " + linear(v, c, 0) + ");");
+      if (nvary == 0) return {{t}};
+      return {{t}};
+    }
+    const bool contiguous = nvary == 1 && last_vary == static_cast<int>(c.size()) - 1 &&
+                            c.back().aligned && sh.dims.back() % W == 0 && sh.dtype == DType::F32 && W == 4;
+    Val r;
+    if (contiguous) {
+      const std::string q = fresh("q");
+      const bool cached = cached_tensors.count(v) > 0;
+      line("const float4 " + q + " = " + (cached ? "ld4c(" : "ld4(") + ptr + " + " + linear(v, c, 0) + ");");
+      for (const char* f : {".x", ".y", ".z", ".w"}) r.lanes.push_back(q + f);
+      return r;
+    }
+    for (int k = 0; k < W; ++k) {
+      const std::string t = fresh("t");
+      line("const float " + t + " = ldv(" + ptr + ", " + linear(v, c, k) + ");");
+      r.lanes.push_back(t);
+    }
+    return r;
+  }
+
+  static std::string round_to(DType d, const std::string& e) {
+    switch (d) {
+      case DType::F32: return e;
+      case DType::F16: return "rnd_f16(" + e + ")";
+      case DType::I32: return "rnd_i32(" + e + ")";
+      case DType::Bool: return "rnd_bool(" + e + ")";
+    }
+    return e;
+  }
+
+  static std::string op_expr(OpKind k, const std::string& a, const std::string& b) {
+    switch (k) {
+      case OpKind::Add: return a + " + " + b;
+      case OpKind::Sub: return a + " - " + b;
+      case OpKind::Mul: return a + " * " + b;
+      case OpKind::Div: return a + " / " + b;
+      case OpKind::Max: return "op_max(" + a + ", " + b + ")";
+      case OpKind::Min: return "op_min(" + a + ", " + b + ")";
+      case OpKind::Power: return "powf(" + a + ", " + b + ")";
+      case OpKind::Exp: return "expf(" + a + ")";
+      case OpKind::Tanh: return "tanhf(" + a + ")";
+      case OpKind::Log: return "logf(" + a + ")";
+      case OpKind::Rsqrt: return "op_rsqrt(" + a + ")";
+      default: break;
+    }
+    throw TemplateMismatch("not an elementwise op");
+  }
+
+  Val compute(int v, const Coords& c) {
+    const OpNode& n = g_.node(v);
+    if (!pattern_.count(v) || n.kind == OpKind::Constant) {
+      if (n.kind == OpKind::Constant) {
+        double val = n.attrs.value;
+        if (n.shape.dtype == DType::F16) val = static_cast<double>(static_cast<float>(val));  // approx
+        if (n.shape.dtype == DType::I32) val = std::llround(val);
+        if (n.shape.dtype == DType::Bool) val = val != 0.0;
+        return {{c_float(val)}};
+      }
+      return load(v, c);
+    }
+    switch (classify_op(n)) {
+      case OpClass::Reduction: {
+        auto it = reduced.find(key(v, c));
+        if (it == reduced.end())
+          throw TemplateMismatch("reduction " + n.name + " read outside the work unit that owns it");
+        return it->second;
+      }
+      case OpClass::LightElementwise:
+      case OpClass::ExpensiveElementwise: {
+        std::vector<Val> ops;
+        bool uni = true;
+        for (int o : n.operands) {
+          ops.push_back(value(o, c));
+          uni = uni && ops.back().uniform();
+        }
+        Val r;
+        const int lanes = uni ? 1 : W;
+        for (int k = 0; k < lanes; ++k) {
+          const std::string a = ops[0].at(k), b = ops.size() > 1 ? ops[1].at(k) : "";
+          const std::string t = fresh("t");
+          line("const float " + t + " = " + round_to(n.shape.dtype, op_expr(n.kind, a, b)) + ";");
+          r.lanes.push_back(t);
+        }
+        return r;
+      }
+      case OpClass::ShapeOp: break;
+      case OpClass::Opaque: throw TemplateMismatch("opaque op inside a pattern");
+    }
+    const int src = n.operands.empty() ? -1 : n.operands[0];
+    switch (n.kind) {
+      case OpKind::Broadcast: {
+        Coords in;
+        for (int d : n.attrs.dims) in.push_back(c[static_cast<size_t>(d)]);
+        return value(src, in);
+      }
+      case OpKind::Transpose: {
+        Coords in(c.size());
+        for (size_t j = 0; j < c.size(); ++j) in[static_cast<size_t>(n.attrs.perm[j])] = c[j];
+        return value(src, in);
+      }
+      case OpKind::Slice: {
+        Coords in = c;
+        for (size_t j = 0; j < c.size(); ++j) {
+          const int s = n.attrs.starts[j];
+          if (!s) continue;
+          in[j].base = "(" + c[j].base + " + " + std::to_string(s) + ")";
+          in[j].aligned = c[j].aligned && s % std::max(W, 1) == 0;
+        }
+        return value(src, in);
+      }
+      case OpKind::Gather: {
+        const int data = n.operands[0], indices = n.operands[1];
+        const int kr = g_.node(indices).shape.rank();
+        Coords ic(c.begin(), c.begin() + kr);
+        const Val iv = value(indices, ic);
+        bool tail_vary = false;
+        for (size_t j = static_cast<size_t>(kr); j < c.size(); ++j) tail_vary = tail_vary || c[j].vary;
+        const int lanes = (iv.uniform() && !tail_vary) ? 1 : W;
+        Val r;
+        for (int k = 0; k < lanes; ++k) {
+          Coords dc;
+          dc.push_back({"(" + ix_ + ")" + iv.at(k), false, false});
+          for (size_t j = static_cast<size_t>(kr); j < c.size(); ++j) {
+            Coord x = c[j];
+            if (x.vary && k) x.base = "(" + x.base + " + " + std::to_string(k) + ")";
+            x.vary = false;
+            dc.push_back(x);
+          }
+          if (pattern_.count(data)) throw TemplateMismatch("gather of in-pattern data");
+          loaded.insert(data);
+          const std::string t = fresh("t");
+          line("const float " + t + " = ldv(T_" + g_.node(data).name + ", " + linear(data, dc, 0) + ");");
+          r.lanes.push_back(t);
+        }
+        return r;
+      }
+      default: break;
+    }
+    throw TemplateMismatch("no dataflow rule for " + n.name);
+  }
+
+  const CompGraph& g_;
+  const std::set<int>& pattern_;
+  std::string ix_;
+  int counter_ = 0;
+  std::map<std::string, Val> memo_;
+  std::vector<std::map<std::string, Val>> scopes_;
+};
+
+// ---- analysis ---------------------------------------------------------------
+struct Component {
+  std::vector<int> members;
+  std::vector<int> outputs;
+  std::vector<int> reductions;
+};
+
+enum class Kind { Local, Row, Column };
+
+struct Body {
+  Kind kind;
+  std::vector<int> dims_a, dims_b;  // local: domain dims; row: outer, inner; column: reduced, kept
+  std::vector<int> outputs;         // outputs handled by this body
+  std::vector<int> reductions;
+  int64_t bytes = 0;
+  int blocks = 1;
+};
+
+std::vector<int64_t> to64(const std::vector<int>& v) { return {v.begin(), v.end()}; }
+
+std::vector<int> dims_of(const TensorShape& s) {
+  std::vector<int> d;
+  for (auto x : s.dims) d.push_back(static_cast<int>(x));
+  return d;
+}
+
+int64_t prod(const std::vector<int>& d) {
+  int64_t p = 1;
+  for (int x : d) p *= x;
+  return p;
+}
+
+// does v (transitively, inside the pattern) depend on a reduction?
+bool downstream_of_reduction(const CompGraph& g, const std::set<int>& pat, int v,
+                             std::map<int, bool>& memo) {
+  if (auto it = memo.find(v); it != memo.end()) return it->second;
+  bool r = false;
+  if (pat.count(v)) {
+    if (classify_op(g.node(v)) == OpClass::Reduction) r = true;
+    for (int o : g.node(v).operands) r = r || downstream_of_reduction(g, pat, o, memo);
+  }
+  memo[v] = r;
+  return r;
+}
+
+int reduction_level(const CompGraph& g, const std::set<int>& pat, int v, std::map<int, int>& memo) {
+  if (!pat.count(v)) return 0;
+  if (auto it = memo.find(v); it != memo.end()) return it->second;
+  int lvl = 0;
+  for (int o : g.node(v).operands) lvl = std::max(lvl, reduction_level(g, pat, o, memo));
+  if (classify_op(g.node(v)) == OpClass::Reduction) ++lvl;
+  memo[v] = lvl;
+  return lvl;
+}
+
+std::vector<Component> components_of(const CompGraph& g, const std::vector<int>& verts) {
+  std::set<int> in(verts.begin(), verts.end());
+  const auto cons = g.consumer_lists();
+  std::set<int> seen;
+  std::vector<Component> out;
+  for (int s : verts) {
+    if (seen.count(s)) continue;
+    Component c;
+    std::vector<int> stack{s};
+    seen.insert(s);
+    while (!stack.empty()) {
+      int v = stack.back();
+      stack.pop_back();
+      c.members.push_back(v);
+      auto visit = [&](int u) {
+        if (in.count(u) && seen.insert(u).second) stack.push_back(u);
+      };
+      for (int o : g.node(v).operands) visit(o);
+      for (int x : cons[static_cast<size_t>(v)]) visit(x);
+    }
+    std::sort(c.members.begin(), c.members.end());
+    for (int v : c.members) {
+      bool ext = g.is_output(v);
+      for (int x : cons[static_cast<size_t>(v)]) ext = ext || !in.count(x);
+      if (ext) c.outputs.push_back(v);
+      if (classify_op(g.node(v)) == OpClass::Reduction) c.reductions.push_back(v);
+    }
+    out.push_back(std::move(c));
+  }
+  return out;
+}
+
+// ---- template emitters --------------------------------------------------------
+constexpr int kBlock = 256;
+
+// decompose linear index `lin` (expression) over dims into coordinate exprs
+std::vector<std::string> decompose(Emitter& em, const std::string& lin, const std::vector<int>& dims,
+                                   const std::string& prefix) {
+  std::vector<std::string> cs(dims.size());
+  int64_t stride = 1;
+  for (size_t i = dims.size(); i-- > 0;) {
+    const std::string name = em.fresh(prefix.c_str());
+    std::string e = lin;
+    if (stride != 1) e = "(" + e + ") / " + std::to_string(stride);
+    if (i != 0) e = "(" + e + ") % " + std::to_string(dims[i]);
+    em.line("const " + em.ix() + " " + name + " = " + e + ";");
+    cs[i] = name;
+    stride *= dims[i];
+  }
+  return cs;
+}
+
+void store_val(Emitter& em, const CompGraph& g, int v, const Coords& c, const Val& val,
+               const std::string& guard) {
+  const TensorShape& sh = g.node(v).shape;
+  const std::string ptr = "T_" + g.node(v).name;
+  int nvary = 0;
+  for (const auto& x : c) nvary += x.vary;
+  const std::string pre = guard.empty() ? "" : "if (" + guard + ") ";
+  if (em.W == 4 && nvary == 1 && c.back().vary && c.back().aligned && sh.dtype == DType::F32) {
+    em.line(pre + "st4(" + ptr + " + " + em.linear(v, c, 0) + ", " + val.at(0) + ", " + val.at(1) + ", " +
+            val.at(2) + ", " + val.at(3) + ");");
+    return;
+  }
+  if (nvary == 0) {
+    em.line(pre + "stv(" + ptr + ", " + em.linear(v, c, 0) + ", " + val.at(0) + ");");
+    return;
+  }
+  for (int k = 0; k < em.W; ++k)
+    em.line(pre + "stv(" + ptr + ", " + em.linear(v, c, k) + ", " + val.at(k) + ");");
+}
+
+// local: grid-stride over W-wide chunks of the domain, U chunks per thread
+void emit_local(Emitter& em, const CompGraph& g, const Body& b) {
+  const std::vector<int>& D = b.dims_a;
+  const int64_t N = prod(D);
+  em.W = (!D.empty() && D.back() % 4 == 0) ? 4 : 1;
+  const int64_t chunks = N / em.W;
+  const int U = chunks >= int64_t(kBlock) * kSmCount * 8 ? 4 : 2;
+  em.line("// local body: domain " + std::to_string(N) + " elements, vector " + std::to_string(em.W));
+  em.open("for (i64 c0_ = (i64)vbid * " + std::to_string(kBlock * U) + " + threadIdx.x; c0_ < " +
+          std::to_string(chunks) + "; c0_ += (i64)vgrid * " + std::to_string(kBlock * U) + ")");
+  std::vector<std::tuple<int, Coords, Val, std::string>> stores;
+  for (int u = 0; u < U; ++u) {
+    const std::string ok = em.fresh("ok"), cc = em.fresh("cc");
+    em.line("const bool " + ok + " = c0_ + " + std::to_string(u * kBlock) + " < " + std::to_string(chunks) + ";");
+    em.line("const " + em.ix() + " " + cc + " = (" + em.ix() + ")(" + ok + " ? c0_ + " +
+            std::to_string(u * kBlock) + " : " + std::to_string(chunks - 1) + ");");
+    Coords c;
+    if (!D.empty()) {
+      const std::string lin = em.W == 1 ? cc : cc + " * " + std::to_string(em.W);
+      auto names = decompose(em, lin, D, "d");
+      for (size_t i = 0; i < D.size(); ++i) c.push_back({names[i], i + 1 == D.size() && em.W > 1, true});
+    }
+    for (int o : b.outputs) stores.emplace_back(o, c, em.value(o, c), ok);
+  }
+  for (auto& [o, c, v, ok] : stores) store_val(em, g, o, c, v, ok);
+  em.close();
+}
+
+struct RowParams {
+  int W, TPR, NJ, RPB, block;
+};
+
+RowParams row_params(const std::vector<int>& inner) {
+  const int64_t L = prod(inner);
+  RowParams p;
+  p.W = inner.back() % 4 == 0 ? 4 : (inner.back() % 2 == 0 ? 2 : 1);
+  const int64_t nch = L / p.W;
+  const int nj_target = std::max(1, env_int("STITCH_ROW_NJ", 4));
+  p.TPR = static_cast<int>(std::clamp<int64_t>(pow2ceil((nch + nj_target - 1) / nj_target), 1, 1024));
+  p.NJ = static_cast<int>((nch + p.TPR - 1) / p.TPR);
+  p.block = std::max(kBlock, p.TPR);
+  p.RPB = p.block / p.TPR;
+  return p;
+}
+
+// regional: a team of TPR threads owns a row; row elements live in registers
+void emit_row(Emitter& em, const CompGraph& g, const std::set<int>& pat, const Body& b) {
+  const std::vector<int>& O = b.dims_a;
+  const std::vector<int>& I = b.dims_b;
+  const int64_t ROWS = prod(O), L = prod(I);
+  const RowParams rp = row_params(I);
+  em.W = rp.W;
+  const int64_t nch = L / rp.W;
+  const bool partial = nch % rp.TPR != 0;
+  em.line("// regional body: " + std::to_string(ROWS) + " rows x " + std::to_string(L) + ", team " +
+          std::to_string(rp.TPR) + " threads x " + std::to_string(rp.NJ) + " chunks x " + std::to_string(rp.W));
+  em.line("const int tl_ = threadIdx.x % " + std::to_string(rp.TPR) + ", team_ = threadIdx.x / " +
+          std::to_string(rp.TPR) + ";");
+  std::map<int, int> lvl_memo;
+  std::map<int, std::vector<int>> levels;
+  for (int r : b.reductions) levels[reduction_level(g, pat, r, lvl_memo)].push_back(r);
+  const int nwarps_team = rp.TPR > 32 ? rp.TPR / 32 : 1;
+  if (rp.TPR > 32) {
+    size_t maxr = 0;
+    for (auto& [l, rs] : levels) maxr = std::max(maxr, rs.size());
+    em.line("__shared__ double red_smem_[" + std::to_string(maxr) + "][" + std::to_string(rp.block / 32) + "];");
+  }
+  em.open("for (i64 rb_ = (i64)vbid * " + std::to_string(rp.RPB) + "; rb_ < " + std::to_string(ROWS) +
+          "; rb_ += (i64)vgrid * " + std::to_string(rp.RPB) + ")");
+  em.line("const bool row_ok = rb_ + team_ < " + std::to_string(ROWS) + ";");
+  em.line("const " + em.ix() + " row = (" + em.ix() + ")(row_ok ? rb_ + team_ : " + std::to_string(ROWS - 1) + ");");
+  Coords rowc;
+  {
+    auto names = decompose(em, "row", O, "o");
+    for (auto& n : names) rowc.push_back({n, false, true});
+  }
+  std::vector<Coords> chunk_c(static_cast<size_t>(rp.NJ));
+  std::vector<std::string> chunk_ok(static_cast<size_t>(rp.NJ));
+  for (int j = 0; j < rp.NJ; ++j) {
+    const std::string raw = "(tl_ + " + std::to_string(j * rp.TPR) + ") * " + std::to_string(rp.W);
+    const std::string p = em.fresh("p");
+    if (partial) {
+      chunk_ok[j] = em.fresh("pok");
+      em.line("const bool " + chunk_ok[j] + " = " + raw + " < " + std::to_string(L) + ";");
+      em.line("const " + em.ix() + " " + p + " = " + chunk_ok[j] + " ? " + raw + " : " + std::to_string(L - rp.W) + ";");
+    } else {
+      em.line("const " + em.ix() + " " + p + " = " + raw + ";");
+    }
+    Coords c = rowc;
+    if (I.size() == 1) {
+      c.push_back({p, rp.W > 1, true});
+    } else {
+      auto names = decompose(em, p, I, "i");
+      for (size_t a = 0; a < I.size(); ++a) c.push_back({names[a], a + 1 == I.size() && rp.W > 1, true});
+    }
+    chunk_c[j] = c;
+  }
+  for (auto& [lvl, rs] : levels) {
+    std::vector<std::string> acc;
+    for (int r : rs) {
+      const bool sum = g.node(r).kind == OpKind::ReduceSum;
+      acc.push_back(em.fresh("acc"));
+      em.line(std::string(sum ? "double " : "float ") + acc.back() + " = " +
+              (sum ? "0.0" : "__int_as_float(0xff800000)") + ";");
+    }
+    for (int j = 0; j < rp.NJ; ++j) {
+      for (size_t i = 0; i < rs.size(); ++i) {
+        const int r = rs[i];
+        const bool sum = g.node(r).kind == OpKind::ReduceSum;
+        const Val v = em.value(g.node(r).operands[0], chunk_c[j]);
+        std::string upd;
+        for (int k = 0; k < rp.W; ++k) {
+          std::string x = v.at(k);
+          if (sum) upd += acc[i] + " += (double)" + x + "; ";
+          else upd += acc[i] + " = op_max(" + acc[i] + ", " + x + "); ";
+        }
+        em.line((partial ? "if (" + chunk_ok[j] + ") { " : "{ ") + upd + "}");
+      }
+    }
+    // team reduction: butterfly inside the warp, smem across the team's warps
+    const int w = std::min(rp.TPR, 32);
+    for (size_t i = 0; i < rs.size(); ++i) {
+      const bool sum = g.node(rs[i]).kind == OpKind::ReduceSum;
+      if (w > 1) em.line(acc[i] + " = " + (sum ? "bfly_sum(" : "bfly_max(") + acc[i] + ", " + std::to_string(w) + ");");
+    }
+    if (rp.TPR > 32) {
+      em.line("if ((threadIdx.x & 31) == 0) {");
+      for (size_t i = 0; i < rs.size(); ++i)
+        em.line("  red_smem_[" + std::to_string(i) + "][threadIdx.x >> 5] = " + acc[i] + ";");
+      em.line("}");
+      em.line("__syncthreads();");
+      for (size_t i = 0; i < rs.size(); ++i) {
+        const bool sum = g.node(rs[i]).kind == OpKind::ReduceSum;
+        em.line("{ const int w0_ = team_ * " + std::to_string(nwarps_team) + "; " + acc[i] +
+                " = red_smem_[" + std::to_string(i) + "][w0_]; for (int q_ = 1; q_ < " +
+                std::to_string(nwarps_team) + "; ++q_) " + acc[i] + " = " +
+                (sum ? acc[i] + " + red_smem_[" + std::to_string(i) + "][w0_ + q_]"
+                     : "op_max(" + acc[i] + ", (float)red_smem_[" + std::to_string(i) + "][w0_ + q_])") +
+                "; }");
+      }
+      em.line("__syncthreads();");
+    }
+    for (size_t i = 0; i < rs.size(); ++i) {
+      const std::string t = em.fresh("red");
+      std::string e = "(float)" + acc[i];
+      const DType d = g.node(rs[i]).shape.dtype;
+      if (d == DType::F16) e = "rnd_f16(" + e + ")";
+      em.line("const float " + t + " = " + e + ";");
+      em.reduced[Emitter::key(rs[i], rowc)] = Val{{t}};
+    }
+  }
+  // outputs
+  for (int o : b.outputs) {
+    const auto& od = g.node(o).shape.dims;
+    if (static_cast<int64_t>(od.size()) == static_cast<int64_t>(O.size())) {
+      const Val v = em.value(o, rowc);
+      em.line("if (row_ok && tl_ == 0) stv(T_" + g.node(o).name + ", " + em.linear(o, rowc, 0) + ", " + v.at(0) + ");");
+      continue;
+    }
+    for (int j = 0; j < rp.NJ; ++j) {
+      const Val v = em.value(o, chunk_c[j]);
+      store_val(em, g, o, chunk_c[j], v, partial ? "row_ok && " + chunk_ok[j] : "row_ok");
+    }
+  }
+  em.close();
+}
+
+struct ColParams {
+  int W, CT, RT, NCB, RB, U;
+  int64_t NCH, ROWS, COLS;
+};
+
+ColParams col_params(const std::vector<int>& P, const std::vector<int>& C, int max_blocks) {
+  ColParams p;
+  p.ROWS = prod(P);
+  p.COLS = prod(C);
+  p.W = C.back() % 4 == 0 ? 4 : 1;
+  p.NCH = p.COLS / p.W;
+  p.CT = static_cast<int>(std::min<int64_t>(32, p.NCH));
+  p.CT = static_cast<int>(pow2ceil(p.CT));
+  p.RT = kBlock / p.CT;
+  p.NCB = static_cast<int>((p.NCH + p.CT - 1) / p.CT);
+  const int64_t want_rb = std::max<int64_t>(1, (p.ROWS + p.RT * 16 - 1) / (p.RT * 16));
+  p.RB = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want_rb, max_blocks / p.NCB)));
+  p.U = 4;
+  return p;
+}
+
+// global phase 1: partial column sums of this CTA's row slab -> scratch
+void emit_column_phase1(Emitter& em, const CompGraph& g, const Body& b, const ColParams& cp,
+                        int64_t partial_off) {
+  const std::vector<int>& P = b.dims_a;
+  const std::vector<int>& C = b.dims_b;
+  em.W = cp.W;
+  em.line("// global body phase 1: " + std::to_string(cp.ROWS) + " reduced rows x " + std::to_string(cp.COLS) +
+          " columns, tile " + std::to_string(cp.CT * cp.W) + " cols x " + std::to_string(cp.RT) + " rows");
+  em.line("const int cx_ = threadIdx.x % " + std::to_string(cp.CT) + ", ry_ = threadIdx.x / " + std::to_string(cp.CT) + ";");
+  em.line("const int cb_ = vbid % " + std::to_string(cp.NCB) + ", rbk_ = vbid / " + std::to_string(cp.NCB) + ";");
+  em.line("const bool col_ok = cb_ * " + std::to_string(cp.CT) + " + cx_ < " + std::to_string(cp.NCH) + ";");
+  em.line("const " + em.ix() + " ch_ = col_ok ? cb_ * " + std::to_string(cp.CT) + " + cx_ : " + std::to_string(cp.NCH - 1) + ";");
+  em.line("const i64 rspan_ = (" + std::to_string(cp.ROWS) + " + " + std::to_string(cp.RB) + " - 1) / " + std::to_string(cp.RB) + ";");
+  em.line("const i64 r0_ = (i64)rbk_ * rspan_, r1_ = min((i64)" + std::to_string(cp.ROWS) + ", r0_ + rspan_);");
+  Coords colc;
+  {
+    const std::string lin = cp.W == 1 ? "ch_" : "ch_ * " + std::to_string(cp.W);
+    auto names = decompose(em, lin, C, "c");
+    for (size_t i = 0; i < C.size(); ++i) colc.push_back({names[i], i + 1 == C.size() && cp.W > 1, true});
+  }
+  const size_t nr = b.reductions.size();
+  std::vector<std::vector<std::string>> acc(nr);
+  for (size_t i = 0; i < nr; ++i) {
+    const bool sum = g.node(b.reductions[i]).kind == OpKind::ReduceSum;
+    for (int k = 0; k < cp.W; ++k) {
+      acc[i].push_back(em.fresh("acc"));
+      em.line(std::string(sum ? "double " : "float ") + acc[i].back() + " = " +
+              (sum ? "0.0" : "__int_as_float(0xff800000)") + ";");
+    }
+  }
+  em.open("for (i64 r_ = r0_ + ry_; r_ < r1_; r_ += " + std::to_string(cp.RT * cp.U) + ")");
+  std::vector<std::tuple<int, Coords, Val, std::string>> stores;
+  for (int u = 0; u < cp.U; ++u) {
+    const std::string ok = em.fresh("ok"), rr = em.fresh("rr");
+    em.line("const bool " + ok + " = r_ + " + std::to_string(u * cp.RT) + " < r1_;");
+    em.line("const " + em.ix() + " " + rr + " = (" + em.ix() + ")(" + ok + " ? r_ + " + std::to_string(u * cp.RT) + " : r_);");
+    Coords c;
+    auto names = decompose(em, rr, P, "r");
+    for (auto& n : names) c.push_back({n, false, true});
+    c.insert(c.end(), colc.begin(), colc.end());
+    for (size_t i = 0; i < nr; ++i) {
+      const int r = b.reductions[i];
+      const bool sum = g.node(r).kind == OpKind::ReduceSum;
+      const Val v = em.value(g.node(r).operands[0], c);
+      std::string upd;
+      for (int k = 0; k < cp.W; ++k)
+        upd += sum ? acc[i][k] + " += (double)" + v.at(k) + "; "
+                   : acc[i][k] + " = op_max(" + acc[i][k] + ", " + v.at(k) + "); ";
+      em.line("if (" + ok + ") { " + upd + "}");
+    }
+    for (int o : b.outputs)
+      if (g.node(o).shape.rank() == static_cast<int>(P.size() + C.size()))
+        stores.emplace_back(o, c, em.value(o, c), "col_ok && " + ok);
+  }
+  for (auto& [o, c, v, ok] : stores) store_val(em, g, o, c, v, ok);
+  em.close();
+  // fold the RT row lanes of the tile in smem (fixed order), write partials
+  if (nr) {
+    em.line("__shared__ double tile_[" + std::to_string(cp.RT) + "][" + std::to_string(cp.CT * cp.W) + "];");
+    for (size_t i = 0; i < nr; ++i) {
+      const bool sum = g.node(b.reductions[i]).kind == OpKind::ReduceSum;
+      for (int k = 0; k < cp.W; ++k)
+        em.line("tile_[ry_][cx_ * " + std::to_string(cp.W) + " + " + std::to_string(k) + "] = " + acc[i][k] + ";");
+      em.line("__syncthreads();");
+      em.open("if (ry_ == 0 && col_ok)");
+      for (int k = 0; k < cp.W; ++k) {
+        const std::string col = "cx_ * " + std::to_string(cp.W) + " + " + std::to_string(k);
+        em.line("{ double s_ = tile_[0][" + col + "]; for (int q_ = 1; q_ < " + std::to_string(cp.RT) +
+                "; ++q_) s_ = " + (sum ? "s_ + tile_[q_][" + col + "]" : "dmax(s_, tile_[q_][" + col + "])") +
+                "; part_[" + std::to_string(partial_off + static_cast<int64_t>(i) * cp.RB * cp.COLS) +
+                " + (i64)rbk_ * " + std::to_string(cp.COLS) + " + (i64)ch_ * " + std::to_string(cp.W) + " + " +
+                std::to_string(k) + "] = s_; }");
+      }
+      em.close();
+      em.line("__syncthreads();");
+    }
+  }
+}
+
+// global phase 2 (after the grid barrier): combine partials in fixed order,
+// then the column-shaped consumers
+void emit_column_phase2(Emitter& em, const CompGraph& g, const Body& b, const ColParams& cp,
+                        int64_t partial_off) {
+  const std::vector<int>& P = b.dims_a;
+  const std::vector<int>& C = b.dims_b;
+  em.W = cp.W;
+  em.line("// global body phase 2: fixed-order combine of " + std::to_string(cp.RB) + " partial slabs");
+  em.open("for (i64 q_ = (i64)vbid * blockDim.x + threadIdx.x; q_ < " + std::to_string(cp.NCH) +
+          "; q_ += (i64)vgrid * blockDim.x)");
+  Coords colc;
+  {
+    const std::string lin = cp.W == 1 ? "q_" : "q_ * " + std::to_string(cp.W);
+    auto names = decompose(em, "(" + em.ix() + ")(" + lin + ")", C, "c");
+    for (size_t i = 0; i < C.size(); ++i) colc.push_back({names[i], i + 1 == C.size() && cp.W > 1, true});
+  }
+  for (size_t i = 0; i < b.reductions.size(); ++i) {
+    const int r = b.reductions[i];
+    const bool sum = g.node(r).kind == OpKind::ReduceSum;
+    Val v;
+    for (int k = 0; k < cp.W; ++k) {
+      const std::string s = em.fresh("s"), t = em.fresh("red");
+      const std::string base = std::to_string(partial_off + static_cast<int64_t>(i) * cp.RB * cp.COLS) +
+                               " + q_ * " + std::to_string(cp.W) + " + " + std::to_string(k);
+      em.line("double " + s + " = part_[" + base + "];");
+      em.line("for (int k_ = 1; k_ < " + std::to_string(cp.RB) + "; ++k_) " + s + " = " +
+              (sum ? s + " + part_[" + base + " + (i64)k_ * " + std::to_string(cp.COLS) + "]"
+                   : "dmax(" + s + ", part_[" + base + " + (i64)k_ * " + std::to_string(cp.COLS) + "])") + ";");
+      em.line("const float " + t + " = (float)" + s + ";");
+      v.lanes.push_back(t);
+    }
+    em.reduced[Emitter::key(r, colc)] = v;
+  }
+  for (int o : b.outputs)
+    if (g.node(o).shape.rank() == static_cast<int>(C.size()) && g.node(o).shape.dims == to64(C))
+      store_val(em, g, o, colc, em.value(o, colc), "");
+  (void)P;
+  em.close();
+}
+
+}  // namespace
+
+KernelSpec generate_pattern_kernel(const CompGraph& g, const std::vector<int>& verts,
+                                   const std::string& name, int sm_count) {
+  (void)sm_count;
+  const std::set<int> pat(verts.begin(), verts.end());
+  std::map<int, bool> dmemo;
+  std::vector<Body> bodies;
+  auto add_body = [&](Body nb) {
+    for (auto& b : bodies)
+      if (b.kind == nb.kind && b.dims_a == nb.dims_a && b.dims_b == nb.dims_b) {
+        b.outputs.insert(b.outputs.end(), nb.outputs.begin(), nb.outputs.end());
+        b.reductions.insert(b.reductions.end(), nb.reductions.begin(), nb.reductions.end());
+        std::sort(b.reductions.begin(), b.reductions.end());
+        return;
+      }
+    bodies.push_back(std::move(nb));
+  };
+  for (const Component& comp : components_of(g, verts)) {
+    if (comp.reductions.empty()) {
+      for (int o : comp.outputs) add_body({Kind::Local, dims_of(g.node(o).shape), {}, {o}, {}});
+      continue;
+    }
+    // common split of every reduction's operand shape
+    bool rows = true, cols = true;
+    std::vector<int> A, B, A2, B2;
+    for (size_t i = 0; i < comp.reductions.size(); ++i) {
+      const OpNode& r = g.node(comp.reductions[i]);
+      const auto in = dims_of(g.node(r.operands[0]).shape);
+      std::set<int> ax(r.attrs.axes.begin(), r.attrs.axes.end());
+      const int m = static_cast<int>(ax.size()), n = static_cast<int>(in.size());
+      bool suffix = true, prefix = m < n;
+      for (int a = 0; a < n; ++a) {
+        suffix = suffix && (ax.count(a) > 0) == (a >= n - m);
+        prefix = prefix && (ax.count(a) > 0) == (a < m);
+      }
+      std::vector<int> o(in.begin(), in.end() - m), inn(in.end() - m, in.end());
+      std::vector<int> pp(in.begin(), in.begin() + std::min(m, n)), cc(in.begin() + std::min(m, n), in.end());
+      if (i == 0) {
+        A = o, B = inn, A2 = pp, B2 = cc;
+      }
+      rows = rows && suffix && o == A && inn == B;
+      cols = cols && prefix && pp == A2 && cc == B2;
+    }
+    Body body;
+    if (rows) {
+      body = {Kind::Row, A, B, {}, comp.reductions};
+    } else if (cols) {
+      body = {Kind::Column, A2, B2, {}, comp.reductions};
+    } else {
+      throw TemplateMismatch("reductions of one component disagree on their split");
+    }
+    std::vector<int> full = body.dims_a;
+    full.insert(full.end(), body.dims_b.begin(), body.dims_b.end());
+    const std::vector<int>& unit = body.kind == Kind::Row ? body.dims_a : body.dims_b;
+    for (int o : comp.outputs) {
+      const auto od = dims_of(g.node(o).shape);
+      const bool dep = downstream_of_reduction(g, pat, o, dmemo);
+      if (od == full && (body.kind == Kind::Row || !dep)) {
+        body.outputs.push_back(o);
+      } else if (od == unit && (dep || body.kind == Kind::Row)) {
+        body.outputs.push_back(o);
+      } else if (!dep) {
+        add_body({Kind::Local, od, {}, {o}, {}});
+      } else {
+        throw TemplateMismatch("output " + g.node(o).name + " does not fit the reduction domain");
+      }
+    }
+    add_body(std::move(body));
+  }
+
+  // index width: 32-bit unless some tensor reaches 2^31 elements
+  bool wide = false;
+  for (int v : verts) {
+    wide = wide || g.node(v).shape.element_count() >= (int64_t(1) << 31);
+    for (int o : g.node(v).operands) wide = wide || g.node(o).shape.element_count() >= (int64_t(1) << 31);
+  }
+  Emitter em(g, pat, wide);
+  // broadcast sources re-read by many threads go through L1
+  for (int v : verts)
+    if (g.node(v).kind == OpKind::Broadcast) {
+      const int s = g.node(v).operands[0];
+      if (!pat.count(s)) em.cached_tensors.insert(s);
+    }
+
+  bool coop = false;
+  int block = kBlock;
+  for (const auto& b : bodies) {
+    if (b.kind == Kind::Column) coop = true;
+    if (b.kind == Kind::Row) block = std::max(block, row_params(b.dims_b).block);
+  }
+  const int per_sm = std::max(1, std::min(2, 2048 / block));
+  const int coop_cap = kSmCount * per_sm;
+
+  // CTA budget per body
+  int64_t scratch_words = 0;
+  std::vector<ColParams> cps(bodies.size());
+  std::vector<int64_t> part_off(bodies.size(), 0);
+  int64_t n_col_bodies = 0;
+  for (const auto& b : bodies) n_col_bodies += b.kind == Kind::Column;
+  for (size_t i = 0; i < bodies.size(); ++i) {
+    Body& b = bodies[i];
+    if (b.kind == Kind::Local) {
+      const int64_t N = prod(b.dims_a);
+      const int w = (!b.dims_a.empty() && b.dims_a.back() % 4 == 0) ? 4 : 1;
+      const int64_t chunks = N / w;
+      const int U = chunks >= int64_t(kBlock) * kSmCount * 8 ? 4 : 2;
+      b.blocks = static_cast<int>(std::clamp<int64_t>((chunks + int64_t(kBlock) * U - 1) / (int64_t(kBlock) * U), 1,
+                                                      int64_t(kSmCount) * 16));
+    } else if (b.kind == Kind::Row) {
+      const RowParams rp = row_params(b.dims_b);
+      b.blocks = static_cast<int>(std::clamp<int64_t>((prod(b.dims_a) + rp.RPB - 1) / rp.RPB, 1,
+                                                      int64_t(kSmCount) * 16));
+    } else {
+      const int cap = static_cast<int>(coop_cap / std::max<int64_t>(1, n_col_bodies));
+      cps[i] = col_params(b.dims_a, b.dims_b, std::max(1, cap - static_cast<int>(bodies.size())));
+      b.blocks = cps[i].NCB * cps[i].RB;
+      part_off[i] = scratch_words;
+      scratch_words += static_cast<int64_t>(b.reductions.size()) * cps[i].RB * cps[i].COLS;
+    }
+    std::vector<int> members;
+    for (int o : b.outputs) members.push_back(o);
+    b.bytes = 0;
+  }
+  if (coop) {  // every CTA must be co-resident: the other bodies share what is left
+    int col_total = 0, others = 0;
+    for (const auto& b : bodies) (b.kind == Kind::Column ? col_total : others) += b.kind == Kind::Column ? b.blocks : 1;
+    const int share = std::max(1, (coop_cap - col_total) / std::max(1, others));
+    for (auto& b : bodies)
+      if (b.kind != Kind::Column) b.blocks = std::min(b.blocks, share);
+  }
+
+  std::ostringstream body_src;
+  int start = 0;
+  std::vector<int> starts;
+  for (size_t i = 0; i < bodies.size(); ++i) {
+    starts.push_back(start);
+    const Body& b = bodies[i];
+    em.out.str("");
+    em.ind = "    ";
+    em.clear_memo();
+    em.reduced.clear();
+    if (b.kind == Kind::Local) emit_local(em, g, b);
+    else if (b.kind == Kind::Row) emit_row(em, g, pat, b);
+    else emit_column_phase1(em, g, b, cps[i], part_off[i]);
+    body_src << "  " << (i ? "else " : "") << "if (blockIdx.x < " << start + b.blocks << ") {\n";
+    body_src << "    const int vbid = blockIdx.x - " << start << ", vgrid = " << b.blocks << ";\n";
+    body_src << "    (void)vbid; (void)vgrid;\n" << em.out.str() << "  }\n";
+    start += b.blocks;
+  }
+  if (coop) {
+    body_src << "  grid_sync(bar_, gridDim.x);\n";
+    for (size_t i = 0; i < bodies.size(); ++i) {
+      if (bodies[i].kind != Kind::Column) continue;
+      em.out.str("");
+      em.ind = "    ";
+      em.clear_memo();
+      em.reduced.clear();
+      emit_column_phase2(em, g, bodies[i], cps[i], part_off[i]);
+      body_src << "  if (blockIdx.x >= " << starts[i] << " && blockIdx.x < " << starts[i] + bodies[i].blocks
+               << ") {\n    const int vbid = blockIdx.x - " << starts[i] << ", vgrid = " << bodies[i].blocks
+               << ";\n" << em.out.str() << "  }\n";
+    }
+  }
+
+  KernelSpec k;
+  k.name = name;
+  k.tmpl = bodies.size() > 1 ? "independent" : bodies[0].kind == Kind::Local ? "local"
+                                             : bodies[0].kind == Kind::Row ? "regional" : "global";
+  if (bodies.size() > 1) {
+    k.tmpl += "(";
+    for (size_t i = 0; i < bodies.size(); ++i)
+      k.tmpl += std::string(i ? "+" : "") +
+                (bodies[i].kind == Kind::Local ? "local" : bodies[i].kind == Kind::Row ? "regional" : "global");
+    k.tmpl += ")";
+  }
+  k.grid = start;
+  k.block = block;
+  k.cooperative = coop;
+  k.alg_bytes = algorithmic_bytes(g, verts);
+  std::set<int> outs;
+  for (const auto& b : bodies) outs.insert(b.outputs.begin(), b.outputs.end());
+  std::ostringstream sig;
+  sig << "extern \"C\" __global__ void __launch_bounds__(" << block << (coop ? ", " + std::to_string(per_sm) : "")
+      << ") " << name << "(";
+  bool first = true;
+  for (int v : em.loaded) {
+    sig << (first ? "" : ", ") << "const " << c_type(g.node(v).shape.dtype) << "* __restrict__ T_" << g.node(v).name;
+    first = false;
+    k.inputs.push_back(g.node(v).name);
+  }
+  for (int v : outs) {
+    sig << (first ? "" : ", ") << c_type(g.node(v).shape.dtype) << "* __restrict__ T_" << g.node(v).name;
+    first = false;
+    k.outputs.push_back(g.node(v).name);
+  }
+  if (coop) {
+    sig << (first ? "" : ", ") << "unsigned* __restrict__ bar_, double* __restrict__ part_";
+    k.scratch_bytes = 256 + scratch_words * 8;
+  }
+  sig << ") {\n";
+  k.source = sig.str() + body_src.str() + "}\n";
+  return k;
+}
+
+// opaque_compute placeholder: mean of every operand element, broadcast
+// (src/sim.cpp:215-226).  Phase 1 per-CTA f64 partial sums, grid barrier,
+// every CTA folds the partials in the same order, then fills the output.
+KernelSpec generate_opaque_kernel(const CompGraph& g, int vertex, const std::string& name, int) {
+  const OpNode& n = g.node(vertex);
+  const int grid = kSmCount;
+  KernelSpec k;
+  k.name = name;
+  k.tmpl = "opaque";
+  k.pattern_key = "op:" + n.name;
+  k.grid = grid;
+  k.block = kBlock;
+  k.cooperative = true;
+  std::ostringstream s;
+  s << "extern \"C\" __global__ void __launch_bounds__(" << kBlock << ", 1) " << name << "(";
+  std::set<int> ops(n.operands.begin(), n.operands.end());
+  int64_t count = 0;
+  for (int o : n.operands) count += g.node(o).shape.element_count();
+  for (int o : ops) {
+    s << "const " << c_type(g.node(o).shape.dtype) << "* __restrict__ T_" << g.node(o).name << ", ";
+    k.inputs.push_back(g.node(o).name);
+  }
+  s << c_type(n.shape.dtype) << "* __restrict__ T_" << n.name << ", unsigned* __restrict__ bar_, double* __restrict__ part_) {\n";
+  k.outputs.push_back(n.name);
+  k.scratch_bytes = 256 + int64_t(grid) * 8;
+  s << "  __shared__ double red_[" << kBlock / 32 << "];\n  double acc = 0.0;\n";
+  for (int o : n.operands) {  // an operand listed twice is counted twice, as upstream
+    s << "  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < " << g.node(o).shape.element_count()
+      << "; i += (i64)gridDim.x * blockDim.x) acc += (double)ldv(T_" << g.node(o).name << ", i);\n";
+  }
+  s << "  acc = bfly_sum(acc, 32);\n  if ((threadIdx.x & 31) == 0) red_[threadIdx.x >> 5] = acc;\n  __syncthreads();\n"
+    << "  if (threadIdx.x == 0) { double t = 0.0; for (int w = 0; w < " << kBlock / 32
+    << "; ++w) t += red_[w]; part_[blockIdx.x] = t; }\n"
+    << "  grid_sync(bar_, gridDim.x);\n"
+    << "  double tot = 0.0;\n  for (int b = 0; b < " << grid << "; ++b) tot += part_[b];\n"
+    << "  const float fill = (float)(" << (count ? "tot / " + std::to_string(count) + ".0" : "0.0") << ");\n"
+    << "  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < " << n.shape.element_count()
+    << "; i += (i64)gridDim.x * blockDim.x) stv(T_" << n.name << ", i, fill);\n}\n";
+  k.source = s.str();
+  int64_t bytes = n.shape.byte_size();
+  for (int o : ops) bytes += g.node(o).shape.byte_size();
+  k.alg_bytes = bytes;
+  return k;
+}
+
+}  // namespace stitch::gpu

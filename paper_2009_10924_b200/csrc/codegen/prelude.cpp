@@ -1,0 +1,131 @@
+// Device-side helpers compiled into every NVRTC module, and small host
+// formatting utilities for the generators.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <set>
+
+#include "codegen/cg.hpp"
+
+namespace stitch::gpu {
+
+const std::string& device_prelude() {
+  static const std::string src = R"CUDA(
+// ---- stitch-b200 device prelude (sm_100a) ----
+typedef long long i64;
+typedef unsigned short f16_t;
+#define FULL_MASK 0xffffffffu
+
+__device__ __forceinline__ float h2f(f16_t h) { float f; asm("cvt.f32.f16 %0, %1;" : "=f"(f) : "h"(h)); return f; }
+__device__ __forceinline__ f16_t f2h(float f) { f16_t h; asm("cvt.rn.f16.f32 %0, %1;" : "=h"(h) : "f"(f)); return h; }
+
+// tensor element <-> f32 value (stitch::DType: f32 / f16 / i32 / bool)
+__device__ __forceinline__ float ldv(const float* p, i64 i) { return __ldg(p + i); }
+__device__ __forceinline__ float ldv(const f16_t* p, i64 i) { return h2f(__ldg(p + i)); }
+__device__ __forceinline__ float ldv(const int* p, i64 i) { return (float)__ldg(p + i); }
+__device__ __forceinline__ float ldv(const unsigned char* p, i64 i) { return __ldg(p + i) ? 1.f : 0.f; }
+__device__ __forceinline__ void stv(float* p, i64 i, float v) { p[i] = v; }
+__device__ __forceinline__ void stv(f16_t* p, i64 i, float v) { p[i] = f2h(v); }
+__device__ __forceinline__ void stv(int* p, i64 i, float v) { p[i] = (int)roundf(v); }
+__device__ __forceinline__ void stv(unsigned char* p, i64 i, float v) { p[i] = v != 0.f; }
+
+// 128-bit streaming load that does not allocate in L1 (read-once data)
+__device__ __forceinline__ float4 ld4(const float* p) {
+  float4 r;
+  asm("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+      : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
+  return r;
+}
+// 128-bit load through L1 (data re-read by many threads, e.g. gamma/beta rows)
+__device__ __forceinline__ float4 ld4c(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
+__device__ __forceinline__ void st4(float* p, float a, float b, float c, float d) {
+  *reinterpret_cast<float4*>(p) = make_float4(a, b, c, d);
+}
+
+// per-op rounding to the node dtype (src/sim.cpp:67-75 semantics)
+__device__ __forceinline__ float rnd_f16(float x) { return h2f(f2h(x)); }
+__device__ __forceinline__ float rnd_i32(float x) { return (float)(int)roundf(x); }
+__device__ __forceinline__ float rnd_bool(float x) { return x != 0.f ? 1.f : 0.f; }
+
+// std::max / std::min argument order (NaN behaviour of the reference)
+__device__ __forceinline__ float op_max(float a, float b) { return a < b ? b : a; }
+__device__ __forceinline__ float op_min(float a, float b) { return b < a ? b : a; }
+__device__ __forceinline__ double dmax(double a, double b) { return a < b ? b : a; }
+__device__ __forceinline__ float op_rsqrt(float a) { return 1.0f / sqrtf(a); }
+
+// butterfly over `width` lanes (power of two <= 32): every lane gets the result
+__device__ __forceinline__ double bfly_sum(double v, int width) {
+  for (int o = width >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(FULL_MASK, v, o);
+  return v;
+}
+__device__ __forceinline__ float bfly_max(float v, int width) {
+  for (int o = width >> 1; o > 0; o >>= 1) v = op_max(v, __shfl_xor_sync(FULL_MASK, v, o));
+  return v;
+}
+
+// Grid-wide barrier for cooperative (co-resident) launches.  bar[0] counts
+// arrivals, bar[1] is the generation; both start at zero and bar[0] returns
+// to zero after every barrier, so the scratch word can be reused forever.
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ void grid_sync(unsigned* bar, unsigned nblocks) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned gen = ld_acquire(bar + 1);
+    __threadfence();
+    if (atomicAdd(bar, 1u) == nblocks - 1) {
+      atomicExch(bar, 0u);
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      while (ld_acquire(bar + 1) == gen) __nanosleep(40);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+)CUDA";
+  return src;
+}
+
+std::string c_float(double v) {
+  const float f = static_cast<float>(v);
+  if (std::isnan(f)) return "__int_as_float(0x7fc00000)";
+  if (std::isinf(f)) return f > 0 ? "__int_as_float(0x7f800000)" : "__int_as_float(0xff800000)";
+  char buf[64];
+  std::snprintf(buf, sizeof buf, "%.9ef", static_cast<double>(f));  // round-trips exactly
+  return buf;
+}
+
+const char* c_type(DType d) {
+  switch (d) {
+    case DType::F32: return "float";
+    case DType::F16: return "f16_t";
+    case DType::I32: return "int";
+    case DType::Bool: return "unsigned char";
+  }
+  return "float";
+}
+
+int64_t algorithmic_bytes(const CompGraph& g, const std::vector<int>& vertices) {
+  std::set<int> in(vertices.begin(), vertices.end());
+  std::set<int> ext_in, ext_out;
+  for (int v : vertices) {
+    for (int o : g.node(v).operands)
+      if (!in.count(o) && g.node(o).kind != OpKind::Constant) ext_in.insert(o);
+    if (g.is_output(v)) ext_out.insert(v);
+  }
+  for (const auto& n : g.nodes)
+    if (!in.count(n.id))
+      for (int o : n.operands)
+        if (in.count(o)) ext_out.insert(o);
+  int64_t b = 0;
+  for (int t : ext_in) b += g.node(t).shape.byte_size();
+  for (int t : ext_out) b += g.node(t).shape.byte_size();
+  return b;
+}
+
+}  // namespace stitch::gpu

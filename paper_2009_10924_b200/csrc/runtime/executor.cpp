@@ -1,0 +1,417 @@
+#include "runtime/executor.hpp"
+
+#include <algorithm>
+#include <cctype>
+#include <cstring>
+#include <set>
+#include <sstream>
+#include <stdexcept>
+
+namespace stitch::gpu {
+
+namespace {
+
+std::string sanitize(const std::string& s) {
+  std::string o;
+  for (char c : s) o += (std::isalnum(static_cast<unsigned char>(c)) ? c : '_');
+  return o;
+}
+
+std::string json_escape(const std::string& s) {
+  std::string o;
+  for (char c : s) {
+    if (c == '"' || c == '\\') o += '\\';
+    o += c;
+  }
+  return o;
+}
+
+}  // namespace
+
+Executor::Executor(const CompGraph& g, const FusionPlan& plan,
+                   const std::map<std::string, KernelPlan>& kernels, const MachineModel& model,
+                   int device, ExecMode mode, bool use_graph)
+    : g_(g), use_graph_(use_graph) {
+  dev_ = &device_init(device);
+  STC_RT(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+  plan_launches(plan, kernels, model, mode);
+  module_ = std::make_unique<Module>(compile_cubin(source_, default_nvrtc_options()));
+  for (const auto& k : specs_) {
+    cudaKernel_t f = module_->fn(k.name);
+    const void* fp = reinterpret_cast<const void*>(f);
+    if (k.smem > 48 * 1024)
+      STC_RT(cudaFuncSetAttribute(fp, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(k.smem)));
+    if (k.cooperative) {
+      int per_sm = 0;
+      STC_RT(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fp, k.block, static_cast<size_t>(k.smem)));
+      if (int64_t(per_sm) * dev_->sm_count < k.grid)
+        throw std::runtime_error("[cuda] cooperative kernel " + k.name + " needs " + std::to_string(k.grid) +
+                                 " co-resident CTAs, device fits " + std::to_string(per_sm * dev_->sm_count));
+    }
+    fns_.push_back(f);
+  }
+  ensure_sets(1);
+}
+
+Executor::~Executor() {
+  for (auto ge : graphs_)
+    if (ge) cudaGraphExecDestroy(ge);
+  for (auto& [n, t] : tensors_)
+    for (void* p : t.dptr) cudaFree(p);
+  for (auto& set : scratch_)
+    for (void* p : set)
+      if (p) cudaFree(p);
+  if (stream_) cudaStreamDestroy(stream_);
+}
+
+PlanKernels generate_plan_kernels(const CompGraph& g_, const FusionPlan& plan,
+                                  const std::map<std::string, KernelPlan>& kernels,
+                                  const MachineModel& model, ExecMode mode, int sm_count) {
+  PlanKernels out;
+  auto& specs_ = out.specs;
+  auto& params_ = out.params;
+  const auto order = topo_sort(g_);
+  std::vector<int> pos(g_.nodes.size());
+  for (size_t i = 0; i < order.size(); ++i) pos[static_cast<size_t>(order[i])] = static_cast<int>(i);
+  std::map<int, const FusionPattern*> fire_at;
+  std::set<int> covered;
+  if (mode != ExecMode::Unfused)
+    for (const auto& p : plan.patterns) {
+      int last = p.vertices.front();
+      for (int v : p.vertices) {
+        covered.insert(v);
+        if (pos[v] > pos[last]) last = v;
+      }
+      fire_at[last] = &p;
+    }
+  const auto cons = g_.consumer_lists();
+  auto need_materialize = [&](int v) {  // constants read as tensors
+    if (g_.is_output(v)) return true;
+    for (int c : cons[static_cast<size_t>(v)])
+      if (classify_op(g_.node(c)) == OpClass::Opaque) return true;
+    return false;
+  };
+  std::map<std::string, KernelPlan> singles;
+  int idx = 0;
+  auto add_pattern = [&](const std::vector<int>& verts, const std::string& key) {
+    const std::string name = "k" + std::to_string(idx++) + "_" + sanitize(g_.node(verts.front()).name);
+    KernelSpec spec;
+    bool done = false;
+    if (mode != ExecMode::Program) {
+      try {
+        spec = generate_pattern_kernel(g_, verts, name, sm_count);
+        done = true;
+      } catch (const TemplateMismatch&) {
+      }
+    }
+    if (!done) {
+      const KernelPlan* kp = nullptr;
+      if (auto it = kernels.find(key); it != kernels.end()) kp = &it->second;
+      if (!kp) {
+        auto it = singles.find(key);
+        if (it == singles.end()) {
+          FusionPattern p;
+          p.vertices = verts;
+          p.producer = verts.front();
+          auto planned = plan_kernel(p, g_, model);
+          if (!planned) throw std::runtime_error("[planner] no feasible kernel for pattern " + key);
+          it = singles.emplace(key, std::move(*planned)).first;
+        }
+        kp = &it->second;
+      }
+      spec = generate_program_kernel(g_, kp->program, name);
+      spec.alg_bytes = algorithmic_bytes(g_, verts);
+    }
+    spec.pattern_key = key;
+    specs_.push_back(std::move(spec));
+  };
+  // Launch units: planned patterns, uncovered fusable ops (singletons),
+  // materialised constants and opaque ops.  The reference fires a pattern at
+  // its topologically last member (sim.cpp:478-488), which can run an
+  // uncovered op before the pattern producing its operand; we order units by
+  // a Kahn sort of the contracted graph with that firing position as the
+  // priority, which reproduces the reference order whenever it is valid.
+  struct Unit {
+    std::vector<int> verts;
+    std::string key;
+    int fire = 0;
+    bool opaque = false;
+  };
+  std::vector<Unit> units;
+  std::vector<int> unit_of(g_.nodes.size(), -1);
+  for (int v : order) {
+    const OpNode& n = g_.node(v);
+    if (n.kind == OpKind::Parameter) {
+      params_.push_back(v);
+      continue;
+    }
+    if (covered.count(v)) {
+      if (auto it = fire_at.find(v); it != fire_at.end()) {
+        units.push_back({it->second->vertices, it->second->key(), pos[v], false});
+        for (int m : it->second->vertices) unit_of[static_cast<size_t>(m)] = static_cast<int>(units.size()) - 1;
+      }
+      continue;
+    }
+    if (n.kind == OpKind::Constant && !need_materialize(v)) continue;
+    units.push_back({{v}, std::to_string(v), pos[v], classify_op(n) == OpClass::Opaque});
+    unit_of[static_cast<size_t>(v)] = static_cast<int>(units.size()) - 1;
+  }
+  std::vector<std::set<int>> deps(units.size());
+  std::vector<std::vector<int>> users(units.size());
+  for (size_t u = 0; u < units.size(); ++u)
+    for (int v : units[u].verts)
+      for (int o : g_.node(v).operands) {
+        const int w = unit_of[static_cast<size_t>(o)];
+        if (w >= 0 && w != static_cast<int>(u) && deps[u].insert(w).second) users[static_cast<size_t>(w)].push_back(static_cast<int>(u));
+      }
+  std::set<std::pair<int, int>> ready;  // (fire position, unit)
+  std::vector<size_t> pending(units.size());
+  for (size_t u = 0; u < units.size(); ++u)
+    if (!(pending[u] = deps[u].size())) ready.insert({units[u].fire, static_cast<int>(u)});
+  while (!ready.empty()) {
+    const int u = ready.begin()->second;
+    ready.erase(ready.begin());
+    const Unit& un = units[static_cast<size_t>(u)];
+    if (un.opaque)
+      specs_.push_back(generate_opaque_kernel(g_, un.verts[0], "k" + std::to_string(idx++) + "_" +
+                                                                   sanitize(g_.node(un.verts[0]).name),
+                                              sm_count));
+    else
+      add_pattern(un.verts, un.key);
+    for (int w : users[static_cast<size_t>(u)])
+      if (--pending[static_cast<size_t>(w)] == 0) ready.insert({units[static_cast<size_t>(w)].fire, w});
+  }
+  if (specs_.size() != units.size()) throw std::runtime_error("[exec] contracted plan graph has a cycle");
+  std::sort(params_.begin(), params_.end());
+  out.source = device_prelude();
+  for (const auto& k : specs_)
+    out.source += "\n// ---- " + k.name + " [" + k.tmpl + "] pattern " + k.pattern_key + "\n" + k.source;
+  return out;
+}
+
+void Executor::plan_launches(const FusionPlan& plan, const std::map<std::string, KernelPlan>& kernels,
+                             const MachineModel& model, ExecMode mode) {
+  PlanKernels pk = generate_plan_kernels(g_, plan, kernels, model, mode, dev_->sm_count);
+  specs_ = std::move(pk.specs);
+  params_ = std::move(pk.params);
+  source_ = std::move(pk.source);
+  // tensors that need device buffers: parameters and every kernel input/output
+  auto add_tensor = [&](const std::string& name) {
+    if (tensors_.count(name)) return;
+    const OpNode& n = g_.node(g_.by_name.at(name));
+    Tensor t;
+    t.name = name;
+    t.vertex = n.id;
+    t.dtype = n.shape.dtype;
+    t.count = n.shape.element_count();
+    t.bytes = static_cast<size_t>(n.shape.byte_size());
+    tensors_[name] = std::move(t);
+  };
+  for (int p : params_) add_tensor(g_.node(p).name);
+  for (const auto& k : specs_) {
+    for (const auto& t : k.inputs) add_tensor(t);
+    for (const auto& t : k.outputs) add_tensor(t);
+  }
+  for (int o : g_.outputs)
+    if (!tensors_.count(g_.node(o).name))
+      throw std::runtime_error("[exec] graph output " + g_.node(o).name + " is produced by no kernel");
+}
+
+void Executor::ensure_sets(int sets) {
+  if (sets <= sets_) return;
+  for (auto& [n, t] : tensors_)
+    while (static_cast<int>(t.dptr.size()) < sets) {
+      void* p = nullptr;
+      STC_RT(cudaMalloc(&p, std::max<size_t>(t.bytes, 16)));
+      STC_RT(cudaMemsetAsync(p, 0, std::max<size_t>(t.bytes, 16), stream_));
+      t.dptr.push_back(p);
+    }
+  while (static_cast<int>(scratch_.size()) < sets) {
+    std::vector<void*> s;
+    for (const auto& k : specs_) {
+      void* p = nullptr;
+      if (k.scratch_bytes > 0) {
+        STC_RT(cudaMalloc(&p, static_cast<size_t>(k.scratch_bytes)));
+        STC_RT(cudaMemsetAsync(p, 0, static_cast<size_t>(k.scratch_bytes), stream_));
+      }
+      s.push_back(p);
+    }
+    scratch_.push_back(std::move(s));
+  }
+  STC_RT(cudaStreamSynchronize(stream_));
+  graphs_.resize(static_cast<size_t>(sets), nullptr);
+  sets_ = sets;
+}
+
+void Executor::launch_kernel(size_t i, int set, cudaStream_t s) {
+  const KernelSpec& k = specs_[i];
+  std::vector<void*> ptrs;
+  for (const auto& t : k.inputs) ptrs.push_back(tensors_.at(t).dptr[static_cast<size_t>(set)]);
+  for (const auto& t : k.outputs) ptrs.push_back(tensors_.at(t).dptr[static_cast<size_t>(set)]);
+  void* bar = nullptr;
+  void* part = nullptr;
+  if (k.scratch_bytes > 0) {
+    bar = scratch_[static_cast<size_t>(set)][i];
+    part = static_cast<char*>(bar) + 256;
+    ptrs.push_back(bar);
+    ptrs.push_back(part);
+  }
+  std::vector<void*> args;
+  for (auto& p : ptrs) args.push_back(&p);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(k.grid), 1, 1);
+  cfg.blockDim = dim3(static_cast<unsigned>(k.block), 1, 1);
+  cfg.dynamicSmemBytes = static_cast<size_t>(k.smem);
+  cfg.stream = s;
+  cudaLaunchAttribute attr{};
+  if (k.cooperative && coop_in_graph_) {
+    attr.id = cudaLaunchAttributeCooperative;
+    attr.val.cooperative = 1;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+  }
+  STC_RT(cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(fns_[i]), args.data()));
+}
+
+void Executor::build_graph(int set) {
+  auto& ge = graphs_[static_cast<size_t>(set)];
+  if (ge) return;
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    cudaGraph_t graph = nullptr;
+    STC_RT(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
+    bool failed = false;
+    try {
+      for (size_t i = 0; i < specs_.size(); ++i) launch_kernel(i, set, stream_);
+    } catch (const std::exception&) {
+      failed = true;
+    }
+    const cudaError_t end = cudaStreamEndCapture(stream_, &graph);
+    if (!failed && end == cudaSuccess) {
+      STC_RT(cudaGraphInstantiate(&ge, graph, 0));
+      cudaGraphDestroy(graph);
+      return;
+    }
+    if (graph) cudaGraphDestroy(graph);
+    cudaGetLastError();
+    // cooperative attribute not capturable here: plain launches; the grids
+    // are sized for co-residency so the grid barrier still holds
+    coop_in_graph_ = false;
+  }
+  throw std::runtime_error("[cuda] stream capture of the plan failed");
+}
+
+const Executor::Tensor* Executor::tensor(const std::string& name) const {
+  auto it = tensors_.find(name);
+  return it == tensors_.end() ? nullptr : &it->second;
+}
+
+void Executor::upload(const void* const* in, int set) {
+  ensure_sets(set + 1);
+  for (size_t i = 0; i < params_.size(); ++i) {
+    const Tensor& t = tensors_.at(g_.node(params_[i]).name);
+    STC_RT(cudaMemcpyAsync(t.dptr[static_cast<size_t>(set)], in[i], t.bytes, cudaMemcpyHostToDevice, stream_));
+  }
+}
+
+void Executor::download(void* const* out, int set) {
+  for (size_t i = 0; i < g_.outputs.size(); ++i) {
+    const Tensor& t = tensors_.at(g_.node(g_.outputs[i]).name);
+    STC_RT(cudaMemcpyAsync(out[i], t.dptr[static_cast<size_t>(set)], t.bytes, cudaMemcpyDeviceToHost, stream_));
+  }
+}
+
+void Executor::launch(cudaStream_t s, int set) {
+  if (!s) s = stream_;
+  ensure_sets(set + 1);
+  if (!use_graph_) {
+    for (size_t i = 0; i < specs_.size(); ++i) launch_kernel(i, set, s);
+    return;
+  }
+  build_graph(set);
+  STC_RT(cudaGraphLaunch(graphs_[static_cast<size_t>(set)], s));
+}
+
+void Executor::sync() { STC_RT(cudaStreamSynchronize(stream_)); }
+
+void Executor::run_host(const void* const* in, void* const* out) {
+  upload(in, 0);
+  launch(stream_, 0);
+  download(out, 0);
+  sync();
+}
+
+void Executor::prepare_sets(int sets) {
+  sets = std::max(1, sets);
+  ensure_sets(sets);
+  // replicate set-0 inputs so every set computes on the same data
+  for (int s = 1; s < sets; ++s)
+    for (int p : params_) {
+      const Tensor& t = tensors_.at(g_.node(p).name);
+      STC_RT(cudaMemcpyAsync(t.dptr[static_cast<size_t>(s)], t.dptr[0], t.bytes, cudaMemcpyDeviceToDevice, stream_));
+    }
+  for (int s = 0; s < sets; ++s)
+    if (use_graph_) build_graph(s);
+  STC_RT(cudaStreamSynchronize(stream_));
+}
+
+double Executor::time(int iters, int warmup, int sets, std::vector<double>* per_kernel) {
+  sets = std::max(1, sets);
+  prepare_sets(sets);
+  for (int w = 0; w < warmup; ++w) launch(stream_, w % sets);
+  cudaEvent_t e0, e1;
+  STC_RT(cudaEventCreate(&e0));
+  STC_RT(cudaEventCreate(&e1));
+  STC_RT(cudaStreamSynchronize(stream_));
+  STC_RT(cudaEventRecord(e0, stream_));
+  for (int it = 0; it < iters; ++it) launch(stream_, it % sets);
+  STC_RT(cudaEventRecord(e1, stream_));
+  STC_RT(cudaEventSynchronize(e1));
+  float ms = 0.f;
+  STC_RT(cudaEventElapsedTime(&ms, e0, e1));
+  const double us = 1000.0 * ms / std::max(1, iters);
+  if (per_kernel) {
+    // per-kernel durations: every kernel bracketed by events, replays rotated
+    // over the sets like above (launch gaps excluded, cold inputs kept)
+    per_kernel->assign(specs_.size(), 0.0);
+    std::vector<cudaEvent_t> ev(specs_.size() + 1);
+    for (auto& e : ev) STC_RT(cudaEventCreate(&e));
+    for (int it = 0; it < iters; ++it) {
+      const int s = it % sets;
+      STC_RT(cudaEventRecord(ev[0], stream_));
+      for (size_t i = 0; i < specs_.size(); ++i) {
+        launch_kernel(i, s, stream_);
+        STC_RT(cudaEventRecord(ev[i + 1], stream_));
+      }
+      STC_RT(cudaEventSynchronize(ev.back()));
+      for (size_t i = 0; i < specs_.size(); ++i) {
+        float kms = 0.f;
+        STC_RT(cudaEventElapsedTime(&kms, ev[i], ev[i + 1]));
+        (*per_kernel)[i] += 1000.0 * kms / iters;
+      }
+    }
+    for (auto& e : ev) cudaEventDestroy(e);
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return us;
+}
+
+std::string Executor::describe_json() const {
+  std::ostringstream o;
+  o << "[";
+  for (size_t i = 0; i < specs_.size(); ++i) {
+    const auto& k = specs_[i];
+    o << (i ? "," : "") << "{\"name\":\"" << k.name << "\",\"template\":\"" << json_escape(k.tmpl)
+      << "\",\"pattern\":\"" << k.pattern_key << "\",\"grid\":" << k.grid << ",\"block\":" << k.block
+      << ",\"smem\":" << k.smem << ",\"cooperative\":" << (k.cooperative ? "true" : "false")
+      << ",\"bytes\":" << k.alg_bytes << ",\"inputs\":[";
+    for (size_t j = 0; j < k.inputs.size(); ++j) o << (j ? "," : "") << "\"" << k.inputs[j] << "\"";
+    o << "],\"outputs\":[";
+    for (size_t j = 0; j < k.outputs.size(); ++j) o << (j ? "," : "") << "\"" << k.outputs[j] << "\"";
+    o << "]}";
+  }
+  o << "]";
+  return o.str();
+}
+
+}  // namespace stitch::gpu

@@ -1,0 +1,100 @@
+// Plan executor on one B200: the GPU replacement for the reference's
+// eval_plan (/root/reference/proj/src/sim.cpp:471-514).
+//
+// Construction walks the graph in topological order exactly like eval_plan:
+// a planned pattern fires at its topologically last member, every uncovered
+// fusable op becomes a singleton kernel, every opaque op a placeholder
+// kernel.  All kernels of the plan are generated into ONE CUDA source,
+// compiled once by NVRTC (cached on disk), and captured into ONE CUDA Graph,
+// so a whole-plan execution is a single cudaGraphLaunch.  Only tensors that
+// cross a kernel boundary get device buffers.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "codegen/cg.hpp"
+#include "runtime/cuda_rt.hpp"
+#include "stitch/device.hpp"
+#include "stitch/graph.hpp"
+#include "stitch/planner.hpp"
+
+namespace stitch::gpu {
+
+enum class ExecMode { Stitched = 0, Program = 1, Unfused = 2 };
+
+// All kernels of a plan, generated without touching a device (codegen only).
+struct PlanKernels {
+  std::vector<KernelSpec> specs;  // launch order
+  std::vector<int> params;        // parameter vertices, ascending id
+  std::string source;             // prelude + every kernel: one NVRTC module
+};
+PlanKernels generate_plan_kernels(const CompGraph& g, const FusionPlan& plan,
+                                  const std::map<std::string, KernelPlan>& kernels,
+                                  const MachineModel& model, ExecMode mode, int sm_count = 148);
+
+class Executor {
+ public:
+  Executor(const CompGraph& g, const FusionPlan& plan,
+           const std::map<std::string, KernelPlan>& kernels, const MachineModel& model,
+           int device, ExecMode mode, bool use_graph = true);
+  ~Executor();
+  Executor(const Executor&) = delete;
+  Executor& operator=(const Executor&) = delete;
+
+  struct Tensor {
+    std::string name;
+    int vertex = -1;
+    DType dtype = DType::F32;
+    int64_t count = 0;
+    size_t bytes = 0;
+    std::vector<void*> dptr;  // one per buffer set
+  };
+
+  const std::vector<KernelSpec>& kernels() const { return specs_; }
+  const std::string& source() const { return source_; }
+  const std::vector<int>& param_vertices() const { return params_; }
+  const std::vector<int>& output_vertices() const { return g_.outputs; }
+  const Tensor* tensor(const std::string& name) const;
+  cudaStream_t stream() const { return stream_; }
+
+  void upload(const void* const* host_inputs, int set = 0);
+  void download(void* const* host_outputs, int set = 0);
+  void launch(cudaStream_t s = nullptr, int set = 0);
+  void prepare_sets(int sets);  // allocate + replicate set-0 parameters
+  void sync();
+  void run_host(const void* const* in, void* const* out);
+
+  // CUDA-event timing (see stc_exec_time in include/stitch_b200.h)
+  double time(int iters, int warmup, int sets, std::vector<double>* per_kernel_us);
+
+  std::string describe_json() const;
+
+ private:
+  void plan_launches(const FusionPlan& plan, const std::map<std::string, KernelPlan>& kernels,
+                     const MachineModel& model, ExecMode mode);
+  void ensure_sets(int sets);
+  void launch_kernel(size_t i, int set, cudaStream_t s);
+  void build_graph(int set);
+
+  CompGraph g_;
+  const DeviceInfo* dev_ = nullptr;
+  bool use_graph_ = true;
+  std::vector<KernelSpec> specs_;
+  std::string source_;
+  std::unique_ptr<Module> module_;
+  std::vector<cudaKernel_t> fns_;
+  std::vector<int> params_;
+  std::map<std::string, Tensor> tensors_;
+  std::vector<std::vector<void*>> scratch_;  // [set][kernel]
+  int sets_ = 0;
+  cudaStream_t stream_ = nullptr;
+  std::vector<cudaGraphExec_t> graphs_;  // per set
+  bool coop_in_graph_ = true;
+};
+
+}  // namespace stitch::gpu

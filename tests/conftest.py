@@ -1,0 +1,39 @@
+import json
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+GOLD = os.path.join(ROOT, "tests", "golden")
+GRAPHS = os.path.join(ROOT, "paper_2009_10924_b200", "graphs")
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a B200 (sm_100) GPU")
+    config.addinivalue_line("markers", "slow: long-running (full-size planning)")
+
+
+def fixture_graphs():
+    with open(os.path.join(GOLD, "fixtures.json")) as f:
+        return json.load(f)
+
+
+def config_graph(name):
+    with open(os.path.join(GRAPHS, name + ".graph")) as f:
+        return f.read()
+
+
+def graph_text(name):
+    fx = fixture_graphs()
+    return fx[name] if name in fx else config_graph(name)
+
+
+def golden_plan(name, cfg):
+    path = os.path.join(GOLD, "plans", "%s__%s.json" % (name, cfg))
+    if not os.path.exists(path):
+        return None
+    with open(path) as f:
+        return json.load(f)

@@ -1,0 +1,102 @@
+"""GPU parity: the B200 executor (C-ABI -> NVRTC sm_100a kernels -> one CUDA
+Graph) against the oracle on the same seeded inputs.
+
+Tolerances (north star / reference compare(), src/sim.cpp:516-547): an output
+passes per element if abs <= 1e-5 OR rel <= tol, with tol = 1e-5 for outputs
+computed only from elementwise ops and 1e-4 for outputs downstream of a
+reduction.  Outputs of graphs made only of + - * / max min are additionally
+required to be bit-identical (f32 without FMA == f64 compute rounded to f32).
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from tests.conftest import GOLD, config_graph, fixture_graphs
+from oracle import numpy_oracle as no
+
+pytestmark = pytest.mark.gpu
+
+FIXTURES = sorted(fixture_graphs())
+LIGHT_ONLY = {"light_chain", "remote"}
+
+
+def _stitch():
+    from paper_2009_10924_b200 import stitch
+    return stitch
+
+
+def _tolerances(og):
+    """per output: 1e-4 if a reduction is upstream, else 1e-5"""
+    red_up = {}
+    for n in og.nodes:
+        red_up[n.id] = n.kind in no.REDUCE or any(red_up[o] for o in n.operands)
+    return {og.nodes[o].name: (1e-4 if red_up[o] else 1e-5) for o in og.outputs}
+
+
+def _check(text, cfg, mode, seed, bitwise=False):
+    stitch = _stitch()
+    g = stitch.Graph(text)
+    plan = stitch.Plan(g, cfg)
+    ex = stitch.Executor(plan, device=0, mode=mode)
+    inputs = stitch.random_inputs(g, seed)
+    got = ex.run(inputs)
+    og = no.parse_graph(text)
+    want = no.eval_reference(og, {k: v.astype(np.float64) for k, v in inputs.items()})
+    for name, tol in _tolerances(og).items():
+        rep = stitch.compare({name: got[name]}, {name: want[name]}, tol, 1e-5)
+        assert rep["pass"], "%s/%s/%s seed %d: %s (max_rel %.3g)" % (cfg, mode, name, seed, rep["message"],
+                                                                   rep["max_rel"])
+        if bitwise:
+            assert np.array_equal(np.asarray(got[name], np.float32), want[name].astype(np.float32)), name
+    return ex
+
+
+@pytest.mark.parametrize("name", FIXTURES)
+@pytest.mark.parametrize("cfg", ["v100", "b200"])
+@pytest.mark.parametrize("mode", ["stitched", "program", "unfused"])
+def test_fixture_parity(name, cfg, mode):
+    text = fixture_graphs()[name]
+    for seed in (1, 2, 3):
+        _check(text, cfg, mode, seed, bitwise=name in LIGHT_ONLY)
+
+
+def test_fixture_kernel_counts_match_plan():
+    """the executor launches exactly the planned kernels: patterns + uncovered
+    fusable singletons + opaque placeholders (== plan.json stitched_kernels)"""
+    stitch = _stitch()
+    for name in FIXTURES:
+        g = stitch.Graph(fixture_graphs()[name])
+        plan = stitch.Plan(g, "v100")
+        ex = stitch.Executor(plan)
+        assert ex.num_kernels == json.loads(plan.json())["stitched_kernels"], name
+
+
+CONFIGS = ["ln_4096x768", "ln2pass_4096x768", "attn_softmax", "colreduce", "bert_gelu",
+           "bert_resln", "dien_T10"]
+
+
+@pytest.mark.parametrize("name", CONFIGS)
+def test_config_parity_full_size(name):
+    """BASELINE.json configs at full size, B200 device profile, stitched templates"""
+    ex = _check(config_graph(name), "b200", "stitched", 1)
+    kinds = {k["template"] for k in ex.describe()}
+    assert "program" not in kinds, kinds  # every config kernel uses a dataflow template
+
+
+def test_random_graphs_stitched():
+    with open(os.path.join(GOLD, "random_plans.json")) as f:
+        rnd = json.load(f)
+    for seed, entry in sorted(rnd.items(), key=lambda kv: int(kv[0]))[:40]:
+        _check(entry["graph"], "v100", "stitched", 1)
+
+
+def test_pipeline_run_sim(tmp_path):
+    """run_pipeline --run-sim: stitched plan vs unfused execution on the GPU"""
+    stitch = _stitch()
+    path = tmp_path / "ln.graph"
+    path.write_text(fixture_graphs()["layernorm"])
+    rc = stitch.run_pipeline(str(path), None, output_dir=str(tmp_path / "out"), run_sim=True, seed=3)
+    assert rc == 0
+    assert "sim comparison: pass" in (tmp_path / "out" / "sim_report.txt").read_text()

@@ -1,0 +1,73 @@
+"""Bit-exact plan parity with the reference planner (SURVEY.md §8a A1-A15,
+A21): same graph + same cfg -> byte-identical plan.json (nlohmann 3.11.3
+dump(2)), identical .stitch program text for every kernel (the emitter's
+histogram and liveness decide plan choice), identical serialize_graph text.
+Goldens were produced by the unmodified reference (tests/golden/make_golden.py)."""
+import hashlib
+import json
+import os
+
+import pytest
+
+from tests.conftest import GOLD, golden_plan, graph_text
+
+PLAN_FILES = sorted(f[:-5] for f in os.listdir(os.path.join(GOLD, "plans")) if f.endswith(".json"))
+SLOW = {"bert_cut", "dien_T20"}
+
+
+def _stitch():
+    from paper_2009_10924_b200 import stitch
+    return stitch
+
+
+@pytest.mark.parametrize("case", [c for c in PLAN_FILES if c.split("__")[0] not in SLOW])
+def test_plan_bytes(case):
+    stitch = _stitch()
+    name, cfg = case.split("__")
+    rec = golden_plan(name, cfg)
+    g = stitch.Graph(graph_text(name))
+    assert g.serialize() == rec["serialized"]
+    plan = stitch.Plan(g, cfg)
+    pj = plan.json()
+    assert pj == rec["plan_json"]
+    keys = [p["key"] for p in json.loads(pj)["patterns"]]
+    for i, k in enumerate(keys):
+        assert plan.kernel_text(i) == rec["programs"][k], (case, k)
+    summary = rec["summary"].split()
+    st = plan.stats()
+    assert st["stitched_kernels"] == int(summary[1]) and st["baseline_kernels"] == int(summary[3])
+    assert st["delta_evaluate_calls"] == int(summary[5])
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("case", [c for c in PLAN_FILES if c.split("__")[0] in SLOW])
+def test_plan_bytes_slow(case):
+    test_plan_bytes(case)
+
+
+def test_random_graphs():
+    stitch = _stitch()
+    with open(os.path.join(GOLD, "random_plans.json")) as f:
+        rnd = json.load(f)
+    assert len(rnd) == 100
+    for seed, entry in rnd.items():
+        g = stitch.Graph(entry["graph"])
+        for cfg in ("v100", "b200"):
+            plan = stitch.Plan(g, cfg)
+            pj = plan.json()
+            assert pj == entry[cfg]["plan_json"], (seed, cfg)
+            keys = [p["key"] for p in json.loads(pj)["patterns"]]
+            for i, k in enumerate(keys):
+                h = hashlib.sha256(plan.kernel_text(i).encode()).hexdigest()
+                assert h == entry[cfg]["programs_sha"][k], (seed, cfg, k)
+
+
+def test_plan_kernel_infeasible_and_explicit_patterns():
+    stitch = _stitch()
+    g = stitch.Graph(graph_text("layernorm"))
+    # parameters are not fusable -> plan_kernel infeasible (planner.cpp:1040-1041)
+    assert stitch.plan_kernel(g, [0, 7]) is None
+    txt = stitch.plan_kernel(g, [7])  # s1 alone
+    assert txt.startswith("stitched v1\n") and "reduce_" in txt
+    plan = stitch.Plan(g, "v100", patterns=[[7, 8]])
+    assert plan.num_patterns == 1 and plan.patterns() == [[7, 8]]
