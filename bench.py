@@ -1,0 +1,322 @@
+"""Benchmark: stitched memory-intensive subgraphs on B200 (BASELINE.json metric:
+stitched-kernel HBM GB/s vs ~8 TB/s peak; subgraph us; kernels launched).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+Headline workload (N=1): BASELINE config C2, the BERT-base attention softmax
+chain (scale, mask-add, row-max, exp, row-sum, div) fp32 [32,12,128,128],
+planned by the bit-exact planner under the B200 device profile (1 stitched
+kernel), executed as an NVRTC sm_100a kernel in one CUDA Graph.
+
+One step = one replay of the plan's CUDA Graph over one batch.  `value` is
+algorithmic HBM bytes (unique inputs read once + outputs written once,
+SURVEY.md §8d) x ranks / max-over-ranks time, inputs HBM-resident; timed with
+CUDA events on the stream the graph is launched on.  Between replays the
+executor rotates through independent buffer sets whose total exceeds L2 (cold
+inputs every step).  Multi-GPU: independent batch shards, one per rank, no
+collective on the data path (weak scaling).  `e2e` is the same metric through
+the C-ABI with pinned HOST buffers (H2D inputs + replay + D2H outputs per step).
+`--impl reference` times the reference's own CPU executor (oracle/_ref, the
+unmodified reference library) on all host threads on the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOAD = "attn_softmax"
+WORKLOAD_DESC = "C2 BERT-base attention softmax chain fp32 [32,12,128,128] (+ key mask [32,128])"
+BATCH_TOKEN = "[32,"  # batch dim of every batched tensor in attn_softmax.graph
+SUBGRAPHS = ["ln_4096x768", "ln2pass_4096x768", "bert_gelu", "bert_resln", "colreduce", "dien_T10"]
+L2_BYTES = 126 * 1024 * 1024
+
+
+def read_graph(name):
+    with open(os.path.join(ROOT, "paper_2009_10924_b200", "graphs", name + ".graph")) as f:
+        return f.read()
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def ncu_traffic(graph):
+    """dram bytes per launch of the dominant kernel from the committed ncu capture"""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            d = json.load(f)
+        return d.get(graph, {}).get("dram_bytes")
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled while the timed region runs"""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device, self.samples, self.proc = device, [], None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), "--query-gpu=" + self.FIELDS,
+                 "--format=csv,noheader,nounits", "-lms", "20"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.samples.append(parts)
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.05)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        rows = [s for s in self.samples if s[0].replace(".", "").isdigit()]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"], "samples": 0}
+        sm = [float(r[0]) for r in rows]
+        load = [float(r[0]) for r in rows if float(r[0]) > 600] or sm
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(load), "sm_max_mhz": float(rows[0][1]), "reasons": reasons,
+                "samples": len(rows)}
+
+
+def cpu_reference_seconds(text, threads, reps):
+    """wall seconds of the unmodified reference eval_reference over the full
+    workload split into `threads` batch shards on `threads` host threads"""
+    from oracle import ref
+    shards = max(d for d in range(1, threads + 1) if 32 % d == 0)
+    shard_text = text.replace(BATCH_TOKEN, "[%d," % (32 // shards))
+    return ref.time_eval([shard_text] * shards, seed=1, reps=reps), shards
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from paper_2009_10924_b200 import stitch  # noqa: F401  (graph bytes only)
+    from oracle import numpy_oracle as no
+    from oracle import ref
+    text = read_graph(WORKLOAD)
+    bytes_step = no.algorithmic_bytes(no.parse_graph(text), [[n.id for n in no.parse_graph(text).nodes
+                                                              if n.kind not in ("parameter", "constant")]])
+    if not ref.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libstitch_ref.so not built"}))
+        return
+    threads = os.cpu_count() or 1
+    times = []
+    for i in range(args.warmup + args.steps):
+        s, shards = cpu_reference_seconds(text, threads, 1)
+        if i >= args.warmup:
+            times.append(s)
+    t = statistics.mean(times)
+    val = bytes_step / t / 1e9
+    line = {"metric": "stitched-subgraph HBM GB/s (algorithmic bytes / time)", "value": round(val, 4),
+            "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(t * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic: reference random_inputs(seed=1)",
+            "config": {"workload": WORKLOAD_DESC, "graph": WORKLOAD}, "impl": "reference",
+            "cpu_baseline": {"value": round(val, 4), "unit": "GB/s", "cores": shards, "kind": "reference",
+                             "sample": "full C2 batch as %d batch shards, eval_reference on %d threads "
+                                       "(unmodified reference library, oracle/_ref)" % (shards, shards)},
+            "e2e": {"value": round(val, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def time_subgraph(stitch, name):
+    g = stitch.Graph(read_graph(name))
+    plan = stitch.Plan(g, "b200")
+    ex = stitch.Executor(plan)
+    ex.upload(stitch.random_inputs(g, 1))
+    desc = ex.describe()
+    per_set = sum(t.nbytes for t in g.params) + sum(t.nbytes for t in g.outputs)
+    sets = min(256, max(2, math.ceil(8 * L2_BYTES / max(per_set, 1))))
+    us, kus = ex.time(iters=200, warmup=20, sets=sets, per_kernel=True)
+    alg = sum(k["bytes"] for k in desc)
+    top = max(range(len(desc)), key=lambda i: kus[i])
+    return {"us": round(us, 3), "GBps": round(alg / us / 1e3, 1), "kernels": len(desc),
+            "templates": sorted({k["template"] for k in desc}), "bytes": alg,
+            "dominant": {"name": desc[top]["name"], "template": desc[top]["template"],
+                         "us_event": round(kus[top], 3)}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=50)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-subgraphs", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_2009_10924_b200 import stitch
+    text = read_graph(WORKLOAD)
+    g = stitch.Graph(text)
+    plan = stitch.Plan(g, "b200")
+    ex = stitch.Executor(plan, device=local)
+    desc = ex.describe()
+    alg_bytes = sum(k["bytes"] for k in desc)
+    inputs = stitch.random_inputs(g, seed=1 + rank)
+    ex.upload(inputs)
+    per_set = sum(t.nbytes for t in g.params) + sum(t.nbytes for t in g.outputs)
+    sets = max(2, math.ceil(8 * L2_BYTES / per_set))
+    ex.prepare_sets(sets)
+    stream = torch.cuda.current_stream()
+    sp = stream.cuda_stream
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    for w in range(args.warmup):
+        ex.launch(sp, w % sets)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(args.steps):
+        ex.launch(sp, i % sets)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    if dist:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    value = alg_bytes * world / (ms_step * 1e-3) / 1e9
+
+    # per-kernel device time (events around each kernel, same rotation) for the roofline
+    _, kus = ex.time(iters=200, warmup=10, sets=sets, per_kernel=True)
+    top = max(range(len(desc)), key=lambda i: kus[i])
+    # dominant kernel's time inside the graph: its share of the step (1-kernel plan -> the step)
+    dom_us = ms_step * 1e3 * (kus[top] / sum(kus)) if len(desc) > 1 else ms_step * 1e3
+    peak, peak_kind = measured_peaks()
+    achieved = desc[top]["bytes"] / (dom_us * 1e-6) / 1e9
+
+    # e2e through the C-ABI with pinned host buffers (inputs and outputs)
+    pin_in = {t.name: torch.from_numpy(inputs[t.name]).pin_memory().numpy() for t in g.params}
+    pin_out = {t.name: torch.empty(t.dims, dtype=torch.float32).pin_memory().numpy() for t in g.outputs}
+    h2d = sum(t.nbytes for t in g.params)
+    d2h = sum(t.nbytes for t in g.outputs)
+    ex.run(pin_in, out=pin_out)
+    e2e_steps = max(5, min(50, args.steps // 20))
+    if dist:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        ex.run(pin_in, out=pin_out)
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    if dist:
+        t = torch.tensor([e2e_s], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_val = alg_bytes * world / e2e_s / 1e9
+
+    result = None
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            try:
+                from oracle import ref
+                if ref.available():
+                    threads = os.cpu_count() or 1
+                    s, shards = cpu_reference_seconds(text, threads, 3)
+                    cpu = {"value": round(alg_bytes / s / 1e9, 4), "unit": "GB/s", "cores": shards,
+                           "kind": "reference",
+                           "sample": "full C2 batch as %d batch shards on %d host threads, unmodified "
+                                     "reference eval_reference (oracle/_ref), best of 3: %.3f s"
+                                     % (shards, shards, s)}
+            except Exception as e:  # reported, never fatal
+                cpu = {"value": None, "unit": "GB/s", "cores": 0, "kind": "reference", "sample": "failed: %s" % e}
+        subs = {}
+        if world == 1 and not args.no_subgraphs:
+            for name in SUBGRAPHS:
+                try:
+                    subs[name] = time_subgraph(stitch, name)
+                except Exception as e:
+                    subs[name] = {"error": str(e)[:300]}
+        result = {
+            "metric": "stitched-subgraph HBM GB/s (algorithmic bytes / time)",
+            "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_step, 6), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic: splitmix64 random_inputs(seed=1+rank), uniform(-1,1) f32",
+            "config": {"workload": WORKLOAD_DESC, "graph": WORKLOAD, "device_cfg": "b200_device.cfg",
+                       "plan_kernels": len(desc), "templates": [k["template"] for k in desc],
+                       "us_per_subgraph": round(ms_step * 1e3, 3),
+                       "bytes_per_step_per_gpu": alg_bytes,
+                       "l2": "inputs larger than L2: %d rotating buffer sets x %.1f MB = %.0f MB (>= 8x the 126 MB L2)"
+                             % (sets, per_set / 1e6, sets * per_set / 1e6),
+                       "parallelism": "independent batch shards, %d rank(s), no collective" % world},
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(achieved / peak, 4), "peak_source": peak_kind + " (MEASURED_PEAKS.json hbm_gbs)"
+                         if peak_kind == "measured" else "fallback 6650 GB/s",
+                         "traffic": ncu_traffic(WORKLOAD), "kernel": desc[top]["name"],
+                         "kernel_us": round(dom_us, 3), "kernel_bytes": desc[top]["bytes"],
+                         "frac_of_8TBps": round(achieved / 8000.0, 4)},
+            "cpu_baseline": cpu,
+            "e2e": {"value": round(e2e_val, 3), "unit": "GB/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "us_per_step": round(e2e_s * 1e6, 1),
+                    "path": "stc_exec_run_host: pinned host -> H2D -> graph -> D2H -> host"},
+            "gpu_launches": len(desc) * args.steps,
+            "clocks": clk,
+            "subgraphs": subs,
+        }
+        print(json.dumps(result))
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

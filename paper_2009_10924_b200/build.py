@@ -47,8 +47,10 @@ CXXFLAGS = ["-std=c++20", "-O2", "-g1", "-fPIC", "-Wall", "-Wno-sign-compare",
             "-I" + os.path.join(ROOT, "include"), "-I" + CSRC, "-I" + os.path.join(CUDA, "include")]
 NVCCFLAGS = ["-std=c++17", "-O3", ARCH, "-lineinfo", "-Xcompiler", "-fPIC",
              "-I" + os.path.join(ROOT, "include"), "-I" + CSRC]
-LDFLAGS = ["-shared", "-static-libstdc++", "-static-libgcc", "-Wl,--exclude-libs,ALL",
-           "-Wl,-Bsymbolic", "-L" + os.path.join(CUDA, "lib64"),
+# shared libstdc++: C++ callers of the drop-in stitch:: API (the reference's
+# tests, stitchc) share one C++ runtime with the library, so exceptions and
+# std:: types cross the boundary; -Bsymbolic keeps our own symbols bound locally.
+LDFLAGS = ["-shared", "-Wl,-Bsymbolic", "-L" + os.path.join(CUDA, "lib64"),
            "-Wl,-rpath," + os.path.join(CUDA, "lib64"),
            "-lnvrtc", "-lcudart", "-lpthread", "-ldl"]
 
@@ -106,7 +108,7 @@ def build(verbose=False, jobs=None):
     tool = os.path.join(ROOT, "tools", "stitchc")
     if os.path.exists(tool_src) and _stale(tool_src, tool, [LIB] + hdrs):
         _run(["g++"] + CXXFLAGS + [tool_src, "-o", tool, "-L" + LIB_DIR, "-lstitch_b200",
-                                   "-Wl,-rpath," + LIB_DIR, "-static-libstdc++", "-static-libgcc"])
+                                   "-Wl,-rpath," + LIB_DIR])
     return LIB
 
 

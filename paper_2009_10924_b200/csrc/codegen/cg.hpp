@@ -57,9 +57,13 @@ KernelSpec generate_pattern_kernel(const CompGraph& g, const std::vector<int>& v
                                    const std::string& name, int sm_count);
 
 // Statement-for-statement translation of an abstract stitched program
-// (the reference interpreter's semantics, src/sim.cpp:256-462).
+// (the reference interpreter's semantics, src/sim.cpp:256-462).  `checked`
+// adds the interpreter's fault detection on the GPU: lockstep statement
+// execution, (epoch, writer)-tagged shared cells for the happens-before rule,
+// global/shared bounds checks; faults land in a trailing `unsigned* fault_`
+// scratch word (code, offset) that run_program turns into SimFault.
 KernelSpec generate_program_kernel(const CompGraph& g, const StitchedProgram& prog,
-                                   const std::string& name);
+                                   const std::string& name, bool checked = false);
 
 // opaque_compute placeholder: mean of all operand elements, broadcast
 // (src/sim.cpp:215-226), one cooperative kernel.

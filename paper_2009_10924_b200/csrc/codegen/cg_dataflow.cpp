@@ -181,6 +181,39 @@ class Emitter {
     throw TemplateMismatch("not an elementwise op");
   }
 
+  // Division by a value shared by all lanes (a row statistic, a constant):
+  // one IEEE reciprocal per divisor, then Markstein's correction per element
+  // (q = a*r; e = fma(-q, b, a); q + e*r) which is the correctly rounded a/b
+  // whenever r is a normal number -- bit-identical to IEEE division, at three
+  // FMA-pipe ops instead of the full division sequence.  Divisors outside
+  // [2^-125, 2^125] take the IEEE path (uniform branch).
+  Val divide_by_uniform(const Val& a, const std::string& b) {
+    const std::string rk = "R|" + b;
+    std::string r, ok;
+    if (auto it = memo_.find(rk); it != memo_.end()) {
+      r = it->second.lanes[0];
+      ok = it->second.lanes[1];
+    } else {
+      r = fresh("rcp");
+      ok = fresh("rok");
+      line("const float " + r + " = 1.0f / " + b + ";");
+      line("const bool " + ok + " = fabsf(" + b + ") >= 0x1p-125f && fabsf(" + b + ") <= 0x1p125f;");
+      memo_[rk] = Val{{r, ok}};
+    }
+    Val out;
+    std::string decl = "float", fast, slow;
+    for (int k = 0; k < W; ++k) {
+      const std::string t = fresh("t");
+      out.lanes.push_back(t);
+      decl += std::string(k ? ", " : " ") + t;
+      fast += t + " = div_rcp(" + a.at(k) + ", " + b + ", " + r + "); ";
+      slow += t + " = " + a.at(k) + " / " + b + "; ";
+    }
+    line(decl + ";");
+    line("if (" + ok + ") { " + fast + "} else { " + slow + "}");
+    return out;
+  }
+
   Val compute(int v, const Coords& c) {
     const OpNode& n = g_.node(v);
     if (!pattern_.count(v) || n.kind == OpKind::Constant) {
@@ -210,6 +243,8 @@ class Emitter {
         }
         Val r;
         const int lanes = uni ? 1 : W;
+        if (n.kind == OpKind::Div && !uni && ops[1].uniform() && n.shape.dtype == DType::F32)
+          return divide_by_uniform(ops[0], ops[1].at(0));
         for (int k = 0; k < lanes; ++k) {
           const std::string a = ops[0].at(k), b = ops.size() > 1 ? ops[1].at(k) : "";
           const std::string t = fresh("t");
@@ -446,7 +481,7 @@ RowParams row_params(const std::vector<int>& inner) {
   RowParams p;
   p.W = inner.back() % 4 == 0 ? 4 : (inner.back() % 2 == 0 ? 2 : 1);
   const int64_t nch = L / p.W;
-  const int nj_target = std::max(1, env_int("STITCH_ROW_NJ", 4));
+  const int nj_target = std::max(1, env_int("STITCH_ROW_NJ", 8));
   p.TPR = static_cast<int>(std::clamp<int64_t>(pow2ceil((nch + nj_target - 1) / nj_target), 1, 1024));
   p.NJ = static_cast<int>((nch + p.TPR - 1) / p.TPR);
   p.block = std::max(kBlock, p.TPR);
@@ -507,12 +542,18 @@ void emit_row(Emitter& em, const CompGraph& g, const std::set<int>& pat, const B
     chunk_c[j] = c;
   }
   for (auto& [lvl, rs] : levels) {
-    std::vector<std::string> acc;
+    // sums: compensated f32 partials per thread (kahan_add), folded to f64
+    // for the cross-thread tree; max: exact in f32
+    std::vector<std::string> acc, ks, kc;
     for (int r : rs) {
       const bool sum = g.node(r).kind == OpKind::ReduceSum;
       acc.push_back(em.fresh("acc"));
-      em.line(std::string(sum ? "double " : "float ") + acc.back() + " = " +
-              (sum ? "0.0" : "__int_as_float(0xff800000)") + ";");
+      ks.push_back(sum ? em.fresh("ks") : "");
+      kc.push_back(sum ? em.fresh("kc") : "");
+      if (sum)
+        em.line("float " + ks.back() + " = 0.f, " + kc.back() + " = 0.f;");
+      else
+        em.line("float " + acc.back() + " = __int_as_float(0xff800000);");
     }
     for (int j = 0; j < rp.NJ; ++j) {
       for (size_t i = 0; i < rs.size(); ++i) {
@@ -520,14 +561,19 @@ void emit_row(Emitter& em, const CompGraph& g, const std::set<int>& pat, const B
         const bool sum = g.node(r).kind == OpKind::ReduceSum;
         const Val v = em.value(g.node(r).operands[0], chunk_c[j]);
         std::string upd;
-        for (int k = 0; k < rp.W; ++k) {
-          std::string x = v.at(k);
-          if (sum) upd += acc[i] + " += (double)" + x + "; ";
-          else upd += acc[i] + " = op_max(" + acc[i] + ", " + x + "); ";
+        if (sum) {  // lanes pairwise, then one compensated add per chunk
+          std::string x = v.at(0);
+          if (rp.W == 2) x = "(" + v.at(0) + " + " + v.at(1) + ")";
+          if (rp.W == 4) x = "((" + v.at(0) + " + " + v.at(1) + ") + (" + v.at(2) + " + " + v.at(3) + "))";
+          upd = "kahan_add(" + ks[i] + ", " + kc[i] + ", " + x + "); ";
+        } else {
+          for (int k = 0; k < rp.W; ++k) upd += acc[i] + " = op_max(" + acc[i] + ", " + v.at(k) + "); ";
         }
         em.line((partial ? "if (" + chunk_ok[j] + ") { " : "{ ") + upd + "}");
       }
     }
+    for (size_t i = 0; i < rs.size(); ++i)
+      if (!ks[i].empty()) em.line("double " + acc[i] + " = (double)" + ks[i] + " - (double)" + kc[i] + ";");
     // team reduction: butterfly inside the warp, smem across the team's warps
     const int w = std::min(rp.TPR, 32);
     for (size_t i = 0; i < rs.size(); ++i) {
@@ -618,13 +664,16 @@ void emit_column_phase1(Emitter& em, const CompGraph& g, const Body& b, const Co
     for (size_t i = 0; i < C.size(); ++i) colc.push_back({names[i], i + 1 == C.size() && cp.W > 1, true});
   }
   const size_t nr = b.reductions.size();
-  std::vector<std::vector<std::string>> acc(nr);
+  std::vector<std::vector<std::string>> acc(nr), kc(nr);
   for (size_t i = 0; i < nr; ++i) {
     const bool sum = g.node(b.reductions[i]).kind == OpKind::ReduceSum;
     for (int k = 0; k < cp.W; ++k) {
       acc[i].push_back(em.fresh("acc"));
-      em.line(std::string(sum ? "double " : "float ") + acc[i].back() + " = " +
-              (sum ? "0.0" : "__int_as_float(0xff800000)") + ";");
+      kc[i].push_back(sum ? em.fresh("kc") : "");
+      if (sum)
+        em.line("float " + acc[i].back() + " = 0.f, " + kc[i].back() + " = 0.f;");
+      else
+        em.line("float " + acc[i].back() + " = __int_as_float(0xff800000);");
     }
   }
   em.open("for (i64 r_ = r0_ + ry_; r_ < r1_; r_ += " + std::to_string(cp.RT * cp.U) + ")");
@@ -643,7 +692,7 @@ void emit_column_phase1(Emitter& em, const CompGraph& g, const Body& b, const Co
       const Val v = em.value(g.node(r).operands[0], c);
       std::string upd;
       for (int k = 0; k < cp.W; ++k)
-        upd += sum ? acc[i][k] + " += (double)" + v.at(k) + "; "
+        upd += sum ? "kahan_add(" + acc[i][k] + ", " + kc[i][k] + ", " + v.at(k) + "); "
                    : acc[i][k] + " = op_max(" + acc[i][k] + ", " + v.at(k) + "); ";
       em.line("if (" + ok + ") { " + upd + "}");
     }
@@ -659,7 +708,8 @@ void emit_column_phase1(Emitter& em, const CompGraph& g, const Body& b, const Co
     for (size_t i = 0; i < nr; ++i) {
       const bool sum = g.node(b.reductions[i]).kind == OpKind::ReduceSum;
       for (int k = 0; k < cp.W; ++k)
-        em.line("tile_[ry_][cx_ * " + std::to_string(cp.W) + " + " + std::to_string(k) + "] = " + acc[i][k] + ";");
+        em.line("tile_[ry_][cx_ * " + std::to_string(cp.W) + " + " + std::to_string(k) + "] = " +
+                (sum ? "(double)" + acc[i][k] + " - (double)" + kc[i][k] : acc[i][k]) + ";");
       em.line("__syncthreads();");
       em.open("if (ry_ == 0 && col_ok)");
       for (int k = 0; k < cp.W; ++k) {
@@ -807,7 +857,9 @@ KernelSpec generate_pattern_kernel(const CompGraph& g, const std::vector<int>& v
     if (b.kind == Kind::Column) coop = true;
     if (b.kind == Kind::Row) block = std::max(block, row_params(b.dims_b).block);
   }
-  const int per_sm = std::max(1, std::min(2, 2048 / block));
+  // co-residency budget for cooperative kernels: 4 CTAs/SM at 256 threads
+  // (<= 64 registers per thread via __launch_bounds__)
+  const int per_sm = std::max(1, std::min(4, 2048 / block));
   const int coop_cap = kSmCount * per_sm;
 
   // CTA budget per body

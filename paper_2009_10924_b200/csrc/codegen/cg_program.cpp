@@ -32,7 +32,8 @@ std::string c_double(double v) {
 
 class ProgramTranslator {
  public:
-  ProgramTranslator(const CompGraph& g, const StitchedProgram& p) : g_(g), p_(p) {}
+  ProgramTranslator(const CompGraph& g, const StitchedProgram& p, bool checked)
+      : g_(g), p_(p), checked_(checked) {}
 
   KernelSpec run(const std::string& name) {
     scan();
@@ -41,7 +42,8 @@ class ProgramTranslator {
     k.tmpl = "program";
     k.grid = p_.launch.grid;
     k.block = p_.launch.block;
-    k.smem = (p_.shmem_bytes / 4) * 8;
+    const int64_t cells = p_.shmem_bytes / 4;
+    k.smem = cells * 8 + (checked_ ? cells * 4 : 0);
     std::ostringstream sig;
     sig << "extern \"C\" __global__ void __launch_bounds__(" << p_.launch.block << ") " << name << "(";
     bool first = true;
@@ -55,9 +57,21 @@ class ProgramTranslator {
       first = false;
       k.outputs.push_back(b.name);
     }
+    if (checked_) {
+      sig << (first ? "" : ", ") << "unsigned* __restrict__ fault_";
+      k.scratch_bytes = 256;
+    }
     sig << ") {\n";
     std::ostringstream body;
     body << "  extern __shared__ double shm[];\n";
+    if (checked_) {
+      // lockstep emulation: every statement is followed by a block barrier,
+      // shared cells carry (epoch, writer) tags, program barriers bump the
+      // epoch -- the interpreter's happens-before rule (sim.cpp:395-419)
+      body << "  int* tag_ = reinterpret_cast<int*>(shm + " << cells << ");\n";
+      body << "  for (int c_ = threadIdx.x; c_ < " << cells << "; c_ += blockDim.x) tag_[c_] = -1;\n";
+      body << "  int epoch_ = 0;\n  __syncthreads();\n";
+    }
     body << "  const i64 bid = blockIdx.x, tid = threadIdx.x, lane = threadIdx.x & 31;\n";
     body << "  const i64 wid = (bid * " << p_.launch.block << " + tid) >> 5;\n";
     body << "  (void)bid; (void)lane; (void)wid; (void)shm;\n";
@@ -68,6 +82,9 @@ class ProgramTranslator {
     for (const auto& s : p_.stmts) {
       if (s.kind == Stmt::EndLoop) --depth;
       body << std::string(static_cast<size_t>(2 * depth), ' ') << stmt(s) << "\n";
+      if (checked_ && s.kind != Stmt::Comment && s.kind != Stmt::Loop && s.kind != Stmt::EndLoop &&
+          s.kind != Stmt::Barrier)
+        body << std::string(static_cast<size_t>(2 * depth), ' ') << "__syncthreads();\n";
       if (s.kind == Stmt::Loop) ++depth;
     }
     body << "}\n";
@@ -77,6 +94,14 @@ class ProgramTranslator {
 
  private:
   static std::string tname(const std::string& n) { return "T_" + n; }
+
+  int64_t count_of(const std::string& tensor) const {
+    for (const auto& b : p_.inputs)
+      if (b.name == tensor) return b.shape.element_count();
+    for (const auto& b : p_.outputs)
+      if (b.name == tensor) return b.shape.element_count();
+    return 0;
+  }
 
   DType dtype_of(const std::string& tensor) const {
     auto it = g_.by_name.find(tensor);
@@ -166,17 +191,35 @@ class ProgramTranslator {
       case Stmt::FMove: return s.dst + " = " + s.srcs[0] + ";";
       case Stmt::FOp: return fop(s);
       case Stmt::GLoad:
+        if (checked_)
+          return "if (" + gd(s.guard) + ") { const i64 i_ = " + ex(s.idx) + "; if (i_ < 0 || i_ >= " +
+                 std::to_string(count_of(s.tensor)) + "ll) { sim_fault(fault_, 2, i_); " + s.dst +
+                 " = 0.0; } else " + s.dst + " = (double)ldv(" + tname(s.tensor) + ", i_); } else " + s.dst + " = 0.0;";
         return s.dst + " = " + gd(s.guard) + " ? (double)ldv(" + tname(s.tensor) + ", " + ex(s.idx) +
                ") : 0.0;";
       case Stmt::GStore: {
+        if (checked_)
+          return "if (" + gd(s.guard) + ") { const i64 i_ = " + ex(s.idx) + "; if (i_ < 0 || i_ >= " +
+                 std::to_string(count_of(s.tensor)) + "ll) sim_fault(fault_, 2, i_); else stv(" + tname(s.tensor) +
+                 ", i_, (float)" + s.srcs[0] + "); }";
         const DType d = dtype_of(s.tensor);
         std::string v = "(float)" + s.srcs[0];
         return "if (" + gd(s.guard) + ") stv(" + tname(s.tensor) + ", " + ex(s.idx) + ", " + v + ");" +
                (d == DType::F32 ? "" : "");
       }
       case Stmt::SLoad:
+        if (checked_)
+          return "if (" + gd(s.guard) + ") { const i64 o_ = " + ex(s.idx) + "; if (o_ < 0 || (o_ & 3) || o_ + 4 > " +
+                 std::to_string(p_.shmem_bytes) + "ll) { sim_fault(fault_, 3, o_); " + s.dst + " = 0.0; } else { " +
+                 "const int tg_ = tag_[o_ >> 2]; if (tg_ >= 0 && (tg_ >> 11) == epoch_ && (tg_ & 2047) != (int)tid) " +
+                 "sim_fault(fault_, 1, o_); " + s.dst + " = shm[o_ >> 2]; } } else " + s.dst + " = 0.0;";
         return s.dst + " = " + gd(s.guard) + " ? shm[(" + ex(s.idx) + ") >> 2] : 0.0;";
-      case Stmt::SStore: return "if (" + gd(s.guard) + ") shm[(" + ex(s.idx) + ") >> 2] = " + s.srcs[0] + ";";
+      case Stmt::SStore:
+        if (checked_)
+          return "if (" + gd(s.guard) + ") { const i64 o_ = " + ex(s.idx) + "; if (o_ < 0 || (o_ & 3) || o_ + 4 > " +
+                 std::to_string(p_.shmem_bytes) + "ll) sim_fault(fault_, 3, o_); else { shm[o_ >> 2] = " + s.srcs[0] +
+                 "; tag_[o_ >> 2] = (epoch_ << 11) | (int)tid; } }";
+        return "if (" + gd(s.guard) + ") shm[(" + ex(s.idx) + ") >> 2] = " + s.srcs[0] + ";";
       case Stmt::RegSet: {
         const int64_t w = arrays_.at(s.dst);
         return "if (" + gd(s.guard) + ") { const i64 s_ = " + ex(s.dst_slot) + "; if (s_ >= 0 && s_ < " +
@@ -196,7 +239,7 @@ class ProgramTranslator {
       case Stmt::Accum:
         return "if (" + gd(s.guard) + ") " + s.dst + " = " +
                (s.op == "sum" ? s.dst + " + " + s.srcs[0] : "dmax(" + s.dst + ", " + s.srcs[0] + ")") + ";";
-      case Stmt::Barrier: return "__syncthreads();";
+      case Stmt::Barrier: return checked_ ? "__syncthreads(); ++epoch_;" : "__syncthreads();";
       case Stmt::Comment: return "// " + s.text;
     }
     return "";
@@ -204,6 +247,7 @@ class ProgramTranslator {
 
   const CompGraph& g_;
   const StitchedProgram& p_;
+  bool checked_ = false;
   std::set<std::string> iregs_, fregs_;
   std::map<std::string, int64_t> arrays_;
 };
@@ -211,8 +255,8 @@ class ProgramTranslator {
 }  // namespace
 
 KernelSpec generate_program_kernel(const CompGraph& g, const StitchedProgram& prog,
-                                   const std::string& name) {
-  return ProgramTranslator(g, prog).run(name);
+                                   const std::string& name, bool checked) {
+  return ProgramTranslator(g, prog, checked).run(name);
 }
 
 }  // namespace stitch::gpu

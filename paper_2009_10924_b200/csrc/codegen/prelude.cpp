@@ -52,6 +52,21 @@ __device__ __forceinline__ float op_max(float a, float b) { return a < b ? b : a
 __device__ __forceinline__ float op_min(float a, float b) { return b < a ? b : a; }
 __device__ __forceinline__ double dmax(double a, double b) { return a < b ? b : a; }
 __device__ __forceinline__ float op_rsqrt(float a) { return 1.0f / sqrtf(a); }
+// a / b given r = RN(1/b), r normal: Markstein's FMA correction yields the
+// correctly rounded quotient (same bits as IEEE division)
+__device__ __forceinline__ float div_rcp(float a, float b, float r) {
+  const float q = a * r;
+  const float e = __fmaf_rn(-q, b, a);
+  return __fmaf_rn(e, r, q);
+}
+// compensated (Kahan) f32 accumulation; the pair is folded to f64 before the
+// cross-thread tree, so partial sums keep ~f64 accuracy at f32 issue cost
+__device__ __forceinline__ void kahan_add(float& s, float& c, float x) {
+  const float y = x - c;
+  const float t = s + y;
+  c = (t - s) - y;
+  s = t;
+}
 
 // butterfly over `width` lanes (power of two <= 32): every lane gets the result
 __device__ __forceinline__ double bfly_sum(double v, int width) {
@@ -61,6 +76,15 @@ __device__ __forceinline__ double bfly_sum(double v, int width) {
 __device__ __forceinline__ float bfly_max(float v, int width) {
   for (int o = width >> 1; o > 0; o >>= 1) v = op_max(v, __shfl_xor_sync(FULL_MASK, v, o));
   return v;
+}
+
+// run_program fault report: first fault wins (code 1 race, 2 global OOB, 3 shared OOB)
+__device__ __forceinline__ void sim_fault(unsigned* f, unsigned code, i64 where) {
+  if (atomicCAS(f, 0u, code) == 0u) {
+    f[1] = (unsigned)(where & 0xffffffff);
+    f[2] = threadIdx.x;
+    f[3] = blockIdx.x;
+  }
 }
 
 // Grid-wide barrier for cooperative (co-resident) launches.  bar[0] counts

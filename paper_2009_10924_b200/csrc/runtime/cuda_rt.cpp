@@ -125,6 +125,13 @@ std::string compile_cubin(const std::string& source, const std::vector<std::stri
     nvrtcDestroyProgram(&prog);
     throw std::runtime_error("[nvrtc] compile failed: " + log.substr(0, 4000));
   }
+  if (const char* v = std::getenv("STITCH_NVRTC_LOG"); v && *v == '1') {
+    size_t ln = 0;
+    nvrtcGetProgramLogSize(prog, &ln);
+    std::string log(ln, '\0');
+    nvrtcGetProgramLog(prog, log.data());
+    std::fprintf(stderr, "[nvrtc] %s\n", log.c_str());
+  }
   size_t n = 0;
   STC_NVRTC(nvrtcGetCUBINSize(prog, &n));
   std::string cubin(n, '\0');

@@ -176,6 +176,32 @@ TensorValue TensorValue::zeros(const TensorShape& s) {
   return t;
 }
 
+// one op as a one-kernel graph: operands become parameters (sim.cpp:111-229 semantics)
+TensorValue eval_node(const OpNode& n, const std::vector<const TensorValue*>& operands) {
+  CompGraph g;
+  TensorMap inputs;
+  std::vector<int> ids;
+  for (size_t i = 0; i < operands.size(); ++i) {
+    OpNode p;
+    p.id = g.num_nodes();
+    p.name = "in" + std::to_string(i);
+    p.kind = OpKind::Parameter;
+    p.shape = operands[i]->shape;
+    g.by_name[p.name] = p.id;
+    g.nodes.push_back(p);
+    inputs[p.name] = *operands[i];
+    ids.push_back(p.id);
+  }
+  OpNode op = n;
+  op.id = g.num_nodes();
+  op.name = "out";
+  op.operands = ids;
+  g.by_name[op.name] = op.id;
+  g.nodes.push_back(op);
+  g.outputs = {op.id};
+  return run_on_gpu(g, FusionPlan{}, {}, inputs, gpu::ExecMode::Unfused).at("out");
+}
+
 TensorMap eval_plan(const CompGraph& g, const FusionPlan& plan,
                     const std::map<std::string, KernelPlan>& kernel_plans, const TensorMap& inputs) {
   return run_on_gpu(g, plan, kernel_plans, inputs, gpu::ExecMode::Stitched);
@@ -202,7 +228,7 @@ void run_program(const StitchedProgram& prog, TensorMap& tensors) {
   for (const auto& b : prog.outputs) add(b);
   const auto& dev = gpu::device_init(device_from_env());
   (void)dev;
-  auto spec = gpu::generate_program_kernel(g, prog, "stitched_program");
+  auto spec = gpu::generate_program_kernel(g, prog, "stitched_program", /*checked=*/true);
   gpu::Module mod(gpu::compile_cubin(gpu::device_prelude() + spec.source, gpu::default_nvrtc_options()));
   const void* f = reinterpret_cast<const void*>(mod.fn(spec.name));
   if (spec.smem > 48 * 1024)
@@ -229,11 +255,25 @@ void run_program(const StitchedProgram& prog, TensorMap& tensors) {
     STC_RT(cudaMemcpy(p, bytes.data(), bytes.size(), cudaMemcpyHostToDevice));
     bufs.push_back(p);
   }
+  void* fault = nullptr;
+  STC_RT(cudaMalloc(&fault, 256));
+  STC_RT(cudaMemset(fault, 0, 256));
   std::vector<void*> args;
   for (auto& p : bufs) args.push_back(&p);
+  args.push_back(&fault);
   STC_RT(cudaLaunchKernel(f, dim3(static_cast<unsigned>(spec.grid)), dim3(static_cast<unsigned>(spec.block)),
                           args.data(), static_cast<size_t>(spec.smem), nullptr));
   STC_RT(cudaDeviceSynchronize());
+  unsigned fw[4] = {0, 0, 0, 0};
+  STC_RT(cudaMemcpy(fw, fault, sizeof fw, cudaMemcpyDeviceToHost));
+  cudaFree(fault);
+  if (fw[0]) {
+    for (void* p : bufs) cudaFree(p);
+    const std::string where = " (thread " + std::to_string(fw[2]) + ", block " + std::to_string(fw[3]) + ")";
+    if (fw[0] == 1) throw SimFault("shared read of un-barriered write at offset " + std::to_string(fw[1]) + where);
+    if (fw[0] == 2) throw SimFault("global access out of bounds at element " + std::to_string(fw[1]) + where);
+    throw SimFault("shared access out of bounds at offset " + std::to_string(fw[1]) + where);
+  }
   for (size_t i = 0; i < prog.outputs.size(); ++i) {
     const auto& b = prog.outputs[i];
     std::vector<uint8_t> bytes(static_cast<size_t>(b.shape.byte_size()));

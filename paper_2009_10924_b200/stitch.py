@@ -288,10 +288,18 @@ class Executor:
         outs = [np.empty(t.dims, dtype=t.np_dtype) for t in self.g.outputs]
         return outs, (ctypes.c_void_p * max(1, len(outs)))(*[o.ctypes.data for o in outs])
 
-    def run(self, inputs: Dict[str, np.ndarray]) -> Dict[str, np.ndarray]:
-        """host inputs -> H2D -> one graph launch -> D2H -> host outputs"""
+    def run(self, inputs: Dict[str, np.ndarray], out: Optional[Dict[str, np.ndarray]] = None):
+        """host inputs -> H2D -> one graph launch -> D2H -> host outputs
+        (`out`: preallocated, e.g. pinned, output arrays to fill)"""
         keep, ip = self._in_ptrs(inputs)
-        outs, op = self._out_ptrs()
+        if out is None:
+            outs, op = self._out_ptrs()
+        else:
+            outs = [out[t.name] for t in self.g.outputs]
+            for o, t in zip(outs, self.g.outputs):
+                if not (o.flags.c_contiguous and o.dtype == t.np_dtype and o.size == t.count):
+                    raise StitchError(4, "bad output buffer for " + t.name)
+            op = (ctypes.c_void_p * max(1, len(outs)))(*[o.ctypes.data for o in outs])
         _check(lib().stc_exec_run_host(self._h, ip, op))
         return {t.name: o for t, o in zip(self.g.outputs, outs)}
 
