@@ -206,8 +206,12 @@ def main():
     per_set = sum(t.nbytes for t in g.params) + sum(t.nbytes for t in g.outputs)
     sets = max(2, math.ceil(8 * L2_BYTES / per_set))
     ex.prepare_sets(sets)
-    stream = torch.cuda.current_stream()
+    # an explicit (non-default) stream: the graph replays AND the timing events
+    # go on it (a NULL handle would mean the executor's internal stream)
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     sp = stream.cuda_stream
+    assert sp != 0
 
     clocks = ClockSampler(local)
     clocks.start()

@@ -98,8 +98,10 @@ int stc_exec_source(const stc_exec* e, char** cuda_source);
  * (f32 / f16 bits / i32 / u8 bool), parameters and outputs in stc_graph_io order. */
 int stc_exec_run_host(stc_exec* e, const void* const* inputs, void* const* outputs);
 int stc_exec_upload(stc_exec* e, const void* const* inputs);
-/* async graph replay on `cuda_stream` (NULL = the executor's stream) using
- * buffer set `set` (0 = the uploaded buffers; see stc_exec_prepare_sets) */
+/* async graph replay on `cuda_stream` using buffer set `set` (0 = the
+ * uploaded buffers; see stc_exec_prepare_sets).  NULL selects the executor's
+ * own non-blocking stream -- NOT the legacy default stream -- so a caller that
+ * times with events must pass the stream it records them on. */
 int stc_exec_launch(stc_exec* e, void* cuda_stream, int set);
 /* allocate `sets` independent copies of every buffer and copy set 0's
  * parameters into them, so timed replays can rotate through more bytes than
@@ -116,6 +118,14 @@ int stc_exec_tensor(const stc_exec* e, const char* name, void** dptr, size_t* by
  * num_kernels) = average duration of kernel i measured by per-kernel events. */
 int stc_exec_time(stc_exec* e, int iters, int warmup, int sets, double* us_per_run,
                   double* kernel_us);
+/* Batched replay: `steps_per_graph` consecutive steps (rotating buffer sets)
+ * captured into ONE CUDA Graph so the graph-launch cost is paid once per
+ * batch (the paper's launch-overhead argument applied across batches).
+ * prepare -> *n_graphs batch graphs; launch_batch replays graph `index`. */
+int stc_exec_prepare_batches(stc_exec* e, int sets, int steps_per_graph, int* n_graphs);
+int stc_exec_launch_batch(stc_exec* e, void* cuda_stream, int index);
+int stc_exec_time_batched(stc_exec* e, int steps, int warmup, int sets, int steps_per_graph,
+                          double* us_per_step);
 
 /* ---- low-level runtime (the CUDA layer the executor is built on) --------- */
 /* NVRTC -arch=sm_100a compile with the on-disk cubin cache; returns the

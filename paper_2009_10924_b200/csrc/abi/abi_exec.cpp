@@ -115,6 +115,25 @@ int stc_exec_time(stc_exec* e, int iters, int warmup, int sets, double* us_per_r
   });
 }
 
+int stc_exec_prepare_batches(stc_exec* e, int sets, int steps_per_graph, int* n_graphs) {
+  return guarded([&] {
+    const int n = e->ex->prepare_batches(sets, steps_per_graph);
+    if (n_graphs) *n_graphs = n;
+  });
+}
+
+int stc_exec_launch_batch(stc_exec* e, void* stream, int index) {
+  return guarded([&] { e->ex->launch_batch(static_cast<cudaStream_t>(stream), index); });
+}
+
+int stc_exec_time_batched(stc_exec* e, int steps, int warmup, int sets, int steps_per_graph,
+                          double* us_per_step) {
+  return guarded([&] {
+    const double us = e->ex->time(steps, warmup, sets, nullptr, steps_per_graph);
+    if (us_per_step) *us_per_step = us;
+  });
+}
+
 int stc_compile(const char* cuda_source, const char* options, char** cubin_key) {
   return guarded([&] {
     std::vector<std::string> opts = gpu::default_nvrtc_options();

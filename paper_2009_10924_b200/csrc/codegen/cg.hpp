@@ -8,9 +8,12 @@
 //             loads it once into registers, reduces with shuffles (+ smem
 //             across warps), and every consumer reads the reduced value from
 //             registers — the paper's warp/block composition
-//   global    column reductions over leading axes: per-CTA partial tiles, a
-//             cooperative grid-wide barrier, deterministic fixed-order
-//             combine, then the column consumers
+//   global    column reductions over leading axes: every CTA folds a row slab
+//             of a column strip into f64 partials; the last CTA of the strip
+//             to arrive (threadfence + arrival counter) combines all slabs in
+//             fixed order and runs the column consumers -- grid-wide
+//             stitching without a co-residency requirement or idle waiting
+//             (the opaque placeholder keeps a cooperative grid barrier)
 //   independent  several components (remote / kernel-packing patterns) in
 //             one launch, each on its own CTA range
 //   program   anything else: the planner's abstract stitched program
@@ -40,7 +43,8 @@ struct KernelSpec {
   bool cooperative = false;          // needs a grid-wide barrier (co-resident launch)
   std::vector<std::string> inputs;   // tensor names bound to the leading pointer params
   std::vector<std::string> outputs;  // then these
-  int64_t scratch_bytes = 0;         // trailing `void* scratch` param when > 0 (zeroed once)
+  int64_t scratch_bytes = 0;         // trailing (bar_, part_) params when > 0 (zeroed once)
+  int64_t scratch_header = 256;      // part_ = scratch + scratch_header
   int64_t alg_bytes = 0;             // algorithmic bytes: unique inputs read once + outputs written once
 };
 

@@ -5,7 +5,7 @@
 //   no reductions                       -> local   (one body per output shape)
 //   all reductions over trailing axes,  -> regional (row-resident teams)
 //     same (outer, inner) split
-//   all reductions over leading axes,   -> global  (partials + grid barrier)
+//   all reductions over leading axes,   -> global  (slab partials, last CTA per strip combines)
 //     same (reduced, kept) split
 // Bodies with the same domain are merged so shared inputs are read once (e.g.
 // the two column reductions of colreduce read dy once), and all bodies of a
@@ -627,39 +627,46 @@ struct ColParams {
   int64_t NCH, ROWS, COLS;
 };
 
-ColParams col_params(const std::vector<int>& P, const std::vector<int>& C, int max_blocks) {
+// CT column chunks x RT row lanes per 256-thread CTA; NCB column strips x RB
+// row slabs of CTAs, sized for ~2 CTAs per SM (each slab >= RT*U rows)
+ColParams col_params(const std::vector<int>& P, const std::vector<int>& C, int target_blocks) {
   ColParams p;
   p.ROWS = prod(P);
   p.COLS = prod(C);
   p.W = C.back() % 4 == 0 ? 4 : 1;
   p.NCH = p.COLS / p.W;
-  p.CT = static_cast<int>(std::min<int64_t>(32, p.NCH));
-  p.CT = static_cast<int>(pow2ceil(p.CT));
+  p.CT = static_cast<int>(pow2ceil(std::min<int64_t>(32, p.NCH)));
   p.RT = kBlock / p.CT;
   p.NCB = static_cast<int>((p.NCH + p.CT - 1) / p.CT);
-  const int64_t want_rb = std::max<int64_t>(1, (p.ROWS + p.RT * 16 - 1) / (p.RT * 16));
-  p.RB = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want_rb, max_blocks / p.NCB)));
-  p.U = 4;
+  p.U = std::max(1, env_int("STITCH_COL_U", 8));
+  const int64_t max_rb = std::max<int64_t>(1, p.ROWS / (int64_t(p.RT) * p.U));
+  p.RB = static_cast<int>(std::clamp<int64_t>(target_blocks / p.NCB, 1, max_rb));
   return p;
 }
 
-// global phase 1: partial column sums of this CTA's row slab -> scratch
-void emit_column_phase1(Emitter& em, const CompGraph& g, const Body& b, const ColParams& cp,
-                        int64_t partial_off) {
+// global body: each CTA folds its row slab of one column strip into per-column
+// f64 partials (compensated f32 per thread, fixed-order smem tree across the
+// CTA), writes them to scratch, and the LAST CTA of the strip to arrive
+// (threadfence + atomic arrival counter) combines all slabs in slab order and
+// runs the column consumers.  Deterministic, no co-residency requirement, no
+// CTA ever waits at a barrier.
+void emit_column(Emitter& em, const CompGraph& g, const Body& b, const ColParams& cp, int64_t partial_off,
+                 int64_t ctr_off) {
   const std::vector<int>& P = b.dims_a;
   const std::vector<int>& C = b.dims_b;
   em.W = cp.W;
-  em.line("// global body phase 1: " + std::to_string(cp.ROWS) + " reduced rows x " + std::to_string(cp.COLS) +
-          " columns, tile " + std::to_string(cp.CT * cp.W) + " cols x " + std::to_string(cp.RT) + " rows");
+  const std::string sW = std::to_string(cp.W), sCOLS = std::to_string(cp.COLS), sRB = std::to_string(cp.RB);
+  em.line("// global body: " + std::to_string(cp.ROWS) + " reduced rows x " + sCOLS + " columns; CTA tile " +
+          std::to_string(cp.CT * cp.W) + " cols x " + std::to_string(cp.RT) + " rows, " + sRB + " slabs per strip");
   em.line("const int cx_ = threadIdx.x % " + std::to_string(cp.CT) + ", ry_ = threadIdx.x / " + std::to_string(cp.CT) + ";");
   em.line("const int cb_ = vbid % " + std::to_string(cp.NCB) + ", rbk_ = vbid / " + std::to_string(cp.NCB) + ";");
   em.line("const bool col_ok = cb_ * " + std::to_string(cp.CT) + " + cx_ < " + std::to_string(cp.NCH) + ";");
   em.line("const " + em.ix() + " ch_ = col_ok ? cb_ * " + std::to_string(cp.CT) + " + cx_ : " + std::to_string(cp.NCH - 1) + ";");
-  em.line("const i64 rspan_ = (" + std::to_string(cp.ROWS) + " + " + std::to_string(cp.RB) + " - 1) / " + std::to_string(cp.RB) + ";");
+  em.line("const i64 rspan_ = (" + std::to_string(cp.ROWS) + " + " + sRB + " - 1) / " + sRB + ";");
   em.line("const i64 r0_ = (i64)rbk_ * rspan_, r1_ = min((i64)" + std::to_string(cp.ROWS) + ", r0_ + rspan_);");
   Coords colc;
   {
-    const std::string lin = cp.W == 1 ? "ch_" : "ch_ * " + std::to_string(cp.W);
+    const std::string lin = cp.W == 1 ? "ch_" : "ch_ * " + sW;
     auto names = decompose(em, lin, C, "c");
     for (size_t i = 0; i < C.size(); ++i) colc.push_back({names[i], i + 1 == C.size() && cp.W > 1, true});
   }
@@ -702,67 +709,62 @@ void emit_column_phase1(Emitter& em, const CompGraph& g, const Body& b, const Co
   }
   for (auto& [o, c, v, ok] : stores) store_val(em, g, o, c, v, ok);
   em.close();
-  // fold the RT row lanes of the tile in smem (fixed order), write partials
-  if (nr) {
-    em.line("__shared__ double tile_[" + std::to_string(cp.RT) + "][" + std::to_string(cp.CT * cp.W) + "];");
-    for (size_t i = 0; i < nr; ++i) {
-      const bool sum = g.node(b.reductions[i]).kind == OpKind::ReduceSum;
-      for (int k = 0; k < cp.W; ++k)
-        em.line("tile_[ry_][cx_ * " + std::to_string(cp.W) + " + " + std::to_string(k) + "] = " +
-                (sum ? "(double)" + acc[i][k] + " - (double)" + kc[i][k] : acc[i][k]) + ";");
-      em.line("__syncthreads();");
-      em.open("if (ry_ == 0 && col_ok)");
-      for (int k = 0; k < cp.W; ++k) {
-        const std::string col = "cx_ * " + std::to_string(cp.W) + " + " + std::to_string(k);
-        em.line("{ double s_ = tile_[0][" + col + "]; for (int q_ = 1; q_ < " + std::to_string(cp.RT) +
-                "; ++q_) s_ = " + (sum ? "s_ + tile_[q_][" + col + "]" : "dmax(s_, tile_[q_][" + col + "])") +
-                "; part_[" + std::to_string(partial_off + static_cast<int64_t>(i) * cp.RB * cp.COLS) +
-                " + (i64)rbk_ * " + std::to_string(cp.COLS) + " + (i64)ch_ * " + std::to_string(cp.W) + " + " +
-                std::to_string(k) + "] = s_; }");
-      }
-      em.close();
-      em.line("__syncthreads();");
+  if (!nr) return;
+  // fold the RT row lanes of the tile in smem (fixed order) -> slab partials
+  const std::string tile = em.fresh("tile_");
+  em.line("__shared__ double " + tile + "[" + std::to_string(cp.RT) + "][" + std::to_string(cp.CT * cp.W) + "];");
+  auto part = [&](size_t i, const std::string& slab, const std::string& k) {
+    return "part_[" + std::to_string(partial_off + static_cast<int64_t>(i) * cp.RB * cp.COLS) + " + (i64)(" + slab +
+           ") * " + sCOLS + " + (i64)ch_ * " + sW + " + " + k + "]";
+  };
+  for (size_t i = 0; i < nr; ++i) {
+    const bool sum = g.node(b.reductions[i]).kind == OpKind::ReduceSum;
+    for (int k = 0; k < cp.W; ++k)
+      em.line(tile + "[ry_][cx_ * " + sW + " + " + std::to_string(k) + "] = " +
+              (sum ? "(double)" + acc[i][k] + " - (double)" + kc[i][k] : acc[i][k]) + ";");
+    em.line("__syncthreads();");
+    em.open("if (ry_ == 0 && col_ok)");
+    for (int k = 0; k < cp.W; ++k) {
+      const std::string col = "cx_ * " + sW + " + " + std::to_string(k);
+      em.line("{ double s_ = " + tile + "[0][" + col + "]; for (int q_ = 1; q_ < " + std::to_string(cp.RT) +
+              "; ++q_) s_ = " + (sum ? "s_ + " + tile + "[q_][" + col + "]" : "dmax(s_, " + tile + "[q_][" + col + "])") +
+              "; " + part(i, "rbk_", std::to_string(k)) + " = s_; }");
     }
+    em.close();
+    em.line("__syncthreads();");
   }
-}
-
-// global phase 2 (after the grid barrier): combine partials in fixed order,
-// then the column-shaped consumers
-void emit_column_phase2(Emitter& em, const CompGraph& g, const Body& b, const ColParams& cp,
-                        int64_t partial_off) {
-  const std::vector<int>& P = b.dims_a;
-  const std::vector<int>& C = b.dims_b;
-  em.W = cp.W;
-  em.line("// global body phase 2: fixed-order combine of " + std::to_string(cp.RB) + " partial slabs");
-  em.open("for (i64 q_ = (i64)vbid * blockDim.x + threadIdx.x; q_ < " + std::to_string(cp.NCH) +
-          "; q_ += (i64)vgrid * blockDim.x)");
-  Coords colc;
-  {
-    const std::string lin = cp.W == 1 ? "q_" : "q_ * " + std::to_string(cp.W);
-    auto names = decompose(em, "(" + em.ix() + ")(" + lin + ")", C, "c");
-    for (size_t i = 0; i < C.size(); ++i) colc.push_back({names[i], i + 1 == C.size() && cp.W > 1, true});
-  }
-  for (size_t i = 0; i < b.reductions.size(); ++i) {
+  // last-arriving CTA of this column strip combines the slabs in order
+  const std::string last = em.fresh("last_");
+  em.line("__shared__ unsigned " + last + ";");
+  em.line("__threadfence();");
+  em.line("__syncthreads();");
+  em.line("if (threadIdx.x == 0) " + last + " = atomicAdd(bar_ + " + std::to_string(ctr_off) + " + cb_, 1u) == " +
+          std::to_string(cp.RB - 1) + "u;");
+  em.line("__syncthreads();");
+  em.open("if (" + last + ")");
+  em.line("__threadfence();");
+  em.open("if (ry_ == 0 && col_ok)");
+  for (size_t i = 0; i < nr; ++i) {
     const int r = b.reductions[i];
     const bool sum = g.node(r).kind == OpKind::ReduceSum;
     Val v;
     for (int k = 0; k < cp.W; ++k) {
       const std::string s = em.fresh("s"), t = em.fresh("red");
-      const std::string base = std::to_string(partial_off + static_cast<int64_t>(i) * cp.RB * cp.COLS) +
-                               " + q_ * " + std::to_string(cp.W) + " + " + std::to_string(k);
-      em.line("double " + s + " = part_[" + base + "];");
-      em.line("for (int k_ = 1; k_ < " + std::to_string(cp.RB) + "; ++k_) " + s + " = " +
-              (sum ? s + " + part_[" + base + " + (i64)k_ * " + std::to_string(cp.COLS) + "]"
-                   : "dmax(" + s + ", part_[" + base + " + (i64)k_ * " + std::to_string(cp.COLS) + "])") + ";");
-      em.line("const float " + t + " = (float)" + s + ";");
+      const std::string k_ = std::to_string(k);
+      em.line("double " + s + " = __ldcg(&" + part(i, "0", k_) + ");");
+      em.line("for (int k_ = 1; k_ < " + sRB + "; ++k_) " + s + " = " +
+              (sum ? s + " + __ldcg(&" + part(i, "k_", k_) + ")" : "dmax(" + s + ", __ldcg(&" + part(i, "k_", k_) + "))") + ";");
+      std::string e = "(float)" + s;
+      if (g.node(r).shape.dtype == DType::F16) e = "rnd_f16(" + e + ")";
+      em.line("const float " + t + " = " + e + ";");
       v.lanes.push_back(t);
     }
     em.reduced[Emitter::key(r, colc)] = v;
   }
   for (int o : b.outputs)
-    if (g.node(o).shape.rank() == static_cast<int>(C.size()) && g.node(o).shape.dims == to64(C))
-      store_val(em, g, o, colc, em.value(o, colc), "");
-  (void)P;
+    if (g.node(o).shape.dims == to64(C)) store_val(em, g, o, colc, em.value(o, colc), "");
+  em.close();
+  em.line("if (threadIdx.x == 0) bar_[" + std::to_string(ctr_off) + " + cb_] = 0u;  // re-arm for the next launch");
   em.close();
 }
 
@@ -851,23 +853,18 @@ KernelSpec generate_pattern_kernel(const CompGraph& g, const std::vector<int>& v
       if (!pat.count(s)) em.cached_tensors.insert(s);
     }
 
-  bool coop = false;
   int block = kBlock;
+  bool has_col = false;
   for (const auto& b : bodies) {
-    if (b.kind == Kind::Column) coop = true;
+    has_col = has_col || b.kind == Kind::Column;
     if (b.kind == Kind::Row) block = std::max(block, row_params(b.dims_b).block);
   }
-  // co-residency budget for cooperative kernels: 4 CTAs/SM at 256 threads
-  // (<= 64 registers per thread via __launch_bounds__)
-  const int per_sm = std::max(1, std::min(4, 2048 / block));
-  const int coop_cap = kSmCount * per_sm;
+  const int per_sm = std::max(1, std::min(2, 2048 / block));
 
-  // CTA budget per body
-  int64_t scratch_words = 0;
+  // CTA budget per body; scratch = [256 B reserved][strip arrival counters][f64 partials]
+  int64_t part_words = 0, ctr_words = 64;
   std::vector<ColParams> cps(bodies.size());
-  std::vector<int64_t> part_off(bodies.size(), 0);
-  int64_t n_col_bodies = 0;
-  for (const auto& b : bodies) n_col_bodies += b.kind == Kind::Column;
+  std::vector<int64_t> part_off(bodies.size(), 0), ctr_off(bodies.size(), 0);
   for (size_t i = 0; i < bodies.size(); ++i) {
     Body& b = bodies[i];
     if (b.kind == Kind::Local) {
@@ -882,29 +879,19 @@ KernelSpec generate_pattern_kernel(const CompGraph& g, const std::vector<int>& v
       b.blocks = static_cast<int>(std::clamp<int64_t>((prod(b.dims_a) + rp.RPB - 1) / rp.RPB, 1,
                                                       int64_t(kSmCount) * 16));
     } else {
-      const int cap = static_cast<int>(coop_cap / std::max<int64_t>(1, n_col_bodies));
-      cps[i] = col_params(b.dims_a, b.dims_b, std::max(1, cap - static_cast<int>(bodies.size())));
+      cps[i] = col_params(b.dims_a, b.dims_b, kSmCount * per_sm);
       b.blocks = cps[i].NCB * cps[i].RB;
-      part_off[i] = scratch_words;
-      scratch_words += static_cast<int64_t>(b.reductions.size()) * cps[i].RB * cps[i].COLS;
+      ctr_off[i] = ctr_words;
+      ctr_words += cps[i].NCB;
+      part_off[i] = part_words;
+      part_words += static_cast<int64_t>(b.reductions.size()) * cps[i].RB * cps[i].COLS;
     }
-    std::vector<int> members;
-    for (int o : b.outputs) members.push_back(o);
-    b.bytes = 0;
   }
-  if (coop) {  // every CTA must be co-resident: the other bodies share what is left
-    int col_total = 0, others = 0;
-    for (const auto& b : bodies) (b.kind == Kind::Column ? col_total : others) += b.kind == Kind::Column ? b.blocks : 1;
-    const int share = std::max(1, (coop_cap - col_total) / std::max(1, others));
-    for (auto& b : bodies)
-      if (b.kind != Kind::Column) b.blocks = std::min(b.blocks, share);
-  }
+  const int64_t header = ((ctr_words * 4 + 255) / 256) * 256;
 
   std::ostringstream body_src;
   int start = 0;
-  std::vector<int> starts;
   for (size_t i = 0; i < bodies.size(); ++i) {
-    starts.push_back(start);
     const Body& b = bodies[i];
     em.out.str("");
     em.ind = "    ";
@@ -912,25 +899,11 @@ KernelSpec generate_pattern_kernel(const CompGraph& g, const std::vector<int>& v
     em.reduced.clear();
     if (b.kind == Kind::Local) emit_local(em, g, b);
     else if (b.kind == Kind::Row) emit_row(em, g, pat, b);
-    else emit_column_phase1(em, g, b, cps[i], part_off[i]);
+    else emit_column(em, g, b, cps[i], part_off[i], ctr_off[i]);
     body_src << "  " << (i ? "else " : "") << "if (blockIdx.x < " << start + b.blocks << ") {\n";
     body_src << "    const int vbid = blockIdx.x - " << start << ", vgrid = " << b.blocks << ";\n";
     body_src << "    (void)vbid; (void)vgrid;\n" << em.out.str() << "  }\n";
     start += b.blocks;
-  }
-  if (coop) {
-    body_src << "  grid_sync(bar_, gridDim.x);\n";
-    for (size_t i = 0; i < bodies.size(); ++i) {
-      if (bodies[i].kind != Kind::Column) continue;
-      em.out.str("");
-      em.ind = "    ";
-      em.clear_memo();
-      em.reduced.clear();
-      emit_column_phase2(em, g, bodies[i], cps[i], part_off[i]);
-      body_src << "  if (blockIdx.x >= " << starts[i] << " && blockIdx.x < " << starts[i] + bodies[i].blocks
-               << ") {\n    const int vbid = blockIdx.x - " << starts[i] << ", vgrid = " << bodies[i].blocks
-               << ";\n" << em.out.str() << "  }\n";
-    }
   }
 
   KernelSpec k;
@@ -946,12 +919,12 @@ KernelSpec generate_pattern_kernel(const CompGraph& g, const std::vector<int>& v
   }
   k.grid = start;
   k.block = block;
-  k.cooperative = coop;
+  k.cooperative = false;
   k.alg_bytes = algorithmic_bytes(g, verts);
   std::set<int> outs;
   for (const auto& b : bodies) outs.insert(b.outputs.begin(), b.outputs.end());
   std::ostringstream sig;
-  sig << "extern \"C\" __global__ void __launch_bounds__(" << block << (coop ? ", " + std::to_string(per_sm) : "")
+  sig << "extern \"C\" __global__ void __launch_bounds__(" << block << (has_col ? ", " + std::to_string(per_sm) : "")
       << ") " << name << "(";
   bool first = true;
   for (int v : em.loaded) {
@@ -964,9 +937,10 @@ KernelSpec generate_pattern_kernel(const CompGraph& g, const std::vector<int>& v
     first = false;
     k.outputs.push_back(g.node(v).name);
   }
-  if (coop) {
+  if (has_col) {
     sig << (first ? "" : ", ") << "unsigned* __restrict__ bar_, double* __restrict__ part_";
-    k.scratch_bytes = 256 + scratch_words * 8;
+    k.scratch_header = header;
+    k.scratch_bytes = header + part_words * 8;
   }
   sig << ") {\n";
   k.source = sig.str() + body_src.str() + "}\n";

@@ -56,6 +56,7 @@ Executor::Executor(const CompGraph& g, const FusionPlan& plan,
 Executor::~Executor() {
   for (auto ge : graphs_)
     if (ge) cudaGraphExecDestroy(ge);
+  for (auto ge : batch_graphs_) cudaGraphExecDestroy(ge);
   for (auto& [n, t] : tensors_)
     for (void* p : t.dptr) cudaFree(p);
   for (auto& set : scratch_)
@@ -252,7 +253,7 @@ void Executor::launch_kernel(size_t i, int set, cudaStream_t s) {
   void* part = nullptr;
   if (k.scratch_bytes > 0) {
     bar = scratch_[static_cast<size_t>(set)][i];
-    part = static_cast<char*>(bar) + 256;
+    part = static_cast<char*>(bar) + k.scratch_header;
     ptrs.push_back(bar);
     ptrs.push_back(part);
   }
@@ -354,13 +355,56 @@ void Executor::prepare_sets(int sets) {
   STC_RT(cudaStreamSynchronize(stream_));
 }
 
-double Executor::time(int iters, int warmup, int sets, std::vector<double>* per_kernel) {
+int Executor::prepare_batches(int sets, int batch) {
+  batch = std::max(1, batch);
+  sets = std::max(batch, (std::max(1, sets) + batch - 1) / batch * batch);
+  prepare_sets(sets);
+  if (batch_ == batch && static_cast<int>(batch_graphs_.size()) == sets / batch) return sets / batch;
+  for (auto ge : batch_graphs_) cudaGraphExecDestroy(ge);
+  batch_graphs_.clear();
+  for (int b = 0; b < sets / batch; ++b) {
+    cudaGraph_t graph = nullptr;
+    STC_RT(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
+    for (int t = 0; t < batch; ++t)
+      for (size_t i = 0; i < specs_.size(); ++i) launch_kernel(i, b * batch + t, stream_);
+    STC_RT(cudaStreamEndCapture(stream_, &graph));
+    cudaGraphExec_t ge = nullptr;
+    STC_RT(cudaGraphInstantiate(&ge, graph, 0));
+    cudaGraphDestroy(graph);
+    batch_graphs_.push_back(ge);
+  }
+  batch_ = batch;
+  return sets / batch;
+}
+
+void Executor::launch_batch(cudaStream_t s, int index) {
+  if (batch_graphs_.empty()) throw std::runtime_error("[exec] prepare_batches() first");
+  STC_RT(cudaGraphLaunch(batch_graphs_[static_cast<size_t>(index) % batch_graphs_.size()], s ? s : stream_));
+}
+
+double Executor::time(int iters, int warmup, int sets, std::vector<double>* per_kernel, int batch) {
   sets = std::max(1, sets);
   prepare_sets(sets);
-  for (int w = 0; w < warmup; ++w) launch(stream_, w % sets);
   cudaEvent_t e0, e1;
   STC_RT(cudaEventCreate(&e0));
   STC_RT(cudaEventCreate(&e1));
+  if (batch > 1) {
+    const int nb = prepare_batches(sets, batch);
+    const int launches = std::max(1, iters / batch);
+    for (int w = 0; w < std::max(1, warmup / batch); ++w) launch_batch(stream_, w);
+    STC_RT(cudaStreamSynchronize(stream_));
+    STC_RT(cudaEventRecord(e0, stream_));
+    for (int it = 0; it < launches; ++it) launch_batch(stream_, it % nb);
+    STC_RT(cudaEventRecord(e1, stream_));
+    STC_RT(cudaEventSynchronize(e1));
+    float bms = 0.f;
+    STC_RT(cudaEventElapsedTime(&bms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (per_kernel) per_kernel->assign(specs_.size(), 0.0);
+    return 1000.0 * bms / (static_cast<double>(launches) * batch);
+  }
+  for (int w = 0; w < warmup; ++w) launch(stream_, w % sets);
   STC_RT(cudaStreamSynchronize(stream_));
   STC_RT(cudaEventRecord(e0, stream_));
   for (int it = 0; it < iters; ++it) launch(stream_, it % sets);

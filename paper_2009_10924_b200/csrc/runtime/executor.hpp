@@ -66,11 +66,15 @@ class Executor {
   void download(void* const* host_outputs, int set = 0);
   void launch(cudaStream_t s = nullptr, int set = 0);
   void prepare_sets(int sets);  // allocate + replicate set-0 parameters
+  // B consecutive replays (rotating sets) captured into ONE graph, so the
+  // host/graph launch cost is paid once per B steps; returns #batch graphs
+  int prepare_batches(int sets, int batch);
+  void launch_batch(cudaStream_t s, int index);
   void sync();
   void run_host(const void* const* in, void* const* out);
 
   // CUDA-event timing (see stc_exec_time in include/stitch_b200.h)
-  double time(int iters, int warmup, int sets, std::vector<double>* per_kernel_us);
+  double time(int iters, int warmup, int sets, std::vector<double>* per_kernel_us, int batch = 1);
 
   std::string describe_json() const;
 
@@ -94,6 +98,8 @@ class Executor {
   int sets_ = 0;
   cudaStream_t stream_ = nullptr;
   std::vector<cudaGraphExec_t> graphs_;  // per set
+  std::vector<cudaGraphExec_t> batch_graphs_;
+  int batch_ = 0;
   bool coop_in_graph_ = true;
 };
 

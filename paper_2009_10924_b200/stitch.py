@@ -79,6 +79,9 @@ def lib():
         "stc_exec_sync": (ip, [vp]),
         "stc_exec_tensor": (ip, [vp, cp, P(vp), P(ctypes.c_size_t)]),
         "stc_exec_time": (ip, [vp, ip, ip, ip, P(ctypes.c_double), P(ctypes.c_double)]),
+        "stc_exec_prepare_batches": (ip, [vp, ip, ip, P(ip)]),
+        "stc_exec_launch_batch": (ip, [vp, vp, ip]),
+        "stc_exec_time_batched": (ip, [vp, ip, ip, ip, ip, P(ctypes.c_double)]),
         "stc_compile": (ip, [cp, cp, P(vp)]), "stc_cache_dir": (cp, []),
         "stc_run_pipeline": (ip, [cp, cp, ip, ip, cp, ip, ip, ip, ctypes.c_uint64]),
     }
@@ -335,6 +338,19 @@ class Executor:
         kus = (ctypes.c_double * max(1, self.num_kernels))() if per_kernel else None
         _check(lib().stc_exec_time(self._h, iters, warmup, sets, ctypes.byref(us), kus))
         return us.value, (list(kus[: self.num_kernels]) if per_kernel else None)
+
+    def prepare_batches(self, sets: int, steps_per_graph: int) -> int:
+        n = ctypes.c_int()
+        _check(lib().stc_exec_prepare_batches(self._h, sets, steps_per_graph, ctypes.byref(n)))
+        return n.value
+
+    def launch_batch(self, stream: int, index: int):
+        _check(lib().stc_exec_launch_batch(self._h, ctypes.c_void_p(stream or None), index))
+
+    def time_batched(self, steps: int = 512, warmup: int = 32, sets: int = 8, steps_per_graph: int = 16):
+        us = ctypes.c_double()
+        _check(lib().stc_exec_time_batched(self._h, steps, warmup, sets, steps_per_graph, ctypes.byref(us)))
+        return us.value
 
     def __del__(self):
         if getattr(self, "_h", None) and _lib is not None:

@@ -55,7 +55,7 @@ def main():
     ctx = ck(cu.cuDevicePrimaryCtxRetain(dev))
     ck(cu.cuCtxSetCurrent(ctx))
     prog = ck(nvrtc.nvrtcCreateProgram(SRC.encode(), b"calib.cu", 0, [], []))
-    opts = [b"-arch=sm_100a", b"-O3"]
+    opts = [b"-arch=sm_100a"]
     r = nvrtc.nvrtcCompileProgram(prog, len(opts), opts)
     if int(r[0]) != 0:
         n = ck(nvrtc.nvrtcGetProgramLogSize(prog))
@@ -93,6 +93,43 @@ def main():
 
     out = []
     out.append({"probe": "empty_kernel_512x256", "us": timed(lambda i: launch(fn["empty_k"], 512, 256, None))})
+
+    # GPU-side per-kernel cost inside ONE CUDA graph (no host launch overhead):
+    # N nodes per graph, graph replayed, time / (replays * N)
+    def graph_of(n, make):
+        ck(cu.cuStreamBeginCapture(stream, cu.CUstreamCaptureMode.CU_STREAM_CAPTURE_MODE_THREAD_LOCAL))
+        keep = [make(i) for i in range(n)]
+        graph = ck(cu.cuStreamEndCapture(stream))
+        gexec = ck(cu.cuGraphInstantiate(graph, 0))
+        return gexec, keep
+
+    def graph_us(gexec, n, reps=20):
+        ck(cu.cuGraphLaunch(gexec, stream))
+        ck(cu.cuStreamSynchronize(stream))
+        ck(cu.cuEventRecord(e0, stream))
+        for _ in range(reps):
+            ck(cu.cuGraphLaunch(gexec, stream))
+        ck(cu.cuEventRecord(e1, stream))
+        ck(cu.cuEventSynchronize(e1))
+        return ck(cu.cuEventElapsedTime(e0, e1)) * 1000.0 / (reps * n)
+
+    for grid in (148, 512, 2048):
+        gexec, _ = graph_of(100, lambda i: launch(fn["empty_k"], grid, 256, None))
+        out.append({"probe": "graph_empty_node_grid%d" % grid, "us_per_node": graph_us(gexec, 100)})
+    for mb in (12.6, 25.2, 50.3):
+        nbytes = int(mb * 1e6) // 16 * 16
+        n = max(8, int(1.2e9 // (2 * nbytes)))
+        bufs = [(alloc(nbytes), alloc(nbytes)) for _ in range(n)]
+        n4 = nbytes // 16
+        grid = int((n4 + 256 * 6 - 1) // (256 * 6))
+        gexec, keep = graph_of(n, lambda i: launch(fn["copy_shot"], grid, 256,
+                                                   [bufs[i][0], bufs[i][1], ctypes.c_int(6), ctypes.c_long(n4)]))
+        us = graph_us(gexec, n)
+        out.append({"probe": "graph_copy_shot_%gMB" % mb, "us_per_node": us, "GBps_rw": 2 * nbytes / us / 1e3,
+                    "nodes": n})
+        for a, b in bufs:
+            cu.cuMemFree(a)
+            cu.cuMemFree(b)
     for mb in (12.6, 25.2, 50.3):
         nbytes = int(mb * 1e6) // 16 * 16
         sets = max(4, int(1.2e9 // (2 * nbytes)))
