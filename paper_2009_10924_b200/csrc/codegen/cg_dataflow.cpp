@@ -80,6 +80,14 @@ class Emitter {
   std::set<int> loaded;                    // external tensors read
   std::map<std::string, Val> reduced;      // (reduction vertex, coords) -> value
   std::set<int> cached_tensors;            // read through L1 (re-read broadcast sources)
+  // regional staging: loads at a row body's own (row, chunk) coordinates of a
+  // tensor staged in shared memory read the CTA's TMA-filled tile instead
+  std::map<std::string, std::string> domain_off;  // coords key -> float offset in a staged tile
+  std::map<int, std::string> staged_ptr;          // tensor -> smem base of its tile (current stage)
+  std::vector<int> domain_dims;                   // O ++ I of the body being emitted
+  std::set<int> staged_hits;                      // tensors seen at domain coordinates
+  // local bodies: coords key -> (linear index expr, domain dims)
+  std::map<std::string, std::pair<std::string, std::vector<int>>> domain_lin;
 
   const std::string& ix() const { return ix_; }
   std::string fresh(const char* p) { return p + std::to_string(counter_++); }
@@ -109,6 +117,14 @@ class Emitter {
 
   // linear element index of `c` for lane k (only varying coords shift)
   std::string linear(int v, const Coords& c, int k) const {
+    // a tensor shaped like the local domain, read at the domain's own
+    // coordinates, is addressed by the chunk's linear index directly (no
+    // re-composition of the div/mod-decomposed coordinates)
+    if (auto it = domain_lin.find(coords_key(c)); it != domain_lin.end()) {
+      const auto& sd = g_.node(v).shape.dims;
+      if (std::vector<int64_t>(it->second.second.begin(), it->second.second.end()) == sd)
+        return k ? "(" + it->second.first + " + " + std::to_string(k) + ")" : it->second.first;
+    }
     const auto strides = g_.node(v).shape.strides();
     std::string s;
     for (size_t i = 0; i < c.size(); ++i) {
@@ -129,6 +145,21 @@ class Emitter {
     int nvary = 0, last_vary = -1;
     for (size_t i = 0; i < c.size(); ++i)
       if (c[i].vary) ++nvary, last_vary = static_cast<int>(i);
+    if (W == 4 && sh.dtype == DType::F32 && !domain_off.empty()) {
+      auto it = domain_off.find(coords_key(c));
+      std::vector<int> dd;
+      for (auto d : sh.dims) dd.push_back(static_cast<int>(d));
+      if (it != domain_off.end() && dd == domain_dims) {
+        staged_hits.insert(v);
+        if (auto sp = staged_ptr.find(v); sp != staged_ptr.end()) {
+          const std::string q = fresh("q");
+          line("const float4 " + q + " = lds4(" + sp->second + " + " + it->second + ");");
+          Val r;
+          for (const char* f : {".x", ".y", ".z", ".w"}) r.lanes.push_back(q + f);
+          return r;
+        }
+      }
+    }
     if (nvary == 0 || W == 1) {
       const std::string t = fresh("t");
       line("const float " + t + " = ldv(" + ptr + ", " + linear(v, c, 0) + ");");
@@ -465,6 +496,7 @@ void emit_local(Emitter& em, const CompGraph& g, const Body& b) {
       const std::string lin = em.W == 1 ? cc : cc + " * " + std::to_string(em.W);
       auto names = decompose(em, lin, D, "d");
       for (size_t i = 0; i < D.size(); ++i) c.push_back({names[i], i + 1 == D.size() && em.W > 1, true});
+      if (env_int("STITCH_DOMAIN_LIN", 1)) em.domain_lin[coords_key(c)] = {"(" + lin + ")", D};
     }
     for (int o : b.outputs) stores.emplace_back(o, c, em.value(o, c), ok);
   }
@@ -474,6 +506,16 @@ void emit_local(Emitter& em, const CompGraph& g, const Body& b) {
 
 struct RowParams {
   int W, TPR, NJ, RPB, block;
+};
+
+// TMA-staged regional pipeline: each persistent CTA owns a contiguous range
+// of row tiles (RPB rows) and keeps `stages` tiles of every staged tensor in
+// flight in shared memory (cp.async.bulk + mbarrier complete_tx).
+struct StageCfg {
+  std::vector<int> tensors;  // staged external inputs (dims == O ++ I, f32)
+  int stages = 3;
+  int64_t tile_floats = 0;   // RPB * L
+  int64_t bytes = 0;         // dynamic smem: barriers + stages * tensors * tile
 };
 
 RowParams row_params(const std::vector<int>& inner) {
@@ -490,7 +532,9 @@ RowParams row_params(const std::vector<int>& inner) {
 }
 
 // regional: a team of TPR threads owns a row; row elements live in registers
-void emit_row(Emitter& em, const CompGraph& g, const std::set<int>& pat, const Body& b) {
+// (st != nullptr: the CTA's rows arrive through the TMA pipeline in smem)
+void emit_row(Emitter& em, const CompGraph& g, const std::set<int>& pat, const Body& b,
+              const StageCfg* st = nullptr) {
   const std::vector<int>& O = b.dims_a;
   const std::vector<int>& I = b.dims_b;
   const int64_t ROWS = prod(O), L = prod(I);
@@ -511,8 +555,45 @@ void emit_row(Emitter& em, const CompGraph& g, const std::set<int>& pat, const B
     for (auto& [l, rs] : levels) maxr = std::max(maxr, rs.size());
     em.line("__shared__ double red_smem_[" + std::to_string(maxr) + "][" + std::to_string(rp.block / 32) + "];");
   }
-  em.open("for (i64 rb_ = (i64)vbid * " + std::to_string(rp.RPB) + "; rb_ < " + std::to_string(ROWS) +
-          "; rb_ += (i64)vgrid * " + std::to_string(rp.RPB) + ")");
+  const std::string sRPB = std::to_string(rp.RPB), sL = std::to_string(L);
+  if (st) {
+    const int64_t ntiles = (ROWS + rp.RPB - 1) / rp.RPB;
+    const std::string S = std::to_string(st->stages), TF = std::to_string(st->tile_floats);
+    const int64_t tile_bytes_full = st->tile_floats * 4;
+    em.line("// TMA pipeline: " + std::to_string(ntiles) + " tiles of " + sRPB + " rows, " + S + " stages x " +
+            std::to_string(st->tensors.size()) + " staged tensor(s) x " + std::to_string(tile_bytes_full) + " B");
+    em.line("const int tb_ = (int)(((i64)vbid * " + std::to_string(ntiles) + ") / vgrid);");
+    em.line("const int te_ = (int)(((i64)(vbid + 1) * " + std::to_string(ntiles) + ") / vgrid);");
+    em.line("unsigned long long* sbar_ = reinterpret_cast<unsigned long long*>(dsmem_);");
+    em.line("float* sbuf_ = reinterpret_cast<float*>(dsmem_ + 128);");
+    em.line("if (threadIdx.x == 0) { for (int s = 0; s < " + S + "; ++s) mbar_init(sbar_ + s, 1); mbar_fence_init(); }");
+    em.line("__syncthreads();");
+    std::string issue = "auto issue_ = [&](int t, int s) { const i64 r0 = (i64)t * " + sRPB +
+                        "; const unsigned rows = (unsigned)min((i64)" + sRPB + ", (i64)" + std::to_string(ROWS) +
+                        " - r0); const unsigned nb = rows * " + std::to_string(L * 4) + "u; mbar_expect_tx(sbar_ + s, nb * " +
+                        std::to_string(st->tensors.size()) + "u); ";
+    for (size_t k = 0; k < st->tensors.size(); ++k)
+      issue += "bulk_g2s(sbuf_ + (i64)s * " + std::to_string(st->tile_floats * static_cast<int64_t>(st->tensors.size())) +
+               " + " + std::to_string(static_cast<int64_t>(k) * st->tile_floats) + ", T_" + g.node(st->tensors[k]).name +
+               " + r0 * " + sL + ", nb, sbar_ + s); ";
+    issue += "};";
+    em.line(issue);
+    em.line("if (threadIdx.x == 0) for (int s = 0; s < " + S + " && tb_ + s < te_; ++s) issue_(tb_ + s, s);");
+    em.open("for (int t_ = tb_, i_ = 0; t_ < te_; ++t_, ++i_)");
+    em.line("const int s_ = i_ % " + S + ";");
+    em.line("mbar_wait(sbar_ + s_, (unsigned)((i_ / " + S + ") & 1));");
+    em.line("const i64 rb_ = (i64)t_ * " + sRPB + ";");
+    for (size_t k = 0; k < st->tensors.size(); ++k) {
+      const std::string nm = em.fresh("stg");
+      em.line("const float* " + nm + " = sbuf_ + (i64)s_ * " +
+              std::to_string(st->tile_floats * static_cast<int64_t>(st->tensors.size())) + " + " +
+              std::to_string(static_cast<int64_t>(k) * st->tile_floats) + " + team_ * " + sL + ";");
+      em.staged_ptr[st->tensors[k]] = nm;
+    }
+  } else {
+    em.open("for (i64 rb_ = (i64)vbid * " + sRPB + "; rb_ < " + std::to_string(ROWS) +
+            "; rb_ += (i64)vgrid * " + sRPB + ")");
+  }
   em.line("const bool row_ok = rb_ + team_ < " + std::to_string(ROWS) + ";");
   em.line("const " + em.ix() + " row = (" + em.ix() + ")(row_ok ? rb_ + team_ : " + std::to_string(ROWS - 1) + ");");
   Coords rowc;
@@ -540,7 +621,10 @@ void emit_row(Emitter& em, const CompGraph& g, const std::set<int>& pat, const B
       for (size_t a = 0; a < I.size(); ++a) c.push_back({names[a], a + 1 == I.size() && rp.W > 1, true});
     }
     chunk_c[j] = c;
+    em.domain_off[coords_key(c)] = p;  // float offset inside this team's row of a staged tile
   }
+  em.domain_dims = O;
+  em.domain_dims.insert(em.domain_dims.end(), I.begin(), I.end());
   for (auto& [lvl, rs] : levels) {
     // sums: compensated f32 partials per thread (kahan_add), folded to f64
     // for the cross-thread tree; max: exact in f32
@@ -619,7 +703,14 @@ void emit_row(Emitter& em, const CompGraph& g, const std::set<int>& pat, const B
       store_val(em, g, o, chunk_c[j], v, partial ? "row_ok && " + chunk_ok[j] : "row_ok");
     }
   }
+  if (st) {  // every thread is done with stage s_: refill it with tile t_ + stages
+    em.line("__syncthreads();");
+    em.line("if (threadIdx.x == 0 && t_ + " + std::to_string(st->stages) + " < te_) { fence_proxy_async(); issue_(t_ + " +
+            std::to_string(st->stages) + ", s_); }");
+  }
   em.close();
+  em.domain_off.clear();
+  em.staged_ptr.clear();
 }
 
 struct ColParams {
@@ -862,7 +953,8 @@ KernelSpec generate_pattern_kernel(const CompGraph& g, const std::vector<int>& v
   const int per_sm = std::max(1, std::min(2, 2048 / block));
 
   // CTA budget per body; scratch = [256 B reserved][strip arrival counters][f64 partials]
-  int64_t part_words = 0, ctr_words = 64;
+  int64_t part_words = 0, ctr_words = 64, dyn_smem = 0;
+  std::vector<StageCfg> stage(bodies.size());
   std::vector<ColParams> cps(bodies.size());
   std::vector<int64_t> part_off(bodies.size(), 0), ctr_off(bodies.size(), 0);
   for (size_t i = 0; i < bodies.size(); ++i) {
@@ -876,8 +968,39 @@ KernelSpec generate_pattern_kernel(const CompGraph& g, const std::vector<int>& v
                                                       int64_t(kSmCount) * 16));
     } else if (b.kind == Kind::Row) {
       const RowParams rp = row_params(b.dims_b);
-      b.blocks = static_cast<int>(std::clamp<int64_t>((prod(b.dims_a) + rp.RPB - 1) / rp.RPB, 1,
-                                                      int64_t(kSmCount) * 16));
+      const int64_t rows = prod(b.dims_a), L = prod(b.dims_b), ntiles = (rows + rp.RPB - 1) / rp.RPB;
+      b.blocks = static_cast<int>(std::clamp<int64_t>(ntiles, 1, int64_t(kSmCount) * 16));
+      // dry run: which inputs does the body read at its own (row, chunk) coordinates?
+      // opt-in (STITCH_STAGE=1): measured slower than register-resident rows
+      // when each SM only sees 1-3 tiles (C1-C3 sizes), see DESIGN.md §5
+      if (env_int("STITCH_STAGE", 0) && rp.W == 4) {
+        em.out.str("");
+        em.clear_memo();
+        em.reduced.clear();
+        em.staged_hits.clear();
+        emit_row(em, g, pat, b);
+        std::vector<int> hits;
+        for (int v : em.staged_hits)
+          if (!pat.count(v) && g.node(v).shape.dtype == DType::F32) hits.push_back(v);
+        if (!hits.empty()) {
+          StageCfg& sc = stage[i];
+          sc.tensors = hits;
+          sc.stages = std::max(2, env_int("STITCH_STAGES", 3));
+          sc.tile_floats = int64_t(rp.RPB) * L;
+          // keep >= 2 CTAs per SM: fewer stages when several tensors are staged
+          while (sc.stages > 2 && 128 + int64_t(sc.stages) * static_cast<int64_t>(hits.size()) * sc.tile_floats * 4 >
+                                      110 * 1024)
+            --sc.stages;
+          sc.bytes = 128 + int64_t(sc.stages) * static_cast<int64_t>(hits.size()) * sc.tile_floats * 4;
+          if (sc.bytes <= 200 * 1024) {
+            const int64_t fit = std::clamp<int64_t>(int64_t(220 * 1024) / sc.bytes, 1, 2048 / rp.block);
+            b.blocks = static_cast<int>(std::min<int64_t>(ntiles, kSmCount * fit));
+            dyn_smem = std::max(dyn_smem, sc.bytes);
+          } else {
+            sc.tensors.clear();  // a tile set this large would starve occupancy: stay in registers
+          }
+        }
+      }
     } else {
       cps[i] = col_params(b.dims_a, b.dims_b, kSmCount * per_sm);
       b.blocks = cps[i].NCB * cps[i].RB;
@@ -898,7 +1021,7 @@ KernelSpec generate_pattern_kernel(const CompGraph& g, const std::vector<int>& v
     em.clear_memo();
     em.reduced.clear();
     if (b.kind == Kind::Local) emit_local(em, g, b);
-    else if (b.kind == Kind::Row) emit_row(em, g, pat, b);
+    else if (b.kind == Kind::Row) emit_row(em, g, pat, b, stage[i].tensors.empty() ? nullptr : &stage[i]);
     else emit_column(em, g, b, cps[i], part_off[i], ctr_off[i]);
     body_src << "  " << (i ? "else " : "") << "if (blockIdx.x < " << start + b.blocks << ") {\n";
     body_src << "    const int vbid = blockIdx.x - " << start << ", vgrid = " << b.blocks << ";\n";
@@ -920,7 +1043,10 @@ KernelSpec generate_pattern_kernel(const CompGraph& g, const std::vector<int>& v
   k.grid = start;
   k.block = block;
   k.cooperative = false;
+  k.smem = dyn_smem;
   k.alg_bytes = algorithmic_bytes(g, verts);
+  for (size_t i = 0; i < bodies.size(); ++i)
+    if (!stage[i].tensors.empty()) k.tmpl += "+tma";
   std::set<int> outs;
   for (const auto& b : bodies) outs.insert(b.outputs.begin(), b.outputs.end());
   std::ostringstream sig;
@@ -943,7 +1069,11 @@ KernelSpec generate_pattern_kernel(const CompGraph& g, const std::vector<int>& v
     k.scratch_bytes = header + part_words * 8;
   }
   sig << ") {\n";
-  k.source = sig.str() + body_src.str() + "}\n";
+  if (dyn_smem) sig << "  extern __shared__ __align__(128) unsigned char dsmem_[];\n";
+  // programmatic dependent launch: wait for the producer grid's memory before
+  // touching inputs; let the next kernel of the plan launch as we finish
+  const bool pdl = env_int("STITCH_PDL", 1) != 0;
+  k.source = sig.str() + (pdl ? "  pdl_wait();\n" : "") + body_src.str() + (pdl ? "  pdl_launch();\n" : "") + "}\n";
   return k;
 }
 
@@ -952,39 +1082,47 @@ KernelSpec generate_pattern_kernel(const CompGraph& g, const std::vector<int>& v
 // every CTA folds the partials in the same order, then fills the output.
 KernelSpec generate_opaque_kernel(const CompGraph& g, int vertex, const std::string& name, int) {
   const OpNode& n = g.node(vertex);
-  const int grid = kSmCount;
-  KernelSpec k;
-  k.name = name;
-  k.tmpl = "opaque";
-  k.pattern_key = "op:" + n.name;
-  k.grid = grid;
-  k.block = kBlock;
-  k.cooperative = true;
-  std::ostringstream s;
-  s << "extern \"C\" __global__ void __launch_bounds__(" << kBlock << ", 1) " << name << "(";
   std::set<int> ops(n.operands.begin(), n.operands.end());
   int64_t count = 0;
   for (int o : n.operands) count += g.node(o).shape.element_count();
+  const int64_t work = count + n.shape.element_count();
+  // small tensors (e.g. DIEN's [256,36] GEMM outputs): one 1024-thread CTA,
+  // no grid-wide barrier; large ones: cooperative grid with a barrier
+  const bool single = work <= (int64_t(1) << 20);
+  const int grid = single ? 1 : kSmCount;
+  const int block = single ? 1024 : kBlock;
+  KernelSpec k;
+  k.name = name;
+  k.tmpl = single ? "opaque" : "opaque(grid)";
+  k.pattern_key = "op:" + n.name;
+  k.grid = grid;
+  k.block = block;
+  k.cooperative = !single;
+  std::ostringstream s;
+  s << "extern \"C\" __global__ void __launch_bounds__(" << block << ", 1) " << name << "(";
   for (int o : ops) {
     s << "const " << c_type(g.node(o).shape.dtype) << "* __restrict__ T_" << g.node(o).name << ", ";
     k.inputs.push_back(g.node(o).name);
   }
-  s << c_type(n.shape.dtype) << "* __restrict__ T_" << n.name << ", unsigned* __restrict__ bar_, double* __restrict__ part_) {\n";
+  s << c_type(n.shape.dtype) << "* __restrict__ T_" << n.name;
+  if (!single) {
+    s << ", unsigned* __restrict__ bar_, double* __restrict__ part_";
+    k.scratch_bytes = 256 + int64_t(grid) * 8;
+  }
+  s << ") {\n  pdl_wait();\n";
   k.outputs.push_back(n.name);
-  k.scratch_bytes = 256 + int64_t(grid) * 8;
-  s << "  __shared__ double red_[" << kBlock / 32 << "];\n  double acc = 0.0;\n";
-  for (int o : n.operands) {  // an operand listed twice is counted twice, as upstream
+  s << "  __shared__ double red_[" << block / 32 << "];\n  double acc = 0.0;\n";
+  for (int o : n.operands)  // an operand listed twice is counted twice, as upstream
     s << "  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < " << g.node(o).shape.element_count()
       << "; i += (i64)gridDim.x * blockDim.x) acc += (double)ldv(T_" << g.node(o).name << ", i);\n";
-  }
   s << "  acc = bfly_sum(acc, 32);\n  if ((threadIdx.x & 31) == 0) red_[threadIdx.x >> 5] = acc;\n  __syncthreads();\n"
-    << "  if (threadIdx.x == 0) { double t = 0.0; for (int w = 0; w < " << kBlock / 32
-    << "; ++w) t += red_[w]; part_[blockIdx.x] = t; }\n"
-    << "  grid_sync(bar_, gridDim.x);\n"
-    << "  double tot = 0.0;\n  for (int b = 0; b < " << grid << "; ++b) tot += part_[b];\n"
-    << "  const float fill = (float)(" << (count ? "tot / " + std::to_string(count) + ".0" : "0.0") << ");\n"
+    << "  double tot = 0.0;\n  for (int w = 0; w < " << block / 32 << "; ++w) tot += red_[w];\n";
+  if (!single)
+    s << "  if (threadIdx.x == 0) part_[blockIdx.x] = tot;\n  grid_sync(bar_, gridDim.x);\n"
+      << "  tot = 0.0;\n  for (int b = 0; b < " << grid << "; ++b) tot += __ldcg(part_ + b);\n";
+  s << "  const float fill = (float)(" << (count ? "tot / " + std::to_string(count) + ".0" : "0.0") << ");\n"
     << "  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < " << n.shape.element_count()
-    << "; i += (i64)gridDim.x * blockDim.x) stv(T_" << n.name << ", i, fill);\n}\n";
+    << "; i += (i64)gridDim.x * blockDim.x) stv(T_" << n.name << ", i, fill);\n  pdl_launch();\n}\n";
   k.source = s.str();
   int64_t bytes = n.shape.byte_size();
   for (int o : ops) bytes += g.node(o).shape.byte_size();

@@ -75,6 +75,7 @@ class ProgramTranslator {
     body << "  const i64 bid = blockIdx.x, tid = threadIdx.x, lane = threadIdx.x & 31;\n";
     body << "  const i64 wid = (bid * " << p_.launch.block << " + tid) >> 5;\n";
     body << "  (void)bid; (void)lane; (void)wid; (void)shm;\n";
+    body << "  pdl_wait();\n";
     for (const auto& r : iregs_) body << "  i64 " << r << " = 0;\n";
     for (const auto& r : fregs_) body << "  double " << r << " = 0.0;\n";
     for (const auto& [a, w] : arrays_) body << "  double " << a << "[" << w << "] = {};\n";

@@ -78,6 +78,34 @@ __device__ __forceinline__ float bfly_max(float v, int width) {
   return v;
 }
 
+// programmatic dependent launch (PDL): no-ops unless launched with the
+// programmatic-stream-serialization attribute
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+// ---- TMA bulk copies + mbarriers (sm_90+; the regional pipeline) ----
+__device__ __forceinline__ unsigned smem_addr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_addr(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(smem_addr(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+  asm volatile("{\n .reg .pred P1;\n LAB_WAIT:\n"
+               " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+               " @P1 bra DONE;\n bra LAB_WAIT;\n DONE:\n}" :: "r"(smem_addr(b)), "r"(parity) : "memory");
+}
+// global -> shared bulk copy (TMA engine, no tensor map), completes on `b`
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* b) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               :: "r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(smem_addr(b)) : "memory");
+}
+// order this CTA's generic-proxy smem accesses before later async-proxy ones
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ float4 lds4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+
 // run_program fault report: first fault wins (code 1 race, 2 global OOB, 3 shared OOB)
 __device__ __forceinline__ void sim_fault(unsigned* f, unsigned code, i64 where) {
   if (atomicCAS(f, 0u, code) == 0u) {

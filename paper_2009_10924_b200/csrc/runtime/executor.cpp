@@ -2,6 +2,7 @@
 
 #include <algorithm>
 #include <cctype>
+#include <cstdlib>
 #include <cstring>
 #include <set>
 #include <sstream>
@@ -33,6 +34,7 @@ Executor::Executor(const CompGraph& g, const FusionPlan& plan,
                    int device, ExecMode mode, bool use_graph)
     : g_(g), use_graph_(use_graph) {
   dev_ = &device_init(device);
+  if (const char* v = std::getenv("STITCH_PDL")) pdl_ = *v != '0';
   STC_RT(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
   plan_launches(plan, kernels, model, mode);
   module_ = std::make_unique<Module>(compile_cubin(source_, default_nvrtc_options()));
@@ -268,6 +270,13 @@ void Executor::launch_kernel(size_t i, int set, cudaStream_t s) {
   if (k.cooperative && coop_in_graph_) {
     attr.id = cudaLaunchAttributeCooperative;
     attr.val.cooperative = 1;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+  } else if (pdl_ && i > 0 && !k.cooperative && !specs_[i - 1].cooperative) {
+    // programmatic dependent launch: kernel i may launch while kernel i-1
+    // drains; it griddepcontrol.wait()s before reading i-1's outputs
+    attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr.val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = &attr;
     cfg.numAttrs = 1;
   }

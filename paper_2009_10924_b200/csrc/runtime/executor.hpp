@@ -101,6 +101,7 @@ class Executor {
   std::vector<cudaGraphExec_t> batch_graphs_;
   int batch_ = 0;
   bool coop_in_graph_ = true;
+  bool pdl_ = true;  // STITCH_PDL=0 disables programmatic dependent launch
 };
 
 }  // namespace stitch::gpu

@@ -80,4 +80,4 @@ def test_dataflow_templates_chosen_for_fixtures():
             "bias_reduce": "regional", "scale_reduce_scale": "regional"}
     for name, tmpl in want.items():
         _, kernels = stitch.Plan(stitch.Graph(fixture_graphs()[name]), "v100").codegen()
-        assert [k["template"] for k in kernels] == [tmpl], name
+        assert [k["template"].split("+")[0] for k in kernels] == [tmpl], name
