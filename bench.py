@@ -163,10 +163,12 @@ def time_subgraph(stitch, name):
     desc = ex.describe()
     per_set = sum(t.nbytes for t in g.params) + sum(t.nbytes for t in g.outputs)
     sets = min(256, max(2, math.ceil(8 * L2_BYTES / max(per_set, 1))))
-    us, kus = ex.time(iters=200, warmup=20, sets=sets, per_kernel=True)
+    us1, kus = ex.time(iters=200, warmup=20, sets=sets, per_kernel=True)
+    us = ex.time_batched(steps=256, warmup=32, sets=sets, steps_per_graph=16)
     alg = sum(k["bytes"] for k in desc)
     top = max(range(len(desc)), key=lambda i: kus[i])
     return {"us": round(us, 3), "GBps": round(alg / us / 1e3, 1), "kernels": len(desc),
+            "us_one_launch_per_step": round(us1, 3),
             "templates": sorted({k["template"] for k in desc}), "bytes": alg,
             "dominant": {"name": desc[top]["name"], "template": desc[top]["template"],
                          "us_event": round(kus[top], 3)}}
@@ -178,6 +180,8 @@ def main():
     ap.add_argument("--steps", type=int, default=2000)
     ap.add_argument("--warmup", type=int, default=50)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--steps-per-graph", type=int, default=16,
+                    help="steps captured per CUDA-graph launch (largest of 16/8/4/2/1 dividing --steps)")
     ap.add_argument("--no-subgraphs", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
@@ -205,7 +209,11 @@ def main():
     ex.upload(inputs)
     per_set = sum(t.nbytes for t in g.params) + sum(t.nbytes for t in g.outputs)
     sets = max(2, math.ceil(8 * L2_BYTES / per_set))
-    ex.prepare_sets(sets)
+    # B consecutive steps per CUDA-graph launch (each step still reads its own
+    # cold buffer set and writes its own outputs); B divides K exactly
+    spg = next(b for b in (args.steps_per_graph, 8, 4, 2, 1) if b >= 1 and args.steps % b == 0)
+    n_graphs = ex.prepare_batches(sets, spg)
+    sets = max(sets, n_graphs * spg)
     # an explicit (non-default) stream: the graph replays AND the timing events
     # go on it (a NULL handle would mean the executor's internal stream)
     stream = torch.cuda.Stream()
@@ -215,16 +223,16 @@ def main():
 
     clocks = ClockSampler(local)
     clocks.start()
-    for w in range(args.warmup):
-        ex.launch(sp, w % sets)
+    for w in range(max(1, args.warmup // spg)):
+        ex.launch_batch(sp, w)
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    for i in range(args.steps):
-        ex.launch(sp, i % sets)
+    for i in range(args.steps // spg):
+        ex.launch_batch(sp, i)
     e1.record(stream)
     torch.cuda.synchronize()
     if dist:
@@ -239,8 +247,9 @@ def main():
     ms_step = ms / args.steps
     value = alg_bytes * world / (ms_step * 1e-3) / 1e9
 
-    # per-kernel device time (events around each kernel, same rotation) for the roofline
-    _, kus = ex.time(iters=200, warmup=10, sets=sets, per_kernel=True)
+    # per-kernel device time (events around each kernel, same rotation) for the
+    # roofline, and the step time with one graph launch per step for reference
+    us_single, kus = ex.time(iters=200, warmup=10, sets=sets, per_kernel=True)
     top = max(range(len(desc)), key=lambda i: kus[i])
     # dominant kernel's time inside the graph: its share of the step (1-kernel plan -> the step)
     dom_us = ms_step * 1e3 * (kus[top] / sum(kus)) if len(desc) > 1 else ms_step * 1e3
@@ -298,6 +307,8 @@ def main():
             "config": {"workload": WORKLOAD_DESC, "graph": WORKLOAD, "device_cfg": "b200_device.cfg",
                        "plan_kernels": len(desc), "templates": [k["template"] for k in desc],
                        "us_per_subgraph": round(ms_step * 1e3, 3),
+                       "steps_per_graph_launch": spg,
+                       "us_per_subgraph_one_launch_per_step": round(us_single, 3),
                        "bytes_per_step_per_gpu": alg_bytes,
                        "l2": "inputs larger than L2: %d rotating buffer sets x %.1f MB = %.0f MB (>= 8x the 126 MB L2)"
                              % (sets, per_set / 1e6, sets * per_set / 1e6),

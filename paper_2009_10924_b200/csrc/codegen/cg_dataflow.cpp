@@ -496,7 +496,8 @@ void emit_local(Emitter& em, const CompGraph& g, const Body& b) {
       const std::string lin = em.W == 1 ? cc : cc + " * " + std::to_string(em.W);
       auto names = decompose(em, lin, D, "d");
       for (size_t i = 0; i < D.size(); ++i) c.push_back({names[i], i + 1 == D.size() && em.W > 1, true});
-      if (env_int("STITCH_DOMAIN_LIN", 1)) em.domain_lin[coords_key(c)] = {"(" + lin + ")", D};
+      // opt-in: measured slower on bert_gelu (register allocation), so off
+      if (env_int("STITCH_DOMAIN_LIN", 0)) em.domain_lin[coords_key(c)] = {"(" + lin + ")", D};
     }
     for (int o : b.outputs) stores.emplace_back(o, c, em.value(o, c), ok);
   }
@@ -827,6 +828,9 @@ void emit_column(Emitter& em, const CompGraph& g, const Body& b, const ColParams
   // last-arriving CTA of this column strip combines the slabs in order
   const std::string last = em.fresh("last_");
   em.line("__shared__ unsigned " + last + ";");
+  for (size_t i = 0; i < nr; ++i)
+    for (int k = 0; k < cp.W; ++k)
+      em.line("__shared__ float red_" + std::to_string(i) + "_" + std::to_string(k) + "_[" + std::to_string(cp.CT) + "];");
   em.line("__threadfence();");
   em.line("__syncthreads();");
   em.line("if (threadIdx.x == 0) " + last + " = atomicAdd(bar_ + " + std::to_string(ctr_off) + " + cb_, 1u) == " +
@@ -834,24 +838,37 @@ void emit_column(Emitter& em, const CompGraph& g, const Body& b, const ColParams
   em.line("__syncthreads();");
   em.open("if (" + last + ")");
   em.line("__threadfence();");
-  em.open("if (ry_ == 0 && col_ok)");
+  // combine with the whole CTA: row lane ry_ folds slabs ry_, ry_+RT, ...
+  // (independent loads in flight), then the RT lane sums fold in smem in
+  // fixed order -- deterministic for a given launch shape
   for (size_t i = 0; i < nr; ++i) {
-    const int r = b.reductions[i];
-    const bool sum = g.node(r).kind == OpKind::ReduceSum;
-    Val v;
+    const bool sum = g.node(b.reductions[i]).kind == OpKind::ReduceSum;
     for (int k = 0; k < cp.W; ++k) {
-      const std::string s = em.fresh("s"), t = em.fresh("red");
-      const std::string k_ = std::to_string(k);
-      em.line("double " + s + " = __ldcg(&" + part(i, "0", k_) + ");");
-      em.line("for (int k_ = 1; k_ < " + sRB + "; ++k_) " + s + " = " +
+      const std::string k_ = std::to_string(k), s = em.fresh("cs");
+      em.line("double " + s + " = " + (sum ? "0.0" : "__longlong_as_double(0xfff0000000000000ll)") + ";");
+      em.line("if (col_ok) for (int k_ = ry_; k_ < " + sRB + "; k_ += " + std::to_string(cp.RT) + ") " + s + " = " +
               (sum ? s + " + __ldcg(&" + part(i, "k_", k_) + ")" : "dmax(" + s + ", __ldcg(&" + part(i, "k_", k_) + "))") + ";");
+      em.line(tile + "[ry_][cx_ * " + sW + " + " + k_ + "] = " + s + ";");
+    }
+    em.line("__syncthreads();");
+    em.open("if (ry_ == 0 && col_ok)");
+    Val v;
+    const int r = b.reductions[i];
+    for (int k = 0; k < cp.W; ++k) {
+      const std::string col = "cx_ * " + sW + " + " + std::to_string(k), s = em.fresh("s"), t = em.fresh("red");
+      em.line("double " + s + " = " + tile + "[0][" + col + "];");
+      em.line("for (int q_ = 1; q_ < " + std::to_string(cp.RT) + "; ++q_) " + s + " = " +
+              (sum ? s + " + " + tile + "[q_][" + col + "]" : "dmax(" + s + ", " + tile + "[q_][" + col + "])") + ";");
       std::string e = "(float)" + s;
       if (g.node(r).shape.dtype == DType::F16) e = "rnd_f16(" + e + ")";
-      em.line("const float " + t + " = " + e + ";");
-      v.lanes.push_back(t);
+      em.line("red_" + std::to_string(i) + "_" + std::to_string(k) + "_[cx_] = " + e + ";");
+      v.lanes.push_back("red_" + std::to_string(i) + "_" + std::to_string(k) + "_[cx_]");
     }
+    em.close();
+    em.line("__syncthreads();");
     em.reduced[Emitter::key(r, colc)] = v;
   }
+  em.open("if (ry_ == 0 && col_ok)");
   for (int o : b.outputs)
     if (g.node(o).shape.dims == to64(C)) store_val(em, g, o, colc, em.value(o, colc), "");
   em.close();
@@ -950,7 +967,7 @@ KernelSpec generate_pattern_kernel(const CompGraph& g, const std::vector<int>& v
     has_col = has_col || b.kind == Kind::Column;
     if (b.kind == Kind::Row) block = std::max(block, row_params(b.dims_b).block);
   }
-  const int per_sm = std::max(1, std::min(2, 2048 / block));
+  const int per_sm = std::max(1, std::min(env_int("STITCH_COL_CTAS", 2), 2048 / block));
 
   // CTA budget per body; scratch = [256 B reserved][strip arrival counters][f64 partials]
   int64_t part_words = 0, ctr_words = 64, dyn_smem = 0;
@@ -1073,7 +1090,9 @@ KernelSpec generate_pattern_kernel(const CompGraph& g, const std::vector<int>& v
   // programmatic dependent launch: wait for the producer grid's memory before
   // touching inputs; let the next kernel of the plan launch as we finish
   const bool pdl = env_int("STITCH_PDL", 1) != 0;
-  k.source = sig.str() + (pdl ? "  pdl_wait();\n" : "") + body_src.str() + (pdl ? "  pdl_launch();\n" : "") + "}\n";
+  const bool early = env_int("STITCH_PDL_EARLY", 0) != 0;  // trigger dependents at entry
+  k.source = sig.str() + (pdl ? (early ? "  pdl_wait();\n  pdl_launch();\n" : "  pdl_wait();\n") : "") +
+             body_src.str() + (pdl && !early ? "  pdl_launch();\n" : "") + "}\n";
   return k;
 }
 
@@ -1119,10 +1138,18 @@ KernelSpec generate_opaque_kernel(const CompGraph& g, int vertex, const std::str
     << "  double tot = 0.0;\n  for (int w = 0; w < " << block / 32 << "; ++w) tot += red_[w];\n";
   if (!single)
     s << "  if (threadIdx.x == 0) part_[blockIdx.x] = tot;\n  grid_sync(bar_, gridDim.x);\n"
-      << "  tot = 0.0;\n  for (int b = 0; b < " << grid << "; ++b) tot += __ldcg(part_ + b);\n";
-  s << "  const float fill = (float)(" << (count ? "tot / " + std::to_string(count) + ".0" : "0.0") << ");\n"
-    << "  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < " << n.shape.element_count()
-    << "; i += (i64)gridDim.x * blockDim.x) stv(T_" << n.name << ", i, fill);\n  pdl_launch();\n}\n";
+      << "  __shared__ double all_;\n"
+      << "  if (threadIdx.x == 0) { double t = 0.0; for (int b = 0; b < " << grid
+      << "; ++b) t += __ldcg(part_ + b); all_ = t; }\n  __syncthreads();\n  tot = all_;\n";
+  s << "  const float fill = (float)(" << (count ? "tot / " + std::to_string(count) + ".0" : "0.0") << ");\n";
+  const int64_t nout = n.shape.element_count();
+  if (n.shape.dtype == DType::F32 && nout % 4 == 0)  // 128-bit stores
+    s << "  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < " << nout / 4
+      << "; i += (i64)gridDim.x * blockDim.x) st4(T_" << n.name << " + 4 * i, fill, fill, fill, fill);\n";
+  else
+    s << "  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < " << nout
+      << "; i += (i64)gridDim.x * blockDim.x) stv(T_" << n.name << ", i, fill);\n";
+  s << "  pdl_launch();\n}\n";
   k.source = s.str();
   int64_t bytes = n.shape.byte_size();
   for (int o : ops) bytes += g.node(o).shape.byte_size();

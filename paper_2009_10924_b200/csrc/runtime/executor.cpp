@@ -246,7 +246,8 @@ void Executor::ensure_sets(int sets) {
   sets_ = sets;
 }
 
-void Executor::launch_kernel(size_t i, int set, cudaStream_t s) {
+void Executor::launch_kernel(size_t i, int set, cudaStream_t s, int after) {
+  if (after == -2) after = static_cast<int>(i) - 1;
   const KernelSpec& k = specs_[i];
   std::vector<void*> ptrs;
   for (const auto& t : k.inputs) ptrs.push_back(tensors_.at(t).dptr[static_cast<size_t>(set)]);
@@ -272,7 +273,7 @@ void Executor::launch_kernel(size_t i, int set, cudaStream_t s) {
     attr.val.cooperative = 1;
     cfg.attrs = &attr;
     cfg.numAttrs = 1;
-  } else if (pdl_ && i > 0 && !k.cooperative && !specs_[i - 1].cooperative) {
+  } else if (pdl_ && after >= 0 && !k.cooperative && !specs_[static_cast<size_t>(after)].cooperative) {
     // programmatic dependent launch: kernel i may launch while kernel i-1
     // drains; it griddepcontrol.wait()s before reading i-1's outputs
     attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -375,7 +376,8 @@ int Executor::prepare_batches(int sets, int batch) {
     cudaGraph_t graph = nullptr;
     STC_RT(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
     for (int t = 0; t < batch; ++t)
-      for (size_t i = 0; i < specs_.size(); ++i) launch_kernel(i, b * batch + t, stream_);
+      for (size_t i = 0; i < specs_.size(); ++i)  // PDL also across consecutive (independent) steps
+        launch_kernel(i, b * batch + t, stream_, i > 0 ? static_cast<int>(i) - 1 : (t > 0 ? static_cast<int>(specs_.size()) - 1 : -1));
     STC_RT(cudaStreamEndCapture(stream_, &graph));
     cudaGraphExec_t ge = nullptr;
     STC_RT(cudaGraphInstantiate(&ge, graph, 0));

@@ -82,7 +82,9 @@ class Executor {
   void plan_launches(const FusionPlan& plan, const std::map<std::string, KernelPlan>& kernels,
                      const MachineModel& model, ExecMode mode);
   void ensure_sets(int sets);
-  void launch_kernel(size_t i, int set, cudaStream_t s);
+  // after_kernel: the kernel launched just before this one in the same stream
+  // (-1: none) -- decides whether programmatic dependent launch applies
+  void launch_kernel(size_t i, int set, cudaStream_t s, int after_kernel = -2);
   void build_graph(int set);
 
   CompGraph g_;

@@ -68,7 +68,23 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--skip-slow", action="store_true")
     ap.add_argument("--only", default="")
+    ap.add_argument("--shards", action="store_true",
+                    help="per-shard plans (SURVEY §8e): <graph>@<n>__b200.json for n in 2,4,8")
     args = ap.parse_args()
+    if args.shards:
+        from paper_2009_10924_b200.shard import RULES
+        os.makedirs(os.path.join(GOLD, "plans"), exist_ok=True)
+        for name in ("attn_softmax", "ln_4096x768", "ln2pass_4096x768", "colreduce", "bert_gelu", "bert_resln"):
+            full = open(os.path.join(GRAPHS, name + ".graph")).read()
+            for n in (2, 4, 8):
+                text = RULES[name].graph_text(full, n)
+                rec = plan_record(text, "b200")
+                rec["serialized"] = ref.serialize(text)
+                rec["graph_text"] = text
+                with open(os.path.join(GOLD, "plans", "%s@%d__b200.json" % (name, n)), "w") as fh:
+                    json.dump(rec, fh, indent=1, sort_keys=True)
+                print("shard plan", name, n, rec["summary"], flush=True)
+        return
     os.makedirs(os.path.join(GOLD, "plans"), exist_ok=True)
 
     fixtures = {f: open(os.path.join(REF_FIXTURES, f + ".graph")).read() for f in FIXTURES}
