@@ -524,7 +524,10 @@ RowParams row_params(const std::vector<int>& inner) {
   RowParams p;
   p.W = inner.back() % 4 == 0 ? 4 : (inner.back() % 2 == 0 ? 2 : 1);
   const int64_t nch = L / p.W;
-  const int nj_target = std::max(1, env_int("STITCH_ROW_NJ", 8));
+  // chunks per thread: short rows (softmax, 32 float4) want more threads per
+  // row and fewer registers (2 chunks); long rows keep ~8 chunks so a team
+  // stays within one warp (B200 sweep, profiles/r01/row_chunk_sweep.jsonl)
+  const int nj_target = std::max(1, env_int("STITCH_ROW_NJ", nch <= 64 ? 2 : 8));
   p.TPR = static_cast<int>(std::clamp<int64_t>(pow2ceil((nch + nj_target - 1) / nj_target), 1, 1024));
   p.NJ = static_cast<int>((nch + p.TPR - 1) / p.TPR);
   p.block = std::max(kBlock, p.TPR);
@@ -828,9 +831,10 @@ void emit_column(Emitter& em, const CompGraph& g, const Body& b, const ColParams
   // last-arriving CTA of this column strip combines the slabs in order
   const std::string last = em.fresh("last_");
   em.line("__shared__ unsigned " + last + ";");
-  for (size_t i = 0; i < nr; ++i)
-    for (int k = 0; k < cp.W; ++k)
-      em.line("__shared__ float red_" + std::to_string(i) + "_" + std::to_string(k) + "_[" + std::to_string(cp.CT) + "];");
+  if (env_int("STITCH_COL_COMBINE", 0) != 0)
+    for (size_t i = 0; i < nr; ++i)
+      for (int k = 0; k < cp.W; ++k)
+        em.line("__shared__ float red_" + std::to_string(i) + "_" + std::to_string(k) + "_[" + std::to_string(cp.CT) + "];");
   em.line("__threadfence();");
   em.line("__syncthreads();");
   em.line("if (threadIdx.x == 0) " + last + " = atomicAdd(bar_ + " + std::to_string(ctr_off) + " + cb_, 1u) == " +
@@ -838,37 +842,53 @@ void emit_column(Emitter& em, const CompGraph& g, const Body& b, const ColParams
   em.line("__syncthreads();");
   em.open("if (" + last + ")");
   em.line("__threadfence();");
-  // combine with the whole CTA: row lane ry_ folds slabs ry_, ry_+RT, ...
-  // (independent loads in flight), then the RT lane sums fold in smem in
-  // fixed order -- deterministic for a given launch shape
+  const bool cta_combine = env_int("STITCH_COL_COMBINE", 0) != 0;
+  if (!cta_combine) em.open("if (ry_ == 0 && col_ok)");
   for (size_t i = 0; i < nr; ++i) {
-    const bool sum = g.node(b.reductions[i]).kind == OpKind::ReduceSum;
-    for (int k = 0; k < cp.W; ++k) {
-      const std::string k_ = std::to_string(k), s = em.fresh("cs");
-      em.line("double " + s + " = " + (sum ? "0.0" : "__longlong_as_double(0xfff0000000000000ll)") + ";");
-      em.line("if (col_ok) for (int k_ = ry_; k_ < " + sRB + "; k_ += " + std::to_string(cp.RT) + ") " + s + " = " +
-              (sum ? s + " + __ldcg(&" + part(i, "k_", k_) + ")" : "dmax(" + s + ", __ldcg(&" + part(i, "k_", k_) + "))") + ";");
-      em.line(tile + "[ry_][cx_ * " + sW + " + " + k_ + "] = " + s + ";");
-    }
-    em.line("__syncthreads();");
-    em.open("if (ry_ == 0 && col_ok)");
-    Val v;
     const int r = b.reductions[i];
-    for (int k = 0; k < cp.W; ++k) {
-      const std::string col = "cx_ * " + sW + " + " + std::to_string(k), s = em.fresh("s"), t = em.fresh("red");
-      em.line("double " + s + " = " + tile + "[0][" + col + "];");
-      em.line("for (int q_ = 1; q_ < " + std::to_string(cp.RT) + "; ++q_) " + s + " = " +
-              (sum ? s + " + " + tile + "[q_][" + col + "]" : "dmax(" + s + ", " + tile + "[q_][" + col + "])") + ";");
-      std::string e = "(float)" + s;
-      if (g.node(r).shape.dtype == DType::F16) e = "rnd_f16(" + e + ")";
-      em.line("red_" + std::to_string(i) + "_" + std::to_string(k) + "_[cx_] = " + e + ";");
-      v.lanes.push_back("red_" + std::to_string(i) + "_" + std::to_string(k) + "_[cx_]");
+    const bool sum = g.node(r).kind == OpKind::ReduceSum;
+    Val v;
+    if (!cta_combine) {
+      // the strip's column threads fold the slabs in slab order
+      for (int k = 0; k < cp.W; ++k) {
+        const std::string s0 = em.fresh("s"), t = em.fresh("red"), k_ = std::to_string(k);
+        em.line("double " + s0 + " = __ldcg(&" + part(i, "0", k_) + ");");
+        em.line("for (int k_ = 1; k_ < " + sRB + "; ++k_) " + s0 + " = " +
+                (sum ? s0 + " + __ldcg(&" + part(i, "k_", k_) + ")" : "dmax(" + s0 + ", __ldcg(&" + part(i, "k_", k_) + "))") + ";");
+        std::string e = "(float)" + s0;
+        if (g.node(r).shape.dtype == DType::F16) e = "rnd_f16(" + e + ")";
+        em.line("const float " + t + " = " + e + ";");
+        v.lanes.push_back(t);
+      }
+    } else {
+      // the whole CTA: row lane ry_ folds slabs ry_, ry_+RT, ..., then the RT
+      // lane sums fold in smem in fixed order
+      for (int k = 0; k < cp.W; ++k) {
+        const std::string k_ = std::to_string(k), s0 = em.fresh("cs");
+        em.line("double " + s0 + " = " + (sum ? "0.0" : "__longlong_as_double(0xfff0000000000000ll)") + ";");
+        em.line("if (col_ok) for (int k_ = ry_; k_ < " + sRB + "; k_ += " + std::to_string(cp.RT) + ") " + s0 + " = " +
+                (sum ? s0 + " + __ldcg(&" + part(i, "k_", k_) + ")" : "dmax(" + s0 + ", __ldcg(&" + part(i, "k_", k_) + "))") + ";");
+        em.line(tile + "[ry_][cx_ * " + sW + " + " + k_ + "] = " + s0 + ";");
+      }
+      em.line("__syncthreads();");
+      em.open("if (ry_ == 0 && col_ok)");
+      for (int k = 0; k < cp.W; ++k) {
+        const std::string col = "cx_ * " + sW + " + " + std::to_string(k), s0 = em.fresh("s");
+        const std::string arr = "red_" + std::to_string(i) + "_" + std::to_string(k) + "_[cx_]";
+        em.line("double " + s0 + " = " + tile + "[0][" + col + "];");
+        em.line("for (int q_ = 1; q_ < " + std::to_string(cp.RT) + "; ++q_) " + s0 + " = " +
+                (sum ? s0 + " + " + tile + "[q_][" + col + "]" : "dmax(" + s0 + ", " + tile + "[q_][" + col + "])") + ";");
+        std::string e = "(float)" + s0;
+        if (g.node(r).shape.dtype == DType::F16) e = "rnd_f16(" + e + ")";
+        em.line(arr + " = " + e + ";");
+        v.lanes.push_back(arr);
+      }
+      em.close();
+      em.line("__syncthreads();");
     }
-    em.close();
-    em.line("__syncthreads();");
     em.reduced[Emitter::key(r, colc)] = v;
   }
-  em.open("if (ry_ == 0 && col_ok)");
+  if (cta_combine) em.open("if (ry_ == 0 && col_ok)");
   for (int o : b.outputs)
     if (g.node(o).shape.dims == to64(C)) store_val(em, g, o, colc, em.value(o, colc), "");
   em.close();
