@@ -1,6 +1,6 @@
 """Summarise an ncu report (read here, no GPU) into profiles/:
 
-    python tools/ncu_summary.py gpurun_out/prof.ncu-rep profiles/r01/<name>.json [graph=kernel ...]
+    python tools/ncu_summary.py gpurun_out/prof.ncu-rep profiles/r01/<name>.json [graph=kernel|graph=#idx ...]
 
 Writes the per-kernel metrics we cite (duration, DRAM bytes, DRAM throughput,
 registers, occupancy, issue activity, top stall reasons) and updates
@@ -71,8 +71,11 @@ def main():
     summ_path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     summ = json.load(open(summ_path)) if os.path.exists(summ_path) else {}
     for g, kname in graph_of.items():
-        for rec in res:
-            if rec["kernel"] == kname:
+        # "graph=<kernel name>" (first launch of that name) or "graph=#<launch index>"
+        cands = [res[int(kname[1:])]] if kname.startswith("#") else res
+        for rec in cands:
+            if rec["kernel"] == kname or kname.startswith("#"):
+                kname = rec["kernel"]
                 summ[g] = {"kernel": kname, "report": os.path.relpath(dest, ROOT),
                            "dram_bytes": int((rec.get("dram_read_MB", 0) + rec.get("dram_write_MB", 0)) * 1e6),
                            "duration_us_cold": rec.get("duration_us")}
