@@ -97,6 +97,15 @@ int stc_exec_source(const stc_exec* e, char** cuda_source);
  * every output, synchronise.  Buffers hold the tensor's dtype natively
  * (f32 / f16 bits / i32 / u8 bool), parameters and outputs in stc_graph_io order. */
 int stc_exec_run_host(stc_exec* e, const void* const* inputs, void* const* outputs);
+/* Pipelined host execution of a batch `nchunks` times larger than the
+ * executor's graph (build `e` from the chunk graph, e.g. batch 32/8):
+ * inputs[i] holds nchunks consecutive chunks when input_chunked[i] != 0
+ * (NULL = all chunked), else one tensor shared by every chunk; outputs[i]
+ * receives nchunks consecutive chunks.  H2D of chunk k+1, the plan's graph
+ * on chunk k and D2H of chunk k-1 overlap (separate copy-engine streams).
+ * Same result as nchunks calls of stc_exec_run_host on the slices. */
+int stc_exec_run_host_chunked(stc_exec* e, const void* const* inputs, void* const* outputs, int nchunks,
+                              const int* input_chunked);
 int stc_exec_upload(stc_exec* e, const void* const* inputs);
 /* async graph replay on `cuda_stream` using buffer set `set` (0 = the
  * uploaded buffers; see stc_exec_prepare_sets).  NULL selects the executor's

@@ -24,19 +24,6 @@ gpu::ExecMode mode_of(int mode) {
   }
 }
 
-std::string specs_json(const std::vector<gpu::KernelSpec>& specs) {
-  std::ostringstream o;
-  o << "[";
-  for (size_t i = 0; i < specs.size(); ++i) {
-    const auto& k = specs[i];
-    o << (i ? "," : "") << "{\"name\":\"" << k.name << "\",\"template\":\"" << k.tmpl << "\",\"pattern\":\""
-      << k.pattern_key << "\",\"grid\":" << k.grid << ",\"block\":" << k.block << ",\"smem\":" << k.smem
-      << ",\"cooperative\":" << (k.cooperative ? "true" : "false") << ",\"bytes\":" << k.alg_bytes << "}";
-  }
-  o << "]";
-  return o.str();
-}
-
 }  // namespace
 
 extern "C" {
@@ -45,7 +32,7 @@ int stc_codegen(const stc_plan* p, int mode, char** cuda_source, char** kernels_
   return guarded([&] {
     auto pk = gpu::generate_plan_kernels(p->graph, p->plan, p->kernels, p->models.machine, mode_of(mode));
     if (cuda_source) *cuda_source = dup_string(pk.source);
-    if (kernels_json) *kernels_json = dup_string(specs_json(pk.specs));
+    if (kernels_json) *kernels_json = dup_string(gpu::describe_specs(pk.specs));
   });
 }
 
@@ -72,6 +59,11 @@ int stc_exec_source(const stc_exec* e, char** src) {
 
 int stc_exec_run_host(stc_exec* e, const void* const* inputs, void* const* outputs) {
   return guarded([&] { e->ex->run_host(inputs, outputs); });
+}
+
+int stc_exec_run_host_chunked(stc_exec* e, const void* const* inputs, void* const* outputs, int nchunks,
+                              const int* input_chunked) {
+  return guarded([&] { e->ex->run_host_chunked(inputs, outputs, nchunks, input_chunked); });
 }
 
 int stc_exec_upload(stc_exec* e, const void* const* inputs) {

@@ -35,6 +35,7 @@ Executor::Executor(const CompGraph& g, const FusionPlan& plan,
     : g_(g), use_graph_(use_graph) {
   dev_ = &device_init(device);
   if (const char* v = std::getenv("STITCH_PDL")) pdl_ = *v != '0';
+  if (const char* v = std::getenv("STITCH_DAG")) dag_ = *v != '0';
   STC_RT(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
   plan_launches(plan, kernels, model, mode);
   module_ = std::make_unique<Module>(compile_cubin(source_, default_nvrtc_options()));
@@ -52,7 +53,88 @@ Executor::Executor(const CompGraph& g, const FusionPlan& plan,
     }
     fns_.push_back(f);
   }
+  compute_deps();
   ensure_sets(1);
+}
+
+void Executor::compute_deps() {
+  std::map<std::string, int> producer;
+  deps_.assign(specs_.size(), {});
+  for (size_t i = 0; i < specs_.size(); ++i) {
+    std::set<int> d;
+    for (const auto& t : specs_[i].inputs)
+      if (auto it = producer.find(t); it != producer.end()) d.insert(it->second);
+    deps_[i].assign(d.begin(), d.end());
+    for (const auto& t : specs_[i].outputs) producer[t] = static_cast<int>(i);
+  }
+}
+
+int Executor::capture_plan(int set, cudaStream_t origin, int prev) {
+  const size_t n = specs_.size();
+  if (!dag_ || n <= 1) {
+    for (size_t i = 0; i < n; ++i) launch_kernel(i, set, origin, i ? static_cast<int>(i) - 1 : prev);
+    return n ? static_cast<int>(n) - 1 : prev;
+  }
+  // list scheduling in launch (topological) order: a kernel joins the stream
+  // whose tail is its latest producer, else a stream whose tail it already
+  // depends on transitively, else a fresh fork of `origin`
+  if (kernel_events_.size() < n) {
+    for (size_t i = kernel_events_.size(); i < n; ++i) {
+      cudaEvent_t e = nullptr;
+      STC_RT(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      kernel_events_.push_back(e);
+    }
+  }
+  if (!fork_event_) STC_RT(cudaEventCreateWithFlags(&fork_event_, cudaEventDisableTiming));
+  std::vector<std::vector<char>> anc(n, std::vector<char>(n, 0));  // anc[i][j]: j precedes i
+  for (size_t i = 0; i < n; ++i)
+    for (int d : deps_[i]) {
+      anc[i][static_cast<size_t>(d)] = 1;
+      for (size_t j = 0; j < n; ++j) anc[i][j] |= anc[static_cast<size_t>(d)][j];
+    }
+  struct Lane {
+    cudaStream_t s;
+    int tail;  // kernel of this replay last launched on the lane (-1: none yet)
+  };
+  std::vector<Lane> lanes{{origin, -1}};
+  STC_RT(cudaEventRecord(fork_event_, origin));
+  const size_t max_lanes = 8;
+  for (size_t i = 0; i < n; ++i) {
+    int best = -1;
+    for (size_t l = 0; l < lanes.size(); ++l) {  // the latest producer at a lane's tail
+      const int t = lanes[l].tail;
+      if (t >= 0 && std::count(deps_[i].begin(), deps_[i].end(), t) && (best < 0 || t > lanes[static_cast<size_t>(best)].tail))
+        best = static_cast<int>(l);
+    }
+    for (size_t l = 0; l < lanes.size() && best < 0; ++l) {  // a lane already ordered before us
+      const int t = lanes[l].tail;
+      if (t < 0 || anc[i][static_cast<size_t>(t)]) best = static_cast<int>(l);
+    }
+    if (best < 0 && lanes.size() < max_lanes) {
+      while (aux_streams_.size() < lanes.size()) {
+        cudaStream_t s2 = nullptr;
+        STC_RT(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+        aux_streams_.push_back(s2);
+      }
+      cudaStream_t s2 = aux_streams_[lanes.size() - 1];
+      STC_RT(cudaStreamWaitEvent(s2, fork_event_, 0));
+      lanes.push_back({s2, -1});
+      best = static_cast<int>(lanes.size()) - 1;
+    }
+    if (best < 0) best = 0;  // lane cap reached: serialise on origin
+    Lane& ln = lanes[static_cast<size_t>(best)];
+    for (int d : deps_[i]) {  // producers not already ordered before the lane's tail
+      if (ln.tail >= 0 && (d == ln.tail || anc[static_cast<size_t>(ln.tail)][static_cast<size_t>(d)])) continue;
+      STC_RT(cudaStreamWaitEvent(ln.s, kernel_events_[static_cast<size_t>(d)], 0));
+    }
+    const int after = ln.tail >= 0 ? ln.tail : (best == 0 ? prev : -1);
+    launch_kernel(i, set, ln.s, after);
+    STC_RT(cudaEventRecord(kernel_events_[i], ln.s));
+    ln.tail = static_cast<int>(i);
+  }
+  for (size_t l = 1; l < lanes.size(); ++l)  // join every fork back into origin
+    STC_RT(cudaStreamWaitEvent(origin, kernel_events_[static_cast<size_t>(lanes[l].tail)], 0));
+  return lanes.size() > 1 ? -1 : lanes[0].tail;  // after a join, no PDL edge into the next replay
 }
 
 Executor::~Executor() {
@@ -64,6 +146,13 @@ Executor::~Executor() {
   for (auto& set : scratch_)
     for (void* p : set)
       if (p) cudaFree(p);
+  for (auto e : kernel_events_) cudaEventDestroy(e);
+  if (fork_event_) cudaEventDestroy(fork_event_);
+  for (auto s : aux_streams_) cudaStreamDestroy(s);
+  for (auto* v : {&ev_in_, &ev_comp_, &ev_out_})
+    for (auto e : *v) cudaEventDestroy(e);
+  if (h2d_) cudaStreamDestroy(h2d_);
+  if (d2h_) cudaStreamDestroy(d2h_);
   if (stream_) cudaStreamDestroy(stream_);
 }
 
@@ -292,7 +381,7 @@ void Executor::build_graph(int set) {
     STC_RT(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
     bool failed = false;
     try {
-      for (size_t i = 0; i < specs_.size(); ++i) launch_kernel(i, set, stream_);
+      capture_plan(set, stream_, -1);
     } catch (const std::exception&) {
       failed = true;
     }
@@ -351,6 +440,53 @@ void Executor::run_host(const void* const* in, void* const* out) {
   sync();
 }
 
+void Executor::run_host_chunked(const void* const* in, void* const* out, int nchunks, const int* in_chunked) {
+  if (nchunks < 1) throw std::runtime_error("[exec] nchunks must be >= 1");
+  const int S = std::min(nchunks, 3);
+  ensure_sets(S);
+  if (use_graph_)
+    for (int s = 0; s < S; ++s) build_graph(s);
+  if (!h2d_) {
+    STC_RT(cudaStreamCreateWithFlags(&h2d_, cudaStreamNonBlocking));
+    STC_RT(cudaStreamCreateWithFlags(&d2h_, cudaStreamNonBlocking));
+  }
+  for (auto* v : {&ev_in_, &ev_comp_, &ev_out_})
+    while (static_cast<int>(v->size()) < S) {
+      cudaEvent_t e = nullptr;
+      STC_RT(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      v->push_back(e);
+    }
+  // the previous call's work on these streams is complete (we synchronise at
+  // the end), so the first use of every set needs no extra ordering
+  for (int k = 0; k < nchunks; ++k) {
+    const int s = k % S;
+    const size_t su = static_cast<size_t>(s);
+    if (k >= S) STC_RT(cudaStreamWaitEvent(h2d_, ev_comp_[su], 0));  // chunk k-S done reading set s
+    for (size_t i = 0; i < params_.size(); ++i) {
+      const Tensor& t = tensors_.at(g_.node(params_[i]).name);
+      const bool chunked = in_chunked ? in_chunked[i] != 0 : true;
+      if (!chunked && k >= S) continue;  // shared input: once per set
+      const char* src = static_cast<const char*>(in[i]) + (chunked ? static_cast<size_t>(k) * t.bytes : 0);
+      STC_RT(cudaMemcpyAsync(t.dptr[su], src, t.bytes, cudaMemcpyHostToDevice, h2d_));
+    }
+    STC_RT(cudaEventRecord(ev_in_[su], h2d_));
+    STC_RT(cudaStreamWaitEvent(stream_, ev_in_[su], 0));
+    if (k >= S) STC_RT(cudaStreamWaitEvent(stream_, ev_out_[su], 0));  // chunk k-S outputs drained
+    launch(stream_, s);
+    STC_RT(cudaEventRecord(ev_comp_[su], stream_));
+    STC_RT(cudaStreamWaitEvent(d2h_, ev_comp_[su], 0));
+    for (size_t i = 0; i < g_.outputs.size(); ++i) {
+      const Tensor& t = tensors_.at(g_.node(g_.outputs[i]).name);
+      STC_RT(cudaMemcpyAsync(static_cast<char*>(out[i]) + static_cast<size_t>(k) * t.bytes, t.dptr[su], t.bytes,
+                             cudaMemcpyDeviceToHost, d2h_));
+    }
+    STC_RT(cudaEventRecord(ev_out_[su], d2h_));
+  }
+  STC_RT(cudaStreamSynchronize(d2h_));
+  STC_RT(cudaStreamSynchronize(stream_));
+  STC_RT(cudaStreamSynchronize(h2d_));
+}
+
 void Executor::prepare_sets(int sets) {
   sets = std::max(1, sets);
   ensure_sets(sets);
@@ -375,9 +511,9 @@ int Executor::prepare_batches(int sets, int batch) {
   for (int b = 0; b < sets / batch; ++b) {
     cudaGraph_t graph = nullptr;
     STC_RT(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
-    for (int t = 0; t < batch; ++t)
-      for (size_t i = 0; i < specs_.size(); ++i)  // PDL also across consecutive (independent) steps
-        launch_kernel(i, b * batch + t, stream_, i > 0 ? static_cast<int>(i) - 1 : (t > 0 ? static_cast<int>(specs_.size()) - 1 : -1));
+    int tail = -1;
+    for (int t = 0; t < batch; ++t)  // PDL also across consecutive (independent) steps
+      tail = capture_plan(b * batch + t, stream_, tail);
     STC_RT(cudaStreamEndCapture(stream_, &graph));
     cudaGraphExec_t ge = nullptr;
     STC_RT(cudaGraphInstantiate(&ge, graph, 0));
@@ -451,11 +587,11 @@ double Executor::time(int iters, int warmup, int sets, std::vector<double>* per_
   return us;
 }
 
-std::string Executor::describe_json() const {
+std::string describe_specs(const std::vector<KernelSpec>& specs) {
   std::ostringstream o;
   o << "[";
-  for (size_t i = 0; i < specs_.size(); ++i) {
-    const auto& k = specs_[i];
+  for (size_t i = 0; i < specs.size(); ++i) {
+    const auto& k = specs[i];
     o << (i ? "," : "") << "{\"name\":\"" << k.name << "\",\"template\":\"" << json_escape(k.tmpl)
       << "\",\"pattern\":\"" << k.pattern_key << "\",\"grid\":" << k.grid << ",\"block\":" << k.block
       << ",\"smem\":" << k.smem << ",\"cooperative\":" << (k.cooperative ? "true" : "false")
@@ -468,5 +604,7 @@ std::string Executor::describe_json() const {
   o << "]";
   return o.str();
 }
+
+std::string Executor::describe_json() const { return describe_specs(specs_); }
 
 }  // namespace stitch::gpu

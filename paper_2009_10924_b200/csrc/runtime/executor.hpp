@@ -37,6 +37,10 @@ PlanKernels generate_plan_kernels(const CompGraph& g, const FusionPlan& plan,
                                   const std::map<std::string, KernelPlan>& kernels,
                                   const MachineModel& model, ExecMode mode, int sm_count = 148);
 
+// JSON array of {name, template, pattern, grid, block, smem, cooperative,
+// bytes, inputs, outputs} per kernel (stc_exec_describe / stc_codegen)
+std::string describe_specs(const std::vector<KernelSpec>& specs);
+
 class Executor {
  public:
   Executor(const CompGraph& g, const FusionPlan& plan,
@@ -72,6 +76,13 @@ class Executor {
   void launch_batch(cudaStream_t s, int index);
   void sync();
   void run_host(const void* const* in, void* const* out);
+  // Host-buffer execution of a batch split into `nchunks` chunks of THIS
+  // executor's graph (the chunk graph): chunk k of a chunked input starts at
+  // byte k * tensor_bytes of its host buffer, unchunked inputs are shared by
+  // every chunk, every output is chunked.  H2D of chunk k+1, the plan on
+  // chunk k and D2H of chunk k-1 overlap on three streams (copy engines are
+  // per direction), through min(nchunks, 3) device buffer sets.
+  void run_host_chunked(const void* const* in, void* const* out, int nchunks, const int* in_chunked);
 
   // CUDA-event timing (see stc_exec_time in include/stitch_b200.h)
   double time(int iters, int warmup, int sets, std::vector<double>* per_kernel_us, int batch = 1);
@@ -86,6 +97,14 @@ class Executor {
   // (-1: none) -- decides whether programmatic dependent launch applies
   void launch_kernel(size_t i, int set, cudaStream_t s, int after_kernel = -2);
   void build_graph(int set);
+  // Capture one plan replay into `origin` (which must be capturing) as a DAG:
+  // kernels whose inputs do not depend on each other go to different streams
+  // (fork/join through events), a kernel that follows its producer on the
+  // same stream keeps programmatic dependent launch.  `prev` = kernel that
+  // ran last on `origin` before this replay (-1: none), for PDL across steps.
+  // Returns the kernel left at the tail of `origin`.
+  int capture_plan(int set, cudaStream_t origin, int prev);
+  void compute_deps();
 
   CompGraph g_;
   const DeviceInfo* dev_ = nullptr;
@@ -104,6 +123,13 @@ class Executor {
   int batch_ = 0;
   bool coop_in_graph_ = true;
   bool pdl_ = true;  // STITCH_PDL=0 disables programmatic dependent launch
+  bool dag_ = true;  // STITCH_DAG=0 captures the plan as one linear chain
+  std::vector<std::vector<int>> deps_;       // [kernel] -> producer kernels
+  std::vector<cudaStream_t> aux_streams_;    // fork targets for independent kernels
+  std::vector<cudaEvent_t> kernel_events_;   // [kernel] done-event (capture only)
+  cudaEvent_t fork_event_ = nullptr;
+  cudaStream_t h2d_ = nullptr, d2h_ = nullptr;   // chunked host runs
+  std::vector<cudaEvent_t> ev_in_, ev_comp_, ev_out_;
 };
 
 }  // namespace stitch::gpu

@@ -74,6 +74,7 @@ def lib():
         "stc_exec_num_kernels": (ip, [vp]), "stc_exec_describe": (ip, [vp, P(vp)]),
         "stc_exec_source": (ip, [vp, P(vp)]),
         "stc_exec_run_host": (ip, [vp, P(vp), P(vp)]), "stc_exec_upload": (ip, [vp, P(vp)]),
+        "stc_exec_run_host_chunked": (ip, [vp, P(vp), P(vp), ip, P(ip)]),
         "stc_exec_launch": (ip, [vp, vp, ip]), "stc_exec_prepare_sets": (ip, [vp, ip]),
         "stc_exec_download": (ip, [vp, P(vp)]),
         "stc_exec_sync": (ip, [vp]),
@@ -356,6 +357,42 @@ class Executor:
         if getattr(self, "_h", None) and _lib is not None:
             _lib.stc_exec_destroy(self._h)
             self._h = None
+
+
+class ChunkedExecutor:
+    """Host-buffer execution of a batch-sharded graph as `nchunks` pipelined
+    chunks: the chunk graph (batch / nchunks, re-planned by the bit-exact
+    planner for its own shape) runs on device while the next chunk's H2D and
+    the previous chunk's D2H are in flight (stc_exec_run_host_chunked).
+    `rule` is a shard.ShardRule whose sharded axis is 0 for every chunked tensor."""
+
+    def __init__(self, text: str, rule, nchunks: int, cfg: str = "b200", device: int = 0):
+        self.rule, self.nchunks = rule, nchunks
+        self.full = Graph(text)
+        self.chunk_graph = Graph(rule.graph_text(text, nchunks))
+        self.ex = Executor(Plan(self.chunk_graph, cfg), device=device)
+        for t in self.full.params:
+            if rule.axis_of.get(t.name) not in (None, 0):
+                raise StitchError(4, "input %s is not sharded along axis 0" % t.name)
+        for t in self.full.outputs:
+            if rule.axis_of.get(t.name) != 0:
+                raise StitchError(4, "output %s is not sharded along axis 0" % t.name)
+        self._flags = (ctypes.c_int * max(1, len(self.full.params)))(
+            *[1 if t.name in rule.axis_of else 0 for t in self.full.params])
+
+    def run(self, inputs: Dict[str, np.ndarray], out: Optional[Dict[str, np.ndarray]] = None):
+        keep = [np.ascontiguousarray(inputs[t.name], dtype=t.np_dtype) for t in self.full.params]
+        for a, t in zip(keep, self.full.params):
+            if a.size != t.count:
+                raise StitchError(4, "input %s has %d elements, expected %d" % (t.name, a.size, t.count))
+        ip = (ctypes.c_void_p * max(1, len(keep)))(*[a.ctypes.data for a in keep])
+        outs = [out[t.name] if out is not None else np.empty(t.dims, dtype=t.np_dtype) for t in self.full.outputs]
+        for o, t in zip(outs, self.full.outputs):
+            if not (o.flags.c_contiguous and o.dtype == t.np_dtype and o.size == t.count):
+                raise StitchError(4, "bad output buffer for " + t.name)
+        op = (ctypes.c_void_p * max(1, len(outs)))(*[o.ctypes.data for o in outs])
+        _check(lib().stc_exec_run_host_chunked(self.ex._h, ip, op, self.nchunks, self._flags))
+        return {t.name: o for t, o in zip(self.full.outputs, outs)}
 
 
 def run_pipeline(graph_path: str, device_config: Optional[str] = None, k: int = 3, beam_width: int = 3,
