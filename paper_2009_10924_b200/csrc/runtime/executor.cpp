@@ -1,6 +1,7 @@
 #include "runtime/executor.hpp"
 
 #include <algorithm>
+#include <cstdio>
 #include <cctype>
 #include <cstdlib>
 #include <cstring>
@@ -456,12 +457,23 @@ void Executor::run_host_chunked(const void* const* in, void* const* out, int nch
       STC_RT(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
       v->push_back(e);
     }
+  // STITCH_CHUNK_TRACE=1: per-chunk timestamps (us since the first H2D) on stderr
+  const bool trace = std::getenv("STITCH_CHUNK_TRACE") && *std::getenv("STITCH_CHUNK_TRACE") == '1';
+  std::vector<cudaEvent_t> tev;
+  auto stamp = [&](cudaStream_t st) {
+    if (!trace) return;
+    cudaEvent_t e = nullptr;
+    STC_RT(cudaEventCreate(&e));
+    STC_RT(cudaEventRecord(e, st));
+    tev.push_back(e);
+  };
   // the previous call's work on these streams is complete (we synchronise at
   // the end), so the first use of every set needs no extra ordering
   for (int k = 0; k < nchunks; ++k) {
     const int s = k % S;
     const size_t su = static_cast<size_t>(s);
     if (k >= S) STC_RT(cudaStreamWaitEvent(h2d_, ev_comp_[su], 0));  // chunk k-S done reading set s
+    stamp(h2d_);
     for (size_t i = 0; i < params_.size(); ++i) {
       const Tensor& t = tensors_.at(g_.node(params_[i]).name);
       const bool chunked = in_chunked ? in_chunked[i] != 0 : true;
@@ -470,10 +482,12 @@ void Executor::run_host_chunked(const void* const* in, void* const* out, int nch
       STC_RT(cudaMemcpyAsync(t.dptr[su], src, t.bytes, cudaMemcpyHostToDevice, h2d_));
     }
     STC_RT(cudaEventRecord(ev_in_[su], h2d_));
+    stamp(h2d_);
     STC_RT(cudaStreamWaitEvent(stream_, ev_in_[su], 0));
     if (k >= S) STC_RT(cudaStreamWaitEvent(stream_, ev_out_[su], 0));  // chunk k-S outputs drained
     launch(stream_, s);
     STC_RT(cudaEventRecord(ev_comp_[su], stream_));
+    stamp(stream_);
     STC_RT(cudaStreamWaitEvent(d2h_, ev_comp_[su], 0));
     for (size_t i = 0; i < g_.outputs.size(); ++i) {
       const Tensor& t = tensors_.at(g_.node(g_.outputs[i]).name);
@@ -481,10 +495,22 @@ void Executor::run_host_chunked(const void* const* in, void* const* out, int nch
                              cudaMemcpyDeviceToHost, d2h_));
     }
     STC_RT(cudaEventRecord(ev_out_[su], d2h_));
+    stamp(d2h_);
   }
   STC_RT(cudaStreamSynchronize(d2h_));
   STC_RT(cudaStreamSynchronize(stream_));
   STC_RT(cudaStreamSynchronize(h2d_));
+  if (trace) {
+    std::ostringstream o;
+    o << "[chunk-trace] h2d_start h2d_end comp_end d2h_end (us)";
+    for (size_t i = 0; i < tev.size(); ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, tev[0], tev[i]);
+      o << (i % 4 ? " " : "\n  ") << static_cast<int>(ms * 1000.f);
+    }
+    std::fprintf(stderr, "%s\n", o.str().c_str());
+    for (auto e : tev) cudaEventDestroy(e);
+  }
 }
 
 void Executor::prepare_sets(int sets) {

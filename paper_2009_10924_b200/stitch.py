@@ -106,13 +106,15 @@ def _take(p: ctypes.c_void_p) -> str:
 
 
 def cfg_path(name: Optional[str]) -> str:
-    """'v100' / 'b200' / a path / None (-> $STITCH_DEVICE_CONFIG or built-in defaults)."""
+    """'v100' / 'b200' (B200 device shape) / 'b200cal' (+ recalibrated costs) / a path / None (-> $STITCH_DEVICE_CONFIG or built-in defaults)."""
     if not name:
         return ""
     if name in ("v100", "default"):
         return os.path.join(CONFIGS, "v100_default.cfg")
     if name == "b200":
         return os.path.join(CONFIGS, "b200_device.cfg")
+    if name == "b200cal":  # cost model recalibrated from B200 measurements
+        return os.path.join(CONFIGS, "b200.cfg")
     return name
 
 

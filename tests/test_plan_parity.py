@@ -72,3 +72,30 @@ def test_plan_kernel_infeasible_and_explicit_patterns():
     assert txt.startswith("stitched v1\n") and "reduce_" in txt
     plan = stitch.Plan(g, "v100", patterns=[[7, 8]])
     assert plan.num_patterns == 1 and plan.patterns() == [[7, 8]]
+
+
+def test_calibrated_cfg_parity_with_reference():
+    """the recalibrated B200 cost model (configs/b200.cfg, measured by
+    tools/calibrate_b200.py) uses only keys the reference loader accepts, so
+    the unmodified reference planner (oracle/_ref) plans with it too: plans
+    must stay byte-identical under the calibrated model"""
+    from oracle import ref
+    if not ref.available():
+        pytest.skip("oracle/_ref not built")
+    stitch = _stitch()
+    cfg = stitch.cfg_path("b200cal")
+    from tests.conftest import fixture_graphs
+    cases = dict(fixture_graphs())
+    for name in ("colreduce", "bert_gelu"):
+        cases[name] = graph_text(name)
+    with open(os.path.join(GOLD, "random_plans.json")) as f:
+        rnd = json.load(f)
+    for seed in sorted(rnd, key=int)[:15]:
+        cases["random%s" % seed] = rnd[seed]["graph"]
+    for name, text in cases.items():
+        want, progs, _ = ref.plan(text, cfg)
+        plan = stitch.Plan(stitch.Graph(text), "b200cal")
+        assert plan.json() == want, name
+        keys = [p["key"] for p in json.loads(want)["patterns"]]
+        for i, k in enumerate(keys):
+            assert plan.kernel_text(i) == progs[k], (name, k)
