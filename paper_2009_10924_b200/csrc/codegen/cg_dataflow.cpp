@@ -723,14 +723,16 @@ struct ColParams {
 };
 
 // CT column chunks x RT row lanes per 256-thread CTA; NCB column strips x RB
-// row slabs of CTAs, sized for ~2 CTAs per SM (each slab >= RT*U rows)
+// row slabs of CTAs, sized for ~3 CTAs per SM (each slab >= RT*U rows).
+// Narrow strips (CT 8 = 32 columns) keep the slab count per strip -- and so
+// the last CTA's combine -- short (B200 sweep: profiles/r01/colreduce_sweep.jsonl)
 ColParams col_params(const std::vector<int>& P, const std::vector<int>& C, int target_blocks) {
   ColParams p;
   p.ROWS = prod(P);
   p.COLS = prod(C);
   p.W = C.back() % 4 == 0 ? 4 : 1;
   p.NCH = p.COLS / p.W;
-  p.CT = static_cast<int>(pow2ceil(std::min<int64_t>(32, p.NCH)));
+  p.CT = static_cast<int>(pow2ceil(std::min<int64_t>(std::clamp(env_int("STITCH_COL_CT", 8), 1, 256), p.NCH)));
   p.RT = kBlock / p.CT;
   p.NCB = static_cast<int>((p.NCH + p.CT - 1) / p.CT);
   p.U = std::max(1, env_int("STITCH_COL_U", 8));
@@ -831,10 +833,6 @@ void emit_column(Emitter& em, const CompGraph& g, const Body& b, const ColParams
   // last-arriving CTA of this column strip combines the slabs in order
   const std::string last = em.fresh("last_");
   em.line("__shared__ unsigned " + last + ";");
-  if (env_int("STITCH_COL_COMBINE", 0) != 0)
-    for (size_t i = 0; i < nr; ++i)
-      for (int k = 0; k < cp.W; ++k)
-        em.line("__shared__ float red_" + std::to_string(i) + "_" + std::to_string(k) + "_[" + std::to_string(cp.CT) + "];");
   em.line("__threadfence();");
   em.line("__syncthreads();");
   em.line("if (threadIdx.x == 0) " + last + " = atomicAdd(bar_ + " + std::to_string(ctr_off) + " + cb_, 1u) == " +
@@ -842,53 +840,40 @@ void emit_column(Emitter& em, const CompGraph& g, const Body& b, const ColParams
   em.line("__syncthreads();");
   em.open("if (" + last + ")");
   em.line("__threadfence();");
-  const bool cta_combine = env_int("STITCH_COL_COMBINE", 0) != 0;
-  if (!cta_combine) em.open("if (ry_ == 0 && col_ok)");
-  for (size_t i = 0; i < nr; ++i) {
-    const int r = b.reductions[i];
-    const bool sum = g.node(r).kind == OpKind::ReduceSum;
-    Val v;
-    if (!cta_combine) {
-      // the strip's column threads fold the slabs in slab order
-      for (int k = 0; k < cp.W; ++k) {
-        const std::string s0 = em.fresh("s"), t = em.fresh("red"), k_ = std::to_string(k);
-        em.line("double " + s0 + " = __ldcg(&" + part(i, "0", k_) + ");");
-        em.line("for (int k_ = 1; k_ < " + sRB + "; ++k_) " + s0 + " = " +
-                (sum ? s0 + " + __ldcg(&" + part(i, "k_", k_) + ")" : "dmax(" + s0 + ", __ldcg(&" + part(i, "k_", k_) + "))") + ";");
-        std::string e = "(float)" + s0;
-        if (g.node(r).shape.dtype == DType::F16) e = "rnd_f16(" + e + ")";
-        em.line("const float " + t + " = " + e + ";");
-        v.lanes.push_back(t);
-      }
-    } else {
-      // the whole CTA: row lane ry_ folds slabs ry_, ry_+RT, ..., then the RT
-      // lane sums fold in smem in fixed order
-      for (int k = 0; k < cp.W; ++k) {
-        const std::string k_ = std::to_string(k), s0 = em.fresh("cs");
-        em.line("double " + s0 + " = " + (sum ? "0.0" : "__longlong_as_double(0xfff0000000000000ll)") + ";");
-        em.line("if (col_ok) for (int k_ = ry_; k_ < " + sRB + "; k_ += " + std::to_string(cp.RT) + ") " + s0 + " = " +
-                (sum ? s0 + " + __ldcg(&" + part(i, "k_", k_) + ")" : "dmax(" + s0 + ", __ldcg(&" + part(i, "k_", k_) + "))") + ";");
-        em.line(tile + "[ry_][cx_ * " + sW + " + " + k_ + "] = " + s0 + ";");
-      }
-      em.line("__syncthreads();");
-      em.open("if (ry_ == 0 && col_ok)");
-      for (int k = 0; k < cp.W; ++k) {
-        const std::string col = "cx_ * " + sW + " + " + std::to_string(k), s0 = em.fresh("s");
-        const std::string arr = "red_" + std::to_string(i) + "_" + std::to_string(k) + "_[cx_]";
-        em.line("double " + s0 + " = " + tile + "[0][" + col + "];");
-        em.line("for (int q_ = 1; q_ < " + std::to_string(cp.RT) + "; ++q_) " + s0 + " = " +
-                (sum ? s0 + " + " + tile + "[q_][" + col + "]" : "dmax(" + s0 + ", " + tile + "[q_][" + col + "])") + ";");
-        std::string e = "(float)" + s0;
-        if (g.node(r).shape.dtype == DType::F16) e = "rnd_f16(" + e + ")";
-        em.line(arr + " = " + e + ";");
-        v.lanes.push_back(arr);
-      }
-      em.close();
-      em.line("__syncthreads();");
+  const int64_t strip_cols = int64_t(cp.CT) * cp.W;
+  {
+    // every thread of the CTA folds one (reduction, column) pair of the strip
+    // over the slabs in slab order (loads independent, adds in fixed order:
+    // deterministic, same bits as a serial fold), then the strip's column
+    // threads read the folded values back from shared memory
+    const std::string cred = em.fresh("cred_");
+    em.line("__shared__ float " + cred + "[" + std::to_string(nr) + "][" + std::to_string(strip_cols) + "];");
+    em.open("for (int q_ = threadIdx.x; q_ < " + std::to_string(int64_t(nr) * strip_cols) + "; q_ += " +
+            std::to_string(kBlock) + ")");
+    em.line("const int ri_ = q_ / " + std::to_string(strip_cols) + ", cl_ = q_ % " + std::to_string(strip_cols) + ";");
+    em.line("const i64 col_ = (i64)cb_ * " + std::to_string(strip_cols) + " + cl_;");
+    em.line("if (col_ >= " + sCOLS + ") continue;");
+    for (size_t i = 0; i < nr; ++i) {
+      const int r = b.reductions[i];
+      const bool sum = g.node(r).kind == OpKind::ReduceSum;
+      const std::string base = "part_ + " + std::to_string(partial_off + static_cast<int64_t>(i) * cp.RB * cp.COLS) + " + col_";
+      std::string e = "(float)s_";
+      if (g.node(r).shape.dtype == DType::F16) e = "rnd_f16(" + e + ")";
+      em.line(std::string(i ? "else " : "") + "if (ri_ == " + std::to_string(i) + ") { const double* p_ = " + base +
+              "; double s_ = __ldcg(p_);\n" + em.ind + "  #pragma unroll 8\n" + em.ind + "  for (int k_ = 1; k_ < " + sRB +
+              "; ++k_) s_ = " + (sum ? "s_ + __ldcg(p_ + (i64)k_ * " + sCOLS + ")" : "dmax(s_, __ldcg(p_ + (i64)k_ * " + sCOLS + "))") +
+              ";\n" + em.ind + "  " + cred + "[" + std::to_string(i) + "][cl_] = " + e + "; }");
     }
-    em.reduced[Emitter::key(r, colc)] = v;
+    em.close();
+    em.line("__syncthreads();");
+    em.open("if (ry_ == 0 && col_ok)");
+    for (size_t i = 0; i < nr; ++i) {
+      Val v;
+      for (int k = 0; k < cp.W; ++k)
+        v.lanes.push_back(cred + "[" + std::to_string(i) + "][cx_ * " + sW + " + " + std::to_string(k) + "]");
+      em.reduced[Emitter::key(b.reductions[i], colc)] = v;
+    }
   }
-  if (cta_combine) em.open("if (ry_ == 0 && col_ok)");
   for (int o : b.outputs)
     if (g.node(o).shape.dims == to64(C)) store_val(em, g, o, colc, em.value(o, colc), "");
   em.close();
@@ -987,7 +972,7 @@ KernelSpec generate_pattern_kernel(const CompGraph& g, const std::vector<int>& v
     has_col = has_col || b.kind == Kind::Column;
     if (b.kind == Kind::Row) block = std::max(block, row_params(b.dims_b).block);
   }
-  const int per_sm = std::max(1, std::min(env_int("STITCH_COL_CTAS", 2), 2048 / block));
+  const int per_sm = std::max(1, std::min(env_int("STITCH_COL_CTAS", 3), 2048 / block));
 
   // CTA budget per body; scratch = [256 B reserved][strip arrival counters][f64 partials]
   int64_t part_words = 0, ctr_words = 64, dyn_smem = 0;

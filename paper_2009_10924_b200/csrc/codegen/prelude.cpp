@@ -32,14 +32,25 @@ __device__ __forceinline__ void stv(unsigned char* p, i64 i, float v) { p[i] = v
 // 128-bit streaming load that does not allocate in L1 (read-once data)
 __device__ __forceinline__ float4 ld4(const float* p) {
   float4 r;
+#ifdef STITCH_L2_256B
+  asm("ld.global.nc.L1::no_allocate.L2::256B.v4.f32 {%0,%1,%2,%3}, [%4];"
+      : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
+#else
   asm("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
       : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
+#endif
   return r;
 }
 // 128-bit load through L1 (data re-read by many threads, e.g. gamma/beta rows)
 __device__ __forceinline__ float4 ld4c(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
+// 128-bit streaming (evict-first) store: outputs are written once and not
+// re-read by this kernel (B200 A/B: profiles/r01/store_hint_sweep.jsonl)
 __device__ __forceinline__ void st4(float* p, float a, float b, float c, float d) {
+#ifndef STITCH_ST_WB
+  asm volatile("st.global.cs.v4.f32 [%0], {%1,%2,%3,%4};" :: "l"(p), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
+#else
   *reinterpret_cast<float4*>(p) = make_float4(a, b, c, d);
+#endif
 }
 
 // per-op rounding to the node dtype (src/sim.cpp:67-75 semantics)

@@ -88,7 +88,20 @@ std::vector<std::string> default_nvrtc_options() {
   // -fmad=false: no FMA contraction, so f32 + - * / match the reference's
   // "compute in f64, round to f32" bit for bit; IEEE div/sqrt are NVRTC's
   // defaults (no fast-math).
-  return {"-arch=sm_100a", "--std=c++17", "-fmad=false", "-lineinfo", "-default-device"};
+  std::vector<std::string> o{"-arch=sm_100a", "--std=c++17", "-fmad=false", "-lineinfo", "-default-device"};
+  // experiment knobs: STITCH_NVRTC_DEFINES="STITCH_L2_256B STITCH_ST_CS"
+  if (const char* d = std::getenv("STITCH_NVRTC_DEFINES")) {
+    std::string s(d), w;
+    for (size_t i = 0; i <= s.size(); ++i) {
+      if (i == s.size() || s[i] == ' ' || s[i] == ',' || s[i] == ':') {
+        if (!w.empty()) o.push_back("-D" + w);
+        w.clear();
+      } else {
+        w += s[i];
+      }
+    }
+  }
+  return o;
 }
 
 std::string compile_cubin(const std::string& source, const std::vector<std::string>& options,

@@ -1,0 +1,31 @@
+"""Sweep codegen knobs (env vars) for one graph: us per subgraph (batched
+graph replays, inputs rotated past L2), registers, grid.
+
+    python tools/sweep_env.py <graph> 'VAR=a,b VAR2=c,d' ...
+"""
+import itertools, json, math, os, subprocess, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+if os.environ.get("SWEEP_CHILD"):
+    from paper_2009_10924_b200 import stitch
+    name = sys.argv[1]
+    g = stitch.Graph.from_file(os.path.join(stitch.GRAPHS, name + ".graph"))
+    ex = stitch.Executor(stitch.Plan(g, os.environ.get("SWEEP_CFG", "b200")))
+    ex.upload(stitch.random_inputs(g, 1))
+    d = ex.describe()
+    per_set = sum(t.nbytes for t in g.params) + sum(t.nbytes for t in g.outputs)
+    sets = min(128, max(2, math.ceil(8 * 126 * 2**20 / per_set)))
+    us = ex.time_batched(steps=256, warmup=32, sets=sets, steps_per_graph=16)
+    print(json.dumps({"us": round(us, 3), "GBps": round(sum(k["bytes"] for k in d) / us / 1e3, 1),
+                      "grid": [k["grid"] for k in d], "block": [k["block"] for k in d]}))
+    sys.exit(0)
+name = sys.argv[1]
+axes = []
+for spec in sys.argv[2:]:
+    for part in spec.split():
+        k, vals = part.split("=")
+        axes.append([(k, v) for v in vals.split(",")])
+for combo in itertools.product(*axes) if axes else [()]:
+    env = dict(os.environ, SWEEP_CHILD="1", **dict(combo))
+    r = subprocess.run([sys.executable, __file__, name], env=env, capture_output=True, text=True)
+    line = r.stdout.strip().splitlines()[-1] if r.stdout.strip() else r.stderr.strip()[-300:]
+    print(json.dumps({"graph": name, "env": dict(combo)}), line, flush=True)
