@@ -77,6 +77,7 @@ class Emitter {
   std::ostringstream out;
   std::string ind = "  ";
   int W = 1;
+  int block = 256;                         // the kernel's CTA size (every body uses it)
   std::set<int> loaded;                    // external tensors read
   std::map<std::string, Val> reduced;      // (reduction vertex, coords) -> value
   std::set<int> cached_tensors;            // read through L1 (re-read broadcast sources)
@@ -481,16 +482,17 @@ void emit_local(Emitter& em, const CompGraph& g, const Body& b) {
   const int64_t N = prod(D);
   em.W = (!D.empty() && D.back() % 4 == 0) ? 4 : 1;
   const int64_t chunks = N / em.W;
-  const int U = chunks >= int64_t(kBlock) * kSmCount * 8 ? 4 : 2;
+  const int B = em.block;
+  const int U = chunks >= int64_t(B) * kSmCount * 8 ? 4 : 2;
   em.line("// local body: domain " + std::to_string(N) + " elements, vector " + std::to_string(em.W));
-  em.open("for (i64 c0_ = (i64)vbid * " + std::to_string(kBlock * U) + " + threadIdx.x; c0_ < " +
-          std::to_string(chunks) + "; c0_ += (i64)vgrid * " + std::to_string(kBlock * U) + ")");
+  em.open("for (i64 c0_ = (i64)vbid * " + std::to_string(B * U) + " + threadIdx.x; c0_ < " +
+          std::to_string(chunks) + "; c0_ += (i64)vgrid * " + std::to_string(B * U) + ")");
   std::vector<std::tuple<int, Coords, Val, std::string>> stores;
   for (int u = 0; u < U; ++u) {
     const std::string ok = em.fresh("ok"), cc = em.fresh("cc");
-    em.line("const bool " + ok + " = c0_ + " + std::to_string(u * kBlock) + " < " + std::to_string(chunks) + ";");
+    em.line("const bool " + ok + " = c0_ + " + std::to_string(u * B) + " < " + std::to_string(chunks) + ";");
     em.line("const " + em.ix() + " " + cc + " = (" + em.ix() + ")(" + ok + " ? c0_ + " +
-            std::to_string(u * kBlock) + " : " + std::to_string(chunks - 1) + ");");
+            std::to_string(u * B) + " : " + std::to_string(chunks - 1) + ");");
     Coords c;
     if (!D.empty()) {
       const std::string lin = em.W == 1 ? cc : cc + " * " + std::to_string(em.W);
@@ -519,7 +521,9 @@ struct StageCfg {
   int64_t bytes = 0;         // dynamic smem: barriers + stages * tensors * tile
 };
 
-RowParams row_params(const std::vector<int>& inner) {
+// block = 0: the team's natural CTA (max(256, TPR)); else the kernel's CTA
+// size, a multiple of TPR
+RowParams row_params(const std::vector<int>& inner, int block = 0) {
   const int64_t L = prod(inner);
   RowParams p;
   p.W = inner.back() % 4 == 0 ? 4 : (inner.back() % 2 == 0 ? 2 : 1);
@@ -530,7 +534,7 @@ RowParams row_params(const std::vector<int>& inner) {
   const int nj_target = std::max(1, env_int("STITCH_ROW_NJ", nch <= 64 ? 2 : 8));
   p.TPR = static_cast<int>(std::clamp<int64_t>(pow2ceil((nch + nj_target - 1) / nj_target), 1, 1024));
   p.NJ = static_cast<int>((nch + p.TPR - 1) / p.TPR);
-  p.block = std::max(kBlock, p.TPR);
+  p.block = block > 0 ? block : std::max(kBlock, p.TPR);
   p.RPB = p.block / p.TPR;
   return p;
 }
@@ -542,7 +546,7 @@ void emit_row(Emitter& em, const CompGraph& g, const std::set<int>& pat, const B
   const std::vector<int>& O = b.dims_a;
   const std::vector<int>& I = b.dims_b;
   const int64_t ROWS = prod(O), L = prod(I);
-  const RowParams rp = row_params(I);
+  const RowParams rp = row_params(I, em.block);
   em.W = rp.W;
   const int64_t nch = L / rp.W;
   const bool partial = nch % rp.TPR != 0;
@@ -726,14 +730,14 @@ struct ColParams {
 // row slabs of CTAs, sized for ~3 CTAs per SM (each slab >= RT*U rows).
 // Narrow strips (CT 8 = 32 columns) keep the slab count per strip -- and so
 // the last CTA's combine -- short (B200 sweep: profiles/r01/colreduce_sweep.jsonl)
-ColParams col_params(const std::vector<int>& P, const std::vector<int>& C, int target_blocks) {
+ColParams col_params(const std::vector<int>& P, const std::vector<int>& C, int target_blocks, int block) {
   ColParams p;
   p.ROWS = prod(P);
   p.COLS = prod(C);
   p.W = C.back() % 4 == 0 ? 4 : 1;
   p.NCH = p.COLS / p.W;
   p.CT = static_cast<int>(pow2ceil(std::min<int64_t>(std::clamp(env_int("STITCH_COL_CT", 8), 1, 256), p.NCH)));
-  p.RT = kBlock / p.CT;
+  p.RT = std::max(1, block / p.CT);
   p.NCB = static_cast<int>((p.NCH + p.CT - 1) / p.CT);
   p.U = std::max(1, env_int("STITCH_COL_U", 8));
   const int64_t max_rb = std::max<int64_t>(1, p.ROWS / (int64_t(p.RT) * p.U));
@@ -849,7 +853,7 @@ void emit_column(Emitter& em, const CompGraph& g, const Body& b, const ColParams
     const std::string cred = em.fresh("cred_");
     em.line("__shared__ float " + cred + "[" + std::to_string(nr) + "][" + std::to_string(strip_cols) + "];");
     em.open("for (int q_ = threadIdx.x; q_ < " + std::to_string(int64_t(nr) * strip_cols) + "; q_ += " +
-            std::to_string(kBlock) + ")");
+            std::to_string(em.block) + ")");
     em.line("const int ri_ = q_ / " + std::to_string(strip_cols) + ", cl_ = q_ % " + std::to_string(strip_cols) + ";");
     em.line("const i64 col_ = (i64)cb_ * " + std::to_string(strip_cols) + " + cl_;");
     em.line("if (col_ >= " + sCOLS + ") continue;");
@@ -966,12 +970,34 @@ KernelSpec generate_pattern_kernel(const CompGraph& g, const std::vector<int>& v
       if (!pat.count(s)) em.cached_tensors.insert(s);
     }
 
-  int block = kBlock;
+  // one CTA size for every body of the kernel: a multiple of every row team
+  int block = kBlock, max_tpr = 1;
   bool has_col = false;
   for (const auto& b : bodies) {
     has_col = has_col || b.kind == Kind::Column;
-    if (b.kind == Kind::Row) block = std::max(block, row_params(b.dims_b).block);
+    if (b.kind == Kind::Row) max_tpr = std::max(max_tpr, row_params(b.dims_b).TPR);
   }
+  block = std::max(block, max_tpr);
+  // long rows (a warp or more per row) run best as small CTAs of two row
+  // teams: many CTAs spread evenly over the 148 SMs (B200 sweep,
+  // profiles/r01/row_block_sweep.jsonl: LN 5.99 -> 5.77 us, residual+LN
+  // 8.26 -> 7.86 us); short rows keep 256-thread CTAs
+  if (max_tpr >= 32 && !has_col) block = std::min(1024, 2 * max_tpr);
+  if (const int want = env_int("STITCH_ROW_BLOCK", 0); want > 0) {
+    block = std::clamp((std::max(want, max_tpr) + max_tpr - 1) / max_tpr * max_tpr, 32, 1024);
+  } else if (want < 0 && bodies.size() == 1 && bodies[0].kind == Kind::Row) {
+    // balanced: the fewest CTAs per SM whose row share fits one CTA, so every
+    // SM gets the same number of rows (+-1)
+    const int64_t rows = prod(bodies[0].dims_a);
+    for (int64_t k = 1; k <= 32; ++k) {
+      const int64_t rpc = (rows + kSmCount * k - 1) / (kSmCount * k);
+      if (rpc * max_tpr <= 1024) {
+        block = static_cast<int>(std::max<int64_t>(32, rpc * max_tpr));
+        break;
+      }
+    }
+  }
+  em.block = block;
   const int per_sm = std::max(1, std::min(env_int("STITCH_COL_CTAS", 3), 2048 / block));
 
   // CTA budget per body; scratch = [256 B reserved][strip arrival counters][f64 partials]
@@ -985,11 +1011,11 @@ KernelSpec generate_pattern_kernel(const CompGraph& g, const std::vector<int>& v
       const int64_t N = prod(b.dims_a);
       const int w = (!b.dims_a.empty() && b.dims_a.back() % 4 == 0) ? 4 : 1;
       const int64_t chunks = N / w;
-      const int U = chunks >= int64_t(kBlock) * kSmCount * 8 ? 4 : 2;
-      b.blocks = static_cast<int>(std::clamp<int64_t>((chunks + int64_t(kBlock) * U - 1) / (int64_t(kBlock) * U), 1,
+      const int U = chunks >= int64_t(block) * kSmCount * 8 ? 4 : 2;
+      b.blocks = static_cast<int>(std::clamp<int64_t>((chunks + int64_t(block) * U - 1) / (int64_t(block) * U), 1,
                                                       int64_t(kSmCount) * 16));
     } else if (b.kind == Kind::Row) {
-      const RowParams rp = row_params(b.dims_b);
+      const RowParams rp = row_params(b.dims_b, block);
       const int64_t rows = prod(b.dims_a), L = prod(b.dims_b), ntiles = (rows + rp.RPB - 1) / rp.RPB;
       b.blocks = static_cast<int>(std::clamp<int64_t>(ntiles, 1, int64_t(kSmCount) * 16));
       // dry run: which inputs does the body read at its own (row, chunk) coordinates?
@@ -1024,7 +1050,7 @@ KernelSpec generate_pattern_kernel(const CompGraph& g, const std::vector<int>& v
         }
       }
     } else {
-      cps[i] = col_params(b.dims_a, b.dims_b, kSmCount * per_sm);
+      cps[i] = col_params(b.dims_a, b.dims_b, kSmCount * per_sm, block);
       b.blocks = cps[i].NCB * cps[i].RB;
       ctr_off[i] = ctr_words;
       ctr_words += cps[i].NCB;
