@@ -106,6 +106,12 @@ int stc_exec_run_host(stc_exec* e, const void* const* inputs, void* const* outpu
  * Same result as nchunks calls of stc_exec_run_host on the slices. */
 int stc_exec_run_host_chunked(stc_exec* e, const void* const* inputs, void* const* outputs, int nchunks,
                               const int* input_chunked);
+/* Zero-copy host execution: every input/output buffer must be pinned host
+ * memory mapped into the device address space (cudaHostAlloc, or any pinned
+ * allocation under UVA); the plan's kernels then read inputs and write
+ * outputs over PCIe directly, the transfer fused with the stitched compute.
+ * Fails (status != 0, nothing launched) for pageable buffers. */
+int stc_exec_run_host_zero_copy(stc_exec* e, const void* const* inputs, void* const* outputs);
 int stc_exec_upload(stc_exec* e, const void* const* inputs);
 /* async graph replay on `cuda_stream` using buffer set `set` (0 = the
  * uploaded buffers; see stc_exec_prepare_sets).  NULL selects the executor's

@@ -61,6 +61,13 @@ int stc_exec_run_host(stc_exec* e, const void* const* inputs, void* const* outpu
   return guarded([&] { e->ex->run_host(inputs, outputs); });
 }
 
+int stc_exec_run_host_zero_copy(stc_exec* e, const void* const* inputs, void* const* outputs) {
+  return guarded([&] {
+    if (!e->ex->run_host_zero_copy(inputs, outputs))
+      throw std::runtime_error("[exec] zero-copy run needs pinned, device-mapped host buffers for every input/output");
+  });
+}
+
 int stc_exec_run_host_chunked(stc_exec* e, const void* const* inputs, void* const* outputs, int nchunks,
                               const int* input_chunked) {
   return guarded([&] { e->ex->run_host_chunked(inputs, outputs, nchunks, input_chunked); });

@@ -1162,9 +1162,53 @@ KernelSpec generate_opaque_kernel(const CompGraph& g, int vertex, const std::str
   s << ") {\n  pdl_wait();\n";
   k.outputs.push_back(n.name);
   s << "  __shared__ double red_[" << block / 32 << "];\n  double acc = 0.0;\n";
-  for (int o : n.operands)  // an operand listed twice is counted twice, as upstream
-    s << "  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < " << g.node(o).shape.element_count()
-      << "; i += (i64)gridDim.x * blockDim.x) acc += (double)ldv(T_" << g.node(o).name << ", i);\n";
+  // an operand listed twice is counted twice, as upstream
+  if (single) {
+    // one CTA: issue every load of every operand first (128-bit where the
+    // tensor allows), then fold -- one memory round trip instead of a chain
+    int vi = 0;
+    std::vector<std::pair<std::string, int>> regs;  // (array, lanes per element)
+    for (int o : n.operands) {
+      const TensorShape& sh = g.node(o).shape;
+      const int64_t cnt = sh.element_count();
+      const bool vec = sh.dtype == DType::F32 && cnt % 4 == 0;
+      const int64_t units = vec ? cnt / 4 : cnt;
+      const int64_t K = (units + block - 1) / block;
+      const std::string a = "v" + std::to_string(vi++) + "_";
+      if (K > 8) {  // large operand: vectorised grid-stride loop
+        if (vec)
+          s << "  for (i64 i = threadIdx.x; i < " << units << "; i += " << block << ") { const float4 q = ld4(T_"
+            << g.node(o).name << " + 4 * i); acc += ((double)q.x + (double)q.y) + ((double)q.z + (double)q.w); }\n";
+        else
+          s << "  for (i64 i = threadIdx.x; i < " << units << "; i += " << block << ") acc += (double)ldv(T_"
+            << g.node(o).name << ", i);\n";
+        continue;
+      }
+      if (vec) {
+        s << "  float4 " << a << "[" << K << "];\n  #pragma unroll\n  for (int k = 0; k < " << K
+          << "; ++k) { const i64 i = threadIdx.x + (i64)k * " << block << "; " << a << "[k] = i < " << units
+          << " ? ld4(T_" << g.node(o).name << " + 4 * i) : make_float4(0.f, 0.f, 0.f, 0.f); }\n";
+        regs.push_back({a, 4});
+      } else {
+        s << "  float " << a << "[" << K << "];\n  #pragma unroll\n  for (int k = 0; k < " << K
+          << "; ++k) { const i64 i = threadIdx.x + (i64)k * " << block << "; " << a << "[k] = i < " << units
+          << " ? ldv(T_" << g.node(o).name << ", i) : 0.f; }\n";
+        regs.push_back({a, 1});
+      }
+    }
+    for (const auto& [a, lanes] : regs) {
+      s << "  #pragma unroll\n  for (int k = 0; k < (int)(sizeof(" << a << ") / sizeof(" << a << "[0])); ++k) ";
+      if (lanes == 4)
+        s << "acc += ((double)" << a << "[k].x + (double)" << a << "[k].y) + ((double)" << a << "[k].z + (double)" << a
+          << "[k].w);\n";
+      else
+        s << "acc += (double)" << a << "[k];\n";
+    }
+  } else {
+    for (int o : n.operands)
+      s << "  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < " << g.node(o).shape.element_count()
+        << "; i += (i64)gridDim.x * blockDim.x) acc += (double)ldv(T_" << g.node(o).name << ", i);\n";
+  }
   s << "  acc = bfly_sum(acc, 32);\n  if ((threadIdx.x & 31) == 0) red_[threadIdx.x >> 5] = acc;\n  __syncthreads();\n"
     << "  double tot = 0.0;\n  for (int w = 0; w < " << block / 32 << "; ++w) tot += red_[w];\n";
   if (!single)

@@ -37,6 +37,7 @@ Executor::Executor(const CompGraph& g, const FusionPlan& plan,
   dev_ = &device_init(device);
   if (const char* v = std::getenv("STITCH_PDL")) pdl_ = *v != '0';
   if (const char* v = std::getenv("STITCH_DAG")) dag_ = *v != '0';
+  if (const char* v = std::getenv("STITCH_PDL_EDGES")) pdl_edges_ = *v != '0';
   STC_RT(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
   plan_launches(plan, kernels, model, mode);
   module_ = std::make_unique<Module>(compile_cubin(source_, default_nvrtc_options()));
@@ -56,6 +57,41 @@ Executor::Executor(const CompGraph& g, const FusionPlan& plan,
   }
   compute_deps();
   ensure_sets(1);
+}
+
+void Executor::promote_edges(cudaGraph_t graph) {
+  if (!pdl_ || !pdl_edges_) return;
+  size_t n = 0;
+  STC_RT(cudaGraphGetEdges_v2(graph, nullptr, nullptr, nullptr, &n));
+  if (!n) return;
+  std::vector<cudaGraphNode_t> from(n), to(n);
+  std::vector<cudaGraphEdgeData> data(n);
+  STC_RT(cudaGraphGetEdges_v2(graph, from.data(), to.data(), data.data(), &n));
+  std::map<const void*, size_t> fn_index;
+  for (size_t i = 0; i < fns_.size(); ++i) fn_index[reinterpret_cast<const void*>(fns_[i])] = i;
+  auto plain_kernel = [&](cudaGraphNode_t node) {
+    cudaGraphNodeType t;
+    if (cudaGraphNodeGetType(node, &t) != cudaSuccess || t != cudaGraphNodeTypeKernel) return false;
+    cudaKernelNodeParams kp{};
+    if (cudaGraphKernelNodeGetParams(node, &kp) != cudaSuccess) return false;
+    auto it = fn_index.find(kp.func);
+    return it != fn_index.end() && !specs_[it->second].cooperative;
+  };
+  std::vector<cudaGraphNode_t> rf, rt;
+  std::vector<cudaGraphEdgeData> rd;
+  for (size_t e = 0; e < n; ++e)
+    if (data[e].type == cudaGraphDependencyTypeDefault && plain_kernel(from[e]) && plain_kernel(to[e])) {
+      rf.push_back(from[e]);
+      rt.push_back(to[e]);
+      rd.push_back(data[e]);
+    }
+  if (rf.empty()) return;
+  STC_RT(cudaGraphRemoveDependencies_v2(graph, rf.data(), rt.data(), rd.data(), rf.size()));
+  for (auto& d : rd) {
+    d.type = cudaGraphDependencyTypeProgrammatic;
+    d.from_port = cudaGraphKernelNodePortProgrammatic;
+  }
+  STC_RT(cudaGraphAddDependencies_v2(graph, rf.data(), rt.data(), rd.data(), rf.size()));
 }
 
 void Executor::compute_deps() {
@@ -336,12 +372,17 @@ void Executor::ensure_sets(int sets) {
   sets_ = sets;
 }
 
-void Executor::launch_kernel(size_t i, int set, cudaStream_t s, int after) {
+void Executor::launch_kernel(size_t i, int set, cudaStream_t s, int after, const std::map<std::string, void*>* bind) {
   if (after == -2) after = static_cast<int>(i) - 1;
   const KernelSpec& k = specs_[i];
   std::vector<void*> ptrs;
-  for (const auto& t : k.inputs) ptrs.push_back(tensors_.at(t).dptr[static_cast<size_t>(set)]);
-  for (const auto& t : k.outputs) ptrs.push_back(tensors_.at(t).dptr[static_cast<size_t>(set)]);
+  auto ptr_of = [&](const std::string& t) {
+    if (bind)
+      if (auto it = bind->find(t); it != bind->end()) return it->second;
+    return tensors_.at(t).dptr[static_cast<size_t>(set)];
+  };
+  for (const auto& t : k.inputs) ptrs.push_back(ptr_of(t));
+  for (const auto& t : k.outputs) ptrs.push_back(ptr_of(t));
   void* bar = nullptr;
   void* part = nullptr;
   if (k.scratch_bytes > 0) {
@@ -388,6 +429,7 @@ void Executor::build_graph(int set) {
     }
     const cudaError_t end = cudaStreamEndCapture(stream_, &graph);
     if (!failed && end == cudaSuccess) {
+      promote_edges(graph);
       STC_RT(cudaGraphInstantiate(&ge, graph, 0));
       cudaGraphDestroy(graph);
       return;
@@ -439,6 +481,36 @@ void Executor::run_host(const void* const* in, void* const* out) {
   launch(stream_, 0);
   download(out, 0);
   sync();
+}
+
+bool Executor::run_host_zero_copy(const void* const* in, void* const* out) {
+  std::map<std::string, void*> bind;
+  auto mapped = [&](const void* h, size_t bytes) -> void* {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, h) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    if (a.type != cudaMemoryTypeHost || !a.devicePointer) return nullptr;
+    (void)bytes;
+    return a.devicePointer;
+  };
+  for (size_t i = 0; i < params_.size(); ++i) {
+    const Tensor& t = tensors_.at(g_.node(params_[i]).name);
+    void* d = mapped(in[i], t.bytes);
+    if (!d) return false;
+    bind[t.name] = d;
+  }
+  for (size_t i = 0; i < g_.outputs.size(); ++i) {
+    const Tensor& t = tensors_.at(g_.node(g_.outputs[i]).name);
+    void* d = mapped(out[i], t.bytes);
+    if (!d) return false;
+    bind[t.name] = d;
+  }
+  ensure_sets(1);
+  for (size_t i = 0; i < specs_.size(); ++i) launch_kernel(i, 0, stream_, static_cast<int>(i) - 1, &bind);
+  STC_RT(cudaStreamSynchronize(stream_));
+  return true;
 }
 
 void Executor::run_host_chunked(const void* const* in, void* const* out, int nchunks, const int* in_chunked) {
@@ -541,6 +613,7 @@ int Executor::prepare_batches(int sets, int batch) {
     for (int t = 0; t < batch; ++t)  // PDL also across consecutive (independent) steps
       tail = capture_plan(b * batch + t, stream_, tail);
     STC_RT(cudaStreamEndCapture(stream_, &graph));
+    promote_edges(graph);
     cudaGraphExec_t ge = nullptr;
     STC_RT(cudaGraphInstantiate(&ge, graph, 0));
     cudaGraphDestroy(graph);

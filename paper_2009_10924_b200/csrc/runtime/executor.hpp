@@ -83,6 +83,13 @@ class Executor {
   // chunk k and D2H of chunk k-1 overlap on three streams (copy engines are
   // per direction), through min(nchunks, 3) device buffer sets.
   void run_host_chunked(const void* const* in, void* const* out, int nchunks, const int* in_chunked);
+  // Zero-copy host execution: when every parameter and output buffer is
+  // pinned host memory mapped into the device address space (cudaHostAlloc /
+  // torch pin_memory under UVA), the plan's kernels read their inputs and
+  // write their outputs over PCIe directly -- transfer fused with compute,
+  // reads and writes overlapping in one pass.  Returns false (nothing done)
+  // if some buffer is not device-accessible host memory.
+  bool run_host_zero_copy(const void* const* in, void* const* out);
 
   // CUDA-event timing (see stc_exec_time in include/stitch_b200.h)
   double time(int iters, int warmup, int sets, std::vector<double>* per_kernel_us, int batch = 1);
@@ -95,7 +102,8 @@ class Executor {
   void ensure_sets(int sets);
   // after_kernel: the kernel launched just before this one in the same stream
   // (-1: none) -- decides whether programmatic dependent launch applies
-  void launch_kernel(size_t i, int set, cudaStream_t s, int after_kernel = -2);
+  void launch_kernel(size_t i, int set, cudaStream_t s, int after_kernel = -2,
+                     const std::map<std::string, void*>* bind = nullptr);
   void build_graph(int set);
   // Capture one plan replay into `origin` (which must be capturing) as a DAG:
   // kernels whose inputs do not depend on each other go to different streams
@@ -105,6 +113,10 @@ class Executor {
   // Returns the kernel left at the tail of `origin`.
   int capture_plan(int set, cudaStream_t origin, int prev);
   void compute_deps();
+  // turn every kernel->kernel edge of a captured plan graph into a
+  // programmatic (PDL) edge: every kernel griddepcontrol.wait()s before its
+  // first read, so the dependent may launch while its producers drain
+  void promote_edges(cudaGraph_t graph);
 
   CompGraph g_;
   const DeviceInfo* dev_ = nullptr;
@@ -124,6 +136,7 @@ class Executor {
   bool coop_in_graph_ = true;
   bool pdl_ = true;  // STITCH_PDL=0 disables programmatic dependent launch
   bool dag_ = true;  // STITCH_DAG=0 captures the plan as one linear chain
+  bool pdl_edges_ = true;  // STITCH_PDL_EDGES=0 keeps cross-stream edges full
   std::vector<std::vector<int>> deps_;       // [kernel] -> producer kernels
   std::vector<cudaStream_t> aux_streams_;    // fork targets for independent kernels
   std::vector<cudaEvent_t> kernel_events_;   // [kernel] done-event (capture only)

@@ -75,6 +75,7 @@ def lib():
         "stc_exec_source": (ip, [vp, P(vp)]),
         "stc_exec_run_host": (ip, [vp, P(vp), P(vp)]), "stc_exec_upload": (ip, [vp, P(vp)]),
         "stc_exec_run_host_chunked": (ip, [vp, P(vp), P(vp), ip, P(ip)]),
+        "stc_exec_run_host_zero_copy": (ip, [vp, P(vp), P(vp)]),
         "stc_exec_launch": (ip, [vp, vp, ip]), "stc_exec_prepare_sets": (ip, [vp, ip]),
         "stc_exec_download": (ip, [vp, P(vp)]),
         "stc_exec_sync": (ip, [vp]),
@@ -307,6 +308,18 @@ class Executor:
                     raise StitchError(4, "bad output buffer for " + t.name)
             op = (ctypes.c_void_p * max(1, len(outs)))(*[o.ctypes.data for o in outs])
         _check(lib().stc_exec_run_host(self._h, ip, op))
+        return {t.name: o for t, o in zip(self.g.outputs, outs)}
+
+    def run_zero_copy(self, inputs: Dict[str, np.ndarray], out: Dict[str, np.ndarray]):
+        """pinned host inputs/outputs read and written by the kernels directly
+        over PCIe (stc_exec_run_host_zero_copy); every buffer must be pinned"""
+        keep, ip = self._in_ptrs(inputs)
+        outs = [out[t.name] for t in self.g.outputs]
+        for o, t in zip(outs, self.g.outputs):
+            if not (o.flags.c_contiguous and o.dtype == t.np_dtype and o.size == t.count):
+                raise StitchError(4, "bad output buffer for " + t.name)
+        op = (ctypes.c_void_p * max(1, len(outs)))(*[o.ctypes.data for o in outs])
+        _check(lib().stc_exec_run_host_zero_copy(self._h, ip, op))
         return {t.name: o for t, o in zip(self.g.outputs, outs)}
 
     def upload(self, inputs: Dict[str, np.ndarray]):
