@@ -117,6 +117,11 @@ def build_oracle():
     if not os.path.isdir("/root/reference/proj/src") or shutil.which("make") is None:
         return None
     _run(["make", "-s", "-C", os.path.join(ROOT, "oracle"), "-j8"])
+    # the reference's own unit tests + acceptance gate, compiled against our
+    # drop-in headers/library (tests/test_ref_unit.py runs them)
+    ref_unit = os.path.join(ROOT, "tests", "ref_unit")
+    _run([sys.executable, os.path.join(ref_unit, "prepare_data.py")])
+    _run(["make", "-s", "-C", ref_unit, "-j8"])
     return os.path.join(ROOT, "oracle", "_ref", "libstitch_ref.so")
 
 
