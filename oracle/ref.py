@@ -40,6 +40,8 @@ def lib():
         L.ref_time_eval.argtypes = [P(c), ctypes.c_int, ctypes.c_uint64, ctypes.c_int,
                                     P(ctypes.c_double)]
         L.ref_free.argtypes = [ctypes.c_void_p]
+        L.ref_run_pipeline.argtypes = [c, c, ctypes.c_int, ctypes.c_int, c, ctypes.c_int, ctypes.c_int,
+                                       ctypes.c_int, ctypes.c_uint64]
         _lib = L
     return _lib
 
@@ -117,3 +119,10 @@ def time_eval(shard_texts, seed: int = 1, reps: int = 3) -> float:
     best = ctypes.c_double()
     _check(lib().ref_time_eval(arr, len(shard_texts), seed, reps, ctypes.byref(best)))
     return best.value
+
+
+def run_pipeline(graph_path: str, cfg_path: str, out_dir: str, k: int = 3, beam: int = 3, emit_dot: bool = False,
+                 run_sim: bool = False, run_baseline: bool = False, seed: int = 0) -> int:
+    """the reference's run_pipeline (src/pipeline.cpp:110-224) -> return code"""
+    return lib().ref_run_pipeline(graph_path.encode(), (cfg_path or "").encode(), k, beam, out_dir.encode(),
+                                  int(emit_dot), int(run_sim), int(run_baseline), seed)

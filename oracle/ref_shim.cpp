@@ -14,6 +14,8 @@
 //   ref_random      random_inputs   (src/sim.cpp:630-659)
 //   ref_eval        eval_reference  (src/sim.cpp:231-250)
 //   ref_eval_plan   eval_plan       (src/sim.cpp:471-514)  (SIMT interpreter)
+//   ref_run_pipeline run_pipeline (src/pipeline.cpp:110-224): plan.json,
+//                   kernels/*.stitch, report.txt, graph.dot artifacts
 //   ref_time_eval   best-of-N wall time of eval_reference over K shard graphs
 //                   run concurrently on K host threads
 #include <chrono>
@@ -72,6 +74,21 @@ int guarded(F&& f) {
 extern "C" {
 
 const char* ref_last_error() { return g_err.c_str(); }
+
+int ref_run_pipeline(const char* graph_path, const char* cfg_path, int k, int beam, const char* out_dir,
+                     int emit_dot, int run_sim, int run_baseline, uint64_t seed) {
+  RunConfig c;
+  c.graph_path = graph_path;
+  c.device_config_path = cfg_path ? cfg_path : "";
+  c.k = k;
+  c.beam_width = beam;
+  c.output_dir = out_dir;
+  c.emit_dot = emit_dot != 0;
+  c.run_sim = run_sim != 0;
+  c.run_baseline = run_baseline != 0;
+  c.seed = seed;
+  return run_pipeline(c);
+}
 void ref_free(void* p) { std::free(p); }
 
 // plan.json exactly as run_pipeline writes it, plus every kernel's program
