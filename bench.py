@@ -156,10 +156,10 @@ def run_reference(args):
     print(json.dumps(line))
 
 
-def time_subgraph(stitch, name):
+def time_subgraph(stitch, name, gemm=False):
     g = stitch.Graph(read_graph(name))
     plan = stitch.Plan(g, "b200")
-    ex = stitch.Executor(plan)
+    ex = stitch.Executor(plan, gemm=gemm)
     ex.upload(stitch.random_inputs(g, 1))
     desc = ex.describe()
     per_set = sum(t.nbytes for t in g.params) + sum(t.nbytes for t in g.outputs)
@@ -309,6 +309,12 @@ def main():
                     subs[name] = time_subgraph(stitch, name)
                 except Exception as e:
                     subs[name] = {"error": str(e)[:300]}
+            # model mode (non-parity): BERT FFN layer with its GEMMs on cuBLASLt
+            # (TF32) between the stitched kernels, one CUDA Graph per layer
+            try:
+                subs["bert_layer_model_tf32"] = time_subgraph(stitch, "bert_layer", gemm=True)
+            except Exception as e:
+                subs["bert_layer_model_tf32"] = {"error": str(e)[:300]}
         result = {
             "metric": "stitched-subgraph HBM GB/s (algorithmic bytes / time)",
             "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,

@@ -82,7 +82,10 @@ enum {
   STC_EXEC_STITCHED = 0, /* dataflow templates (local/regional/global/independent) */
   STC_EXEC_PROGRAM = 1,  /* translate each planned abstract program statement for statement */
   STC_EXEC_UNFUSED = 2,  /* one kernel per op: eval_reference semantics on the GPU */
-  STC_EXEC_NO_GRAPH = 8  /* flag: plain stream launches instead of a CUDA Graph */
+  STC_EXEC_NO_GRAPH = 8, /* flag: plain stream launches instead of a CUDA Graph */
+  STC_EXEC_GEMM = 16     /* flag (model mode, non-parity): opaque_compute ops shaped like a matmul
+                            A[..,M,K].B[K,N] run as cuBLASLt GEMMs (TF32 tensor cores; STITCH_GEMM_FP32=1
+                            for full f32) instead of the reference's mean-of-operands placeholder */
 };
 /* code generation only (no device needed): the plan's CUDA module source and
  * a JSON description of its kernels */

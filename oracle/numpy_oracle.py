@@ -275,15 +275,28 @@ def eval_node(n: Node, ops, g: Graph):
     raise ValueError("no evaluation rule for " + k)
 
 
-def eval_reference(g: Graph, inputs: dict) -> dict:
-    """inputs: name -> float64 array (dtype-rounded).  Returns outputs by name."""
+def eval_reference(g: Graph, inputs: dict, opaque=None) -> dict:
+    """inputs: name -> float64 array (dtype-rounded).  Returns outputs by name.
+    `opaque(node, operand_values)` may replace the placeholder semantics of
+    opaque_compute (model-mode checks; None -> the reference's mean)."""
     vals = {}
     for n in g.nodes:  # parsed graphs are topologically ordered by id
         if n.kind == "parameter":
             vals[n.id] = np.asarray(inputs[n.name], dtype=np.float64).reshape(n.dims)
             continue
-        vals[n.id] = eval_node(n, [vals[o] for o in n.operands], g)
+        ops = [vals[o] for o in n.operands]
+        r = opaque(n, ops) if (opaque is not None and n.kind == "opaque_compute") else None
+        vals[n.id] = r if r is not None else eval_node(n, ops, g)
     return {g.nodes[o].name: vals[o] for o in g.outputs}
+
+
+def matmul_opaque(n: Node, ops):
+    """model-mode semantics of a matmul-shaped opaque_compute (A[..,M,K] .
+    B[K,N] -> [..,M,N]): the f64 product rounded to the node dtype; None for
+    any other opaque op (keeps the placeholder)"""
+    if len(ops) != 2 or ops[1].ndim != 2 or ops[0].ndim < 2 or ops[0].shape[-1] != ops[1].shape[0]:
+        return None
+    return round_to_dtype(ops[0] @ ops[1], n.dtype)
 
 
 def _splitmix(seed, start, count):

@@ -52,7 +52,7 @@ NVCCFLAGS = ["-std=c++17", "-O3", ARCH, "-lineinfo", "-Xcompiler", "-fPIC",
 # std:: types cross the boundary; -Bsymbolic keeps our own symbols bound locally.
 LDFLAGS = ["-shared", "-Wl,-Bsymbolic", "-L" + os.path.join(CUDA, "lib64"),
            "-Wl,-rpath," + os.path.join(CUDA, "lib64"),
-           "-lnvrtc", "-lcudart", "-lpthread", "-ldl"]
+           "-lnvrtc", "-lcudart", "-lcublasLt", "-lpthread", "-ldl"]
 
 
 def _stale(src, obj, extra=()):

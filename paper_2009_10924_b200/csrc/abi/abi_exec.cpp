@@ -30,7 +30,8 @@ extern "C" {
 
 int stc_codegen(const stc_plan* p, int mode, char** cuda_source, char** kernels_json) {
   return guarded([&] {
-    auto pk = gpu::generate_plan_kernels(p->graph, p->plan, p->kernels, p->models.machine, mode_of(mode));
+    auto pk = gpu::generate_plan_kernels(p->graph, p->plan, p->kernels, p->models.machine, mode_of(mode), 148,
+                                         (mode & STC_EXEC_GEMM) != 0);
     if (cuda_source) *cuda_source = dup_string(pk.source);
     if (kernels_json) *kernels_json = dup_string(gpu::describe_specs(pk.specs));
   });
@@ -40,7 +41,8 @@ int stc_exec_create(const stc_plan* p, int device, int mode, stc_exec** out) {
   return guarded([&] {
     auto e = std::make_unique<stc_exec>();
     e->ex = std::make_unique<gpu::Executor>(p->graph, p->plan, p->kernels, p->models.machine, device,
-                                            mode_of(mode), (mode & STC_EXEC_NO_GRAPH) == 0);
+                                            mode_of(mode), (mode & STC_EXEC_NO_GRAPH) == 0,
+                                            (mode & STC_EXEC_GEMM) != 0);
     *out = e.release();
   });
 }

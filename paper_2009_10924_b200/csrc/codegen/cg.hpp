@@ -46,6 +46,10 @@ struct KernelSpec {
   int64_t scratch_bytes = 0;         // trailing (bar_, part_) params when > 0 (zeroed once)
   int64_t scratch_header = 256;      // part_ = scratch + scratch_header
   int64_t alg_bytes = 0;             // algorithmic bytes: unique inputs read once + outputs written once
+  // library GEMM launch unit (model mode: an opaque_compute that is a
+  // matmul C[M,N] = A[M,K] . B[K,N] runs as cuBLASLt; no generated source)
+  bool is_gemm = false;
+  int64_t gemm_m = 0, gemm_n = 0, gemm_k = 0;
 };
 
 // Thrown when a dataflow template cannot express a component; the caller

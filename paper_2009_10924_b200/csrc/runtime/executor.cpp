@@ -1,5 +1,7 @@
 #include "runtime/executor.hpp"
 
+#include <cublasLt.h>
+
 #include <algorithm>
 #include <cstdio>
 #include <cctype>
@@ -30,18 +32,100 @@ std::string json_escape(const std::string& s) {
 
 }  // namespace
 
+// cuBLASLt state for the plan's GEMM units (model mode)
+struct Executor::GemmState {
+  cublasLtHandle_t lt = nullptr;
+  void* workspace = nullptr;
+  size_t ws_bytes = size_t(32) << 20;
+  struct Unit {
+    cublasLtMatmulDesc_t op = nullptr;
+    cublasLtMatrixLayout_t a = nullptr, b = nullptr, c = nullptr;
+    cublasLtMatmulAlgo_t algo{};
+  };
+  std::map<size_t, Unit> units;
+  ~GemmState() {
+    for (auto& [i, u] : units) {
+      if (u.op) cublasLtMatmulDescDestroy(u.op);
+      if (u.a) cublasLtMatrixLayoutDestroy(u.a);
+      if (u.b) cublasLtMatrixLayoutDestroy(u.b);
+      if (u.c) cublasLtMatrixLayoutDestroy(u.c);
+    }
+    if (workspace) cudaFree(workspace);
+    if (lt) cublasLtDestroy(lt);
+  }
+};
+
+#define STC_LT(x)                                                                          \
+  do {                                                                                     \
+    cublasStatus_t st_ = (x);                                                              \
+    if (st_ != CUBLAS_STATUS_SUCCESS)                                                      \
+      throw std::runtime_error(std::string("[cublasLt] ") + #x + " failed: status " + std::to_string(int(st_))); \
+  } while (0)
+
+bool opaque_is_matmul(const CompGraph& g, int v, int64_t* m, int64_t* n, int64_t* k) {
+  const OpNode& node = g.node(v);
+  if (classify_op(node) != OpClass::Opaque || node.operands.size() != 2) return false;
+  const TensorShape& a = g.node(node.operands[0]).shape;
+  const TensorShape& b = g.node(node.operands[1]).shape;
+  const TensorShape& c = node.shape;
+  if (a.dtype != DType::F32 || b.dtype != DType::F32 || c.dtype != DType::F32) return false;
+  if (a.rank() < 2 || b.rank() != 2 || c.rank() != a.rank()) return false;
+  const int64_t K = a.dims.back(), N = b.dims[1];
+  if (b.dims[0] != K || c.dims.back() != N) return false;
+  for (int i = 0; i + 1 < a.rank(); ++i)
+    if (a.dims[static_cast<size_t>(i)] != c.dims[static_cast<size_t>(i)]) return false;
+  if (m) *m = a.element_count() / K;
+  if (n) *n = N;
+  if (k) *k = K;
+  return true;
+}
+
 Executor::Executor(const CompGraph& g, const FusionPlan& plan,
                    const std::map<std::string, KernelPlan>& kernels, const MachineModel& model,
-                   int device, ExecMode mode, bool use_graph)
+                   int device, ExecMode mode, bool use_graph, bool gemm_opaque)
     : g_(g), use_graph_(use_graph) {
   dev_ = &device_init(device);
   if (const char* v = std::getenv("STITCH_PDL")) pdl_ = *v != '0';
   if (const char* v = std::getenv("STITCH_DAG")) dag_ = *v != '0';
   if (const char* v = std::getenv("STITCH_PDL_EDGES")) pdl_edges_ = *v != '0';
   STC_RT(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
-  plan_launches(plan, kernels, model, mode);
+  plan_launches(plan, kernels, model, mode, gemm_opaque);
   module_ = std::make_unique<Module>(compile_cubin(source_, default_nvrtc_options()));
-  for (const auto& k : specs_) {
+  for (size_t ki = 0; ki < specs_.size(); ++ki) {
+    const KernelSpec& k = specs_[ki];
+    if (k.is_gemm) {
+      // C[M,N] = A[M,K] . B[K,N] row-major == column-major C^T = B^T . A^T:
+      // cuBLASLt (m, n, k) = (N, M, K) with B first, all non-transposed
+      if (!gemm_) {
+        gemm_ = std::make_unique<GemmState>();
+        STC_LT(cublasLtCreate(&gemm_->lt));
+        STC_RT(cudaMalloc(&gemm_->workspace, gemm_->ws_bytes));
+      }
+      const char* fp32 = std::getenv("STITCH_GEMM_FP32");
+      const cublasComputeType_t ct = fp32 && *fp32 == '1' ? CUBLAS_COMPUTE_32F : CUBLAS_COMPUTE_32F_FAST_TF32;
+      GemmState::Unit u;
+      STC_LT(cublasLtMatmulDescCreate(&u.op, ct, CUDA_R_32F));
+      const uint64_t M = static_cast<uint64_t>(k.gemm_m), N = static_cast<uint64_t>(k.gemm_n),
+                     K = static_cast<uint64_t>(k.gemm_k);
+      STC_LT(cublasLtMatrixLayoutCreate(&u.b, CUDA_R_32F, N, K, static_cast<int64_t>(N)));
+      STC_LT(cublasLtMatrixLayoutCreate(&u.a, CUDA_R_32F, K, M, static_cast<int64_t>(K)));
+      STC_LT(cublasLtMatrixLayoutCreate(&u.c, CUDA_R_32F, N, M, static_cast<int64_t>(N)));
+      cublasLtMatmulPreference_t pref = nullptr;
+      STC_LT(cublasLtMatmulPreferenceCreate(&pref));
+      STC_LT(cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES, &gemm_->ws_bytes,
+                                                  sizeof(gemm_->ws_bytes)));
+      cublasLtMatmulHeuristicResult_t res{};
+      int found = 0;
+      const cublasStatus_t hs =
+          cublasLtMatmulAlgoGetHeuristic(gemm_->lt, u.op, u.b, u.a, u.c, u.c, pref, 1, &res, &found);
+      cublasLtMatmulPreferenceDestroy(pref);
+      if (hs != CUBLAS_STATUS_SUCCESS || found < 1)
+        throw std::runtime_error("[cublasLt] no algorithm for GEMM " + k.name);
+      u.algo = res.algo;
+      gemm_->units[ki] = u;
+      fns_.push_back(nullptr);
+      continue;
+    }
     cudaKernel_t f = module_->fn(k.name);
     const void* fp = reinterpret_cast<const void*>(f);
     if (k.smem > 48 * 1024)
@@ -195,7 +279,7 @@ Executor::~Executor() {
 
 PlanKernels generate_plan_kernels(const CompGraph& g_, const FusionPlan& plan,
                                   const std::map<std::string, KernelPlan>& kernels,
-                                  const MachineModel& model, ExecMode mode, int sm_count) {
+                                  const MachineModel& model, ExecMode mode, int sm_count, bool gemm_opaque) {
   PlanKernels out;
   auto& specs_ = out.specs;
   auto& params_ = out.params;
@@ -301,7 +385,22 @@ PlanKernels generate_plan_kernels(const CompGraph& g_, const FusionPlan& plan,
     const int u = ready.begin()->second;
     ready.erase(ready.begin());
     const Unit& un = units[static_cast<size_t>(u)];
-    if (un.opaque)
+    int64_t gm = 0, gn = 0, gk = 0;
+    if (un.opaque && gemm_opaque && opaque_is_matmul(g_, un.verts[0], &gm, &gn, &gk)) {
+      const OpNode& n = g_.node(un.verts[0]);
+      KernelSpec k;
+      k.name = "k" + std::to_string(idx++) + "_" + sanitize(n.name);
+      k.tmpl = "gemm(cublasLt)";
+      k.pattern_key = "op:" + n.name;
+      k.is_gemm = true;
+      k.gemm_m = gm, k.gemm_n = gn, k.gemm_k = gk;
+      k.grid = k.block = 0;
+      k.inputs = {g_.node(n.operands[0]).name, g_.node(n.operands[1]).name};
+      k.outputs = {n.name};
+      k.alg_bytes = g_.node(n.operands[0]).shape.byte_size() + g_.node(n.operands[1]).shape.byte_size() +
+                    n.shape.byte_size();
+      specs_.push_back(std::move(k));
+    } else if (un.opaque)
       specs_.push_back(generate_opaque_kernel(g_, un.verts[0], "k" + std::to_string(idx++) + "_" +
                                                                    sanitize(g_.node(un.verts[0]).name),
                                               sm_count));
@@ -314,13 +413,14 @@ PlanKernels generate_plan_kernels(const CompGraph& g_, const FusionPlan& plan,
   std::sort(params_.begin(), params_.end());
   out.source = device_prelude();
   for (const auto& k : specs_)
-    out.source += "\n// ---- " + k.name + " [" + k.tmpl + "] pattern " + k.pattern_key + "\n" + k.source;
+    if (!k.is_gemm)
+      out.source += "\n// ---- " + k.name + " [" + k.tmpl + "] pattern " + k.pattern_key + "\n" + k.source;
   return out;
 }
 
 void Executor::plan_launches(const FusionPlan& plan, const std::map<std::string, KernelPlan>& kernels,
-                             const MachineModel& model, ExecMode mode) {
-  PlanKernels pk = generate_plan_kernels(g_, plan, kernels, model, mode, dev_->sm_count);
+                             const MachineModel& model, ExecMode mode, bool gemm_opaque) {
+  PlanKernels pk = generate_plan_kernels(g_, plan, kernels, model, mode, dev_->sm_count, gemm_opaque);
   specs_ = std::move(pk.specs);
   params_ = std::move(pk.params);
   source_ = std::move(pk.source);
@@ -381,6 +481,10 @@ void Executor::launch_kernel(size_t i, int set, cudaStream_t s, int after, const
       if (auto it = bind->find(t); it != bind->end()) return it->second;
     return tensors_.at(t).dptr[static_cast<size_t>(set)];
   };
+  if (k.is_gemm) {
+    launch_gemm(i, ptr_of(k.inputs[0]), ptr_of(k.inputs[1]), ptr_of(k.outputs[0]), s);
+    return;
+  }
   for (const auto& t : k.inputs) ptrs.push_back(ptr_of(t));
   for (const auto& t : k.outputs) ptrs.push_back(ptr_of(t));
   void* bar = nullptr;
@@ -413,6 +517,13 @@ void Executor::launch_kernel(size_t i, int set, cudaStream_t s, int after, const
     cfg.numAttrs = 1;
   }
   STC_RT(cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(fns_[i]), args.data()));
+}
+
+void Executor::launch_gemm(size_t i, void* a, void* b, void* c, cudaStream_t s) {
+  const GemmState::Unit& u = gemm_->units.at(i);
+  const float alpha = 1.f, beta = 0.f;
+  STC_LT(cublasLtMatmul(gemm_->lt, u.op, &alpha, b, u.b, a, u.a, &beta, c, u.c, c, u.c, &u.algo, gemm_->workspace,
+                        gemm_->ws_bytes, s));
 }
 
 void Executor::build_graph(int set) {

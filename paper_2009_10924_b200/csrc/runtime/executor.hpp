@@ -33,9 +33,15 @@ struct PlanKernels {
   std::vector<int> params;        // parameter vertices, ascending id
   std::string source;             // prelude + every kernel: one NVRTC module
 };
+// gemm_opaque (model mode, non-parity): opaque_compute ops shaped like a
+// matmul (A[..,M,K] . B[K,N] -> [..,M,N], f32) become cuBLASLt GEMM units
+// instead of the reference's mean-of-operands placeholder.
 PlanKernels generate_plan_kernels(const CompGraph& g, const FusionPlan& plan,
                                   const std::map<std::string, KernelPlan>& kernels,
-                                  const MachineModel& model, ExecMode mode, int sm_count = 148);
+                                  const MachineModel& model, ExecMode mode, int sm_count = 148,
+                                  bool gemm_opaque = false);
+// is opaque vertex v a matmul A[..,M,K] . B[K,N] -> [..,M,N] (all f32)?
+bool opaque_is_matmul(const CompGraph& g, int v, int64_t* m = nullptr, int64_t* n = nullptr, int64_t* k = nullptr);
 
 // JSON array of {name, template, pattern, grid, block, smem, cooperative,
 // bytes, inputs, outputs} per kernel (stc_exec_describe / stc_codegen)
@@ -45,7 +51,7 @@ class Executor {
  public:
   Executor(const CompGraph& g, const FusionPlan& plan,
            const std::map<std::string, KernelPlan>& kernels, const MachineModel& model,
-           int device, ExecMode mode, bool use_graph = true);
+           int device, ExecMode mode, bool use_graph = true, bool gemm_opaque = false);
   ~Executor();
   Executor(const Executor&) = delete;
   Executor& operator=(const Executor&) = delete;
@@ -98,7 +104,7 @@ class Executor {
 
  private:
   void plan_launches(const FusionPlan& plan, const std::map<std::string, KernelPlan>& kernels,
-                     const MachineModel& model, ExecMode mode);
+                     const MachineModel& model, ExecMode mode, bool gemm_opaque);
   void ensure_sets(int sets);
   // after_kernel: the kernel launched just before this one in the same stream
   // (-1: none) -- decides whether programmatic dependent launch applies
@@ -142,6 +148,9 @@ class Executor {
   std::vector<cudaEvent_t> kernel_events_;   // [kernel] done-event (capture only)
   cudaEvent_t fork_event_ = nullptr;
   cudaStream_t h2d_ = nullptr, d2h_ = nullptr;   // chunked host runs
+  struct GemmState;                               // cuBLASLt handle, descriptors, workspace
+  std::unique_ptr<GemmState> gemm_;
+  void launch_gemm(size_t i, void* a, void* b, void* c, cudaStream_t s);
   std::vector<cudaEvent_t> ev_in_, ev_comp_, ev_out_;
 };
 

@@ -36,6 +36,7 @@ GRAPHS = os.path.join(PKG, "graphs")
 DTYPES = {0: ("f32", np.float32), 1: ("f16", np.float16), 2: ("i32", np.int32), 3: ("bool", np.uint8)}
 MODES = {"stitched": 0, "program": 1, "unfused": 2}
 NO_GRAPH = 8
+GEMM = 16  # model mode: matmul-shaped opaque_compute ops as cuBLASLt GEMMs
 
 
 class StitchError(RuntimeError):
@@ -227,10 +228,10 @@ class Plan:
         lib().stc_plan_stats(self._h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c))
         return {"stitched_kernels": a.value, "baseline_kernels": b.value, "delta_evaluate_calls": c.value}
 
-    def codegen(self, mode: str = "stitched"):
+    def codegen(self, mode: str = "stitched", gemm: bool = False):
         """(cuda_source, [kernel descriptions]) without touching a device"""
         s, j = ctypes.c_void_p(), ctypes.c_void_p()
-        _check(lib().stc_codegen(self._h, MODES[mode], ctypes.byref(s), ctypes.byref(j)))
+        _check(lib().stc_codegen(self._h, MODES[mode] | (GEMM if gemm else 0), ctypes.byref(s), ctypes.byref(j)))
         return _take(s), json.loads(_take(j))
 
     def __del__(self):
@@ -261,11 +262,11 @@ class Executor:
     """A plan compiled for one B200 and replayed as one CUDA Graph
     (eval_plan / run_program / eval_reference, src/sim.cpp:231-514)."""
 
-    def __init__(self, plan: Plan, device: int = 0, mode: str = "stitched", graph: bool = True):
+    def __init__(self, plan: Plan, device: int = 0, mode: str = "stitched", graph: bool = True, gemm: bool = False):
         self.plan = plan
         self.g = plan.graph
         self._h = ctypes.c_void_p()
-        flags = MODES[mode] | (0 if graph else NO_GRAPH)
+        flags = MODES[mode] | (0 if graph else NO_GRAPH) | (GEMM if gemm else 0)
         _check(lib().stc_exec_create(plan._h, device, flags, ctypes.byref(self._h)))
 
     @property

@@ -141,3 +141,33 @@ def test_dag_capture_matches_linear_chain(monkeypatch):
         monkeypatch.delenv("STITCH_DAG")
         for k in lin:
             assert np.array_equal(dag[k], lin[k]), (name, k)
+
+
+@pytest.mark.parametrize("precision", ["fp32", "tf32"])
+def test_model_mode_gemm_bert_layer(monkeypatch, precision):
+    """model mode (non-parity): the BERT FFN layer's
+    opaque_compute GEMMs run as cuBLASLt between the stitched kernels, in the
+    same CUDA Graph.  Oracle: the f64 matmul rounded to f32, everything else
+    eval_reference.  Tolerance (stated): fp32 GEMM -> per element abs <= 1e-3
+    OR rel <= 1e-3 (K=3072 summation order); TF32 tensor cores (10-bit
+    mantissa operands) -> abs <= 3e-2 OR rel <= 3e-2 on the LayerNorm output."""
+    stitch = _stitch()
+    if precision == "fp32":
+        monkeypatch.setenv("STITCH_GEMM_FP32", "1")
+    text = config_graph("bert_layer")
+    g = stitch.Graph(text)
+    ex = stitch.Executor(stitch.Plan(g, "b200"), gemm=True)
+    kinds = [k["template"] for k in ex.describe()]
+    assert kinds.count("gemm(cublasLt)") == 2, kinds
+    inputs = stitch.random_inputs(g, 1)
+    got = ex.run(inputs)
+    og = no.parse_graph(text)
+    want = no.eval_reference(og, {k: v.astype(np.float64) for k, v in inputs.items()}, opaque=no.matmul_opaque)
+    tol = 1e-3 if precision == "fp32" else 3e-2
+    for k in want:
+        rep = stitch.compare({k: got[k]}, {k: want[k]}, tol, tol)
+        assert rep["pass"], (precision, k, rep["message"], rep["max_abs"], rep["max_rel"])
+    # the graph replays what the direct launches compute
+    again = ex.run(inputs)
+    for k in got:
+        assert np.array_equal(again[k], got[k])
