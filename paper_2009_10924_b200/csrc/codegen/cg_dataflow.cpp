@@ -97,13 +97,30 @@ class Emitter {
     line(s + " {");
     ind += "  ";
     scopes_.push_back(memo_);
+    wait_scopes_.push_back(waited_);
   }
   void close() {
     ind.resize(ind.size() - 2);
     line("}");
     memo_ = scopes_.back();
     scopes_.pop_back();
+    waited_ = wait_scopes_.back();
+    wait_scopes_.pop_back();
   }
+
+  // Programmatic dependent launch with a hoisted prologue: graph parameters
+  // are never written by a kernel, so their loads may be issued before
+  // griddepcontrol.wait -- overlapping the previous kernel's drain.  Every
+  // load of a kernel-produced tensor and every global write comes after the
+  // wait (emitted lazily, once per control path); the CTA triggers its
+  // dependents right after its own wait.
+  bool hoist = false;
+  void ensure_wait() {
+    if (!hoist || waited_) return;
+    line("pdl_wait(); pdl_launch();");
+    waited_ = true;
+  }
+  bool is_param(int v) const { return g_.node(v).kind == OpKind::Parameter; }
   void clear_memo() { memo_.clear(); }
 
   static std::string key(int v, const Coords& c) { return std::to_string(v) + "@" + coords_key(c); }
@@ -141,6 +158,7 @@ class Emitter {
  private:
   Val load(int v, const Coords& c) {
     loaded.insert(v);
+    if (!is_param(v)) ensure_wait();
     const TensorShape& sh = g_.node(v).shape;
     const std::string ptr = "T_" + g_.node(v).name;
     int nvary = 0, last_vary = -1;
@@ -330,6 +348,7 @@ class Emitter {
           }
           if (pattern_.count(data)) throw TemplateMismatch("gather of in-pattern data");
           loaded.insert(data);
+          if (!is_param(data)) ensure_wait();
           const std::string t = fresh("t");
           line("const float " + t + " = ldv(T_" + g_.node(data).name + ", " + linear(data, dc, 0) + ");");
           r.lanes.push_back(t);
@@ -347,6 +366,8 @@ class Emitter {
   int counter_ = 0;
   std::map<std::string, Val> memo_;
   std::vector<std::map<std::string, Val>> scopes_;
+  bool waited_ = false;
+  std::vector<bool> wait_scopes_;
 };
 
 // ---- analysis ---------------------------------------------------------------
@@ -463,6 +484,7 @@ void store_val(Emitter& em, const CompGraph& g, int v, const Coords& c, const Va
   int nvary = 0;
   for (const auto& x : c) nvary += x.vary;
   const std::string pre = guard.empty() ? "" : "if (" + guard + ") ";
+  em.ensure_wait();
   if (em.W == 4 && nvary == 1 && c.back().vary && c.back().aligned && sh.dtype == DType::F32) {
     em.line(pre + "st4(" + ptr + " + " + em.linear(v, c, 0) + ", " + val.at(0) + ", " + val.at(1) + ", " +
             val.at(2) + ", " + val.at(3) + ");");
@@ -565,6 +587,7 @@ void emit_row(Emitter& em, const CompGraph& g, const std::set<int>& pat, const B
   }
   const std::string sRPB = std::to_string(rp.RPB), sL = std::to_string(L);
   if (st) {
+    em.ensure_wait();  // TMA-staged inputs may be kernel-produced
     const int64_t ntiles = (ROWS + rp.RPB - 1) / rp.RPB;
     const std::string S = std::to_string(st->stages), TF = std::to_string(st->tile_floats);
     const int64_t tile_bytes_full = st->tile_floats * 4;
@@ -703,6 +726,7 @@ void emit_row(Emitter& em, const CompGraph& g, const std::set<int>& pat, const B
     const auto& od = g.node(o).shape.dims;
     if (static_cast<int64_t>(od.size()) == static_cast<int64_t>(O.size())) {
       const Val v = em.value(o, rowc);
+      em.ensure_wait();
       em.line("if (row_ok && tl_ == 0) stv(T_" + g.node(o).name + ", " + em.linear(o, rowc, 0) + ", " + v.at(0) + ");");
       continue;
     }
@@ -811,6 +835,7 @@ void emit_column(Emitter& em, const CompGraph& g, const Body& b, const ColParams
   for (auto& [o, c, v, ok] : stores) store_val(em, g, o, c, v, ok);
   em.close();
   if (!nr) return;
+  em.ensure_wait();  // slab partials / arrival counters are global writes
   // fold the RT row lanes of the tile in smem (fixed order) -> slab partials
   const std::string tile = em.fresh("tile_");
   em.line("__shared__ double " + tile + "[" + std::to_string(cp.RT) + "][" + std::to_string(cp.CT * cp.W) + "];");
@@ -998,6 +1023,7 @@ KernelSpec generate_pattern_kernel(const CompGraph& g, const std::vector<int>& v
     }
   }
   em.block = block;
+  em.hoist = env_int("STITCH_PDL", 1) != 0 && env_int("STITCH_PDL_HOIST", 1) != 0;
   const int per_sm = std::max(1, std::min(env_int("STITCH_COL_CTAS", 3), 2048 / block));
 
   // CTA budget per body; scratch = [256 B reserved][strip arrival counters][f64 partials]
@@ -1071,6 +1097,7 @@ KernelSpec generate_pattern_kernel(const CompGraph& g, const std::vector<int>& v
     if (b.kind == Kind::Local) emit_local(em, g, b);
     else if (b.kind == Kind::Row) emit_row(em, g, pat, b, stage[i].tensors.empty() ? nullptr : &stage[i]);
     else emit_column(em, g, b, cps[i], part_off[i], ctr_off[i]);
+    em.ensure_wait();  // every path waits before the CTA retires
     body_src << "  " << (i ? "else " : "") << "if (blockIdx.x < " << start + b.blocks << ") {\n";
     body_src << "    const int vbid = blockIdx.x - " << start << ", vgrid = " << b.blocks << ";\n";
     body_src << "    (void)vbid; (void)vgrid;\n" << em.out.str() << "  }\n";
@@ -1118,12 +1145,13 @@ KernelSpec generate_pattern_kernel(const CompGraph& g, const std::vector<int>& v
   }
   sig << ") {\n";
   if (dyn_smem) sig << "  extern __shared__ __align__(128) unsigned char dsmem_[];\n";
-  // programmatic dependent launch: wait for the producer grid's memory before
-  // touching inputs; let the next kernel of the plan launch as we finish
+  // programmatic dependent launch: hoisted prologue (parameter loads before
+  // griddepcontrol.wait, Emitter::ensure_wait) unless STITCH_PDL_HOIST=0,
+  // which waits at entry and triggers dependents at exit
   const bool pdl = env_int("STITCH_PDL", 1) != 0;
-  const bool early = env_int("STITCH_PDL_EARLY", 0) != 0;  // trigger dependents at entry
-  k.source = sig.str() + (pdl ? (early ? "  pdl_wait();\n  pdl_launch();\n" : "  pdl_wait();\n") : "") +
-             body_src.str() + (pdl && !early ? "  pdl_launch();\n" : "") + "}\n";
+  const bool hoist = pdl && env_int("STITCH_PDL_HOIST", 1) != 0;
+  k.source = sig.str() + (pdl && !hoist ? "  pdl_wait();\n" : "") + body_src.str() + (pdl ? "  pdl_launch();\n" : "") +
+             "}\n";
   return k;
 }
 

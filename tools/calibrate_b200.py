@@ -77,7 +77,7 @@ CHAIN(log, float, BAR_F, x = logf(x))
 CHAIN(rsqrt, float, BAR_F, x = 1.0f / sqrtf(x))
 CHAIN(power, float, BAR_F, x = powf(x, y))
 CHAIN(reduce_step, double, BAR_D, x = x + y)
-CHAIN(shuffle, float, BAR_F, asm volatile("shfl.sync.idx.b32 %0, %0, 0, 0x1f, 0xffffffff;" : "+f"(x)))
+CHAIN(shuffle, float, BAR_F, asm volatile("shfl.sync.bfly.b32 %0, %0, 1, 0x1f, 0xffffffff;" : "+f"(x)))
 CHAIN(index_calc, int, BAR_I, x = x * y + 3)
 
 extern "C" __global__ void lat_shared_access(const int* in, int* out, long long* cyc, int n) {
