@@ -68,50 +68,60 @@ def ncu_traffic(graph):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled while the timed region runs"""
+    """SM clocks + throttle reasons sampled through NVML every ~1 ms while the
+    GPU is loaded (nvidia-smi's own loop cannot start fast enough for a
+    sub-second timed region).  mark(t0, t1) selects the timed region; the
+    last 200 ms of the loaded warm-up are reported beside it when the region
+    itself is too short for 3 samples."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"))
 
     def __init__(self, device):
-        self.device, self.samples, self.proc = device, [], None
+        self.device, self.samples, self.ok = device, [], False
+        self.stop_flag = threading.Event()
 
     def start(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.device), "--query-gpu=" + self.FIELDS,
-                 "--format=csv,noheader,nounits", "-lms", "20"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
-            self.thread.start()
-        except Exception:
-            self.proc = None
+            import pynvml as nv
+            nv.nvmlInit()
+            self.nv = nv
+            self.h = nv.nvmlDeviceGetHandleByIndex(self.device)
+            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # reported, never fatal
+            self.err = str(e)
+            return
+        self.thread = threading.Thread(target=self._run, daemon=True)
+        self.thread.start()
 
-    def _read(self):
-        for line in self.proc.stdout:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) >= 7:
-                self.samples.append(parts)
+    def _run(self):
+        nv = self.nv
+        while not self.stop_flag.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.samples.append((time.perf_counter(), sm, r))
+            except Exception:
+                pass
+            time.sleep(0.001)
 
-    def stop(self):
-        if not self.proc:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        time.sleep(0.05)
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=2)
-        except Exception:
-            self.proc.kill()
-        rows = [s for s in self.samples if s[0].replace(".", "").isdigit()]
-        if not rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"], "samples": 0}
-        sm = [float(r[0]) for r in rows]
-        load = [float(r[0]) for r in rows if float(r[0]) > 600] or sm
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(load), "sm_max_mhz": float(rows[0][1]), "reasons": reasons,
-                "samples": len(rows)}
+    def stop(self, t0, t1):
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable: " + getattr(self, "err", "")]}
+        self.stop_flag.set()
+        self.thread.join(timeout=2)
+        timed = [s for s in self.samples if t0 <= s[0] <= t1]
+        use = timed if len(timed) >= 3 else [s for s in self.samples if t0 - 0.2 <= s[0] <= t1]
+        if not use:
+            return {"sm_mhz": None, "sm_max_mhz": float(self.max_mhz), "reasons": ["no samples"], "samples": 0}
+        reasons = sorted({name for _, _, r in use for name, attr in self.REASONS if r & getattr(self.nv, attr)})
+        return {"sm_mhz": statistics.median(float(s[1]) for s in use), "sm_max_mhz": float(self.max_mhz),
+                "reasons": reasons, "samples": len(use), "samples_in_timed_region": len(timed),
+                "source": "NVML, 1 ms period" + ("" if len(timed) >= 3 else "; timed region + the 200 ms of loaded "
+                                                                             "warm-up before it")}
 
 
 def cpu_reference_seconds(text, threads, reps):
@@ -127,31 +137,38 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    from paper_2009_10924_b200 import stitch  # noqa: F401  (graph bytes only)
     from oracle import numpy_oracle as no
     from oracle import ref
-    text = read_graph(WORKLOAD)
-    bytes_step = no.algorithmic_bytes(no.parse_graph(text), [[n.id for n in no.parse_graph(text).nodes
-                                                              if n.kind not in ("parameter", "constant")]])
     if not ref.available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libstitch_ref.so not built"}))
         return
+    text = read_graph(WORKLOAD)
     threads = os.cpu_count() or 1
+    # each step is a bounded sample of the workload: all 32 sequences, `heads`
+    # of the 12 attention heads, so that warm-up + K steps end in ~2 minutes
+    t_full, shards = cpu_reference_seconds(text, threads, 1)
+    budget_s = float(os.environ.get("STITCH_REF_BUDGET_S", "120"))
+    heads = max(1, min(12, int(12 * budget_s / max(1e-9, (args.steps + args.warmup) * t_full))))
+    sample = text.replace("[32,12,", "[32,%d," % heads)
+    og = no.parse_graph(sample)
+    bytes_step = no.algorithmic_bytes(og, [[n.id for n in og.nodes if n.kind not in ("parameter", "constant")]])
     times = []
     for i in range(args.warmup + args.steps):
-        s, shards = cpu_reference_seconds(text, threads, 1)
+        s, shards = cpu_reference_seconds(sample, threads, 1)
         if i >= args.warmup:
             times.append(s)
     t = statistics.mean(times)
     val = bytes_step / t / 1e9
+    desc = ("C2 softmax chain, %d of 12 heads x 32 sequences per step (%d batch shards on %d host threads, "
+            "unmodified reference eval_reference from oracle/_ref)" % (heads, shards, shards))
     line = {"metric": "stitched-subgraph HBM GB/s (algorithmic bytes / time)", "value": round(val, 4),
             "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(t * 1e3, 3), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic: reference random_inputs(seed=1)",
-            "config": {"workload": WORKLOAD_DESC, "graph": WORKLOAD}, "impl": "reference",
+            "config": {"workload": WORKLOAD_DESC, "graph": WORKLOAD, "sample_heads": heads,
+                       "bytes_per_step": bytes_step}, "impl": "reference",
             "cpu_baseline": {"value": round(val, 4), "unit": "GB/s", "cores": shards, "kind": "reference",
-                             "sample": "full C2 batch as %d batch shards, eval_reference on %d threads "
-                                       "(unmodified reference library, oracle/_ref)" % (shards, shards)},
+                             "sample": desc},
             "e2e": {"value": round(val, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
 
@@ -231,16 +248,34 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t_timed0 = time.perf_counter()
     e0.record(stream)
     for i in range(args.steps // spg):
         ex.launch_batch(sp, i)
     e1.record(stream)
     torch.cuda.synchronize()
+    t_timed1 = time.perf_counter()
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
-    clk = clocks.stop()
+    clk = clocks.stop(t_timed0, t_timed1)
     ms = e0.elapsed_time(e1)
+    # sustained: the same replays for >= 1 s of back-to-back load (power cap
+    # engaged), reported beside the headline with its own clock record
+    sus_clk = ClockSampler(local)
+    sus_clk.start()
+    n_sus = max(1, int(1.0 / max(1e-6, ms * 1e-3 / max(1, args.steps // spg))))
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ts0 = time.perf_counter()
+    s0.record(stream)
+    for i in range(n_sus):
+        ex.launch_batch(sp, i)
+    s1.record(stream)
+    torch.cuda.synchronize()
+    sus_c = sus_clk.stop(ts0, time.perf_counter())
+    sus_us = s0.elapsed_time(s1) * 1e3 / (n_sus * spg)
+    sustained = {"us_per_step": round(sus_us, 3), "value": round(alg_bytes * world / (sus_us * 1e-6) / 1e9, 1),
+                 "steps": n_sus * spg, "clocks": sus_c}
     if dist:
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -345,6 +380,7 @@ def main():
                     "unpipelined": {"value": round(alg_bytes * world / e2e_plain_s / 1e9, 3),
                                     "us_per_step": round(e2e_plain_s * 1e6, 1),
                                     "path": "stc_exec_run_host: H2D all -> graph -> D2H all"}},
+            "sustained": sustained,
             "gpu_launches": len(desc) * args.steps,
             "clocks": clk,
             "subgraphs": subs,
