@@ -115,6 +115,11 @@ int stc_exec_run_host_chunked(stc_exec* e, const void* const* inputs, void* cons
  * outputs over PCIe directly, the transfer fused with the stitched compute.
  * Fails (status != 0, nothing launched) for pageable buffers. */
 int stc_exec_run_host_zero_copy(stc_exec* e, const void* const* inputs, void* const* outputs);
+/* In-graph kernel timeline of one replay (diagnostics; the exec must have been
+ * created with STITCH_TRACE=1 in the environment): start_us[i] / end_us[i] =
+ * first CTA entry / last CTA exit of kernel i (%globaltimer), us since the
+ * earliest entry; -1 for library (GEMM) units.  Arrays of num_kernels. */
+int stc_exec_trace(stc_exec* e, double* start_us, double* end_us);
 int stc_exec_upload(stc_exec* e, const void* const* inputs);
 /* async graph replay on `cuda_stream` using buffer set `set` (0 = the
  * uploaded buffers; see stc_exec_prepare_sets).  NULL selects the executor's

@@ -63,6 +63,16 @@ int stc_exec_run_host(stc_exec* e, const void* const* inputs, void* const* outpu
   return guarded([&] { e->ex->run_host(inputs, outputs); });
 }
 
+int stc_exec_trace(stc_exec* e, double* start_us, double* end_us) {
+  return guarded([&] {
+    const auto t = e->ex->trace(0);
+    for (size_t i = 0; i < t.size(); ++i) {
+      if (start_us) start_us[i] = t[i].first;
+      if (end_us) end_us[i] = t[i].second;
+    }
+  });
+}
+
 int stc_exec_run_host_zero_copy(stc_exec* e, const void* const* inputs, void* const* outputs) {
   return guarded([&] {
     if (!e->ex->run_host_zero_copy(inputs, outputs))

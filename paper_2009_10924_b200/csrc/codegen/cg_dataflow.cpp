@@ -1187,7 +1187,11 @@ KernelSpec generate_opaque_kernel(const CompGraph& g, int vertex, const std::str
     s << ", unsigned* __restrict__ bar_, double* __restrict__ part_";
     k.scratch_bytes = 256 + int64_t(grid) * 8;
   }
-  s << ") {\n  pdl_wait();\n";
+  // trigger dependents as soon as our own prerequisites are met: a dependent
+  // then launches (and becomes resident) while we run, hiding its launch
+  // latency behind our body (STITCH_OPAQUE_EARLY=0: trigger at exit)
+  const bool early = env_int("STITCH_OPAQUE_EARLY", 1) != 0;
+  s << ") {\n  pdl_wait();\n" << (early ? "  pdl_launch();\n" : "");
   k.outputs.push_back(n.name);
   s << "  __shared__ double red_[" << block / 32 << "];\n  double acc = 0.0;\n";
   // an operand listed twice is counted twice, as upstream

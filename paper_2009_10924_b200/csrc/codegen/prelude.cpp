@@ -89,6 +89,22 @@ __device__ __forceinline__ float bfly_max(float v, int width) {
   return v;
 }
 
+// in-graph kernel timeline (STITCH_TRACE=1 builds): per kernel slot k,
+// [2k] = earliest CTA entry, [2k+1] = latest CTA exit (%globaltimer, ns)
+#ifdef STITCH_TRACE
+__device__ unsigned long long stc_trace_[2 * 4096];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define STC_TRACE_BEGIN(k) do { if (threadIdx.x == 0) atomicMin(&stc_trace_[2 * (k)], gtimer()); } while (0)
+#define STC_TRACE_END(k) do { __syncthreads(); if (threadIdx.x == 0) atomicMax(&stc_trace_[2 * (k) + 1], gtimer()); } while (0)
+#else
+#define STC_TRACE_BEGIN(k) do {} while (0)
+#define STC_TRACE_END(k) do {} while (0)
+#endif
+
 // programmatic dependent launch (PDL): no-ops unless launched with the
 // programmatic-stream-serialization attribute
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }

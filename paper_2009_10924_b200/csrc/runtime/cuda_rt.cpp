@@ -168,6 +168,17 @@ Module::~Module() {
   if (lib_) cudaLibraryUnload(lib_);
 }
 
+void* Module::global(const std::string& name, size_t* bytes) {
+  void* p = nullptr;
+  size_t n = 0;
+  if (cudaLibraryGetGlobal(&p, &n, lib_, name.c_str()) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  if (bytes) *bytes = n;
+  return p;
+}
+
 cudaKernel_t Module::fn(const std::string& name) {
   auto it = fns_.find(name);
   if (it != fns_.end()) return it->second;

@@ -47,6 +47,8 @@ class Module {
   Module(const Module&) = delete;
   Module& operator=(const Module&) = delete;
   cudaKernel_t fn(const std::string& name);
+  // device address + size of a __device__ global of the module (nullptr if absent)
+  void* global(const std::string& name, size_t* bytes = nullptr);
 
  private:
   cudaLibrary_t lib_ = nullptr;

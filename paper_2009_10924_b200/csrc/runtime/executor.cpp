@@ -86,11 +86,21 @@ Executor::Executor(const CompGraph& g, const FusionPlan& plan,
     : g_(g), use_graph_(use_graph) {
   dev_ = &device_init(device);
   if (const char* v = std::getenv("STITCH_PDL")) pdl_ = *v != '0';
-  if (const char* v = std::getenv("STITCH_DAG")) dag_ = *v != '0';
+  if (const char* v = std::getenv("STITCH_DAG")) {
+    dag_ = *v != '0';
+    sources_only_ = *v == '2';
+  }
   if (const char* v = std::getenv("STITCH_PDL_EDGES")) pdl_edges_ = *v != '0';
   STC_RT(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
   plan_launches(plan, kernels, model, mode, gemm_opaque);
-  module_ = std::make_unique<Module>(compile_cubin(source_, default_nvrtc_options()));
+  {
+    auto opts = default_nvrtc_options();
+    if (const char* t = std::getenv("STITCH_TRACE"); t && *t == '1') {
+      opts.push_back("-DSTITCH_TRACE");
+      tracing_ = true;
+    }
+    module_ = std::make_unique<Module>(compile_cubin(source_, opts));
+  }
   for (size_t ki = 0; ki < specs_.size(); ++ki) {
     const KernelSpec& k = specs_[ki];
     if (k.is_gemm) {
@@ -169,6 +179,11 @@ void Executor::promote_edges(cudaGraph_t graph) {
       rt.push_back(to[e]);
       rd.push_back(data[e]);
     }
+  if (std::getenv("STITCH_DEBUG")) {
+    size_t prog = 0;
+    for (size_t e = 0; e < n; ++e) prog += data[e].type == cudaGraphDependencyTypeProgrammatic;
+    std::fprintf(stderr, "[exec] graph edges %zu: %zu already programmatic, %zu to promote\n", n, prog, rf.size());
+  }
   if (rf.empty()) return;
   STC_RT(cudaGraphRemoveDependencies_v2(graph, rf.data(), rt.data(), rd.data(), rf.size()));
   for (auto& d : rd) {
@@ -176,6 +191,15 @@ void Executor::promote_edges(cudaGraph_t graph) {
     d.from_port = cudaGraphKernelNodePortProgrammatic;
   }
   STC_RT(cudaGraphAddDependencies_v2(graph, rf.data(), rt.data(), rd.data(), rf.size()));
+  if (std::getenv("STITCH_DEBUG")) {
+    size_t m = 0, prog = 0;
+    STC_RT(cudaGraphGetEdges_v2(graph, nullptr, nullptr, nullptr, &m));
+    std::vector<cudaGraphNode_t> f2(m), t2(m);
+    std::vector<cudaGraphEdgeData> d2(m);
+    STC_RT(cudaGraphGetEdges_v2(graph, f2.data(), t2.data(), d2.data(), &m));
+    for (auto& d : d2) prog += d.type == cudaGraphDependencyTypeProgrammatic;
+    std::fprintf(stderr, "[exec] after promotion: %zu edges, %zu programmatic\n", m, prog);
+  }
 }
 
 void Executor::compute_deps() {
@@ -220,17 +244,32 @@ int Executor::capture_plan(int set, cudaStream_t origin, int prev) {
   std::vector<Lane> lanes{{origin, -1}};
   STC_RT(cudaEventRecord(fork_event_, origin));
   const size_t max_lanes = 8;
+  // estimated finish time of every kernel (fixed launch/latency cost + its
+  // bytes at HBM speed, after its latest producer): a kernel follows the
+  // producer expected to finish LAST on that producer's lane, so the edge
+  // that gates it is a same-stream PDL edge (cross-lane edges pay a full
+  // launch latency, profiles/r01/dien_timeline.txt)
+  std::vector<double> fin(n, 0.0);
+  for (size_t i = 0; i < n; ++i) {
+    double ready = 0.0;
+    for (int d : deps_[i]) ready = std::max(ready, fin[static_cast<size_t>(d)]);
+    fin[i] = ready + 1.5 + static_cast<double>(specs_[i].alg_bytes) / 5.0e3;
+  }
   for (size_t i = 0; i < n; ++i) {
     int best = -1;
-    for (size_t l = 0; l < lanes.size(); ++l) {  // the latest producer at a lane's tail
+    for (size_t l = 0; l < lanes.size(); ++l) {  // the producer finishing last, at a lane's tail
       const int t = lanes[l].tail;
-      if (t >= 0 && std::count(deps_[i].begin(), deps_[i].end(), t) && (best < 0 || t > lanes[static_cast<size_t>(best)].tail))
+      if (t >= 0 && std::count(deps_[i].begin(), deps_[i].end(), t) &&
+          (best < 0 || fin[static_cast<size_t>(t)] > fin[static_cast<size_t>(lanes[static_cast<size_t>(best)].tail)]))
         best = static_cast<int>(l);
     }
     for (size_t l = 0; l < lanes.size() && best < 0; ++l) {  // a lane already ordered before us
       const int t = lanes[l].tail;
       if (t < 0 || anc[i][static_cast<size_t>(t)]) best = static_cast<int>(l);
     }
+    // STITCH_DAG=2: only kernels without producers (e.g. per-step input
+    // transforms) fork; everything else stays on the origin chain
+    if (best < 0 && sources_only_ && !deps_[i].empty()) best = 0;
     if (best < 0 && lanes.size() < max_lanes) {
       while (aux_streams_.size() < lanes.size()) {
         cudaStream_t s2 = nullptr;
@@ -410,6 +449,16 @@ PlanKernels generate_plan_kernels(const CompGraph& g_, const FusionPlan& plan,
       if (--pending[static_cast<size_t>(w)] == 0) ready.insert({units[static_cast<size_t>(w)].fire, w});
   }
   if (specs_.size() != units.size()) throw std::runtime_error("[exec] contracted plan graph has a cycle");
+  // timeline hooks (no-ops unless compiled with -DSTITCH_TRACE, Executor::trace)
+  for (size_t i = 0; i < specs_.size(); ++i) {
+    auto& src = specs_[i].source;
+    if (specs_[i].is_gemm || src.empty()) continue;
+    const size_t open = src.find("{\n");
+    const size_t close = src.rfind("}\n");
+    if (open == std::string::npos || close == std::string::npos || close < open) continue;
+    src.insert(close, "  STC_TRACE_END(" + std::to_string(i) + ");\n");
+    src.insert(open + 2, "  STC_TRACE_BEGIN(" + std::to_string(i) + ");\n");
+  }
   std::sort(params_.begin(), params_.end());
   out.source = device_prelude();
   for (const auto& k : specs_)
@@ -795,6 +844,32 @@ double Executor::time(int iters, int warmup, int sets, std::vector<double>* per_
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   return us;
+}
+
+std::vector<std::pair<double, double>> Executor::trace(int set) {
+  if (!tracing_) throw std::runtime_error("[exec] trace() needs an executor built with STITCH_TRACE=1");
+  size_t bytes = 0;
+  void* buf = module_->global("stc_trace_", &bytes);
+  if (!buf) throw std::runtime_error("[exec] trace buffer missing from the module");
+  const size_t n = specs_.size();
+  std::vector<unsigned long long> init(2 * n);
+  for (size_t i = 0; i < n; ++i) init[2 * i] = ~0ull, init[2 * i + 1] = 0ull;
+  ensure_sets(set + 1);
+  if (use_graph_) build_graph(set);
+  STC_RT(cudaStreamSynchronize(stream_));
+  STC_RT(cudaMemcpy(buf, init.data(), init.size() * 8, cudaMemcpyHostToDevice));
+  launch(stream_, set);
+  STC_RT(cudaStreamSynchronize(stream_));
+  std::vector<unsigned long long> t(2 * n);
+  STC_RT(cudaMemcpy(t.data(), buf, t.size() * 8, cudaMemcpyDeviceToHost));
+  unsigned long long t0 = ~0ull;
+  for (size_t i = 0; i < n; ++i)
+    if (!specs_[i].is_gemm) t0 = std::min(t0, t[2 * i]);
+  std::vector<std::pair<double, double>> out(n, {-1.0, -1.0});
+  for (size_t i = 0; i < n; ++i)
+    if (!specs_[i].is_gemm && t[2 * i + 1])
+      out[i] = {1e-3 * static_cast<double>(t[2 * i] - t0), 1e-3 * static_cast<double>(t[2 * i + 1] - t0)};
+  return out;
 }
 
 std::string describe_specs(const std::vector<KernelSpec>& specs) {

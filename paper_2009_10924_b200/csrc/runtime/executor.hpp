@@ -101,6 +101,10 @@ class Executor {
   double time(int iters, int warmup, int sets, std::vector<double>* per_kernel_us, int batch = 1);
 
   std::string describe_json() const;
+  // one replay of set `set` with the in-graph timeline: per kernel (first CTA
+  // entry, last CTA exit) in us since the earliest entry (-1 for GEMM units).
+  // Needs STITCH_TRACE=1 at construction (adds -DSTITCH_TRACE to NVRTC).
+  std::vector<std::pair<double, double>> trace(int set = 0);
 
  private:
   void plan_launches(const FusionPlan& plan, const std::map<std::string, KernelPlan>& kernels,
@@ -141,7 +145,9 @@ class Executor {
   int batch_ = 0;
   bool coop_in_graph_ = true;
   bool pdl_ = true;  // STITCH_PDL=0 disables programmatic dependent launch
+  bool tracing_ = false;
   bool dag_ = true;  // STITCH_DAG=0 captures the plan as one linear chain
+  bool sources_only_ = false;  // STITCH_DAG=2: fork only producer-less kernels
   bool pdl_edges_ = true;  // STITCH_PDL_EDGES=0 keeps cross-stream edges full
   std::vector<std::vector<int>> deps_;       // [kernel] -> producer kernels
   std::vector<cudaStream_t> aux_streams_;    // fork targets for independent kernels

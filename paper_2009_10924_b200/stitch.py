@@ -77,6 +77,7 @@ def lib():
         "stc_exec_run_host": (ip, [vp, P(vp), P(vp)]), "stc_exec_upload": (ip, [vp, P(vp)]),
         "stc_exec_run_host_chunked": (ip, [vp, P(vp), P(vp), ip, P(ip)]),
         "stc_exec_run_host_zero_copy": (ip, [vp, P(vp), P(vp)]),
+        "stc_exec_trace": (ip, [vp, P(ctypes.c_double), P(ctypes.c_double)]),
         "stc_exec_launch": (ip, [vp, vp, ip]), "stc_exec_prepare_sets": (ip, [vp, ip]),
         "stc_exec_download": (ip, [vp, P(vp)]),
         "stc_exec_sync": (ip, [vp]),
@@ -322,6 +323,14 @@ class Executor:
         op = (ctypes.c_void_p * max(1, len(outs)))(*[o.ctypes.data for o in outs])
         _check(lib().stc_exec_run_host_zero_copy(self._h, ip, op))
         return {t.name: o for t, o in zip(self.g.outputs, outs)}
+
+    def trace(self):
+        """[(start_us, end_us)] per kernel of one replay (needs STITCH_TRACE=1
+        in the environment when the executor was created)"""
+        n = self.num_kernels
+        a, b = (ctypes.c_double * max(1, n))(), (ctypes.c_double * max(1, n))()
+        _check(lib().stc_exec_trace(self._h, a, b))
+        return list(zip(a[:n], b[:n]))
 
     def upload(self, inputs: Dict[str, np.ndarray]):
         keep, ip = self._in_ptrs(inputs)
