@@ -120,6 +120,13 @@ int stc_exec_run_host_zero_copy(stc_exec* e, const void* const* inputs, void* co
  * first CTA entry / last CTA exit of kernel i (%globaltimer), us since the
  * earliest entry; -1 for library (GEMM) units.  Arrays of num_kernels. */
 int stc_exec_trace(stc_exec* e, double* start_us, double* end_us);
+/* Pipelined host execution over chunks of DIFFERENT sizes: chunk k runs on
+ * execs[exec_of_chunk[k]] (each exec built from a shard graph of the same
+ * graph, e.g. batch 1 / 3 / 4); chunk k of a chunked input starts right after
+ * chunk k-1's bytes.  Small first/last chunks shorten the pipeline's fill and
+ * drain.  Same result as running the chunks one by one. */
+int stc_exec_run_host_pipeline(stc_exec* const* execs, const int* exec_of_chunk, int nchunks,
+                               const void* const* inputs, void* const* outputs, const int* input_chunked);
 int stc_exec_upload(stc_exec* e, const void* const* inputs);
 /* async graph replay on `cuda_stream` using buffer set `set` (0 = the
  * uploaded buffers; see stc_exec_prepare_sets).  NULL selects the executor's

@@ -85,6 +85,16 @@ int stc_exec_run_host_chunked(stc_exec* e, const void* const* inputs, void* cons
   return guarded([&] { e->ex->run_host_chunked(inputs, outputs, nchunks, input_chunked); });
 }
 
+int stc_exec_run_host_pipeline(stc_exec* const* execs, const int* exec_of_chunk, int nchunks,
+                               const void* const* inputs, void* const* outputs, const int* input_chunked) {
+  return guarded([&] {
+    if (nchunks < 1 || !execs || !exec_of_chunk) throw std::invalid_argument("[abi] bad pipeline arguments");
+    std::vector<gpu::Executor*> ex;
+    for (int k = 0; k < nchunks; ++k) ex.push_back(execs[exec_of_chunk[k]]->ex.get());
+    gpu::Executor::run_host_pipeline(ex, inputs, outputs, input_chunked);
+  });
+}
+
 int stc_exec_upload(stc_exec* e, const void* const* inputs) {
   return guarded([&] { e->ex->upload(inputs, 0); });
 }

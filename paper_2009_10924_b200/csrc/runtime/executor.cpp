@@ -675,20 +675,36 @@ bool Executor::run_host_zero_copy(const void* const* in, void* const* out) {
 
 void Executor::run_host_chunked(const void* const* in, void* const* out, int nchunks, const int* in_chunked) {
   if (nchunks < 1) throw std::runtime_error("[exec] nchunks must be >= 1");
-  const int S = std::min(nchunks, 3);
-  ensure_sets(S);
-  if (use_graph_)
-    for (int s = 0; s < S; ++s) build_graph(s);
-  if (!h2d_) {
-    STC_RT(cudaStreamCreateWithFlags(&h2d_, cudaStreamNonBlocking));
-    STC_RT(cudaStreamCreateWithFlags(&d2h_, cudaStreamNonBlocking));
+  run_host_pipeline(std::vector<Executor*>(static_cast<size_t>(nchunks), this), in, out, in_chunked);
+}
+
+void Executor::run_host_pipeline(const std::vector<Executor*>& chunk_exec, const void* const* in, void* const* out,
+                                 const int* in_chunked) {
+  if (chunk_exec.empty()) throw std::runtime_error("[exec] no chunks");
+  Executor* lead = chunk_exec[0];
+  // every chunk graph is a shard of the same graph: same parameter/output lists
+  for (Executor* e : chunk_exec)
+    if (e->params_.size() != lead->params_.size() || e->g_.outputs.size() != lead->g_.outputs.size())
+      throw std::runtime_error("[exec] pipeline chunks come from different graphs");
+  std::map<Executor*, int> uses, seen;
+  for (Executor* e : chunk_exec) ++uses[e];
+  for (auto& [e, n] : uses) {
+    const int S = std::min(n, 3);
+    e->ensure_sets(S);
+    if (e->use_graph_)
+      for (int s = 0; s < S; ++s) e->build_graph(s);
+    for (auto* v : {&e->ev_in_, &e->ev_comp_, &e->ev_out_})
+      while (static_cast<int>(v->size()) < S) {
+        cudaEvent_t ev = nullptr;
+        STC_RT(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        v->push_back(ev);
+      }
   }
-  for (auto* v : {&ev_in_, &ev_comp_, &ev_out_})
-    while (static_cast<int>(v->size()) < S) {
-      cudaEvent_t e = nullptr;
-      STC_RT(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-      v->push_back(e);
-    }
+  if (!lead->h2d_) {
+    STC_RT(cudaStreamCreateWithFlags(&lead->h2d_, cudaStreamNonBlocking));
+    STC_RT(cudaStreamCreateWithFlags(&lead->d2h_, cudaStreamNonBlocking));
+  }
+  cudaStream_t h2d = lead->h2d_, d2h = lead->d2h_, comp = lead->stream_;
   // STITCH_CHUNK_TRACE=1: per-chunk timestamps (us since the first H2D) on stderr
   const bool trace = std::getenv("STITCH_CHUNK_TRACE") && *std::getenv("STITCH_CHUNK_TRACE") == '1';
   std::vector<cudaEvent_t> tev;
@@ -699,39 +715,47 @@ void Executor::run_host_chunked(const void* const* in, void* const* out, int nch
     STC_RT(cudaEventRecord(e, st));
     tev.push_back(e);
   };
+  std::vector<size_t> in_off(lead->params_.size(), 0), out_off(lead->g_.outputs.size(), 0);
   // the previous call's work on these streams is complete (we synchronise at
-  // the end), so the first use of every set needs no extra ordering
-  for (int k = 0; k < nchunks; ++k) {
-    const int s = k % S;
+  // the end), so the first use of every (executor, set) needs no ordering
+  for (Executor* e : chunk_exec) {
+    const int j = seen[e]++;
+    const int S = std::min(uses[e], 3);
+    const int s = j % S;
     const size_t su = static_cast<size_t>(s);
-    if (k >= S) STC_RT(cudaStreamWaitEvent(h2d_, ev_comp_[su], 0));  // chunk k-S done reading set s
-    stamp(h2d_);
-    for (size_t i = 0; i < params_.size(); ++i) {
-      const Tensor& t = tensors_.at(g_.node(params_[i]).name);
+    if (j >= S) STC_RT(cudaStreamWaitEvent(h2d, e->ev_comp_[su], 0));  // use j-S done reading set s
+    stamp(h2d);
+    for (size_t i = 0; i < e->params_.size(); ++i) {
+      const Tensor& t = e->tensors_.at(e->g_.node(e->params_[i]).name);
       const bool chunked = in_chunked ? in_chunked[i] != 0 : true;
-      if (!chunked && k >= S) continue;  // shared input: once per set
-      const char* src = static_cast<const char*>(in[i]) + (chunked ? static_cast<size_t>(k) * t.bytes : 0);
-      STC_RT(cudaMemcpyAsync(t.dptr[su], src, t.bytes, cudaMemcpyHostToDevice, h2d_));
+      if (chunked) {
+        STC_RT(cudaMemcpyAsync(t.dptr[su], static_cast<const char*>(in[i]) + in_off[i], t.bytes,
+                               cudaMemcpyHostToDevice, h2d));
+        in_off[i] += t.bytes;
+      } else if (j < S) {  // shared input: once per (executor, set)
+        STC_RT(cudaMemcpyAsync(t.dptr[su], in[i], t.bytes, cudaMemcpyHostToDevice, h2d));
+      }
     }
-    STC_RT(cudaEventRecord(ev_in_[su], h2d_));
-    stamp(h2d_);
-    STC_RT(cudaStreamWaitEvent(stream_, ev_in_[su], 0));
-    if (k >= S) STC_RT(cudaStreamWaitEvent(stream_, ev_out_[su], 0));  // chunk k-S outputs drained
-    launch(stream_, s);
-    STC_RT(cudaEventRecord(ev_comp_[su], stream_));
-    stamp(stream_);
-    STC_RT(cudaStreamWaitEvent(d2h_, ev_comp_[su], 0));
-    for (size_t i = 0; i < g_.outputs.size(); ++i) {
-      const Tensor& t = tensors_.at(g_.node(g_.outputs[i]).name);
-      STC_RT(cudaMemcpyAsync(static_cast<char*>(out[i]) + static_cast<size_t>(k) * t.bytes, t.dptr[su], t.bytes,
-                             cudaMemcpyDeviceToHost, d2h_));
+    STC_RT(cudaEventRecord(e->ev_in_[su], h2d));
+    stamp(h2d);
+    STC_RT(cudaStreamWaitEvent(comp, e->ev_in_[su], 0));
+    if (j >= S) STC_RT(cudaStreamWaitEvent(comp, e->ev_out_[su], 0));  // use j-S outputs drained
+    e->launch(comp, s);
+    STC_RT(cudaEventRecord(e->ev_comp_[su], comp));
+    stamp(comp);
+    STC_RT(cudaStreamWaitEvent(d2h, e->ev_comp_[su], 0));
+    for (size_t i = 0; i < e->g_.outputs.size(); ++i) {
+      const Tensor& t = e->tensors_.at(e->g_.node(e->g_.outputs[i]).name);
+      STC_RT(cudaMemcpyAsync(static_cast<char*>(out[i]) + out_off[i], t.dptr[su], t.bytes, cudaMemcpyDeviceToHost,
+                             d2h));
+      out_off[i] += t.bytes;
     }
-    STC_RT(cudaEventRecord(ev_out_[su], d2h_));
-    stamp(d2h_);
+    STC_RT(cudaEventRecord(e->ev_out_[su], d2h));
+    stamp(d2h);
   }
-  STC_RT(cudaStreamSynchronize(d2h_));
-  STC_RT(cudaStreamSynchronize(stream_));
-  STC_RT(cudaStreamSynchronize(h2d_));
+  STC_RT(cudaStreamSynchronize(d2h));
+  STC_RT(cudaStreamSynchronize(comp));
+  STC_RT(cudaStreamSynchronize(h2d));
   if (trace) {
     std::ostringstream o;
     o << "[chunk-trace] h2d_start h2d_end comp_end d2h_end (us)";

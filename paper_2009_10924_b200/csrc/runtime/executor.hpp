@@ -89,6 +89,12 @@ class Executor {
   // chunk k and D2H of chunk k-1 overlap on three streams (copy engines are
   // per direction), through min(nchunks, 3) device buffer sets.
   void run_host_chunked(const void* const* in, void* const* out, int nchunks, const int* in_chunked);
+  // Generalisation: chunk k runs on chunk_exec[k] (shard graphs of one graph,
+  // possibly of different batch sizes -- e.g. small first/last chunks to
+  // shorten pipeline fill and drain); chunk offsets accumulate each chunk
+  // executor's tensor bytes.  Copies on the first executor's streams.
+  static void run_host_pipeline(const std::vector<Executor*>& chunk_exec, const void* const* in,
+                                void* const* out, const int* in_chunked);
   // Zero-copy host execution: when every parameter and output buffer is
   // pinned host memory mapped into the device address space (cudaHostAlloc /
   // torch pin_memory under UVA), the plan's kernels read their inputs and

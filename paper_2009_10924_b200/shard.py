@@ -33,7 +33,12 @@ class ShardRule:
         return self.full // n
 
     def graph_text(self, text: str, n: int) -> str:
-        b = self.shard_size(n)
+        return self.extent_text(text, self.shard_size(n))
+
+    def extent_text(self, text: str, b: int) -> str:
+        """the graph with the sharded axis set to extent b (any 1 <= b <= full)"""
+        if not 1 <= b <= self.full:
+            raise ValueError("extent %d outside [1, %d]" % (b, self.full))
         return re.sub(self.token, lambda m: m.group(0).replace(str(self.full), str(b)), text)
 
     def slice_inputs(self, inputs: Dict[str, np.ndarray], n: int, rank: int) -> Dict[str, np.ndarray]:

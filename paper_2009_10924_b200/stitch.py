@@ -77,6 +77,7 @@ def lib():
         "stc_exec_run_host": (ip, [vp, P(vp), P(vp)]), "stc_exec_upload": (ip, [vp, P(vp)]),
         "stc_exec_run_host_chunked": (ip, [vp, P(vp), P(vp), ip, P(ip)]),
         "stc_exec_run_host_zero_copy": (ip, [vp, P(vp), P(vp)]),
+        "stc_exec_run_host_pipeline": (ip, [P(vp), P(ip), ip, P(vp), P(vp), P(ip)]),
         "stc_exec_trace": (ip, [vp, P(ctypes.c_double), P(ctypes.c_double)]),
         "stc_exec_launch": (ip, [vp, vp, ip]), "stc_exec_prepare_sets": (ip, [vp, ip]),
         "stc_exec_download": (ip, [vp, P(vp)]),
@@ -385,17 +386,30 @@ class Executor:
 
 
 class ChunkedExecutor:
-    """Host-buffer execution of a batch-sharded graph as `nchunks` pipelined
-    chunks: the chunk graph (batch / nchunks, re-planned by the bit-exact
-    planner for its own shape) runs on device while the next chunk's H2D and
-    the previous chunk's D2H are in flight (stc_exec_run_host_chunked).
-    `rule` is a shard.ShardRule whose sharded axis is 0 for every chunked tensor."""
+    """Host-buffer execution of a batch-sharded graph as pipelined chunks:
+    each chunk graph (re-planned by the bit-exact planner for its own shape)
+    runs on device while the next chunk's H2D and the previous chunk's D2H are
+    in flight.  `chunks` = number of equal chunks, or a list of chunk extents
+    along the sharded axis (e.g. [1, 3, 4, 4, 4, 4, 4, 4, 3, 1]: small first /
+    last chunks shorten the pipeline's fill and drain) -> one executor per
+    distinct extent, stc_exec_run_host_pipeline.  `rule` is a
+    shard.ShardRule whose sharded axis is 0 for every chunked tensor."""
 
-    def __init__(self, text: str, rule, nchunks: int, cfg: str = "b200", device: int = 0):
-        self.rule, self.nchunks = rule, nchunks
+    def __init__(self, text: str, rule, chunks, cfg: str = "b200", device: int = 0):
+        if isinstance(chunks, int):
+            chunks = [rule.shard_size(chunks)] * chunks
+        if sum(chunks) != rule.full:
+            raise StitchError(4, "chunk extents %s do not sum to %d" % (chunks, rule.full))
+        self.rule, self.chunks = rule, list(chunks)
+        self.nchunks = len(chunks)
         self.full = Graph(text)
-        self.chunk_graph = Graph(rule.graph_text(text, nchunks))
-        self.ex = Executor(Plan(self.chunk_graph, cfg), device=device)
+        self.execs = {}
+        for b in sorted(set(chunks)):
+            self.execs[b] = Executor(Plan(Graph(rule.extent_text(text, b)), cfg), device=device)
+        self.ex = self.execs[chunks[0]]
+        sizes = sorted(self.execs)
+        self._handles = (ctypes.c_void_p * len(sizes))(*[self.execs[b]._h.value for b in sizes])
+        self._of_chunk = (ctypes.c_int * len(chunks))(*[sizes.index(b) for b in chunks])
         for t in self.full.params:
             if rule.axis_of.get(t.name) not in (None, 0):
                 raise StitchError(4, "input %s is not sharded along axis 0" % t.name)
@@ -416,17 +430,8 @@ class ChunkedExecutor:
             if not (o.flags.c_contiguous and o.dtype == t.np_dtype and o.size == t.count):
                 raise StitchError(4, "bad output buffer for " + t.name)
         op = (ctypes.c_void_p * max(1, len(outs)))(*[o.ctypes.data for o in outs])
-        _check(lib().stc_exec_run_host_chunked(self.ex._h, ip, op, self.nchunks, self._flags))
+        _check(lib().stc_exec_run_host_pipeline(self._handles, self._of_chunk, self.nchunks, ip, op, self._flags))
         return {t.name: o for t, o in zip(self.full.outputs, outs)}
-
-
-def run_pipeline(graph_path: str, device_config: Optional[str] = None, k: int = 3, beam_width: int = 3,
-                 output_dir: str = "out", emit_dot: bool = False, run_sim: bool = False,
-                 run_baseline: bool = False, seed: int = 0) -> int:
-    """stitch::run_pipeline: 0 ok, 1 parse/config/planner error, 2 sim mismatch."""
-    return lib().stc_run_pipeline(graph_path.encode(), cfg_path(device_config).encode(), k, beam_width,
-                                  output_dir.encode(), int(emit_dot), int(run_sim), int(run_baseline),
-                                  seed)
 
 
 # ---- host-side utilities (sim.hpp) ----------------------------------------

@@ -103,7 +103,8 @@ def test_pipeline_run_sim(tmp_path):
 
 
 @pytest.mark.parametrize("name,nchunks", [("attn_softmax", 8), ("ln_4096x768", 4), ("bert_resln", 8),
-                                          ("bert_gelu", 4)])
+                                          ("bert_gelu", 4), ("attn_softmax", [1, 3, 4, 4, 4, 4, 4, 4, 3, 1]),
+                                          ("ln_4096x768", [128, 1024, 2048, 768, 128])])
 def test_chunked_host_run_matches_full_plan(name, nchunks):
     """stc_exec_run_host_chunked (pipelined H2D / graph / D2H over batch
     chunks, each chunk re-planned for its shape) == the full-batch plan, bit

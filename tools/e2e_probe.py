@@ -24,9 +24,17 @@ for name in sys.argv[1:] or ["attn_softmax", "ln_4096x768", "bert_gelu", "bert_r
         return (time.perf_counter() - t0) / reps
 
     rows = [("plain", lambda: ex.run(pin_in, out=pin_out))]
-    for n in (4, 8):
-        cx = stitch.ChunkedExecutor(text, shard.RULES[name], n)
-        rows.append(("chunked%d" % n, lambda cx=cx: cx.run(pin_in, out=pin_out)))
+    full = shard.RULES[name].full
+    shapes = {"chunked4": 4, "chunked8": 8}
+    if full == 32:
+        shapes.update({"taper_1_3_4x6_3_1": [1, 3, 4, 4, 4, 4, 4, 4, 3, 1], "taper_2_6x5_2": [2, 6, 6, 6, 6, 4, 2],
+                       "taper_1_2_4x6_4_1": [1, 2, 4, 4, 4, 4, 4, 4, 4, 1]})
+    else:
+        u = full // 32
+        shapes.update({"taper_1_3_4x6_3_1": [u * c for c in [1, 3, 4, 4, 4, 4, 4, 4, 3, 1]]})
+    for label, ch in shapes.items():
+        cx = stitch.ChunkedExecutor(text, shard.RULES[name], ch)
+        rows.append((label, lambda cx=cx: cx.run(pin_in, out=pin_out)))
     rows.append(("zero_copy", lambda: ex.run_zero_copy(pin_in, pin_out)))
     for label, fn in rows:
         s = timed(fn)
