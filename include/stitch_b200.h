@@ -91,6 +91,17 @@ enum {
  * a JSON description of its kernels */
 int stc_codegen(const stc_plan* p, int mode, char** cuda_source, char** kernels_json);
 int stc_exec_create(const stc_plan* p, int device, int mode, stc_exec** out);
+/* Asynchronous compilation (the paper's async mode): returns
+ * as soon as code generation is done; NVRTC runs on a worker thread.
+ * stc_exec_ready() polls (1 = compiled), stc_exec_wait() blocks; every
+ * execution call waits implicitly. */
+int stc_exec_create_async(const stc_plan* p, int device, int mode, stc_exec** out);
+int stc_exec_ready(const stc_exec* e);
+int stc_exec_wait(stc_exec* e);
+/* Persistent cubin-cache warm-up: generate and NVRTC-compile the modules of n
+ * plans on `threads` host threads (no GPU needed), so later stc_exec_create
+ * calls are cache hits.  *compiled / *cached: modules built now / found. */
+int stc_cache_warm(const stc_plan* const* plans, int n, int mode, int threads, int* compiled, int* cached);
 void stc_exec_destroy(stc_exec* e);
 int stc_exec_num_kernels(const stc_exec* e);
 /* JSON array: per launched kernel {name, template, pattern, grid, block, smem, bytes} */

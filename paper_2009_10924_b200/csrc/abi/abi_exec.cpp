@@ -1,3 +1,6 @@
+#include <thread>
+#include <mutex>
+#include <atomic>
 // extern "C" boundary, device half: code generation, NVRTC, the CUDA-Graph
 // executor (include/stitch_b200.h).
 #include <cstring>
@@ -44,6 +47,54 @@ int stc_exec_create(const stc_plan* p, int device, int mode, stc_exec** out) {
                                             mode_of(mode), (mode & STC_EXEC_NO_GRAPH) == 0,
                                             (mode & STC_EXEC_GEMM) != 0);
     *out = e.release();
+  });
+}
+
+int stc_exec_create_async(const stc_plan* p, int device, int mode, stc_exec** out) {
+  return guarded([&] {
+    auto e = std::make_unique<stc_exec>();
+    e->ex = std::make_unique<gpu::Executor>(p->graph, p->plan, p->kernels, p->models.machine, device,
+                                            mode_of(mode), (mode & STC_EXEC_NO_GRAPH) == 0,
+                                            (mode & STC_EXEC_GEMM) != 0, /*async_compile=*/true);
+    *out = e.release();
+  });
+}
+
+int stc_exec_ready(const stc_exec* e) { return e && e->ex->ready() ? 1 : 0; }
+
+int stc_exec_wait(stc_exec* e) {
+  return guarded([&] { e->ex->ensure_ready(); });
+}
+
+int stc_cache_warm(const stc_plan* const* plans, int n, int mode, int threads, int* compiled, int* cached) {
+  return guarded([&] {
+    std::vector<std::string> sources;
+    for (int i = 0; i < n; ++i)
+      sources.push_back(gpu::generate_plan_kernels(plans[i]->graph, plans[i]->plan, plans[i]->kernels,
+                                                   plans[i]->models.machine, mode_of(mode), 148,
+                                                   (mode & STC_EXEC_GEMM) != 0)
+                            .source);
+    std::atomic<int> next{0}, comp{0}, hit{0};
+    std::string err;
+    std::mutex mu;
+    auto work = [&] {
+      for (int i; (i = next++) < static_cast<int>(sources.size());) {
+        try {
+          bool h = false;
+          gpu::compile_cubin(sources[static_cast<size_t>(i)], gpu::default_nvrtc_options(), nullptr, &h);
+          (h ? hit : comp)++;
+        } catch (const std::exception& ex) {
+          std::lock_guard<std::mutex> lk(mu);
+          if (err.empty()) err = ex.what();
+        }
+      }
+    };
+    std::vector<std::thread> pool;
+    for (int t = 0; t < std::max(1, std::min(threads, n)); ++t) pool.emplace_back(work);
+    for (auto& t : pool) t.join();
+    if (!err.empty()) throw std::runtime_error(err);
+    if (compiled) *compiled = comp;
+    if (cached) *cached = hit;
   });
 }
 

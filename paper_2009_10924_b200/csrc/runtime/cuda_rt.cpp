@@ -9,6 +9,8 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <functional>
+#include <thread>
 #include <fstream>
 #include <mutex>
 #include <sstream>
@@ -105,7 +107,8 @@ std::vector<std::string> default_nvrtc_options() {
 }
 
 std::string compile_cubin(const std::string& source, const std::vector<std::string>& options,
-                          std::string* key_out) {
+                          std::string* key_out, bool* cache_hit) {
+  if (cache_hit) *cache_hit = false;
   int maj = 0, min = 0;
   STC_NVRTC(nvrtcVersion(&maj, &min));
   std::string salt = std::to_string(maj) + "." + std::to_string(min);
@@ -122,7 +125,10 @@ std::string compile_cubin(const std::string& source, const std::vector<std::stri
     if (in) {
       std::ostringstream ss;
       ss << in.rdbuf();
-      if (!ss.str().empty()) return ss.str();
+      if (!ss.str().empty()) {
+        if (cache_hit) *cache_hit = true;
+        return ss.str();
+      }
     }
   }
   nvrtcProgram prog;
@@ -151,7 +157,9 @@ std::string compile_cubin(const std::string& source, const std::vector<std::stri
   STC_NVRTC(nvrtcGetCUBIN(prog, cubin.data()));
   nvrtcDestroyProgram(&prog);
   mkdirs(dir);
-  const std::string tmp = path + ".tmp" + std::to_string(getpid());
+  // unique per process AND thread (cache warm-up compiles concurrently)
+  const std::string tmp = path + ".tmp" + std::to_string(getpid()) + "_" +
+                          std::to_string(std::hash<std::thread::id>{}(std::this_thread::get_id()));
   {
     std::ofstream out(tmp, std::ios::binary);
     out.write(cubin.data(), static_cast<std::streamsize>(cubin.size()));

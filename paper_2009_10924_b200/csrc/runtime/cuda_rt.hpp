@@ -33,7 +33,7 @@ const DeviceInfo& device_init(int ordinal);
 // NVRTC for sm_100a; returns the cubin image, using/refreshing the cache.
 // `key_out` receives the content hash that names the cache entry.
 std::string compile_cubin(const std::string& source, const std::vector<std::string>& options,
-                          std::string* key_out = nullptr);
+                          std::string* key_out = nullptr, bool* cache_hit = nullptr);
 std::string cubin_cache_dir();
 std::vector<std::string> default_nvrtc_options();
 

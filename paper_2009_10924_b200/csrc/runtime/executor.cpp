@@ -3,6 +3,8 @@
 #include <cublasLt.h>
 
 #include <algorithm>
+#include <chrono>
+#include <future>
 #include <cstdio>
 #include <cctype>
 #include <cstdlib>
@@ -82,7 +84,7 @@ bool opaque_is_matmul(const CompGraph& g, int v, int64_t* m, int64_t* n, int64_t
 
 Executor::Executor(const CompGraph& g, const FusionPlan& plan,
                    const std::map<std::string, KernelPlan>& kernels, const MachineModel& model,
-                   int device, ExecMode mode, bool use_graph, bool gemm_opaque)
+                   int device, ExecMode mode, bool use_graph, bool gemm_opaque, bool async_compile)
     : g_(g), use_graph_(use_graph) {
   dev_ = &device_init(device);
   if (const char* v = std::getenv("STITCH_PDL")) pdl_ = *v != '0';
@@ -93,14 +95,35 @@ Executor::Executor(const CompGraph& g, const FusionPlan& plan,
   if (const char* v = std::getenv("STITCH_PDL_EDGES")) pdl_edges_ = *v != '0';
   STC_RT(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
   plan_launches(plan, kernels, model, mode, gemm_opaque);
-  {
-    auto opts = default_nvrtc_options();
-    if (const char* t = std::getenv("STITCH_TRACE"); t && *t == '1') {
-      opts.push_back("-DSTITCH_TRACE");
-      tracing_ = true;
-    }
-    module_ = std::make_unique<Module>(compile_cubin(source_, opts));
+  auto opts = default_nvrtc_options();
+  if (const char* t = std::getenv("STITCH_TRACE"); t && *t == '1') {
+    opts.push_back("-DSTITCH_TRACE");
+    tracing_ = true;
   }
+  ensure_sets(1);
+  if (async_compile) {
+    // NVRTC on a worker thread (no device work); the first call that needs
+    // the kernels waits for it (ensure_ready)
+    pending_ = std::async(std::launch::async, [src = source_, opts] { return compile_cubin(src, opts); });
+    return;
+  }
+  finish_init(compile_cubin(source_, opts));
+}
+
+bool Executor::ready() const {
+  return module_ != nullptr ||
+         (pending_.valid() && pending_.wait_for(std::chrono::seconds(0)) == std::future_status::ready);
+}
+
+void Executor::ensure_ready() {
+  if (module_) return;
+  if (!pending_.valid()) throw std::runtime_error("[exec] executor has no module");
+  STC_RT(cudaSetDevice(dev_->ordinal));
+  finish_init(pending_.get());
+}
+
+void Executor::finish_init(const std::string& cubin) {
+  module_ = std::make_unique<Module>(cubin);
   for (size_t ki = 0; ki < specs_.size(); ++ki) {
     const KernelSpec& k = specs_[ki];
     if (k.is_gemm) {
@@ -150,7 +173,6 @@ Executor::Executor(const CompGraph& g, const FusionPlan& plan,
     fns_.push_back(f);
   }
   compute_deps();
-  ensure_sets(1);
 }
 
 void Executor::promote_edges(cudaGraph_t graph) {
@@ -576,6 +598,7 @@ void Executor::launch_gemm(size_t i, void* a, void* b, void* c, cudaStream_t s) 
 }
 
 void Executor::build_graph(int set) {
+  ensure_ready();
   auto& ge = graphs_[static_cast<size_t>(set)];
   if (ge) return;
   for (int attempt = 0; attempt < 2; ++attempt) {
@@ -624,6 +647,7 @@ void Executor::download(void* const* out, int set) {
 }
 
 void Executor::launch(cudaStream_t s, int set) {
+  ensure_ready();
   if (!s) s = stream_;
   ensure_sets(set + 1);
   if (!use_graph_) {
@@ -637,6 +661,7 @@ void Executor::launch(cudaStream_t s, int set) {
 void Executor::sync() { STC_RT(cudaStreamSynchronize(stream_)); }
 
 void Executor::run_host(const void* const* in, void* const* out) {
+  ensure_ready();
   upload(in, 0);
   launch(stream_, 0);
   download(out, 0);
@@ -644,6 +669,7 @@ void Executor::run_host(const void* const* in, void* const* out) {
 }
 
 bool Executor::run_host_zero_copy(const void* const* in, void* const* out) {
+  ensure_ready();
   std::map<std::string, void*> bind;
   auto mapped = [&](const void* h, size_t bytes) -> void* {
     cudaPointerAttributes a{};
@@ -688,6 +714,7 @@ void Executor::run_host_pipeline(const std::vector<Executor*>& chunk_exec, const
       throw std::runtime_error("[exec] pipeline chunks come from different graphs");
   std::map<Executor*, int> uses, seen;
   for (Executor* e : chunk_exec) ++uses[e];
+  for (auto& [e, n] : uses) e->ensure_ready();
   for (auto& [e, n] : uses) {
     const int S = std::min(n, 3);
     e->ensure_sets(S);
@@ -770,6 +797,7 @@ void Executor::run_host_pipeline(const std::vector<Executor*>& chunk_exec, const
 }
 
 void Executor::prepare_sets(int sets) {
+  ensure_ready();
   sets = std::max(1, sets);
   ensure_sets(sets);
   // replicate set-0 inputs so every set computes on the same data
@@ -784,6 +812,7 @@ void Executor::prepare_sets(int sets) {
 }
 
 int Executor::prepare_batches(int sets, int batch) {
+  ensure_ready();
   batch = std::max(1, batch);
   sets = std::max(batch, (std::max(1, sets) + batch - 1) / batch * batch);
   prepare_sets(sets);
@@ -808,11 +837,13 @@ int Executor::prepare_batches(int sets, int batch) {
 }
 
 void Executor::launch_batch(cudaStream_t s, int index) {
+  ensure_ready();
   if (batch_graphs_.empty()) throw std::runtime_error("[exec] prepare_batches() first");
   STC_RT(cudaGraphLaunch(batch_graphs_[static_cast<size_t>(index) % batch_graphs_.size()], s ? s : stream_));
 }
 
 double Executor::time(int iters, int warmup, int sets, std::vector<double>* per_kernel, int batch) {
+  ensure_ready();
   sets = std::max(1, sets);
   prepare_sets(sets);
   cudaEvent_t e0, e1;
@@ -871,6 +902,7 @@ double Executor::time(int iters, int warmup, int sets, std::vector<double>* per_
 }
 
 std::vector<std::pair<double, double>> Executor::trace(int set) {
+  ensure_ready();
   if (!tracing_) throw std::runtime_error("[exec] trace() needs an executor built with STITCH_TRACE=1");
   size_t bytes = 0;
   void* buf = module_->global("stc_trace_", &bytes);

@@ -12,6 +12,7 @@
 
 #include <cuda_runtime.h>
 
+#include <future>
 #include <map>
 #include <memory>
 #include <string>
@@ -51,7 +52,8 @@ class Executor {
  public:
   Executor(const CompGraph& g, const FusionPlan& plan,
            const std::map<std::string, KernelPlan>& kernels, const MachineModel& model,
-           int device, ExecMode mode, bool use_graph = true, bool gemm_opaque = false);
+           int device, ExecMode mode, bool use_graph = true, bool gemm_opaque = false,
+           bool async_compile = false);
   ~Executor();
   Executor(const Executor&) = delete;
   Executor& operator=(const Executor&) = delete;
@@ -66,6 +68,11 @@ class Executor {
   };
 
   const std::vector<KernelSpec>& kernels() const { return specs_; }
+  // async construction (paper's asynchronous compilation mode): NVRTC runs on
+  // a worker thread; ready() polls, ensure_ready() waits + loads the module.
+  // Every execution entry point calls ensure_ready() first.
+  bool ready() const;
+  void ensure_ready();
   const std::string& source() const { return source_; }
   const std::vector<int>& param_vertices() const { return params_; }
   const std::vector<int>& output_vertices() const { return g_.outputs; }
@@ -129,6 +136,7 @@ class Executor {
   // Returns the kernel left at the tail of `origin`.
   int capture_plan(int set, cudaStream_t origin, int prev);
   void compute_deps();
+  void finish_init(const std::string& cubin);  // load module, resolve kernels, GEMM setup
   // turn every kernel->kernel edge of a captured plan graph into a
   // programmatic (PDL) edge: every kernel griddepcontrol.wait()s before its
   // first read, so the dependent may launch while its producers drain
@@ -140,6 +148,7 @@ class Executor {
   std::vector<KernelSpec> specs_;
   std::string source_;
   std::unique_ptr<Module> module_;
+  std::future<std::string> pending_;  // async NVRTC compile
   std::vector<cudaKernel_t> fns_;
   std::vector<int> params_;
   std::map<std::string, Tensor> tensors_;

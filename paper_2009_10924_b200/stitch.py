@@ -72,6 +72,8 @@ def lib():
         "stc_plan_kernel": (ip, [vp, cp, P(ip), ip, P(vp)]),
         "stc_codegen": (ip, [vp, ip, P(vp), P(vp)]),
         "stc_exec_create": (ip, [vp, ip, ip, P(vp)]), "stc_exec_destroy": (None, [vp]),
+        "stc_exec_create_async": (ip, [vp, ip, ip, P(vp)]), "stc_exec_ready": (ip, [vp]),
+        "stc_exec_wait": (ip, [vp]), "stc_cache_warm": (ip, [P(vp), ip, ip, ip, P(ip), P(ip)]),
         "stc_exec_num_kernels": (ip, [vp]), "stc_exec_describe": (ip, [vp, P(vp)]),
         "stc_exec_source": (ip, [vp, P(vp)]),
         "stc_exec_run_host": (ip, [vp, P(vp), P(vp)]), "stc_exec_upload": (ip, [vp, P(vp)]),
@@ -242,6 +244,16 @@ class Plan:
             self._h = None
 
 
+def warm_cache(plans: Sequence["Plan"], mode: str = "stitched", threads: int = 8, gemm: bool = False):
+    """NVRTC-compile the modules of `plans` into the persistent cubin cache
+    (no GPU needed) -> (compiled_now, already_cached)"""
+    arr = (ctypes.c_void_p * max(1, len(plans)))(*[p._h.value for p in plans])
+    c, h = ctypes.c_int(), ctypes.c_int()
+    _check(lib().stc_cache_warm(arr, len(plans), MODES[mode] | (GEMM if gemm else 0), threads, ctypes.byref(c),
+                                ctypes.byref(h)))
+    return c.value, h.value
+
+
 def plan_kernel(graph: Graph, vertices: Sequence[int], cfg: Optional[str] = None) -> Optional[str]:
     """stitch::plan_kernel for one vertex set -> program text, None if infeasible."""
     arr = (ctypes.c_int * len(vertices))(*vertices)
@@ -264,12 +276,22 @@ class Executor:
     """A plan compiled for one B200 and replayed as one CUDA Graph
     (eval_plan / run_program / eval_reference, src/sim.cpp:231-514)."""
 
-    def __init__(self, plan: Plan, device: int = 0, mode: str = "stitched", graph: bool = True, gemm: bool = False):
+    def __init__(self, plan: Plan, device: int = 0, mode: str = "stitched", graph: bool = True, gemm: bool = False,
+                 async_compile: bool = False):
         self.plan = plan
         self.g = plan.graph
         self._h = ctypes.c_void_p()
         flags = MODES[mode] | (0 if graph else NO_GRAPH) | (GEMM if gemm else 0)
-        _check(lib().stc_exec_create(plan._h, device, flags, ctypes.byref(self._h)))
+        create = lib().stc_exec_create_async if async_compile else lib().stc_exec_create
+        _check(create(plan._h, device, flags, ctypes.byref(self._h)))
+
+    @property
+    def ready(self) -> bool:
+        """module compiled (always True for synchronous construction)"""
+        return bool(lib().stc_exec_ready(self._h))
+
+    def wait(self):
+        _check(lib().stc_exec_wait(self._h))
 
     @property
     def num_kernels(self) -> int:
@@ -432,6 +454,15 @@ class ChunkedExecutor:
         op = (ctypes.c_void_p * max(1, len(outs)))(*[o.ctypes.data for o in outs])
         _check(lib().stc_exec_run_host_pipeline(self._handles, self._of_chunk, self.nchunks, ip, op, self._flags))
         return {t.name: o for t, o in zip(self.full.outputs, outs)}
+
+
+def run_pipeline(graph_path: str, device_config: Optional[str] = None, k: int = 3, beam_width: int = 3,
+                 output_dir: str = "out", emit_dot: bool = False, run_sim: bool = False,
+                 run_baseline: bool = False, seed: int = 0) -> int:
+    """stitch::run_pipeline: 0 ok, 1 parse/config/planner error, 2 sim mismatch."""
+    return lib().stc_run_pipeline(graph_path.encode(), cfg_path(device_config).encode(), k, beam_width,
+                                  output_dir.encode(), int(emit_dot), int(run_sim), int(run_baseline),
+                                  seed)
 
 
 # ---- host-side utilities (sim.hpp) ----------------------------------------

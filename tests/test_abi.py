@@ -81,3 +81,16 @@ def test_dataflow_templates_chosen_for_fixtures():
     for name, tmpl in want.items():
         _, kernels = stitch.Plan(stitch.Graph(fixture_graphs()[name]), "v100").codegen()
         assert [k["template"].split("+")[0] for k in kernels] == [tmpl], name
+
+
+def test_cubin_cache_warm_up(tmp_path, monkeypatch):
+    """stc_cache_warm: NVRTC-compiles plan modules into
+    the persistent cache on host threads without a GPU; a second warm-up is
+    all cache hits"""
+    monkeypatch.setenv("STITCH_CACHE_DIR", str(tmp_path))
+    stitch = _stitch()
+    from tests.conftest import fixture_graphs
+    plans = [stitch.Plan(stitch.Graph(t), "b200") for _, t in sorted(fixture_graphs().items())[:4]]
+    assert stitch.warm_cache(plans, threads=4) == (4, 0)
+    assert stitch.warm_cache(plans, threads=4) == (0, 4)
+    assert len([f for f in os.listdir(tmp_path) if f.endswith(".cubin")]) == 4

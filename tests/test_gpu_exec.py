@@ -172,3 +172,18 @@ def test_model_mode_gemm_bert_layer(monkeypatch, precision):
     again = ex.run(inputs)
     for k in got:
         assert np.array_equal(again[k], got[k])
+
+
+def test_async_compile_matches_sync():
+    """stc_exec_create_async: NVRTC on a worker thread, first run waits"""
+    stitch = _stitch()
+    text = config_graph("attn_softmax")
+    g = stitch.Graph(text)
+    plan = stitch.Plan(g, "b200")
+    inputs = stitch.random_inputs(g, 4)
+    want = stitch.Executor(plan).run(inputs)
+    ex = stitch.Executor(plan, async_compile=True)
+    got = ex.run(inputs)  # implicit wait
+    assert ex.ready
+    for k in want:
+        assert np.array_equal(got[k], want[k])
