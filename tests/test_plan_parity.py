@@ -47,20 +47,28 @@ def test_plan_bytes_slow(case):
 
 
 def test_random_graphs():
+    """100 random graphs x 2 cfgs; planned on host threads (ctypes releases
+    the GIL and every Plan owns its CostModels, as in the reference)"""
+    from concurrent.futures import ThreadPoolExecutor
     stitch = _stitch()
     with open(os.path.join(GOLD, "random_plans.json")) as f:
         rnd = json.load(f)
     assert len(rnd) == 100
-    for seed, entry in rnd.items():
+
+    def check(item):
+        seed, entry, cfg = item
         g = stitch.Graph(entry["graph"])
-        for cfg in ("v100", "b200"):
-            plan = stitch.Plan(g, cfg)
-            pj = plan.json()
-            assert pj == entry[cfg]["plan_json"], (seed, cfg)
-            keys = [p["key"] for p in json.loads(pj)["patterns"]]
-            for i, k in enumerate(keys):
-                h = hashlib.sha256(plan.kernel_text(i).encode()).hexdigest()
-                assert h == entry[cfg]["programs_sha"][k], (seed, cfg, k)
+        plan = stitch.Plan(g, cfg)
+        pj = plan.json()
+        assert pj == entry[cfg]["plan_json"], (seed, cfg)
+        keys = [p["key"] for p in json.loads(pj)["patterns"]]
+        for i, k in enumerate(keys):
+            h = hashlib.sha256(plan.kernel_text(i).encode()).hexdigest()
+            assert h == entry[cfg]["programs_sha"][k], (seed, cfg, k)
+
+    work = [(seed, entry, cfg) for seed, entry in rnd.items() for cfg in ("v100", "b200")]
+    with ThreadPoolExecutor(max_workers=min(16, os.cpu_count() or 1)) as pool:
+        list(pool.map(check, work))
 
 
 def test_plan_kernel_infeasible_and_explicit_patterns():
