@@ -498,6 +498,15 @@ void store_val(Emitter& em, const CompGraph& g, int v, const Coords& c, const Va
     em.line(pre + "stv(" + ptr + ", " + em.linear(v, c, k) + ", " + val.at(k) + ");");
 }
 
+// 128-bit chunks in flight per thread per grid-stride step: 2, with up to
+// 32 CTAs per SM so big domains take ~one pass (B200 sweep,
+// profiles/r01/local_sweep.jsonl: bias+GELU 18.4 -> 16.3 us)
+int local_unroll(int64_t chunks, int block) {
+  (void)chunks, (void)block;
+  if (const int u = env_int("STITCH_LOCAL_U", 0); u > 0) return u;
+  return 2;
+}
+
 // local: grid-stride over W-wide chunks of the domain, U chunks per thread
 void emit_local(Emitter& em, const CompGraph& g, const Body& b) {
   const std::vector<int>& D = b.dims_a;
@@ -505,7 +514,7 @@ void emit_local(Emitter& em, const CompGraph& g, const Body& b) {
   em.W = (!D.empty() && D.back() % 4 == 0) ? 4 : 1;
   const int64_t chunks = N / em.W;
   const int B = em.block;
-  const int U = chunks >= int64_t(B) * kSmCount * 8 ? 4 : 2;
+  const int U = local_unroll(chunks, B);
   em.line("// local body: domain " + std::to_string(N) + " elements, vector " + std::to_string(em.W));
   em.open("for (i64 c0_ = (i64)vbid * " + std::to_string(B * U) + " + threadIdx.x; c0_ < " +
           std::to_string(chunks) + "; c0_ += (i64)vgrid * " + std::to_string(B * U) + ")");
@@ -1037,9 +1046,9 @@ KernelSpec generate_pattern_kernel(const CompGraph& g, const std::vector<int>& v
       const int64_t N = prod(b.dims_a);
       const int w = (!b.dims_a.empty() && b.dims_a.back() % 4 == 0) ? 4 : 1;
       const int64_t chunks = N / w;
-      const int U = chunks >= int64_t(block) * kSmCount * 8 ? 4 : 2;
+      const int U = local_unroll(chunks, block);
       b.blocks = static_cast<int>(std::clamp<int64_t>((chunks + int64_t(block) * U - 1) / (int64_t(block) * U), 1,
-                                                      int64_t(kSmCount) * 16));
+                                                      int64_t(kSmCount) * env_int("STITCH_LOCAL_CTAS", 32)));
     } else if (b.kind == Kind::Row) {
       const RowParams rp = row_params(b.dims_b, block);
       const int64_t rows = prod(b.dims_a), L = prod(b.dims_b), ntiles = (rows + rp.RPB - 1) / rp.RPB;
