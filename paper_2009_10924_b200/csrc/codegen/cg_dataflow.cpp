@@ -1052,7 +1052,7 @@ KernelSpec generate_pattern_kernel(const CompGraph& g, const std::vector<int>& v
     } else if (b.kind == Kind::Row) {
       const RowParams rp = row_params(b.dims_b, block);
       const int64_t rows = prod(b.dims_a), L = prod(b.dims_b), ntiles = (rows + rp.RPB - 1) / rp.RPB;
-      b.blocks = static_cast<int>(std::clamp<int64_t>(ntiles, 1, int64_t(kSmCount) * 16));
+      b.blocks = static_cast<int>(std::clamp<int64_t>(ntiles, 1, int64_t(kSmCount) * env_int("STITCH_ROW_CTAS", 16)));
       // dry run: which inputs does the body read at its own (row, chunk) coordinates?
       // opt-in (STITCH_STAGE=1): measured slower than register-resident rows
       // when each SM only sees 1-3 tiles (C1-C3 sizes), see DESIGN.md §5

@@ -187,3 +187,38 @@ def test_async_compile_matches_sync():
     assert ex.ready
     for k in want:
         assert np.array_equal(got[k], want[k])
+
+
+def _ln_text(rows, cols):
+    t = config_graph("ln2pass_4096x768").replace("4096", str(rows)).replace("768", str(cols))
+    return t.replace("0.0013020833333333333", repr(1.0 / cols))
+
+
+def _softmax_text(rows, cols):
+    return ("x = parameter : f32[%d,%d]\nm = reduce_max(x) axes=1\nmb = broadcast(m) dims=0 : f32[%d,%d]\n"
+            "sh = sub(x, mb)\ne = exp(sh)\ns = reduce_sum(e) axes=1\nsb = broadcast(s) dims=0 : f32[%d,%d]\n"
+            "y = div(e, sb)\noutput y\n" % (rows, cols, rows, cols, rows, cols))
+
+
+def _colreduce_text(rows, cols):
+    return config_graph("colreduce").replace("16384", str(rows)).replace("1024", str(cols))
+
+
+EDGE_SHAPES = {
+    "ln_long_rows_smem_team": _ln_text(3, 5000),      # TPR 256: cross-warp team reduction, 512-thread CTAs
+    "ln_single_row": _ln_text(1, 768),                # fewer rows than one CTA's teams
+    "softmax_w2": _softmax_text(7, 130),              # rows of 130: 64-bit vectors, partial chunks
+    "softmax_w1": _softmax_text(33, 17),              # odd rows: scalar path
+    "softmax_many_short_rows": _softmax_text(20000, 8),
+    "colreduce_odd_cols": _colreduce_text(1000, 70),  # partial column strips, scalar lanes
+    "colreduce_few_rows": _colreduce_text(5, 4096),   # one slab per strip
+    "colreduce_tall": _colreduce_text(70001, 36),     # many slabs, ragged last slab
+}
+
+
+@pytest.mark.parametrize("name", sorted(EDGE_SHAPES))
+def test_template_edge_shapes(name):
+    """template edge cases (ragged rows/columns, vector widths 1/2/4, team
+    sizes from 1 to 256 threads, single row / slab) under the B200 profile"""
+    ex = _check(EDGE_SHAPES[name], "b200", "stitched", 5)
+    assert all(k["template"] != "program" for k in ex.describe()), name
