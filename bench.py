@@ -32,6 +32,8 @@ import sys
 import threading
 import time
 
+import numpy as np
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -209,12 +211,19 @@ def main():
     import torch
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    # one GPU per rank; STITCH_DIST_BACKEND=gloo + fewer GPUs than ranks is a
+    # logic-only test mode (ranks share devices; collectives on host tensors)
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
+    backend = os.environ.get("STITCH_DIST_BACKEND", "nccl")
+    coll_dev = "cuda" if backend == "nccl" else "cpu"
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
 
     from paper_2009_10924_b200 import stitch
     text = read_graph(WORKLOAD)
@@ -277,7 +286,7 @@ def main():
     sustained = {"us_per_step": round(sus_us, 3), "value": round(alg_bytes * world / (sus_us * 1e-6) / 1e9, 1),
                  "steps": n_sus * spg, "clocks": sus_c}
     if dist:
-        t = torch.tensor([ms], device="cuda")
+        t = torch.tensor([ms], device=coll_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     ms_step = ms / args.steps
@@ -312,7 +321,7 @@ def main():
             fn()
         s = (time.perf_counter() - t0) / n
         if dist:
-            t = torch.tensor([s], device="cuda")
+            t = torch.tensor([s], device=coll_dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             s = float(t.item())
         return s
@@ -320,6 +329,36 @@ def main():
     e2e_s = host_loop(lambda: cx.run(pin_in, out=pin_out), e2e_steps)
     e2e_plain_s = host_loop(lambda: ex.run(pin_in, out=pin_out), max(3, e2e_steps // 4))
     e2e_val = alg_bytes * world / e2e_s / 1e9
+
+    # verification outside every timed region: each rank's sequence-0 outputs
+    # (set 0 holds this rank's inputs) are gathered to rank 0 over NCCL and
+    # checked against the numpy oracle on the same inputs
+    ex.launch(sp, 0)
+    torch.cuda.synchronize()
+    outs = ex.download()
+    seq0 = {t.name: np.ascontiguousarray(outs[t.name][0:1]) for t in g.outputs}
+    gathered = {}
+    for name_, a in seq0.items():
+        tt = torch.from_numpy(a).to(coll_dev)
+        if dist:
+            parts = [torch.empty_like(tt) for _ in range(world)]
+            dist.all_gather(parts, tt)
+            gathered[name_] = [p.cpu().numpy() for p in parts]
+        else:
+            gathered[name_] = [a]
+    verification = None
+    if rank == 0:
+        from oracle import numpy_oracle as no
+        one = no.parse_graph(text.replace(BATCH_TOKEN, "[1,"))
+        ok, worst = True, 0.0
+        for r in range(world):
+            full_in = stitch.random_inputs(g, seed=1 + r)
+            want = no.eval_reference(one, {k: v[0:1].astype(np.float64) for k, v in full_in.items()})
+            rep = stitch.compare({k: gathered[k][r] for k in want}, want, 1e-4, 1e-5)
+            ok, worst = ok and rep["pass"], max(worst, rep["max_rel"])
+        verification = {"pass": ok, "ranks": world, "max_rel": worst,
+                        "method": "after timing: each rank's sequence-0 outputs gathered to rank 0 (NCCL all_gather "
+                                  "when N>1) and compared with the numpy oracle (rel 1e-4 / abs 1e-5)"}
 
     result = None
     if rank == 0:
@@ -364,6 +403,7 @@ def main():
                        "bytes_per_step_per_gpu": alg_bytes,
                        "l2": "inputs larger than L2: %d rotating buffer sets x %.1f MB = %.0f MB (>= 8x the 126 MB L2)"
                              % (sets, per_set / 1e6, sets * per_set / 1e6),
+                       "global_batch": 32 * world,
                        "parallelism": "independent batch shards, %d rank(s), no collective" % world},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "peak_source": peak_kind + " (MEASURED_PEAKS.json hbm_gbs)"
@@ -381,6 +421,7 @@ def main():
                                     "us_per_step": round(e2e_plain_s * 1e6, 1),
                                     "path": "stc_exec_run_host: H2D all -> graph -> D2H all"}},
             "sustained": sustained,
+            "verification": verification,
             "gpu_launches": len(desc) * args.steps,
             "clocks": clk,
             "subgraphs": subs,
