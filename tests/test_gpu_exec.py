@@ -222,3 +222,31 @@ def test_template_edge_shapes(name):
     sizes from 1 to 256 threads, single row / slab) under the B200 profile"""
     ex = _check(EDGE_SHAPES[name], "b200", "stitched", 5)
     assert all(k["template"] != "program" for k in ex.describe()), name
+
+
+OP_COVERAGE = {
+    # shape ops folded into the index math of local / regional bodies
+    "transpose_chain": "x = parameter : f32[64,96]\ne = exp(x)\nt = transpose(e) perm=[1,0]\nc = parameter : f32[96,64]\n"
+                       "y = mul(t, c)\noutput y\n",
+    "transpose_then_rowsum": "x = parameter : f32[48,80]\nt = transpose(x) perm=[1,0]\nt2 = mul(t, t)\ne = exp(t2)\n"
+                             "l = log(e)\ns = reduce_sum(l) axes=1\noutput s\n",
+    "slice_chain": "x = parameter : f32[64,260]\nsl = slice(x) starts=[0,4] limits=[64,260]\nb = tanh(sl)\n"
+                   "m = reduce_max(b) axes=1\nmb = broadcast(m) dims=0 : f32[64,256]\ny = sub(b, mb)\noutput y\n",
+    "gather_rows": "d = parameter : f32[100,32]\ni = parameter : i32[40]\ng = gather(d, i)\nw = parameter : f32[40,32]\n"
+                   "y = add(g, w)\ns = reduce_sum(y) axes=1\noutput s\noutput y\n",
+    "power_min": "a = parameter : f32[128,64]\nb = parameter : f32[128,64]\nab = mul(a, a)\np = power(ab, b)\n"
+                 "q = min(p, a)\npa = add(p, ab)\ny = rsqrt(pa)\noutput q\noutput y\n",
+    "f16_softmax": "x = parameter : f16[32,128]\nm = reduce_max(x) axes=1\nmb = broadcast(m) dims=0 : f16[32,128]\n"
+                   "c = sub(x, mb)\ne = exp(c)\ns = reduce_sum(e) axes=1\nsb = broadcast(s) dims=0 : f16[32,128]\n"
+                   "y = div(e, sb)\noutput y\n",
+    "f16_colsum": "x = parameter : f16[300,40]\nh = mul(x, x)\ns = reduce_sum(h) axes=0\noutput s\n",
+}
+
+
+@pytest.mark.parametrize("name", sorted(OP_COVERAGE))
+@pytest.mark.parametrize("mode", ["stitched", "unfused"])
+def test_op_and_dtype_coverage(name, mode):
+    """every op kind and dtype of the reference's format (docs/formats.md):
+    transpose / slice / gather (i32 indices) / power / log / min / rsqrt and
+    f16 tensors, through the stitched templates and the per-op path"""
+    _check(OP_COVERAGE[name], "b200", mode, 2)
