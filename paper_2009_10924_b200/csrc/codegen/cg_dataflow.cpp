@@ -596,7 +596,10 @@ void emit_row(Emitter& em, const CompGraph& g, const std::set<int>& pat, const B
   }
   const std::string sRPB = std::to_string(rp.RPB), sL = std::to_string(L);
   if (st) {
-    em.ensure_wait();  // TMA-staged inputs may be kernel-produced
+    // TMA-staged inputs that a kernel produces must wait; graph parameters
+    // are streamed before the wait (hoisted prologue)
+    for (int v : st->tensors)
+      if (!em.is_param(v)) em.ensure_wait();
     const int64_t ntiles = (ROWS + rp.RPB - 1) / rp.RPB;
     const std::string S = std::to_string(st->stages), TF = std::to_string(st->tile_floats);
     const int64_t tile_bytes_full = st->tile_floats * 4;
