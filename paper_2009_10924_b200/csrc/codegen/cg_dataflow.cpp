@@ -1074,8 +1074,9 @@ KernelSpec generate_pattern_kernel(const CompGraph& g, const std::vector<int>& v
           sc.stages = std::max(2, env_int("STITCH_STAGES", 3));
           sc.tile_floats = int64_t(rp.RPB) * L;
           // keep >= 2 CTAs per SM: fewer stages when several tensors are staged
+          const int64_t smem_cap = int64_t(env_int("STITCH_STAGE_SMEM_KB", 110)) * 1024;
           while (sc.stages > 2 && 128 + int64_t(sc.stages) * static_cast<int64_t>(hits.size()) * sc.tile_floats * 4 >
-                                      110 * 1024)
+                                      smem_cap)
             --sc.stages;
           sc.bytes = 128 + int64_t(sc.stages) * static_cast<int64_t>(hits.size()) * sc.tile_floats * 4;
           if (sc.bytes <= 200 * 1024) {
