@@ -175,6 +175,20 @@ def run_reference(args):
     print(json.dumps(line))
 
 
+def cpu_reference_subgraph(name, threads):
+    """wall seconds of the unmodified reference eval_reference on the whole
+    config graph, as `shards` independent shard graphs on as many host threads
+    (best of 3); shards = the largest divisor of the sharded extent <= threads"""
+    from oracle import ref
+    from paper_2009_10924_b200 import shard
+    text = read_graph(name)
+    rule = shard.RULES.get(name)
+    if rule is None:
+        return ref.time_eval([text], seed=1, reps=3), 1
+    n = max(d for d in range(1, threads + 1) if rule.full % d == 0)
+    return ref.time_eval([rule.graph_text(text, n)] * n, seed=1, reps=3), n
+
+
 def time_subgraph(stitch, name, gemm=False):
     g = stitch.Graph(read_graph(name))
     plan = stitch.Plan(g, "b200")
@@ -187,7 +201,19 @@ def time_subgraph(stitch, name, gemm=False):
     us = ex.time_batched(steps=256, warmup=32, sets=sets, steps_per_graph=16)
     alg = sum(k["bytes"] for k in desc)
     top = max(range(len(desc)), key=lambda i: kus[i])
-    return {"us": round(us, 3), "GBps": round(alg / us / 1e3, 1), "kernels": len(desc),
+    peak, _ = measured_peaks()
+    cpu = None
+    if not gemm:
+        try:
+            from oracle import ref
+            if ref.available():
+                s, n = cpu_reference_subgraph(name, os.cpu_count() or 1)
+                cpu = {"us": round(s * 1e6, 1), "threads": n, "kind": "reference",
+                       "gpu_speedup": round(s * 1e6 / us, 1)}
+        except Exception as e:  # reported, never fatal
+            cpu = {"error": str(e)[:200]}
+    return {"us": round(us, 3), "GBps": round(alg / us / 1e3, 1), "frac_of_measured_peak": round(alg / us / 1e3 / peak, 4),
+            "kernels": len(desc), "cpu_reference": cpu,
             "us_one_launch_per_step": round(us1, 3),
             "templates": sorted({k["template"] for k in desc}), "bytes": alg,
             "dominant": {"name": desc[top]["name"], "template": desc[top]["template"],

@@ -70,6 +70,12 @@ RULES = {
     "bert_gelu": ShardRule(4096, r"\[4096,", {"ffn1": 0, "gl": 0}),
     "bert_resln": ShardRule(4096, r"\[4096[,\]]", {"h": 0, "ffn2": 0, "y": 0}),
     "bert_cut": ShardRule(4096, r"\[4096[,\]]", {"h": 0, "ffn1": 0, "ffn2": 0, "gl": 0, "y": 0}),
+    # DIEN AUGRU (batch 256): every per-step tensor is batch-leading.  Shape
+    # rewriting only (CPU-baseline timing on host threads): the opaque
+    # placeholders average over their whole operands, so shards are NOT
+    # equivalent to the full graph -- no tensor mapping, no gather
+    "dien_T10": ShardRule(256, r"\[256[,\]]", {}),
+    "dien_T20": ShardRule(256, r"\[256[,\]]", {}),
     # column reductions: shard the kept (column) axis; each GPU reduces all rows
     "colreduce": ShardRule(1024, r"1024\]", {"dy": 1, "xhat": 1, "dbias": 0, "dgamma": 0}),
 }
