@@ -87,6 +87,10 @@ class Emitter {
   std::map<int, std::string> staged_ptr;          // tensor -> smem base of its tile (current stage)
   std::vector<int> domain_dims;                   // O ++ I of the body being emitted
   std::set<int> staged_hits;                      // tensors seen at domain coordinates
+  // register pipeline (regional): coords key -> chunk index, tensors whose
+  // current row lives in registers cu_<name>_<chunk> (prefetched a row ahead)
+  std::map<std::string, int> domain_chunk;
+  std::set<int> reg_staged;
   // local bodies: coords key -> (linear index expr, domain dims)
   std::map<std::string, std::pair<std::string, std::vector<int>>> domain_lin;
 
@@ -121,6 +125,10 @@ class Emitter {
     waited_ = true;
   }
   bool is_param(int v) const { return g_.node(v).kind == OpKind::Parameter; }
+  void reset_wait() {
+    waited_ = false;
+    wait_scopes_.clear();
+  }
   void clear_memo() { memo_.clear(); }
 
   static std::string key(int v, const Coords& c) { return std::to_string(v) + "@" + coords_key(c); }
@@ -170,6 +178,12 @@ class Emitter {
       for (auto d : sh.dims) dd.push_back(static_cast<int>(d));
       if (it != domain_off.end() && dd == domain_dims) {
         staged_hits.insert(v);
+        if (reg_staged.count(v)) {
+          const std::string q = "cu_" + g_.node(v).name + "_" + std::to_string(domain_chunk.at(it->first));
+          Val r;
+          for (const char* f : {".x", ".y", ".z", ".w"}) r.lanes.push_back(q + f);
+          return r;
+        }
         if (auto sp = staged_ptr.find(v); sp != staged_ptr.end()) {
           const std::string q = fresh("q");
           line("const float4 " + q + " = lds4(" + sp->second + " + " + it->second + ");");
@@ -573,7 +587,7 @@ RowParams row_params(const std::vector<int>& inner, int block = 0) {
 // regional: a team of TPR threads owns a row; row elements live in registers
 // (st != nullptr: the CTA's rows arrive through the TMA pipeline in smem)
 void emit_row(Emitter& em, const CompGraph& g, const std::set<int>& pat, const Body& b,
-              const StageCfg* st = nullptr) {
+              const StageCfg* st = nullptr, const std::vector<int>* pipe = nullptr) {
   const std::vector<int>& O = b.dims_a;
   const std::vector<int>& I = b.dims_b;
   const int64_t ROWS = prod(O), L = prod(I);
@@ -633,6 +647,36 @@ void emit_row(Emitter& em, const CompGraph& g, const std::set<int>& pat, const B
               std::to_string(static_cast<int64_t>(k) * st->tile_floats) + " + team_ * " + sL + ";");
       em.staged_ptr[st->tensors[k]] = nm;
     }
+  } else if (pipe && !pipe->empty() && rp.W == 4) {
+    // register pipeline: every team prefetches its NEXT row of the streamed
+    // inputs while it reduces and writes the current one
+    for (int v : *pipe)
+      if (!em.is_param(v)) em.ensure_wait();
+    const std::string sROWS = std::to_string(ROWS);
+    auto off = [&](int j) {
+      const std::string raw = "(tl_ + " + std::to_string(j * rp.TPR) + ") * 4";
+      return partial ? "(" + raw + " < " + sL + " ? " + raw + " : " + std::to_string(L - 4) + ")" : raw;
+    };
+    std::string decl = "float4", first;
+    for (int v : *pipe)
+      for (int j = 0; j < rp.NJ; ++j) {
+        const std::string nm = "pf_" + g.node(v).name + "_" + std::to_string(j);
+        decl += std::string(decl == "float4" ? " " : ", ") + nm;
+        first += nm + " = ld4(T_" + g.node(v).name + " + r0_ * " + sL + " + " + off(j) + "); ";
+      }
+    em.line(decl + ";");
+    em.line("{ const i64 r0_ = min((i64)vbid * " + sRPB + " + team_, (i64)" + std::to_string(ROWS - 1) + "); " + first + "}");
+    em.open("for (i64 rb_ = (i64)vbid * " + sRPB + "; rb_ < " + sROWS + "; rb_ += (i64)vgrid * " + sRPB + ")");
+    std::string cur = "float4", next;
+    for (int v : *pipe)
+      for (int j = 0; j < rp.NJ; ++j) {
+        const std::string sfx = g.node(v).name + "_" + std::to_string(j);
+        cur += std::string(cur == "float4" ? " " : ", ") + "cu_" + sfx + " = pf_" + sfx;
+        next += "pf_" + sfx + " = ld4(T_" + g.node(v).name + " + n_ * " + sL + " + " + off(j) + "); ";
+      }
+    em.line("const " + cur + ";");
+    em.line("{ const i64 n_ = rb_ + (i64)vgrid * " + sRPB + " + team_; if (n_ < " + sROWS + ") { " + next + "} }");
+    em.reg_staged.insert(pipe->begin(), pipe->end());
   } else {
     em.open("for (i64 rb_ = (i64)vbid * " + sRPB + "; rb_ < " + std::to_string(ROWS) +
             "; rb_ += (i64)vgrid * " + sRPB + ")");
@@ -665,6 +709,7 @@ void emit_row(Emitter& em, const CompGraph& g, const std::set<int>& pat, const B
     }
     chunk_c[j] = c;
     em.domain_off[coords_key(c)] = p;  // float offset inside this team's row of a staged tile
+    em.domain_chunk[coords_key(c)] = j;
   }
   em.domain_dims = O;
   em.domain_dims.insert(em.domain_dims.end(), I.begin(), I.end());
@@ -754,7 +799,9 @@ void emit_row(Emitter& em, const CompGraph& g, const std::set<int>& pat, const B
   }
   em.close();
   em.domain_off.clear();
+  em.domain_chunk.clear();
   em.staged_ptr.clear();
+  em.reg_staged.clear();
 }
 
 struct ColParams {
@@ -1015,11 +1062,17 @@ KernelSpec generate_pattern_kernel(const CompGraph& g, const std::vector<int>& v
     if (b.kind == Kind::Row) max_tpr = std::max(max_tpr, row_params(b.dims_b).TPR);
   }
   block = std::max(block, max_tpr);
-  // long rows (a warp or more per row) run best as small CTAs of two row
-  // teams: many CTAs spread evenly over the 148 SMs (B200 sweep,
-  // profiles/r01/row_block_sweep.jsonl: LN 5.99 -> 5.77 us, residual+LN
-  // 8.26 -> 7.86 us); short rows keep 256-thread CTAs
-  if (max_tpr >= 32 && !has_col) block = std::min(1024, 2 * max_tpr);
+  // long rows (a warp or more per row) stream through a register pipeline
+  // (each team prefetches its next row while it reduces and writes the
+  // current one, 2 rows per team) in 256-thread CTAs (B200 sweeps,
+  // profiles/r01/row_pipe_sweep.jsonl: LN 5.39 -> 4.88 us, residual+LN
+  // 7.36 -> 7.15 us); short rows keep 256-thread CTAs without the pipeline
+  // (a kernel that packs other bodies keeps small 2-team CTAs and no
+  // pipeline: its register allocation is shared with those bodies -- bias+GELU
+  // packed with residual+LN runs 23 us that way vs 36 us pipelined)
+  const bool long_rows = max_tpr >= 32 && !has_col;
+  const bool single_row_body = long_rows && bodies.size() == 1;
+  if (long_rows) block = std::min(1024, single_row_body ? std::max(256, 2 * max_tpr) : 2 * max_tpr);
   if (const int want = env_int("STITCH_ROW_BLOCK", 0); want > 0) {
     block = std::clamp((std::max(want, max_tpr) + max_tpr - 1) / max_tpr * max_tpr, 32, 1024);
   } else if (want < 0 && bodies.size() == 1 && bodies[0].kind == Kind::Row) {
@@ -1041,6 +1094,7 @@ KernelSpec generate_pattern_kernel(const CompGraph& g, const std::vector<int>& v
   // CTA budget per body; scratch = [256 B reserved][strip arrival counters][f64 partials]
   int64_t part_words = 0, ctr_words = 64, dyn_smem = 0;
   std::vector<StageCfg> stage(bodies.size());
+  std::vector<std::vector<int>> pipe(bodies.size());
   std::vector<ColParams> cps(bodies.size());
   std::vector<int64_t> part_off(bodies.size(), 0), ctr_off(bodies.size(), 0);
   for (size_t i = 0; i < bodies.size(); ++i) {
@@ -1056,19 +1110,31 @@ KernelSpec generate_pattern_kernel(const CompGraph& g, const std::vector<int>& v
       const RowParams rp = row_params(b.dims_b, block);
       const int64_t rows = prod(b.dims_a), L = prod(b.dims_b), ntiles = (rows + rp.RPB - 1) / rp.RPB;
       b.blocks = static_cast<int>(std::clamp<int64_t>(ntiles, 1, int64_t(kSmCount) * env_int("STITCH_ROW_CTAS", 16)));
-      // dry run: which inputs does the body read at its own (row, chunk) coordinates?
-      // opt-in (STITCH_STAGE=1): measured slower than register-resident rows
-      // when each SM only sees 1-3 tiles (C1-C3 sizes), see DESIGN.md §5
-      if (env_int("STITCH_STAGE", 0) && rp.W == 4) {
+      // dry run: which inputs does the body read at its own (row, chunk)
+      // coordinates?  Those can be streamed a row ahead in registers
+      // (default, STITCH_ROW_PIPE >= 2 rows per team) or through the opt-in
+      // TMA pipeline (STITCH_STAGE=1: measured slower)
+      const int pipe_rows = env_int("STITCH_ROW_PIPE", single_row_body ? 2 : 1);
+      if ((env_int("STITCH_STAGE", 0) || pipe_rows > 1) && rp.W == 4) {
         em.out.str("");
         em.clear_memo();
         em.reduced.clear();
         em.staged_hits.clear();
+        em.reset_wait();
         emit_row(em, g, pat, b);
+        em.reset_wait();
         std::vector<int> hits;
         for (int v : em.staged_hits)
           if (!pat.count(v) && g.node(v).shape.dtype == DType::F32) hits.push_back(v);
-        if (!hits.empty()) {
+        // one streamed tensor per team row: 2 x NJ float4 registers; with more
+        // the register pressure costs more than the prefetch hides
+        // (residual+LN, 2 streamed tensors: 7.08 -> 7.16 us pipelined)
+        const bool pipe_ok = hits.size() == 1 || env_int("STITCH_ROW_PIPE", 0) > 1;
+        if (!hits.empty() && !env_int("STITCH_STAGE", 0) && pipe_ok) {
+          pipe[i] = hits;
+          b.blocks = static_cast<int>(std::clamp<int64_t>((ntiles + pipe_rows - 1) / pipe_rows, 1,
+                                                          int64_t(kSmCount) * env_int("STITCH_ROW_CTAS", 16)));
+        } else if (!hits.empty() && env_int("STITCH_STAGE", 0)) {
           StageCfg& sc = stage[i];
           sc.tensors = hits;
           sc.stages = std::max(2, env_int("STITCH_STAGES", 3));
@@ -1107,8 +1173,10 @@ KernelSpec generate_pattern_kernel(const CompGraph& g, const std::vector<int>& v
     em.ind = "    ";
     em.clear_memo();
     em.reduced.clear();
+    em.reset_wait();
     if (b.kind == Kind::Local) emit_local(em, g, b);
-    else if (b.kind == Kind::Row) emit_row(em, g, pat, b, stage[i].tensors.empty() ? nullptr : &stage[i]);
+    else if (b.kind == Kind::Row)
+      emit_row(em, g, pat, b, stage[i].tensors.empty() ? nullptr : &stage[i], pipe[i].empty() ? nullptr : &pipe[i]);
     else emit_column(em, g, b, cps[i], part_off[i], ctr_off[i]);
     em.ensure_wait();  // every path waits before the CTA retires
     body_src << "  " << (i ? "else " : "") << "if (blockIdx.x < " << start + b.blocks << ") {\n";
