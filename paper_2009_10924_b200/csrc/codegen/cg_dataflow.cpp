@@ -1322,8 +1322,12 @@ KernelSpec generate_opaque_kernel(const CompGraph& g, int vertex, const std::str
       s << "  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < " << g.node(o).shape.element_count()
         << "; i += (i64)gridDim.x * blockDim.x) acc += (double)ldv(T_" << g.node(o).name << ", i);\n";
   }
+  // warp sums -> warp 0 folds them with one butterfly (fixed order,
+  // deterministic) -> broadcast through shared memory
   s << "  acc = bfly_sum(acc, 32);\n  if ((threadIdx.x & 31) == 0) red_[threadIdx.x >> 5] = acc;\n  __syncthreads();\n"
-    << "  double tot = 0.0;\n  for (int w = 0; w < " << block / 32 << "; ++w) tot += red_[w];\n";
+    << "  __shared__ double tot_;\n  if (threadIdx.x < 32) {\n    double w_ = threadIdx.x < " << block / 32
+    << " ? red_[threadIdx.x] : 0.0;\n    w_ = bfly_sum(w_, 32);\n    if (threadIdx.x == 0) tot_ = w_;\n  }\n"
+    << "  __syncthreads();\n  double tot = tot_;\n";
   if (!single)
     s << "  if (threadIdx.x == 0) part_[blockIdx.x] = tot;\n  grid_sync(bar_, gridDim.x);\n"
       << "  __shared__ double all_;\n"

@@ -277,10 +277,21 @@ int Executor::capture_plan(int set, cudaStream_t origin, int prev) {
     for (int d : deps_[i]) ready = std::max(ready, fin[static_cast<size_t>(d)]);
     fin[i] = ready + 1.5 + static_cast<double>(specs_[i].alg_bytes) / 5.0e3;
   }
-  for (size_t i = 0; i < n; ++i) {
+  // producer-less kernels (per-step input transforms such as DIEN's x.W
+  // placeholders) share one dedicated lane: they run ahead of the critical
+  // chain instead of taking its slots once the lane cap is reached
+  // and are captured first, so the graph launches them ahead of the chain
+  int source_lane = -1;
+  std::vector<size_t> order;
+  for (size_t i = 0; i < n; ++i)
+    if (deps_[i].empty()) order.push_back(i);
+  for (size_t i = 0; i < n; ++i)
+    if (!deps_[i].empty()) order.push_back(i);
+  for (size_t i : order) {
     int best = -1;
-    for (size_t l = 0; l < lanes.size(); ++l) {  // the producer finishing last, at a lane's tail
-      const int t = lanes[l].tail;
+    if (deps_[i].empty() && source_lane >= 0) best = source_lane;
+    for (size_t l = 0; l < lanes.size() && !(deps_[i].empty() && source_lane >= 0); ++l) {  // the producer
+      const int t = lanes[l].tail;                                                        // finishing last
       if (t >= 0 && std::count(deps_[i].begin(), deps_[i].end(), t) &&
           (best < 0 || fin[static_cast<size_t>(t)] > fin[static_cast<size_t>(lanes[static_cast<size_t>(best)].tail)]))
         best = static_cast<int>(l);
@@ -304,6 +315,7 @@ int Executor::capture_plan(int set, cudaStream_t origin, int prev) {
       best = static_cast<int>(lanes.size()) - 1;
     }
     if (best < 0) best = 0;  // lane cap reached: serialise on origin
+    if (deps_[i].empty() && source_lane < 0 && best > 0) source_lane = best;
     Lane& ln = lanes[static_cast<size_t>(best)];
     for (int d : deps_[i]) {  // producers not already ordered before the lane's tail
       if (ln.tail >= 0 && (d == ln.tail || anc[static_cast<size_t>(ln.tail)][static_cast<size_t>(d)])) continue;
