@@ -281,12 +281,40 @@ int Executor::capture_plan(int set, cudaStream_t origin, int prev) {
   // placeholders) share one dedicated lane: they run ahead of the critical
   // chain instead of taking its slots once the lane cap is reached
   // and are captured first, so the graph launches them ahead of the chain
+  // The rest is captured in priority-list order (longest remaining path
+  // first among the ready kernels), so the kernel that gates the critical
+  // path claims its producer's lane (a same-stream PDL edge) before its
+  // siblings fork.
   int source_lane = -1;
   std::vector<size_t> order;
   for (size_t i = 0; i < n; ++i)
     if (deps_[i].empty()) order.push_back(i);
-  for (size_t i = 0; i < n; ++i)
-    if (!deps_[i].empty()) order.push_back(i);
+  {
+    std::vector<std::vector<int>> users(n);
+    for (size_t i = 0; i < n; ++i)
+      for (int d : deps_[i]) users[static_cast<size_t>(d)].push_back(static_cast<int>(i));
+    std::vector<double> bottom(n, 0.0);  // cost of i + the longest path after it
+    for (size_t i = n; i-- > 0;) {
+      double tail = 0.0;
+      for (int u : users[i]) tail = std::max(tail, bottom[static_cast<size_t>(u)]);
+      bottom[i] = 1.5 + static_cast<double>(specs_[i].alg_bytes) / 5.0e3 + tail;
+    }
+    std::vector<size_t> pending(n);
+    std::set<std::pair<double, size_t>> ready;  // (-bottom, index)
+    for (size_t i = 0; i < n; ++i) pending[i] = deps_[i].size();
+    for (size_t i = 0; i < n; ++i)
+      if (deps_[i].empty())
+        for (int u : users[i])
+          if (--pending[static_cast<size_t>(u)] == 0) ready.insert({-bottom[static_cast<size_t>(u)], static_cast<size_t>(u)});
+    while (!ready.empty()) {
+      const size_t i = ready.begin()->second;
+      ready.erase(ready.begin());
+      order.push_back(i);
+      for (int u : users[i])
+        if (--pending[static_cast<size_t>(u)] == 0) ready.insert({-bottom[static_cast<size_t>(u)], static_cast<size_t>(u)});
+    }
+    if (order.size() != n) throw std::runtime_error("[exec] kernel dependency cycle");
+  }
   for (size_t i : order) {
     int best = -1;
     if (deps_[i].empty() && source_lane >= 0) best = source_lane;
