@@ -1248,7 +1248,7 @@ KernelSpec generate_opaque_kernel(const CompGraph& g, int vertex, const std::str
   // small tensors (e.g. DIEN's [256,36] GEMM outputs): one 1024-thread CTA,
   // no grid-wide barrier; large ones: cooperative grid with a barrier
   const bool single = work <= (int64_t(1) << 20);
-  const int grid = single ? 1 : kSmCount;
+  const int grid = single ? 1 : kSmCount * 4;  // cooperative: 4 co-resident 256-thread CTAs per SM
   const int block = single ? 1024 : kBlock;
   KernelSpec k;
   k.name = name;
@@ -1258,7 +1258,7 @@ KernelSpec generate_opaque_kernel(const CompGraph& g, int vertex, const std::str
   k.block = block;
   k.cooperative = !single;
   std::ostringstream s;
-  s << "extern \"C\" __global__ void __launch_bounds__(" << block << ", 1) " << name << "(";
+  s << "extern \"C\" __global__ void __launch_bounds__(" << block << ", " << (single ? 1 : 4) << ") " << name << "(";
   for (int o : ops) {
     s << "const " << c_type(g.node(o).shape.dtype) << "* __restrict__ T_" << g.node(o).name << ", ";
     k.inputs.push_back(g.node(o).name);
@@ -1318,9 +1318,30 @@ KernelSpec generate_opaque_kernel(const CompGraph& g, int vertex, const std::str
         s << "acc += (double)" << a << "[k];\n";
     }
   } else {
-    for (int o : n.operands)
-      s << "  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < " << g.node(o).shape.element_count()
-        << "; i += (i64)gridDim.x * blockDim.x) acc += (double)ldv(T_" << g.node(o).name << ", i);\n";
+    // grid: 128-bit grid-stride loads, 4 independent accumulators per thread
+    // so each thread keeps 4 loads in flight
+    s << "  const i64 gt_ = (i64)blockIdx.x * blockDim.x + threadIdx.x, gs_ = (i64)gridDim.x * blockDim.x;\n"
+      << "  double a0_ = 0.0, a1_ = 0.0, a2_ = 0.0, a3_ = 0.0;\n";
+    for (int o : n.operands) {
+      const TensorShape& sh = g.node(o).shape;
+      const int64_t cnt = sh.element_count();
+      const std::string T = "T_" + g.node(o).name;
+      if (sh.dtype == DType::F32 && cnt % 4 == 0) {
+        const std::string u = std::to_string(cnt / 4);
+        s << "  for (i64 i = gt_; i < " << u << "; i += 4 * gs_) {\n"
+          << "    float4 q0 = ld4(" << T << " + 4 * i), q1 = make_float4(0.f, 0.f, 0.f, 0.f), q2 = q1, q3 = q1;\n"
+          << "    if (i + gs_ < " << u << ") q1 = ld4(" << T << " + 4 * (i + gs_));\n"
+          << "    if (i + 2 * gs_ < " << u << ") q2 = ld4(" << T << " + 4 * (i + 2 * gs_));\n"
+          << "    if (i + 3 * gs_ < " << u << ") q3 = ld4(" << T << " + 4 * (i + 3 * gs_));\n"
+          << "    a0_ += ((double)q0.x + (double)q0.y) + ((double)q0.z + (double)q0.w);\n"
+          << "    a1_ += ((double)q1.x + (double)q1.y) + ((double)q1.z + (double)q1.w);\n"
+          << "    a2_ += ((double)q2.x + (double)q2.y) + ((double)q2.z + (double)q2.w);\n"
+          << "    a3_ += ((double)q3.x + (double)q3.y) + ((double)q3.z + (double)q3.w);\n  }\n";
+      } else {
+        s << "  for (i64 i = gt_; i < " << cnt << "; i += gs_) a0_ += (double)ldv(" << T << ", i);\n";
+      }
+    }
+    s << "  acc = (a0_ + a1_) + (a2_ + a3_);\n";
   }
   // warp sums -> warp 0 folds them with one butterfly (fixed order,
   // deterministic) -> broadcast through shared memory
@@ -1331,8 +1352,9 @@ KernelSpec generate_opaque_kernel(const CompGraph& g, int vertex, const std::str
   if (!single)
     s << "  if (threadIdx.x == 0) part_[blockIdx.x] = tot;\n  grid_sync(bar_, gridDim.x);\n"
       << "  __shared__ double all_;\n"
-      << "  if (threadIdx.x == 0) { double t = 0.0; for (int b = 0; b < " << grid
-      << "; ++b) t += __ldcg(part_ + b); all_ = t; }\n  __syncthreads();\n  tot = all_;\n";
+      << "  if (threadIdx.x < 32) {\n    double t = 0.0;\n    for (int b = threadIdx.x; b < " << grid
+      << "; b += 32) t += __ldcg(part_ + b);\n    t = bfly_sum(t, 32);\n    if (threadIdx.x == 0) all_ = t;\n  }\n"
+      << "  __syncthreads();\n  tot = all_;\n";
   s << "  const float fill = (float)(" << (count ? "tot / " + std::to_string(count) + ".0" : "0.0") << ");\n";
   const int64_t nout = n.shape.element_count();
   if (n.shape.dtype == DType::F32 && nout % 4 == 0)  // 128-bit stores
