@@ -54,7 +54,15 @@ def lib():
     if _lib is not None:
         return _lib
     if not os.path.exists(LIB_PATH):
-        raise StitchError(4, "libstitch_b200.so is not built (run __graft_entry__.build())")
+        # a fresh checkout: build the native library in-tree (g++/nvcc/NVRTC;
+        # no GPU needed) -- there is no non-native fallback
+        try:
+            from paper_2009_10924_b200 import build as _build
+            _build.build()
+        except Exception as e:
+            raise StitchError(4, "libstitch_b200.so is not built and the in-tree build failed: %s" % e)
+        if not os.path.exists(LIB_PATH):
+            raise StitchError(4, "libstitch_b200.so is not built (run __graft_entry__.build())")
     L = ctypes.CDLL(LIB_PATH)
     vp, cp, ip, i64 = ctypes.c_void_p, ctypes.c_char_p, ctypes.c_int, ctypes.c_int64
     P = ctypes.POINTER
