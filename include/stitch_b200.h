@@ -175,6 +175,46 @@ int stc_compile(const char* cuda_source, const char* options, char** cubin_key);
 /* directory of the cubin cache ($STITCH_CACHE_DIR or <pkg>/lib/cubin_cache) */
 const char* stc_cache_dir(void);
 
+/* Device context, modules, ctx-owned buffers and explicit CUDA Graphs
+ * (stc_init / stc_compile(ctx, ...) / stc_alloc / stc_free /
+ * stc_upload / stc_download / stc_graph_* / stc_nccl_gather; renamed
+ * stc_ctx_* / stc_cgraph_* because stc_graph_* and stc_free already name the
+ * IR graph and the string deallocator).  Lifetime: the ctx owns its buffers;
+ * modules and graphs are destroyed by their own *_destroy.  One ctx per GPU,
+ * driven by one host thread. */
+typedef struct stc_ctx stc_ctx;
+typedef struct stc_module stc_module;
+typedef struct stc_cgraph stc_cgraph;
+typedef struct stc_comm stc_comm;
+int stc_ctx_create(int device, stc_ctx** out);
+void stc_ctx_destroy(stc_ctx* c);
+/* NVRTC sm_100a (cached); every named kernel is resolved now */
+int stc_ctx_compile(stc_ctx* c, const char* cuda_source, const char* const* kernel_names, int n,
+                    stc_module** out);
+void stc_module_destroy(stc_module* m);
+int stc_ctx_alloc(stc_ctx* c, size_t bytes, void** dptr);
+int stc_ctx_release(stc_ctx* c, void* dptr);
+int stc_ctx_upload(stc_ctx* c, void* dptr, const void* host, size_t bytes);
+int stc_ctx_download(stc_ctx* c, void* host, const void* dptr, size_t bytes);
+/* kernels added in order run in order (each depends on the previous);
+ * args = array of pointers to the argument values, as cudaLaunchKernel */
+int stc_cgraph_create(stc_ctx* c, stc_cgraph** out);
+int stc_cgraph_add_kernel(stc_cgraph* g, stc_module* m, const char* name, int grid, int block, int smem_bytes,
+                          int cooperative, void** args);
+int stc_cgraph_instantiate(stc_cgraph* g);
+int stc_cgraph_launch(stc_cgraph* g, void* cuda_stream);
+/* average CUDA-event time of one replay over `iters`, L2 flushed before each
+ * replay when flush_bytes > 0 (a buffer that large is written) */
+int stc_cgraph_time(stc_cgraph* g, int iters, size_t flush_bytes, float* us_per_iter);
+void stc_cgraph_destroy(stc_cgraph* g);
+/* NCCL (libnccl.so.2 loaded on first use) for the verification gather of
+ * shard outputs -- never on the timed data path.  The 128-byte unique id is
+ * created on one rank and shared out of band. */
+int stc_nccl_unique_id(char* id128);
+int stc_nccl_comm_init(stc_ctx* c, int nranks, int rank, const char* id128, stc_comm** out);
+int stc_nccl_gather(stc_comm* cm, const void* send, void* recv, size_t bytes_per_rank, void* cuda_stream);
+void stc_nccl_comm_destroy(stc_comm* cm);
+
 /* ---- drop-in pipeline ------------------------------------------------------
  * replaces stitch::run_pipeline (include/stitch/pipeline.hpp:28): writes
  * plan.json, kernels/kNNN_<producer>.stitch, report.txt, [graph.dot];

@@ -98,6 +98,16 @@ def lib():
         "stc_exec_launch_batch": (ip, [vp, vp, ip]),
         "stc_exec_time_batched": (ip, [vp, ip, ip, ip, ip, P(ctypes.c_double)]),
         "stc_compile": (ip, [cp, cp, P(vp)]), "stc_cache_dir": (cp, []),
+        "stc_ctx_create": (ip, [ip, P(vp)]), "stc_ctx_destroy": (None, [vp]),
+        "stc_ctx_compile": (ip, [vp, cp, P(cp), ip, P(vp)]), "stc_module_destroy": (None, [vp]),
+        "stc_ctx_alloc": (ip, [vp, ctypes.c_size_t, P(vp)]), "stc_ctx_release": (ip, [vp, vp]),
+        "stc_ctx_upload": (ip, [vp, vp, vp, ctypes.c_size_t]), "stc_ctx_download": (ip, [vp, vp, vp, ctypes.c_size_t]),
+        "stc_cgraph_create": (ip, [vp, P(vp)]),
+        "stc_cgraph_add_kernel": (ip, [vp, vp, cp, ip, ip, ip, ip, P(vp)]),
+        "stc_cgraph_instantiate": (ip, [vp]), "stc_cgraph_launch": (ip, [vp, vp]),
+        "stc_cgraph_time": (ip, [vp, ip, ctypes.c_size_t, P(ctypes.c_float)]), "stc_cgraph_destroy": (None, [vp]),
+        "stc_nccl_unique_id": (ip, [ctypes.c_char_p]), "stc_nccl_comm_init": (ip, [vp, ip, ip, ctypes.c_char_p, P(vp)]),
+        "stc_nccl_gather": (ip, [vp, vp, vp, ctypes.c_size_t, vp]), "stc_nccl_comm_destroy": (None, [vp]),
         "stc_run_pipeline": (ip, [cp, cp, ip, ip, cp, ip, ip, ip, ctypes.c_uint64]),
     }
     for name, (res, args) in sig.items():
@@ -250,6 +260,90 @@ class Plan:
         if getattr(self, "_h", None) and _lib is not None:
             _lib.stc_plan_destroy(self._h)
             self._h = None
+
+
+class Context:
+    """Low-level runtime (stc_ctx_* / stc_cgraph_* / stc_nccl_*): a device
+    context owning buffers, NVRTC modules, explicit CUDA Graphs of launches."""
+
+    def __init__(self, device: int = 0):
+        self._h = ctypes.c_void_p()
+        _check(lib().stc_ctx_create(device, ctypes.byref(self._h)))
+        self._keep = []
+
+    def compile(self, source: str, kernels: Sequence[str]):
+        m = ctypes.c_void_p()
+        names = (ctypes.c_char_p * len(kernels))(*[k.encode() for k in kernels])
+        _check(lib().stc_ctx_compile(self._h, source.encode(), names, len(kernels), ctypes.byref(m)))
+        self._keep.append(m)
+        return m
+
+    def alloc(self, nbytes: int) -> int:
+        p = ctypes.c_void_p()
+        _check(lib().stc_ctx_alloc(self._h, nbytes, ctypes.byref(p)))
+        return p.value
+
+    def upload(self, dptr: int, a: np.ndarray):
+        a = np.ascontiguousarray(a)
+        _check(lib().stc_ctx_upload(self._h, ctypes.c_void_p(dptr), a.ctypes.data, a.nbytes))
+
+    def download(self, dptr: int, out: np.ndarray) -> np.ndarray:
+        _check(lib().stc_ctx_download(self._h, out.ctypes.data, ctypes.c_void_p(dptr), out.nbytes))
+        return out
+
+    def graph(self):
+        return CudaGraph(self)
+
+    def nccl_comm(self, nranks: int, rank: int, unique_id: bytes):
+        c = ctypes.c_void_p()
+        _check(lib().stc_nccl_comm_init(self._h, nranks, rank, unique_id, ctypes.byref(c)))
+        return c
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            for m in self._keep:
+                _lib.stc_module_destroy(m)
+            _lib.stc_ctx_destroy(self._h)
+            self._h = None
+
+
+class CudaGraph:
+    def __init__(self, ctx: Context):
+        self.ctx = ctx
+        self._h = ctypes.c_void_p()
+        _check(lib().stc_cgraph_create(ctx._h, ctypes.byref(self._h)))
+
+    def add_kernel(self, module, name: str, grid: int, block: int, args, smem: int = 0, cooperative: bool = False):
+        """args: ctypes values (c_void_p for device pointers, c_int, c_float, ...)"""
+        ptrs = (ctypes.c_void_p * max(1, len(args)))(*[ctypes.addressof(a) for a in args])
+        _check(lib().stc_cgraph_add_kernel(self._h, module, name.encode(), grid, block, smem, int(cooperative), ptrs))
+
+    def instantiate(self):
+        _check(lib().stc_cgraph_instantiate(self._h))
+
+    def launch(self, stream: int = 0):
+        _check(lib().stc_cgraph_launch(self._h, ctypes.c_void_p(stream or None)))
+
+    def time(self, iters: int = 20, flush_bytes: int = 0) -> float:
+        us = ctypes.c_float()
+        _check(lib().stc_cgraph_time(self._h, iters, flush_bytes, ctypes.byref(us)))
+        return us.value
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.stc_cgraph_destroy(self._h)
+            self._h = None
+
+
+def nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().stc_nccl_unique_id(buf))
+    return buf.raw
+
+
+def nccl_gather(comm, send_dptr: int, recv_dptr: int, bytes_per_rank: int, stream: int = 0):
+    _check(lib().stc_nccl_gather(comm, ctypes.c_void_p(send_dptr), ctypes.c_void_p(recv_dptr), bytes_per_rank,
+                                 ctypes.c_void_p(stream or None)))
 
 
 def warm_cache(plans: Sequence["Plan"], mode: str = "stitched", threads: int = 8, gemm: bool = False):

@@ -250,3 +250,39 @@ def test_op_and_dtype_coverage(name, mode):
     transpose / slice / gather (i32 indices) / power / log / min / rsqrt and
     f16 tensors, through the stitched templates and the per-op path"""
     _check(OP_COVERAGE[name], "b200", mode, 2)
+
+
+def test_low_level_runtime_cgraph_and_nccl():
+    """§8b runtime C-ABI: ctx-owned buffers, an NVRTC module, an explicit
+    CUDA Graph of two dependent launches, event timing with L2 flush, and a
+    single-rank NCCL gather (the verification collective)"""
+    import ctypes
+    stitch = _stitch()
+    src = r'''
+    extern "C" __global__ void axpy(float* y, const float* x, float a, int n) {
+      int i = blockIdx.x * blockDim.x + threadIdx.x; if (i < n) y[i] = a * x[i] + y[i]; }
+    extern "C" __global__ void scale(float* y, float s, int n) {
+      int i = blockIdx.x * blockDim.x + threadIdx.x; if (i < n) y[i] = y[i] * s; }
+    '''
+    ctx = stitch.Context(0)
+    mod = ctx.compile(src, ["axpy", "scale"])
+    n = 10000
+    x = np.arange(n, dtype=np.float32)
+    y = np.ones(n, dtype=np.float32)
+    dx, dy = ctx.alloc(x.nbytes), ctx.alloc(y.nbytes)
+    ctx.upload(dx, x)
+    ctx.upload(dy, y)
+    g = ctx.graph()
+    g.add_kernel(mod, "axpy", (n + 255) // 256, 256, [ctypes.c_void_p(dy), ctypes.c_void_p(dx), ctypes.c_float(2.0),
+                                                      ctypes.c_int(n)])
+    g.add_kernel(mod, "scale", (n + 255) // 256, 256, [ctypes.c_void_p(dy), ctypes.c_float(0.5), ctypes.c_int(n)])
+    g.instantiate()
+    g.launch()
+    out = ctx.download(dy, np.empty_like(y))
+    assert np.array_equal(out, (2.0 * x + 1.0) * 0.5)
+    assert g.time(iters=5, flush_bytes=256 << 20) > 0
+    comm = ctx.nccl_comm(1, 0, stitch.nccl_unique_id())
+    dr = ctx.alloc(x.nbytes)
+    stitch.nccl_gather(comm, dx, dr, x.nbytes)
+    assert np.array_equal(ctx.download(dr, np.empty_like(x)), x)
+    stitch.lib().stc_nccl_comm_destroy(comm)
