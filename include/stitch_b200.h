@@ -66,6 +66,12 @@ int stc_plan_num_patterns(const stc_plan* p);
 /* pattern i: vertex ids (up to cap) -> count; program text via kernel_text */
 int stc_plan_pattern(const stc_plan* p, int i, int* verts, int cap);
 int stc_plan_kernel_text(const stc_plan* p, int i, char** out);
+/* NON-PARITY refinement: after the reference explorer,
+ * greedily merge launch units along graph edges whenever the merge saves HBM
+ * bytes or a launch and the merged pattern is plannable (reference
+ * plan_kernel) and expressible by a stitching template.  The plan then no
+ * longer equals the reference's; plan.json / kernel texts follow it. */
+int stc_plan_refine(stc_plan* p, int* merges, int64_t* bytes_saved);
 int stc_plan_stats(const stc_plan* p, int* stitched_kernels, int* baseline_kernels,
                    int64_t* delta_evaluate_calls);
 /* stitch::plan_kernel on one vertex set -> program text; rc 1 = infeasible */

@@ -4,6 +4,7 @@
 #include <memory>
 
 #include "abi/abi_common.h"
+#include "codegen/cg.hpp"
 #include "stitch/baseline.hpp"
 #include "stitch/parser.hpp"
 #include "stitch/pipeline.hpp"
@@ -139,6 +140,16 @@ int stc_plan_kernel_text(const stc_plan* p, int i, char** out) {
   return guarded([&] {
     const auto& pat = p->plan.patterns.at(static_cast<size_t>(i));
     *out = dup_string(emit_kernel_text(p->kernels.at(pat.key())));
+  });
+}
+
+int stc_plan_refine(stc_plan* p, int* merges, int64_t* bytes_saved) {
+  return guarded([&] {
+    stitch::gpu::RefineStats st;
+    p->plan = stitch::gpu::refine_plan(p->graph, p->plan, p->models.machine, p->kernels, &st);
+    p->stitched = kernel_count(p->graph, p->plan);
+    if (merges) *merges = st.merges;
+    if (bytes_saved) *bytes_saved = st.bytes_saved;
   });
 }
 

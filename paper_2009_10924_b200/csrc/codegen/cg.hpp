@@ -84,6 +84,17 @@ const std::string& device_prelude();
 // algorithmic bytes of a vertex set
 int64_t algorithmic_bytes(const CompGraph& g, const std::vector<int>& vertices);
 
+// Non-parity plan refinement (cg_refine.cpp): greedily
+// merge launch units along graph edges while the merge saves HBM bytes or a
+// launch and stays plannable + template-expressible.  New patterns' KernelPlans
+// are added to `kernels`.
+struct RefineStats {
+  int merges = 0;
+  int64_t bytes_saved = 0;
+};
+FusionPlan refine_plan(const CompGraph& g, const FusionPlan& plan, const MachineModel& model,
+                       std::map<std::string, KernelPlan>& kernels, RefineStats* stats = nullptr);
+
 // small formatting helpers shared by the generators
 std::string c_float(double v);  // exact float literal of (float)v
 const char* c_type(DType d);

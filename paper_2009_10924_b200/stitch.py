@@ -77,6 +77,7 @@ def lib():
         "stc_plan_num_patterns": (ip, [vp]), "stc_plan_pattern": (ip, [vp, ip, P(ip), ip]),
         "stc_plan_kernel_text": (ip, [vp, ip, P(vp)]),
         "stc_plan_stats": (ip, [vp, P(ip), P(ip), P(i64)]),
+        "stc_plan_refine": (ip, [vp, P(ip), P(i64)]),
         "stc_plan_kernel": (ip, [vp, cp, P(ip), ip, P(vp)]),
         "stc_codegen": (ip, [vp, ip, P(vp), P(vp)]),
         "stc_exec_create": (ip, [vp, ip, ip, P(vp)]), "stc_exec_destroy": (None, [vp]),
@@ -222,6 +223,13 @@ class Plan:
             oa = (ctypes.c_int * len(offs))(*offs)
             _check(lib().stc_plan_from_patterns(graph._h, self.cfg.encode(), va, oa, len(patterns),
                                                 ctypes.byref(self._h)))
+
+    def refine(self):
+        """NON-PARITY: merge launch units while it saves HBM bytes or launches
+        (stc_plan_refine) -> (merges, bytes_saved)"""
+        m, b = ctypes.c_int(), ctypes.c_int64()
+        _check(lib().stc_plan_refine(self._h, ctypes.byref(m), ctypes.byref(b)))
+        return m.value, b.value
 
     def json(self, seed: int = 0) -> str:
         p = ctypes.c_void_p()

@@ -286,3 +286,23 @@ def test_low_level_runtime_cgraph_and_nccl():
     stitch.nccl_gather(comm, dx, dr, x.nbytes)
     assert np.array_equal(ctx.download(dr, np.empty_like(x)), x)
     stitch.lib().stc_nccl_comm_destroy(comm)
+
+
+@pytest.mark.parametrize("name,cfg", [("bert_layer", "v100"), ("bert_cut", "v100"), ("dien_T10", "b200")])
+def test_refined_plan_matches_oracle(name, cfg):
+    """refined (non-parity) plans compute the same graph: oracle tolerance"""
+    stitch = _stitch()
+    text = config_graph(name)
+    g = stitch.Graph(text)
+    plan = stitch.Plan(g, cfg)
+    n0 = plan.stats()["stitched_kernels"]
+    plan.refine()
+    assert plan.stats()["stitched_kernels"] < n0
+    ex = stitch.Executor(plan)
+    inputs = stitch.random_inputs(g, 3)
+    got = ex.run(inputs)
+    og = no.parse_graph(text)
+    want = no.eval_reference(og, {k: v.astype(np.float64) for k, v in inputs.items()})
+    for k, tol in _tolerances(og).items():
+        rep = stitch.compare({k: got[k]}, {k: want[k]}, tol, 1e-5)
+        assert rep["pass"], (name, k, rep["message"])

@@ -107,3 +107,18 @@ def test_calibrated_cfg_parity_with_reference():
         keys = [p["key"] for p in json.loads(want)["patterns"]]
         for i, k in enumerate(keys):
             assert plan.kernel_text(i) == progs[k], (name, k)
+
+
+def test_refined_plans_merge_units():
+    """NON-PARITY refinement (stc_plan_refine): starting
+    from the reference plan, merges along graph edges that save HBM bytes or
+    launches; every merged pattern stays plannable by the reference planner"""
+    stitch = _stitch()
+    for name, cfg, before, after in (("bert_layer", "b200", 8, 4), ("bert_gelu", "v100", 3, 1),
+                                     ("attn_softmax", "b200", 1, 1)):
+        p = stitch.Plan(stitch.Graph(graph_text(name)), cfg)
+        assert p.stats()["stitched_kernels"] == before
+        p.refine()
+        assert p.stats()["stitched_kernels"] == after, name
+        for i in range(p.num_patterns):
+            assert p.kernel_text(i).startswith("stitched v1")
