@@ -425,6 +425,10 @@ def main():
                        "plan_kernels": len(desc), "templates": [k["template"] for k in desc],
                        "us_per_subgraph": round(ms_step * 1e3, 3),
                        "steps_per_graph_launch": spg,
+                       "timing": "steps run back to back, %d per CUDA-graph launch, each on its own cold buffer "
+                                 "set; programmatic dependent launch lets a step's parameter loads start while the "
+                                 "previous step drains (us_per_subgraph_one_launch_per_step: one graph launch per "
+                                 "step, no cross-step overlap)" % spg,
                        "us_per_subgraph_one_launch_per_step": round(us_single, 3),
                        "bytes_per_step_per_gpu": alg_bytes,
                        "l2": "inputs larger than L2: %d rotating buffer sets x %.1f MB = %.0f MB (>= 8x the 126 MB L2)"
