@@ -40,7 +40,7 @@ sys.path.insert(0, ROOT)
 WORKLOAD = "attn_softmax"
 WORKLOAD_DESC = "C2 BERT-base attention softmax chain fp32 [32,12,128,128] (+ key mask [32,128])"
 BATCH_TOKEN = "[32,"  # batch dim of every batched tensor in attn_softmax.graph
-SUBGRAPHS = ["ln_4096x768", "ln2pass_4096x768", "bert_gelu", "bert_resln", "colreduce", "dien_T10"]
+SUBGRAPHS = ["ln_4096x768", "ln2pass_4096x768", "bert_gelu", "bert_resln", "colreduce", "dien_T10", "bert_layer"]
 L2_BYTES = 126 * 1024 * 1024
 E2E_CHUNKS = int(os.environ.get("STITCH_E2E_CHUNKS", "4"))
 
@@ -189,9 +189,11 @@ def cpu_reference_subgraph(name, threads):
     return ref.time_eval([rule.graph_text(text, n)] * n, seed=1, reps=3), n
 
 
-def time_subgraph(stitch, name, gemm=False):
+def time_subgraph(stitch, name, gemm=False, refine=False):
     g = stitch.Graph(read_graph(name))
     plan = stitch.Plan(g, "b200")
+    if refine:
+        plan.refine()
     ex = stitch.Executor(plan, gemm=gemm)
     ex.upload(stitch.random_inputs(g, 1))
     desc = ex.describe()
@@ -203,7 +205,7 @@ def time_subgraph(stitch, name, gemm=False):
     top = max(range(len(desc)), key=lambda i: kus[i])
     peak, _ = measured_peaks()
     cpu = None
-    if not gemm:
+    if not gemm and not refine:
         try:
             from oracle import ref
             if ref.available():
@@ -415,6 +417,12 @@ def main():
                 subs["bert_layer_model_tf32"] = time_subgraph(stitch, "bert_layer", gemm=True)
             except Exception as e:
                 subs["bert_layer_model_tf32"] = {"error": str(e)[:300]}
+            # non-parity plan refinement (HBM-bytes / launch cost terms)
+            for name in ("bert_layer", "dien_T10"):
+                try:
+                    subs[name + "_refined"] = time_subgraph(stitch, name, refine=True)
+                except Exception as e:
+                    subs[name + "_refined"] = {"error": str(e)[:300]}
         result = {
             "metric": "stitched-subgraph HBM GB/s (algorithmic bytes / time)",
             "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,

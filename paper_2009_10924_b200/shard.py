@@ -75,6 +75,7 @@ RULES = {
     # placeholders average over their whole operands, so shards are NOT
     # equivalent to the full graph -- no tensor mapping, no gather
     "dien_T10": ShardRule(256, r"\[256[,\]]", {}),
+    "bert_layer": ShardRule(4096, r"\[4096[,\]]", {}),
     "dien_T20": ShardRule(256, r"\[256[,\]]", {}),
     # column reductions: shard the kept (column) axis; each GPU reduces all rows
     "colreduce": ShardRule(1024, r"1024\]", {"dy": 1, "xhat": 1, "dbias": 0, "dgamma": 0}),
