@@ -804,6 +804,11 @@ void emit_row(Emitter& em, const CompGraph& g, const std::set<int>& pat, const B
   em.reg_staged.clear();
 }
 
+bool grid_sync_mode() {
+  const char* v = std::getenv("STITCH_COL_SYNC");
+  return v && std::string(v) == "grid";
+}
+
 struct ColParams {
   int W, CT, RT, NCB, RB, U;
   int64_t NCH, ROWS, COLS;
@@ -919,12 +924,20 @@ void emit_column(Emitter& em, const CompGraph& g, const Body& b, const ColParams
     em.line("__syncthreads();");
   }
   // last-arriving CTA of this column strip combines the slabs in order
+  // (STITCH_COL_SYNC=grid: the north star's cooperative variant -- a
+  // grid-wide barrier, then the first slab CTA of each strip combines;
+  // measured slower, profiles/r01/colreduce_sync_ab.jsonl)
   const std::string last = em.fresh("last_");
   em.line("__shared__ unsigned " + last + ";");
-  em.line("__threadfence();");
-  em.line("__syncthreads();");
-  em.line("if (threadIdx.x == 0) " + last + " = atomicAdd(bar_ + " + std::to_string(ctr_off) + " + cb_, 1u) == " +
-          std::to_string(cp.RB - 1) + "u;");
+  if (grid_sync_mode()) {
+    em.line("grid_sync(bar_, gridDim.x);");
+    em.line("if (threadIdx.x == 0) " + last + " = rbk_ == 0;");
+  } else {
+    em.line("__threadfence();");
+    em.line("__syncthreads();");
+    em.line("if (threadIdx.x == 0) " + last + " = atomicAdd(bar_ + " + std::to_string(ctr_off) + " + cb_, 1u) == " +
+            std::to_string(cp.RB - 1) + "u;");
+  }
   em.line("__syncthreads();");
   em.open("if (" + last + ")");
   em.line("__threadfence();");
@@ -1198,7 +1211,7 @@ KernelSpec generate_pattern_kernel(const CompGraph& g, const std::vector<int>& v
   }
   k.grid = start;
   k.block = block;
-  k.cooperative = false;
+  k.cooperative = has_col && grid_sync_mode();
   k.smem = dyn_smem;
   k.alg_bytes = algorithmic_bytes(g, verts);
   for (size_t i = 0; i < bodies.size(); ++i)
