@@ -41,6 +41,7 @@ struct KernelSpec {
   int block = 256;
   int64_t smem = 0;                  // dynamic shared memory bytes
   bool cooperative = false;          // needs a grid-wide barrier (co-resident launch)
+  int cluster = 1;                   // thread-block cluster size (regional-cluster template)
   std::vector<std::string> inputs;   // tensor names bound to the leading pointer params
   std::vector<std::string> outputs;  // then these
   int64_t scratch_bytes = 0;         // trailing (bar_, part_) params when > 0 (zeroed once)

@@ -586,28 +586,47 @@ RowParams row_params(const std::vector<int>& inner, int block = 0) {
 
 // regional: a team of TPR threads owns a row; row elements live in registers
 // (st != nullptr: the CTA's rows arrive through the TMA pipeline in smem)
+// cluster > 1: regional-cluster mapping -- one row per thread-block cluster,
+// the row's chunks spread over cluster x block threads, team reductions
+// finished across the cluster through distributed shared memory
+RowParams cluster_row_params(const std::vector<int>& inner, int cluster, int block) {
+  RowParams p;
+  const int64_t L = prod(inner);
+  p.W = inner.back() % 4 == 0 ? 4 : (inner.back() % 2 == 0 ? 2 : 1);
+  p.TPR = cluster * block;
+  p.NJ = static_cast<int>((L / p.W + p.TPR - 1) / p.TPR);
+  p.block = block;
+  p.RPB = 1;
+  return p;
+}
+
 void emit_row(Emitter& em, const CompGraph& g, const std::set<int>& pat, const Body& b,
-              const StageCfg* st = nullptr, const std::vector<int>* pipe = nullptr) {
+              const StageCfg* st = nullptr, const std::vector<int>* pipe = nullptr, int cluster = 1) {
   const std::vector<int>& O = b.dims_a;
   const std::vector<int>& I = b.dims_b;
   const int64_t ROWS = prod(O), L = prod(I);
-  const RowParams rp = row_params(I, em.block);
+  const RowParams rp = cluster > 1 ? cluster_row_params(I, cluster, em.block) : row_params(I, em.block);
   em.W = rp.W;
   const int64_t nch = L / rp.W;
   const bool partial = nch % rp.TPR != 0;
   em.line("// regional body: " + std::to_string(ROWS) + " rows x " + std::to_string(L) + ", team " +
           std::to_string(rp.TPR) + " threads x " + std::to_string(rp.NJ) + " chunks x " + std::to_string(rp.W));
-  em.line("const int tl_ = threadIdx.x % " + std::to_string(rp.TPR) + ", team_ = threadIdx.x / " +
-          std::to_string(rp.TPR) + ";");
+  if (cluster > 1)
+    em.line("const int crank_ = (int)cluster_ctarank(), tl_ = crank_ * " + std::to_string(rp.block) +
+            " + (int)threadIdx.x, team_ = 0;  // cluster of " + std::to_string(cluster) + " CTAs per row");
+  else
+    em.line("const int tl_ = threadIdx.x % " + std::to_string(rp.TPR) + ", team_ = threadIdx.x / " +
+            std::to_string(rp.TPR) + ";");
   std::map<int, int> lvl_memo;
   std::map<int, std::vector<int>> levels;
   for (int r : b.reductions) levels[reduction_level(g, pat, r, lvl_memo)].push_back(r);
-  const int nwarps_team = rp.TPR > 32 ? rp.TPR / 32 : 1;
-  if (rp.TPR > 32) {
-    size_t maxr = 0;
-    for (auto& [l, rs] : levels) maxr = std::max(maxr, rs.size());
+  const int cta_team = cluster > 1 ? rp.block : rp.TPR;  // threads of one team inside this CTA
+  const int nwarps_team = cta_team > 32 ? cta_team / 32 : 1;
+  size_t maxr = 0;
+  for (auto& [l, rs] : levels) maxr = std::max(maxr, rs.size());
+  if (cta_team > 32)
     em.line("__shared__ double red_smem_[" + std::to_string(maxr) + "][" + std::to_string(rp.block / 32) + "];");
-  }
+  if (cluster > 1 && maxr) em.line("__shared__ double cl_red_[" + std::to_string(maxr) + "];");
   const std::string sRPB = std::to_string(rp.RPB), sL = std::to_string(L);
   if (st) {
     // TMA-staged inputs that a kernel produces must wait; graph parameters
@@ -677,6 +696,9 @@ void emit_row(Emitter& em, const CompGraph& g, const std::set<int>& pat, const B
     em.line("const " + cur + ";");
     em.line("{ const i64 n_ = rb_ + (i64)vgrid * " + sRPB + " + team_; if (n_ < " + sROWS + ") { " + next + "} }");
     em.reg_staged.insert(pipe->begin(), pipe->end());
+  } else if (cluster > 1) {
+    const std::string C = std::to_string(cluster);
+    em.open("for (i64 rb_ = (i64)(vbid / " + C + "); rb_ < " + std::to_string(ROWS) + "; rb_ += (i64)(vgrid / " + C + "))");
   } else {
     em.open("for (i64 rb_ = (i64)vbid * " + sRPB + "; rb_ < " + std::to_string(ROWS) +
             "; rb_ += (i64)vgrid * " + sRPB + ")");
@@ -747,12 +769,13 @@ void emit_row(Emitter& em, const CompGraph& g, const std::set<int>& pat, const B
     for (size_t i = 0; i < rs.size(); ++i)
       if (!ks[i].empty()) em.line("double " + acc[i] + " = (double)" + ks[i] + " - (double)" + kc[i] + ";");
     // team reduction: butterfly inside the warp, smem across the team's warps
-    const int w = std::min(rp.TPR, 32);
+    // (and DSMEM across the cluster's CTAs)
+    const int w = std::min(cta_team, 32);
     for (size_t i = 0; i < rs.size(); ++i) {
       const bool sum = g.node(rs[i]).kind == OpKind::ReduceSum;
       if (w > 1) em.line(acc[i] + " = " + (sum ? "bfly_sum(" : "bfly_max(") + acc[i] + ", " + std::to_string(w) + ");");
     }
-    if (rp.TPR > 32) {
+    if (cta_team > 32) {
       em.line("if ((threadIdx.x & 31) == 0) {");
       for (size_t i = 0; i < rs.size(); ++i)
         em.line("  red_smem_[" + std::to_string(i) + "][threadIdx.x >> 5] = " + acc[i] + ";");
@@ -768,6 +791,20 @@ void emit_row(Emitter& em, const CompGraph& g, const std::set<int>& pat, const B
                 "; }");
       }
       em.line("__syncthreads();");
+    }
+    if (cluster > 1) {  // CTA partials -> every thread folds the cluster's in rank order
+      em.line("if (threadIdx.x == 0) {");
+      for (size_t i = 0; i < rs.size(); ++i) em.line("  cl_red_[" + std::to_string(i) + "] = " + acc[i] + ";");
+      em.line("}");
+      em.line("cluster_sync_all();");
+      for (size_t i = 0; i < rs.size(); ++i) {
+        const bool sum = g.node(rs[i]).kind == OpKind::ReduceSum;
+        const std::string src = "ld_dsmem_f64(cl_red_ + " + std::to_string(i) + ", q_)";
+        em.line("{ " + acc[i] + " = ld_dsmem_f64(cl_red_ + " + std::to_string(i) + ", 0u); for (unsigned q_ = 1; q_ < " +
+                std::to_string(cluster) + "u; ++q_) " + acc[i] + " = " +
+                (sum ? acc[i] + " + " + src : "op_max(" + acc[i] + ", (float)" + src + ")") + "; }");
+      }
+      em.line("cluster_sync_all();  // every CTA read the partials before cl_red_ is reused");
     }
     for (size_t i = 0; i < rs.size(); ++i) {
       const std::string t = em.fresh("red");
@@ -1100,6 +1137,25 @@ KernelSpec generate_pattern_kernel(const CompGraph& g, const std::vector<int>& v
       }
     }
   }
+  // regional-cluster: a single row body with too few rows to fill the GPU
+  // (fewer row teams than SMs) and long rows spreads each row over a
+  // thread-block cluster (<= 16 CTAs, DSMEM team reduction) so ROWS x C CTAs
+  // share the row stream
+  int cluster = 1;
+  if (bodies.size() == 1 && bodies[0].kind == Kind::Row && env_int("STITCH_ROW_CLUSTER", 1) != 0) {
+    const RowParams rp = row_params(bodies[0].dims_b, block);
+    const int64_t rows = prod(bodies[0].dims_a), nch = prod(bodies[0].dims_b) / rp.W;
+    const int64_t ntiles = (rows + rp.RPB - 1) / rp.RPB;
+    if (ntiles < kSmCount && nch >= 512) {
+      int c = 2;
+      while (c < 16 && rows * c < 2 * kSmCount) c *= 2;
+      const int b2 = static_cast<int>(std::clamp<int64_t>(pow2ceil((nch + int64_t(c) * 4 - 1) / (int64_t(c) * 4)), 128, 1024));
+      if ((nch + int64_t(c) * b2 - 1) / (int64_t(c) * b2) <= 16 && int64_t(c) * b2 <= nch) {
+        cluster = c;
+        block = b2;
+      }
+    }
+  }
   em.block = block;
   em.hoist = env_int("STITCH_PDL", 1) != 0 && env_int("STITCH_PDL_HOIST", 1) != 0;
   const int per_sm = std::max(1, std::min(env_int("STITCH_COL_CTAS", 3), 2048 / block));
@@ -1119,6 +1175,9 @@ KernelSpec generate_pattern_kernel(const CompGraph& g, const std::vector<int>& v
       const int U = local_unroll(chunks, block);
       b.blocks = static_cast<int>(std::clamp<int64_t>((chunks + int64_t(block) * U - 1) / (int64_t(block) * U), 1,
                                                       int64_t(kSmCount) * env_int("STITCH_LOCAL_CTAS", 32)));
+    } else if (b.kind == Kind::Row && cluster > 1) {
+      const int64_t rows = prod(b.dims_a);
+      b.blocks = static_cast<int>(std::min<int64_t>(rows, std::max<int64_t>(1, 4 * kSmCount / cluster)) * cluster);
     } else if (b.kind == Kind::Row) {
       const RowParams rp = row_params(b.dims_b, block);
       const int64_t rows = prod(b.dims_a), L = prod(b.dims_b), ntiles = (rows + rp.RPB - 1) / rp.RPB;
@@ -1128,7 +1187,7 @@ KernelSpec generate_pattern_kernel(const CompGraph& g, const std::vector<int>& v
       // (default, STITCH_ROW_PIPE >= 2 rows per team) or through the opt-in
       // TMA pipeline (STITCH_STAGE=1: measured slower)
       const int pipe_rows = env_int("STITCH_ROW_PIPE", single_row_body ? 2 : 1);
-      if ((env_int("STITCH_STAGE", 0) || pipe_rows > 1) && rp.W == 4) {
+      if ((env_int("STITCH_STAGE", 0) || pipe_rows > 1) && rp.W == 4 && cluster == 1) {
         em.out.str("");
         em.clear_memo();
         em.reduced.clear();
@@ -1189,7 +1248,8 @@ KernelSpec generate_pattern_kernel(const CompGraph& g, const std::vector<int>& v
     em.reset_wait();
     if (b.kind == Kind::Local) emit_local(em, g, b);
     else if (b.kind == Kind::Row)
-      emit_row(em, g, pat, b, stage[i].tensors.empty() ? nullptr : &stage[i], pipe[i].empty() ? nullptr : &pipe[i]);
+      emit_row(em, g, pat, b, stage[i].tensors.empty() ? nullptr : &stage[i], pipe[i].empty() ? nullptr : &pipe[i],
+               cluster);
     else emit_column(em, g, b, cps[i], part_off[i], ctr_off[i]);
     em.ensure_wait();  // every path waits before the CTA retires
     body_src << "  " << (i ? "else " : "") << "if (blockIdx.x < " << start + b.blocks << ") {\n";
@@ -1212,6 +1272,8 @@ KernelSpec generate_pattern_kernel(const CompGraph& g, const std::vector<int>& v
   k.grid = start;
   k.block = block;
   k.cooperative = has_col && grid_sync_mode();
+  k.cluster = cluster;
+  if (cluster > 1) k.tmpl += "-cluster" + std::to_string(cluster);
   k.smem = dyn_smem;
   k.alg_bytes = algorithmic_bytes(g, verts);
   for (size_t i = 0; i < bodies.size(); ++i)

@@ -163,6 +163,7 @@ void Executor::finish_init(const std::string& cubin) {
     const void* fp = reinterpret_cast<const void*>(f);
     if (k.smem > 48 * 1024)
       STC_RT(cudaFuncSetAttribute(fp, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(k.smem)));
+    if (k.cluster > 8) STC_RT(cudaFuncSetAttribute(fp, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     if (k.cooperative) {
       int per_sm = 0;
       STC_RT(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fp, k.block, static_cast<size_t>(k.smem)));
@@ -613,20 +614,25 @@ void Executor::launch_kernel(size_t i, int set, cudaStream_t s, int after, const
   cfg.blockDim = dim3(static_cast<unsigned>(k.block), 1, 1);
   cfg.dynamicSmemBytes = static_cast<size_t>(k.smem);
   cfg.stream = s;
-  cudaLaunchAttribute attr{};
+  cudaLaunchAttribute attrs[2]{};
+  unsigned na = 0;
   if (k.cooperative && coop_in_graph_) {
-    attr.id = cudaLaunchAttributeCooperative;
-    attr.val.cooperative = 1;
-    cfg.attrs = &attr;
-    cfg.numAttrs = 1;
+    attrs[na].id = cudaLaunchAttributeCooperative;
+    attrs[na++].val.cooperative = 1;
   } else if (pdl_ && after >= 0 && !k.cooperative && !specs_[static_cast<size_t>(after)].cooperative) {
     // programmatic dependent launch: kernel i may launch while kernel i-1
     // drains; it griddepcontrol.wait()s before reading i-1's outputs
-    attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr.val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = &attr;
-    cfg.numAttrs = 1;
+    attrs[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attrs[na++].val.programmaticStreamSerializationAllowed = 1;
   }
+  if (k.cluster > 1) {  // regional-cluster template: one row per cluster
+    attrs[na].id = cudaLaunchAttributeClusterDimension;
+    attrs[na].val.clusterDim.x = static_cast<unsigned>(k.cluster);
+    attrs[na].val.clusterDim.y = 1;
+    attrs[na++].val.clusterDim.z = 1;
+  }
+  cfg.attrs = na ? attrs : nullptr;
+  cfg.numAttrs = na;
   STC_RT(cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(fns_[i]), args.data()));
 }
 
@@ -976,6 +982,7 @@ std::string describe_specs(const std::vector<KernelSpec>& specs) {
     o << (i ? "," : "") << "{\"name\":\"" << k.name << "\",\"template\":\"" << json_escape(k.tmpl)
       << "\",\"pattern\":\"" << k.pattern_key << "\",\"grid\":" << k.grid << ",\"block\":" << k.block
       << ",\"smem\":" << k.smem << ",\"cooperative\":" << (k.cooperative ? "true" : "false")
+      << ",\"cluster\":" << k.cluster
       << ",\"bytes\":" << k.alg_bytes << ",\"inputs\":[";
     for (size_t j = 0; j < k.inputs.size(); ++j) o << (j ? "," : "") << "\"" << k.inputs[j] << "\"";
     o << "],\"outputs\":[";

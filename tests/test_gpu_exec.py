@@ -213,6 +213,12 @@ EDGE_SHAPES = {
     "colreduce_odd_cols": _colreduce_text(1000, 70),  # partial column strips, scalar lanes
     "colreduce_few_rows": _colreduce_text(5, 4096),   # one slab per strip
     "colreduce_tall": _colreduce_text(70001, 36),     # many slabs, ragged last slab
+    # few long rows: regional-cluster template (one row per thread-block
+    # cluster, DSMEM team reduction)
+    "softmax_cluster_8x65536": _softmax_text(8, 65536),
+    "softmax_cluster_16x8192": _softmax_text(16, 8192),
+    "ln_cluster_4x40000": _ln_text(4, 40000),
+    "softmax_cluster_ragged_5x9002": _softmax_text(5, 9002),
 }
 
 
