@@ -232,6 +232,8 @@ def main():
                     help="steps captured per CUDA-graph launch (largest of 16/8/4/2/1 dividing --steps)")
     ap.add_argument("--no-subgraphs", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--strong", action="store_true",
+                    help="strong scaling: the 32-sequence batch is sharded over the ranks (32/N each, per-shard plans)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -255,6 +257,9 @@ def main():
 
     from paper_2009_10924_b200 import stitch
     text = read_graph(WORKLOAD)
+    if args.strong and world > 1:  # this rank's shard of ONE 32-sequence batch, re-planned for its shape
+        from paper_2009_10924_b200 import shard as _shard
+        text = _shard.RULES[WORKLOAD].graph_text(text, world)
     g = stitch.Graph(text)
     plan = stitch.Plan(g, "b200")
     ex = stitch.Executor(plan, device=local)
@@ -337,7 +342,11 @@ def main():
     # pipelined: the batch as E2E_CHUNKS chunk plans, H2D / graph / D2H of
     # consecutive chunks overlapped (stc_exec_run_host_chunked)
     from paper_2009_10924_b200 import shard
-    cx = stitch.ChunkedExecutor(text, shard.RULES[WORKLOAD], E2E_CHUNKS, device=local)
+    rule = shard.RULES[WORKLOAD]
+    if args.strong and world > 1:  # chunk this rank's shard
+        rule = shard.ShardRule(32 // world, r"\[%d," % (32 // world), rule.axis_of)
+    cx = stitch.ChunkedExecutor(text, rule, max(d for d in range(1, E2E_CHUNKS + 1) if rule.full % d == 0),
+                                device=local)
     e2e_steps = max(5, min(50, args.steps // 20))
 
     def host_loop(fn, n):
@@ -377,7 +386,8 @@ def main():
     verification = None
     if rank == 0:
         from oracle import numpy_oracle as no
-        one = no.parse_graph(text.replace(BATCH_TOKEN, "[1,"))
+        from paper_2009_10924_b200 import shard as _sh
+        one = no.parse_graph(_sh.RULES[WORKLOAD].extent_text(read_graph(WORKLOAD), 1))
         ok, worst = True, 0.0
         for r in range(world):
             full_in = stitch.random_inputs(g, seed=1 + r)
@@ -427,7 +437,7 @@ def main():
             "metric": "stitched-subgraph HBM GB/s (algorithmic bytes / time)",
             "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_step, 6), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "scaling": "strong" if args.strong else "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic: splitmix64 random_inputs(seed=1+rank), uniform(-1,1) f32",
             "config": {"workload": WORKLOAD_DESC, "graph": WORKLOAD, "device_cfg": "b200_device.cfg",
                        "plan_kernels": len(desc), "templates": [k["template"] for k in desc],
@@ -441,7 +451,7 @@ def main():
                        "bytes_per_step_per_gpu": alg_bytes,
                        "l2": "inputs larger than L2: %d rotating buffer sets x %.1f MB = %.0f MB (>= 8x the 126 MB L2)"
                              % (sets, per_set / 1e6, sets * per_set / 1e6),
-                       "global_batch": 32 * world,
+                       "global_batch": 32 if args.strong else 32 * world,
                        "parallelism": "independent batch shards, %d rank(s), no collective" % world},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "peak_source": peak_kind + " (MEASURED_PEAKS.json hbm_gbs)"
