@@ -98,6 +98,9 @@ class ClockSampler:
             return
         self.thread = threading.Thread(target=self._run, daemon=True)
         self.thread.start()
+        t0 = time.perf_counter()  # sampling is live before anything is timed
+        while not self.samples and time.perf_counter() - t0 < 2.0:
+            time.sleep(0.001)
 
     def _run(self):
         nv = self.nv
@@ -116,7 +119,7 @@ class ClockSampler:
         self.stop_flag.set()
         self.thread.join(timeout=2)
         timed = [s for s in self.samples if t0 <= s[0] <= t1]
-        use = timed if len(timed) >= 3 else [s for s in self.samples if t0 - 0.2 <= s[0] <= t1]
+        use = timed if len(timed) >= 3 else [s for s in self.samples if t0 - 0.2 <= s[0] <= t1 + 0.05]
         if not use:
             return {"sm_mhz": None, "sm_max_mhz": float(self.max_mhz), "reasons": ["no samples"], "samples": 0}
         reasons = sorted({name for _, _, r in use for name, attr in self.REASONS if r & getattr(self.nv, attr)})
@@ -200,7 +203,7 @@ def time_subgraph(stitch, name, gemm=False, refine=False):
     per_set = sum(t.nbytes for t in g.params) + sum(t.nbytes for t in g.outputs)
     sets = min(256, max(2, math.ceil(8 * L2_BYTES / max(per_set, 1))))
     us1, kus = ex.time(iters=200, warmup=20, sets=sets, per_kernel=True)
-    us = ex.time_batched(steps=256, warmup=32, sets=sets, steps_per_graph=16)
+    us = ex.time_batched(steps=256, warmup=64, sets=sets, steps_per_graph=64)
     alg = sum(k["bytes"] for k in desc)
     top = max(range(len(desc)), key=lambda i: kus[i])
     peak, _ = measured_peaks()
@@ -225,10 +228,10 @@ def time_subgraph(stitch, name, gemm=False, refine=False):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--steps", type=int, default=2048)
     ap.add_argument("--warmup", type=int, default=50)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--steps-per-graph", type=int, default=16,
+    ap.add_argument("--steps-per-graph", type=int, default=64,
                     help="steps captured per CUDA-graph launch (largest of 16/8/4/2/1 dividing --steps)")
     ap.add_argument("--no-subgraphs", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -271,7 +274,7 @@ def main():
     sets = max(2, math.ceil(8 * L2_BYTES / per_set))
     # B consecutive steps per CUDA-graph launch (each step still reads its own
     # cold buffer set and writes its own outputs); B divides K exactly
-    spg = next(b for b in (args.steps_per_graph, 8, 4, 2, 1) if b >= 1 and args.steps % b == 0)
+    spg = next(b for b in (args.steps_per_graph, 32, 16, 8, 4, 2, 1) if b >= 1 and args.steps % b == 0)
     n_graphs = ex.prepare_batches(sets, spg)
     sets = max(sets, n_graphs * spg)
     # an explicit (non-default) stream: the graph replays AND the timing events
