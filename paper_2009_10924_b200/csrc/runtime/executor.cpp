@@ -92,7 +92,6 @@ Executor::Executor(const CompGraph& g, const FusionPlan& plan,
     dag_ = *v != '0';
     sources_only_ = *v == '2';
   }
-  if (const char* v = std::getenv("STITCH_PDL_EDGES")) pdl_edges_ = *v != '0';
   STC_RT(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
   plan_launches(plan, kernels, model, mode, gemm_opaque);
   auto opts = default_nvrtc_options();
@@ -174,55 +173,6 @@ void Executor::finish_init(const std::string& cubin) {
     fns_.push_back(f);
   }
   compute_deps();
-}
-
-void Executor::promote_edges(cudaGraph_t graph) {
-  if (!pdl_ || !pdl_edges_) return;
-  size_t n = 0;
-  STC_RT(cudaGraphGetEdges_v2(graph, nullptr, nullptr, nullptr, &n));
-  if (!n) return;
-  std::vector<cudaGraphNode_t> from(n), to(n);
-  std::vector<cudaGraphEdgeData> data(n);
-  STC_RT(cudaGraphGetEdges_v2(graph, from.data(), to.data(), data.data(), &n));
-  std::map<const void*, size_t> fn_index;
-  for (size_t i = 0; i < fns_.size(); ++i) fn_index[reinterpret_cast<const void*>(fns_[i])] = i;
-  auto plain_kernel = [&](cudaGraphNode_t node) {
-    cudaGraphNodeType t;
-    if (cudaGraphNodeGetType(node, &t) != cudaSuccess || t != cudaGraphNodeTypeKernel) return false;
-    cudaKernelNodeParams kp{};
-    if (cudaGraphKernelNodeGetParams(node, &kp) != cudaSuccess) return false;
-    auto it = fn_index.find(kp.func);
-    return it != fn_index.end() && !specs_[it->second].cooperative;
-  };
-  std::vector<cudaGraphNode_t> rf, rt;
-  std::vector<cudaGraphEdgeData> rd;
-  for (size_t e = 0; e < n; ++e)
-    if (data[e].type == cudaGraphDependencyTypeDefault && plain_kernel(from[e]) && plain_kernel(to[e])) {
-      rf.push_back(from[e]);
-      rt.push_back(to[e]);
-      rd.push_back(data[e]);
-    }
-  if (std::getenv("STITCH_DEBUG")) {
-    size_t prog = 0;
-    for (size_t e = 0; e < n; ++e) prog += data[e].type == cudaGraphDependencyTypeProgrammatic;
-    std::fprintf(stderr, "[exec] graph edges %zu: %zu already programmatic, %zu to promote\n", n, prog, rf.size());
-  }
-  if (rf.empty()) return;
-  STC_RT(cudaGraphRemoveDependencies_v2(graph, rf.data(), rt.data(), rd.data(), rf.size()));
-  for (auto& d : rd) {
-    d.type = cudaGraphDependencyTypeProgrammatic;
-    d.from_port = cudaGraphKernelNodePortProgrammatic;
-  }
-  STC_RT(cudaGraphAddDependencies_v2(graph, rf.data(), rt.data(), rd.data(), rf.size()));
-  if (std::getenv("STITCH_DEBUG")) {
-    size_t m = 0, prog = 0;
-    STC_RT(cudaGraphGetEdges_v2(graph, nullptr, nullptr, nullptr, &m));
-    std::vector<cudaGraphNode_t> f2(m), t2(m);
-    std::vector<cudaGraphEdgeData> d2(m);
-    STC_RT(cudaGraphGetEdges_v2(graph, f2.data(), t2.data(), d2.data(), &m));
-    for (auto& d : d2) prog += d.type == cudaGraphDependencyTypeProgrammatic;
-    std::fprintf(stderr, "[exec] after promotion: %zu edges, %zu programmatic\n", m, prog);
-  }
 }
 
 void Executor::compute_deps() {
@@ -350,7 +300,10 @@ int Executor::capture_plan(int set, cudaStream_t origin, int prev) {
       if (ln.tail >= 0 && (d == ln.tail || anc[static_cast<size_t>(ln.tail)][static_cast<size_t>(d)])) continue;
       STC_RT(cudaStreamWaitEvent(ln.s, kernel_events_[static_cast<size_t>(d)], 0));
     }
-    const int after = ln.tail >= 0 ? ln.tail : (best == 0 ? prev : -1);
+    // launched with the PDL attribute whenever it has a kernel predecessor:
+    // stream capture then makes every incoming kernel edge programmatic,
+    // including the cross-lane ones from event waits
+    const int after = ln.tail >= 0 ? ln.tail : !deps_[i].empty() ? deps_[i].front() : (best == 0 ? prev : -1);
     launch_kernel(i, set, ln.s, after);
     STC_RT(cudaEventRecord(kernel_events_[i], ln.s));
     ln.tail = static_cast<int>(i);
@@ -658,7 +611,6 @@ void Executor::build_graph(int set) {
     }
     const cudaError_t end = cudaStreamEndCapture(stream_, &graph);
     if (!failed && end == cudaSuccess) {
-      promote_edges(graph);
       STC_RT(cudaGraphInstantiate(&ge, graph, 0));
       cudaGraphDestroy(graph);
       return;
@@ -872,7 +824,6 @@ int Executor::prepare_batches(int sets, int batch) {
     for (int t = 0; t < batch; ++t)  // PDL also across consecutive (independent) steps
       tail = capture_plan(b * batch + t, stream_, tail);
     STC_RT(cudaStreamEndCapture(stream_, &graph));
-    promote_edges(graph);
     cudaGraphExec_t ge = nullptr;
     STC_RT(cudaGraphInstantiate(&ge, graph, 0));
     cudaGraphDestroy(graph);

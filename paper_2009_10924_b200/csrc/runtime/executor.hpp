@@ -137,10 +137,6 @@ class Executor {
   int capture_plan(int set, cudaStream_t origin, int prev);
   void compute_deps();
   void finish_init(const std::string& cubin);  // load module, resolve kernels, GEMM setup
-  // turn every kernel->kernel edge of a captured plan graph into a
-  // programmatic (PDL) edge: every kernel griddepcontrol.wait()s before its
-  // first read, so the dependent may launch while its producers drain
-  void promote_edges(cudaGraph_t graph);
 
   CompGraph g_;
   const DeviceInfo* dev_ = nullptr;
@@ -163,7 +159,6 @@ class Executor {
   bool tracing_ = false;
   bool dag_ = true;  // STITCH_DAG=0 captures the plan as one linear chain
   bool sources_only_ = false;  // STITCH_DAG=2: fork only producer-less kernels
-  bool pdl_edges_ = true;  // STITCH_PDL_EDGES=0 keeps cross-stream edges full
   std::vector<std::vector<int>> deps_;       // [kernel] -> producer kernels
   std::vector<cudaStream_t> aux_streams_;    // fork targets for independent kernels
   std::vector<cudaEvent_t> kernel_events_;   // [kernel] done-event (capture only)
