@@ -1,0 +1,12 @@
+#!/bin/bash
+# compute-sanitizer passes over the generated kernels (run under gpurun):
+# memcheck (out-of-bounds / misaligned), racecheck (shared-memory hazards),
+# synccheck (barrier misuse).  Summaries land in gpurun_out/.
+mkdir -p gpurun_out
+timeout 1500 compute-sanitizer --tool memcheck --print-limit 20 python -m pytest tests/test_gpu_exec.py -q -x \
+  -k "edge_shapes or op_and_dtype or (fixture_parity and stitched) or dag or low_level" > gpurun_out/memcheck.log 2>&1
+timeout 900 compute-sanitizer --tool racecheck --print-limit 10 python -m pytest tests/test_gpu_exec.py -q -x \
+  -k "edge_shapes or softmax or layernorm or variance" > gpurun_out/racecheck.log 2>&1
+timeout 900 compute-sanitizer --tool synccheck --print-limit 10 python -m pytest tests/test_gpu_exec.py -q -x \
+  -k "edge_shapes" > gpurun_out/synccheck.log 2>&1
+tail -n 2 gpurun_out/memcheck.log gpurun_out/racecheck.log gpurun_out/synccheck.log
