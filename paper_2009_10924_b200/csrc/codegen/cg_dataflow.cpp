@@ -91,8 +91,6 @@ class Emitter {
   // current row lives in registers cu_<name>_<chunk> (prefetched a row ahead)
   std::map<std::string, int> domain_chunk;
   std::set<int> reg_staged;
-  // local bodies: coords key -> (linear index expr, domain dims)
-  std::map<std::string, std::pair<std::string, std::vector<int>>> domain_lin;
 
   const std::string& ix() const { return ix_; }
   std::string fresh(const char* p) { return p + std::to_string(counter_++); }
@@ -143,14 +141,6 @@ class Emitter {
 
   // linear element index of `c` for lane k (only varying coords shift)
   std::string linear(int v, const Coords& c, int k) const {
-    // a tensor shaped like the local domain, read at the domain's own
-    // coordinates, is addressed by the chunk's linear index directly (no
-    // re-composition of the div/mod-decomposed coordinates)
-    if (auto it = domain_lin.find(coords_key(c)); it != domain_lin.end()) {
-      const auto& sd = g_.node(v).shape.dims;
-      if (std::vector<int64_t>(it->second.second.begin(), it->second.second.end()) == sd)
-        return k ? "(" + it->second.first + " + " + std::to_string(k) + ")" : it->second.first;
-    }
     const auto strides = g_.node(v).shape.strides();
     std::string s;
     for (size_t i = 0; i < c.size(); ++i) {
@@ -543,8 +533,6 @@ void emit_local(Emitter& em, const CompGraph& g, const Body& b) {
       const std::string lin = em.W == 1 ? cc : cc + " * " + std::to_string(em.W);
       auto names = decompose(em, lin, D, "d");
       for (size_t i = 0; i < D.size(); ++i) c.push_back({names[i], i + 1 == D.size() && em.W > 1, true});
-      // opt-in: measured slower on bert_gelu (register allocation), so off
-      if (env_int("STITCH_DOMAIN_LIN", 0)) em.domain_lin[coords_key(c)] = {"(" + lin + ")", D};
     }
     for (int o : b.outputs) stores.emplace_back(o, c, em.value(o, c), ok);
   }
