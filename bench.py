@@ -466,7 +466,8 @@ def main():
             "e2e": {"value": round(e2e_val, 3), "unit": "GB/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "us_per_step": round(e2e_s * 1e6, 1),
                     "path": "stc_exec_run_host_chunked: pinned host -> %d batch chunks (chunk plans re-planned "
-                            "for batch %d), H2D / CUDA graph / D2H of consecutive chunks overlapped on 3 streams"
+                            "for batch %d); H2D of chunk k+1 on the copy engine overlaps the stitched kernels of "
+                            "chunk k, which write their outputs straight into the mapped pinned host buffer"
                             % (E2E_CHUNKS, 32 // E2E_CHUNKS),
                     "unpipelined": {"value": round(alg_bytes * world / e2e_plain_s / 1e9, 3),
                                     "us_per_step": round(e2e_plain_s * 1e6, 1),

@@ -312,3 +312,20 @@ def test_refined_plan_matches_oracle(name, cfg):
     for k, tol in _tolerances(og).items():
         rep = stitch.compare({k: got[k]}, {k: want[k]}, tol, 1e-5)
         assert rep["pass"], (name, k, rep["message"])
+
+
+def test_chunked_host_run_zero_copy_outputs():
+    """pinned (device-mapped) output buffers: the chunk kernels write straight
+    into host memory, no D2H stage -- same bits as the copy-engine path"""
+    import torch
+    from paper_2009_10924_b200 import shard
+    stitch = _stitch()
+    text = config_graph("attn_softmax")
+    g = stitch.Graph(text)
+    inputs = stitch.random_inputs(g, 5)
+    want = stitch.Executor(stitch.Plan(g, "b200")).run(inputs)
+    pin_in = {t.name: torch.from_numpy(inputs[t.name]).pin_memory().numpy() for t in g.params}
+    pin_out = {t.name: torch.zeros(t.dims, dtype=torch.float32).pin_memory().numpy() for t in g.outputs}
+    got = stitch.ChunkedExecutor(text, shard.RULES["attn_softmax"], 4).run(pin_in, out=pin_out)
+    for k in want:
+        assert np.array_equal(got[k], want[k]), k

@@ -32,10 +32,23 @@ for name in sys.argv[1:] or ["attn_softmax", "ln_4096x768", "bert_gelu", "bert_r
     else:
         u = full // 32
         shapes.update({"taper_1_3_4x6_3_1": [u * c for c in [1, 3, 4, 4, 4, 4, 4, 4, 3, 1]]})
+    def d2h_copy(cx):
+        def f():
+            os.environ["STITCH_E2E_ZC_OUT"] = "0"
+            try:
+                cx.run(pin_in, out=pin_out)
+            finally:
+                os.environ.pop("STITCH_E2E_ZC_OUT", None)
+        return f
+
     for label, ch in shapes.items():
         cx = stitch.ChunkedExecutor(text, shard.RULES[name], ch)
-        rows.append((label, lambda cx=cx: cx.run(pin_in, out=pin_out)))
+        rows.append((label, d2h_copy(cx)))
     rows.append(("zero_copy", lambda: ex.run_zero_copy(pin_in, pin_out)))
+    for n in (2, 4, 8):
+        cz = stitch.ChunkedExecutor(text, shard.RULES[name], n)
+
+        rows.append(("chunked%d_zc_out" % n, lambda cz=cz: cz.run(pin_in, out=pin_out)))
     for label, fn in rows:
         s = timed(fn)
         same = all(np.array_equal(pin_out[k], ref[k]) for k in ref)
