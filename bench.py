@@ -415,6 +415,10 @@ def main():
                            "sample": "full C2 batch as %d batch shards on %d host threads, unmodified "
                                      "reference eval_reference (oracle/_ref), best of 3: %.3f s"
                                      % (shards, shards, s)}
+                    # the reference executor is single-threaded by design: one core, whole batch
+                    s1 = ref.time_eval([text], seed=1, reps=2)
+                    cpu["single_core"] = {"value": round(alg_bytes / s1 / 1e9, 4), "seconds": round(s1, 3),
+                                          "sample": "full C2 batch, one thread, best of 2"}
             except Exception as e:  # reported, never fatal
                 cpu = {"value": None, "unit": "GB/s", "cores": 0, "kind": "reference", "sample": "failed: %s" % e}
         subs = {}
