@@ -190,9 +190,15 @@ class Emitter {
       return {{t}};
     }
     const bool contiguous = nvary == 1 && last_vary == static_cast<int>(c.size()) - 1 &&
-                            c.back().aligned && sh.dims.back() % W == 0 && sh.dtype == DType::F32 && W == 4;
+                            c.back().aligned && sh.dims.back() % W == 0 && W == 4;
     Val r;
-    if (contiguous) {
+    if (contiguous && sh.dtype == DType::F16) {  // 4 halves, one 64-bit load
+      const std::string q = fresh("q");
+      line("const float4 " + q + " = ld4h(" + ptr + " + " + linear(v, c, 0) + ");");
+      for (const char* f : {".x", ".y", ".z", ".w"}) r.lanes.push_back(q + f);
+      return r;
+    }
+    if (contiguous && sh.dtype == DType::F32) {
       const std::string q = fresh("q");
       const bool cached = cached_tensors.count(v) > 0;
       line("const float4 " + q + " = " + (cached ? "ld4c(" : "ld4(") + ptr + " + " + linear(v, c, 0) + ");");
@@ -489,9 +495,10 @@ void store_val(Emitter& em, const CompGraph& g, int v, const Coords& c, const Va
   for (const auto& x : c) nvary += x.vary;
   const std::string pre = guard.empty() ? "" : "if (" + guard + ") ";
   em.ensure_wait();
-  if (em.W == 4 && nvary == 1 && c.back().vary && c.back().aligned && sh.dtype == DType::F32) {
-    em.line(pre + "st4(" + ptr + " + " + em.linear(v, c, 0) + ", " + val.at(0) + ", " + val.at(1) + ", " +
-            val.at(2) + ", " + val.at(3) + ");");
+  if (em.W == 4 && nvary == 1 && c.back().vary && c.back().aligned &&
+      (sh.dtype == DType::F32 || (sh.dtype == DType::F16 && sh.dims.back() % 4 == 0))) {
+    em.line(pre + (sh.dtype == DType::F32 ? "st4(" : "st4h(") + ptr + " + " + em.linear(v, c, 0) + ", " + val.at(0) +
+            ", " + val.at(1) + ", " + val.at(2) + ", " + val.at(3) + ");");
     return;
   }
   if (nvary == 0) {

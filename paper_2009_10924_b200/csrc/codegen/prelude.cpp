@@ -53,6 +53,17 @@ __device__ __forceinline__ void st4(float* p, float a, float b, float c, float d
 #endif
 }
 
+// 4 halves as one 64-bit access (f16 tensors, 4-aligned element index)
+__device__ __forceinline__ float4 ld4h(const f16_t* p) {
+  unsigned a, b;
+  asm("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(a), "=r"(b) : "l"(p));
+  return make_float4(h2f((f16_t)(a & 0xffffu)), h2f((f16_t)(a >> 16)), h2f((f16_t)(b & 0xffffu)), h2f((f16_t)(b >> 16)));
+}
+__device__ __forceinline__ void st4h(f16_t* p, float x, float y, float z, float w) {
+  const unsigned a = (unsigned)f2h(x) | ((unsigned)f2h(y) << 16), b = (unsigned)f2h(z) | ((unsigned)f2h(w) << 16);
+  asm volatile("st.global.cs.v2.u32 [%0], {%1,%2};" :: "l"(p), "r"(a), "r"(b) : "memory");
+}
+
 // per-op rounding to the node dtype (src/sim.cpp:67-75 semantics)
 __device__ __forceinline__ float rnd_f16(float x) { return h2f(f2h(x)); }
 __device__ __forceinline__ float rnd_i32(float x) { return (float)(int)roundf(x); }
