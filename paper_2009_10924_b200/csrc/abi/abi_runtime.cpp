@@ -8,9 +8,12 @@
 // NCCL is loaded lazily (dlopen libnccl.so.2) so the library keeps loading on
 // hosts without it; the communicator's unique id travels out of band (the
 // caller broadcasts the 128 bytes, e.g. over torch.distributed or a file).
+// dlopen resolves by soname, so if the host process already loaded an NCCL
+// (e.g. torch's bundled build) that one is shared; STITCH_NCCL_LIB overrides.
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -70,9 +73,10 @@ struct NcclApi {
 NcclApi& nccl() {
   static NcclApi api;
   if (api.h) return api;
+  if (const char* p = std::getenv("STITCH_NCCL_LIB"); p && *p) api.h = dlopen(p, RTLD_NOW | RTLD_LOCAL);
   for (const char* name : {"libnccl.so.2", "libnccl.so"}) {
-    api.h = dlopen(name, RTLD_NOW | RTLD_LOCAL);
     if (api.h) break;
+    api.h = dlopen(name, RTLD_NOW | RTLD_LOCAL);
   }
   if (!api.h) throw std::runtime_error("[nccl] libnccl.so.2 not found");
   api.get_id = reinterpret_cast<NcclApi::GetUniqueId>(dlsym(api.h, "ncclGetUniqueId"));

@@ -275,6 +275,10 @@ def test_low_level_runtime_cgraph_and_nccl():
     CUDA Graph of two dependent launches, event timing with L2 flush, and a
     single-rank NCCL gather (the verification collective)"""
     import ctypes
+    # NCCL is dlopen'ed by soname: whichever libnccl.so.2 the process has
+    # loaded first is the one everybody shares -- load torch's (newer) build
+    # first, as a host application using torch.distributed would
+    import torch  # noqa: F401
     stitch = _stitch()
     src = r'''
     extern "C" __global__ void axpy(float* y, const float* x, float a, int n) {
