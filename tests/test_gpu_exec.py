@@ -345,3 +345,33 @@ def test_chunked_host_run_zero_copy_outputs():
     got = stitch.ChunkedExecutor(text, shard.RULES["attn_softmax"], 4).run(pin_in, out=pin_out)
     for k in want:
         assert np.array_equal(got[k], want[k]), k
+
+
+HETERO = """x = parameter : f32[64,4096]
+m = reduce_max(x) axes=1
+d = parameter : f32[2048,256]
+cs = reduce_sum(d) axes=0
+z = parameter : f32[1000]
+e = exp(z)
+output m
+output cs
+output e
+"""
+
+
+@pytest.mark.parametrize("patterns", [[[1, 3, 5]], [[1, 3]], [[3, 5]], [[1, 5]]])
+def test_heterogeneous_packing(patterns):
+    """remote (independent) kernels packing regional, global and local bodies
+    in one launch on disjoint CTA ranges, with singletons around them (incl.
+    a regional-cluster singleton) -- explicit patterns via stc_plan_from_patterns"""
+    stitch = _stitch()
+    g = stitch.Graph(HETERO)
+    plan = stitch.Plan(g, "b200", patterns=patterns)
+    ex = stitch.Executor(plan)
+    inputs = stitch.random_inputs(g, 6)
+    got = ex.run(inputs)
+    og = no.parse_graph(HETERO)
+    want = no.eval_reference(og, {k: v.astype(np.float64) for k, v in inputs.items()})
+    for k, tol in _tolerances(og).items():
+        rep = stitch.compare({k: got[k]}, {k: want[k]}, tol, 1e-5)
+        assert rep["pass"], (patterns, k, rep["message"])
