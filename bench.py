@@ -463,7 +463,10 @@ def main():
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "peak_source": peak_kind + " (MEASURED_PEAKS.json hbm_gbs)"
                          if peak_kind == "measured" else "fallback 6650 GB/s",
-                         "traffic": ncu_traffic(WORKLOAD), "kernel": desc[top]["name"],
+                         "traffic": ncu_traffic(WORKLOAD),
+                         "traffic_note": "ncu dram__bytes_read+write during one cold launch (profiles/ncu_summary.json); "
+                                         "equals the algorithmic READ bytes -- the outputs are still dirty in the "
+                                         "126 MB L2 when the kernel ends and are written back later", "kernel": desc[top]["name"],
                          "kernel_us": round(dom_us, 3), "kernel_bytes": desc[top]["bytes"],
                          "frac_of_8TBps": round(achieved / 8000.0, 4)},
             "cpu_baseline": cpu,
