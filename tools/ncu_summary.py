@@ -19,6 +19,7 @@ KEYS = {
     "gpu__time_duration.sum": "duration_us",
     "dram__bytes_read.sum": "dram_read_MB",
     "dram__bytes_write.sum": "dram_write_MB",
+    "l1tex__m_l1tex2xbar_write_bytes.sum": "sm_to_l2_write_MB",
     "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed": "dram_throughput_pct",
     "launch__registers_per_thread": "registers",
     "launch__grid_size": "grid",
@@ -78,6 +79,7 @@ def main():
                 kname = rec["kernel"]
                 summ[g] = {"kernel": kname, "report": os.path.relpath(dest, ROOT),
                            "dram_bytes": int((rec.get("dram_read_MB", 0) + rec.get("dram_write_MB", 0)) * 1e6),
+                           "sm_to_l2_write_bytes": int(rec.get("sm_to_l2_write_MB", 0) * 1e6),
                            "duration_us_cold": rec.get("duration_us")}
                 break
     with open(summ_path, "w") as f:
