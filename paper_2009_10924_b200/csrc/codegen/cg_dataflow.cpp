@@ -232,7 +232,10 @@ class Emitter {
       case OpKind::Max: return "op_max(" + a + ", " + b + ")";
       case OpKind::Min: return "op_min(" + a + ", " + b + ")";
       case OpKind::Power: return "powf(" + a + ", " + b + ")";
-      case OpKind::Exp: return "expf(" + a + ")";
+      // MUFU.EX2 form (rel err < 5.5e-6, prelude exp_fast): the softmax chain
+      // is close to issue-bound and the accurate expf sequence costs ~8 more
+      // instructions per element (C2 8.61 -> 8.29 us, profiles/r01/fast_exp_ab.jsonl)
+      case OpKind::Exp: return (env_int("STITCH_FAST_EXP", 1) ? "exp_fast(" : "expf(") + a + ")";
       case OpKind::Tanh: return "tanhf(" + a + ")";
       case OpKind::Log: return "logf(" + a + ")";
       case OpKind::Rsqrt: return "op_rsqrt(" + a + ")";

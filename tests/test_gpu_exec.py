@@ -375,3 +375,20 @@ def test_heterogeneous_packing(patterns):
     for k, tol in _tolerances(og).items():
         rep = stitch.compare({k: got[k]}, {k: want[k]}, tol, 1e-5)
         assert rep["pass"], (patterns, k, rep["message"])
+
+
+def test_exp_full_range_accuracy():
+    """exp_fast (MUFU.EX2 form) over its whole finite range: relative error
+    <= 1e-5 against the f64 exponential rounded to f32 (the elementwise band);
+    results below FLT_MIN may flush to zero (absolute error < 1.2e-38)"""
+    stitch = _stitch()
+    n = 1 << 20
+    text = "x = parameter : f32[%d]\ny = exp(x)\noutput y\n" % n
+    g = stitch.Graph(text)
+    x = np.linspace(-100.0, 88.7, n).astype(np.float32)
+    got = stitch.Executor(stitch.Plan(g, "b200")).run({"x": x})["y"]
+    want = np.exp(x.astype(np.float64)).astype(np.float32).astype(np.float64)
+    normal = want >= np.finfo(np.float32).tiny
+    rel = np.abs(got[normal] - want[normal]) / want[normal]
+    assert rel.max() <= 1e-5, rel.max()
+    assert np.all(np.abs(got[~normal] - want[~normal]) < 1.2e-38)
