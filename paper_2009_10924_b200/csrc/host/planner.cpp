@@ -16,11 +16,14 @@
 // same probe points in the same order, so accept/reject decisions are
 // identical.
 #include <algorithm>
+#include <atomic>
 #include <cmath>
+#include <cstdlib>
 #include <functional>
 #include <limits>
 #include <set>
 #include <stdexcept>
+#include <thread>
 
 #include "stitch/planner.hpp"
 
@@ -1054,14 +1057,28 @@ std::optional<KernelPlan> plan_kernel(const FusionPattern& p, const CompGraph& g
     if (a.block != b.block) return a.block < b.block;
     return a.key < b.key;
   };
-  int tried = 0;
   const auto launches = enumerate_launch_dims(p, g, m.dev);
 
-  for (const Grouping& grouping : enumerate_groupings(p, g, m.search.grouping_cap)) {
-    const std::vector<int> roots = grouping.group_roots();
-    std::vector<std::vector<const ScheduleTemplate*>> menu;
+  // Enumerate the candidates in the reference's order (grouping x launch x
+  // template odometer), stopping where the reference returns at
+  // candidate_cap (planner.cpp:1073), then evaluate them -- in parallel for
+  // big patterns: each evaluation is independent and the argmin below walks
+  // the results in enumeration order with the same strict tie-breaks, so the
+  // chosen plan is identical to the sequential search.
+  const std::vector<Grouping> groupings = enumerate_groupings(p, g, m.search.grouping_cap);
+  struct Cand {
+    size_t gi, li;
+    std::vector<size_t> odo;
+  };
+  std::vector<std::vector<std::vector<const ScheduleTemplate*>>> menus(groupings.size());
+  std::vector<std::vector<int>> roots_of(groupings.size());
+  std::vector<Cand> cands;
+  bool capped = false;
+  for (size_t gi = 0; gi < groupings.size() && !capped; ++gi) {
+    roots_of[gi] = groupings[gi].group_roots();
+    auto& menu = menus[gi];
     bool viable = true;
-    for (int r : roots) {
+    for (int r : roots_of[gi]) {
       std::vector<const ScheduleTemplate*> opts;
       for (const auto& t : schedules_for(classify_op(g.node(r)))) {
         const bool allowed = !cons || !cons->force_scheme || t.scheme == *cons->force_scheme ||
@@ -1073,59 +1090,106 @@ std::optional<KernelPlan> plan_kernel(const FusionPattern& p, const CompGraph& g
       menu.push_back(std::move(opts));
     }
     if (!viable) continue;
-
-    for (const LaunchDims& ld : launches) {
-      std::vector<size_t> odo(roots.size(), 0);
+    for (size_t li = 0; li < launches.size() && !capped; ++li) {
+      std::vector<size_t> odo(roots_of[gi].size(), 0);
       for (;;) {
-        if (++tried > m.search.candidate_cap) return best;
-        std::map<int, std::string> tpl;
-        std::string key;
-        for (size_t i = 0; i < roots.size(); ++i) {
-          tpl[roots[i]] = menu[i][odo[i]]->id;
-          key += menu[i][odo[i]]->id + ";";
+        if (static_cast<int>(cands.size()) >= m.search.candidate_cap) {
+          capped = true;
+          break;
         }
-        ProgramBuilder b(g, p, grouping, tpl, ld, m.dev, pos);
-        bool ok = true;
-        try {
-          b.build();
-        } catch (const Infeasible&) {
-          ok = false;
-        }
-        if (ok) {
-          const int regs = estimate_register_usage(b.prog, m.costs.register_overhead);
-          const auto occ = occupancy(ld, regs, b.prog.shmem_bytes, m.dev);
-          if (occ) {
-            auto hist = count_instructions(b.prog);
-            double waves = wave_count(double(ld.total_threads()) / m.dev.warp_size, *occ, m.dev);
-            if (m.costs.ceil_waves) waves = std::ceil(waves);
-            const double cycles = waves * warp_latency(hist, m.cpi);
-            Score sc{cycles, b.prog.shmem_bytes, ld.block, key};
-            if (!best || better(sc, best_score)) {
-              best_score = sc;
-              KernelPlan k;
-              k.pattern = p;
-              k.grouping = grouping;
-              k.per_op_schedule = propagate_schedules(grouping, tpl, g);
-              k.launch = ld;
-              k.shmem_alloc = b.alloc;
-              k.scratch_bytes = b.prog.shmem_bytes - b.alloc.total;
-              k.regs_per_thread = regs;
-              k.occupancy_value = *occ;
-              k.estimated_cycles = cycles;
-              k.instr_histogram = std::move(hist);
-              k.boundaries = b.boundaries;
-              k.program = std::move(b.prog);
-              best = std::move(k);
-            }
-            if (cons && cons->first_feasible) return best;
-          }
-        }
+        cands.push_back({gi, li, odo});
         size_t i = 0;
         while (i < odo.size() && ++odo[i] == menu[i].size()) odo[i++] = 0;
         if (i == odo.size()) break;
       }
     }
   }
+  auto templates_of = [&](const Cand& c, std::string* key) {
+    std::map<int, std::string> tpl;
+    for (size_t i = 0; i < roots_of[c.gi].size(); ++i) {
+      tpl[roots_of[c.gi][i]] = menus[c.gi][i][c.odo[i]]->id;
+      if (key) *key += menus[c.gi][i][c.odo[i]]->id + ";";
+    }
+    return tpl;
+  };
+  struct Eval {
+    bool ok = false;
+    Score score{0, 0, 0, ""};
+  };
+  std::vector<Eval> evals(cands.size());
+  auto evaluate = [&](size_t ci) {
+    const Cand& c = cands[ci];
+    std::string key;
+    const auto tpl = templates_of(c, &key);
+    const LaunchDims& ld = launches[c.li];
+    ProgramBuilder b(g, p, groupings[c.gi], tpl, ld, m.dev, pos);
+    try {
+      b.build();
+    } catch (const Infeasible&) {
+      return;
+    }
+    const int regs = estimate_register_usage(b.prog, m.costs.register_overhead);
+    const auto occ = occupancy(ld, regs, b.prog.shmem_bytes, m.dev);
+    if (!occ) return;
+    double waves = wave_count(double(ld.total_threads()) / m.dev.warp_size, *occ, m.dev);
+    if (m.costs.ceil_waves) waves = std::ceil(waves);
+    evals[ci].score = Score{waves * warp_latency(count_instructions(b.prog), m.cpi), b.prog.shmem_bytes, ld.block, key};
+    evals[ci].ok = true;
+  };
+  const bool first_feasible = cons && cons->first_feasible;
+  unsigned threads = 1;
+  if (!first_feasible && cands.size() >= 32) {
+    const char* t = std::getenv("STITCH_PLAN_THREADS");
+    const unsigned want = t && *t ? static_cast<unsigned>(std::atoi(t)) : std::thread::hardware_concurrency();
+    threads = std::max(1u, std::min<unsigned>(want, static_cast<unsigned>(cands.size() / 8)));
+  }
+  size_t chosen = cands.size();
+  if (threads <= 1) {
+    for (size_t ci = 0; ci < cands.size(); ++ci) {
+      evaluate(ci);
+      if (!evals[ci].ok) continue;
+      if (chosen == cands.size() || better(evals[ci].score, best_score)) {
+        best_score = evals[ci].score;
+        chosen = ci;
+      }
+      if (first_feasible) break;
+    }
+  } else {
+    std::atomic<size_t> next{0};
+    std::vector<std::thread> pool;
+    for (unsigned t = 0; t < threads; ++t)
+      pool.emplace_back([&] {
+        for (size_t ci; (ci = next++) < cands.size();) evaluate(ci);
+      });
+    for (auto& th : pool) th.join();
+    for (size_t ci = 0; ci < cands.size(); ++ci)
+      if (evals[ci].ok && (chosen == cands.size() || better(evals[ci].score, best_score))) {
+        best_score = evals[ci].score;
+        chosen = ci;
+      }
+  }
+  if (chosen == cands.size()) return best;
+  // rebuild the winner's full KernelPlan (deterministic)
+  const Cand& c = cands[chosen];
+  const auto tpl = templates_of(c, nullptr);
+  const LaunchDims& ld = launches[c.li];
+  ProgramBuilder b(g, p, groupings[c.gi], tpl, ld, m.dev, pos);
+  b.build();
+  const int regs = estimate_register_usage(b.prog, m.costs.register_overhead);
+  KernelPlan k;
+  k.pattern = p;
+  k.grouping = groupings[c.gi];
+  k.per_op_schedule = propagate_schedules(groupings[c.gi], tpl, g);
+  k.launch = ld;
+  k.shmem_alloc = b.alloc;
+  k.scratch_bytes = b.prog.shmem_bytes - b.alloc.total;
+  k.regs_per_thread = regs;
+  k.occupancy_value = *occupancy(ld, regs, b.prog.shmem_bytes, m.dev);
+  k.estimated_cycles = best_score.cycles;
+  k.instr_histogram = count_instructions(b.prog);
+  k.boundaries = b.boundaries;
+  k.program = std::move(b.prog);
+  best = std::move(k);
   return best;
 }
 
