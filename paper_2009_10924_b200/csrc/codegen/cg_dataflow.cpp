@@ -626,6 +626,37 @@ void emit_row(Emitter& em, const CompGraph& g, const std::set<int>& pat, const B
     em.line("__shared__ double red_smem_[" + std::to_string(maxr) + "][" + std::to_string(rp.block / 32) + "];");
   if (cluster > 1 && maxr) em.line("__shared__ double cl_red_[" + std::to_string(maxr) + "];");
   const std::string sRPB = std::to_string(rp.RPB), sL = std::to_string(L);
+  // chunk offsets inside a row depend only on the thread: defined once,
+  // outside the row loop
+  std::vector<std::string> chunk_p(static_cast<size_t>(rp.NJ)), chunk_ok(static_cast<size_t>(rp.NJ));
+  for (int j = 0; j < rp.NJ; ++j) {
+    const std::string raw = "(tl_ + " + std::to_string(j * rp.TPR) + ") * " + std::to_string(rp.W);
+    chunk_p[j] = em.fresh("p");
+    if (partial) {
+      chunk_ok[j] = em.fresh("pok");
+      em.line("const bool " + chunk_ok[j] + " = " + raw + " < " + std::to_string(L) + ";");
+      em.line("const " + em.ix() + " " + chunk_p[j] + " = " + chunk_ok[j] + " ? " + raw + " : " + std::to_string(L - rp.W) + ";");
+    } else {
+      em.line("const " + em.ix() + " " + chunk_p[j] + " = " + raw + ";");
+    }
+  }
+  // row-invariant operands (a [L] tensor broadcast along the rows, e.g.
+  // LayerNorm's gamma/beta): loaded once per thread before the row loop; the
+  // memo hands the registers to every row.  Only where a team walks several
+  // rows (the register pipeline): with one row per team it just costs
+  // registers (residual+LN 7.09 -> 8.11 us; LN 4.69 -> 4.27 us pipelined,
+  // profiles/r01/row_hoist_ab.jsonl)
+  const bool multi_row = pipe && !pipe->empty() && rp.W == 4;
+  if (I.size() == 1 && multi_row && env_int("STITCH_ROW_HOIST_BCAST", 1))
+    for (int v : pat) {
+      const OpNode& n = g.node(v);
+      if (n.kind != OpKind::Broadcast || pat.count(n.operands[0])) continue;
+      const OpNode& src = g.node(n.operands[0]);
+      if (src.kind == OpKind::Constant || src.shape.rank() != 1 || src.shape.dims[0] != L) continue;
+      if (n.attrs.dims.size() != 1 || n.attrs.dims[0] != static_cast<int>(O.size())) continue;
+      if (n.shape.rank() != static_cast<int>(O.size() + 1)) continue;
+      for (int j = 0; j < rp.NJ; ++j) em.value(src.id, Coords{{chunk_p[j], rp.W > 1, true}});
+    }
   if (st) {
     // TMA-staged inputs that a kernel produces must wait; graph parameters
     // are streamed before the wait (hoisted prologue)
@@ -709,17 +740,8 @@ void emit_row(Emitter& em, const CompGraph& g, const std::set<int>& pat, const B
     for (auto& n : names) rowc.push_back({n, false, true});
   }
   std::vector<Coords> chunk_c(static_cast<size_t>(rp.NJ));
-  std::vector<std::string> chunk_ok(static_cast<size_t>(rp.NJ));
   for (int j = 0; j < rp.NJ; ++j) {
-    const std::string raw = "(tl_ + " + std::to_string(j * rp.TPR) + ") * " + std::to_string(rp.W);
-    const std::string p = em.fresh("p");
-    if (partial) {
-      chunk_ok[j] = em.fresh("pok");
-      em.line("const bool " + chunk_ok[j] + " = " + raw + " < " + std::to_string(L) + ";");
-      em.line("const " + em.ix() + " " + p + " = " + chunk_ok[j] + " ? " + raw + " : " + std::to_string(L - rp.W) + ";");
-    } else {
-      em.line("const " + em.ix() + " " + p + " = " + raw + ";");
-    }
+    const std::string& p = chunk_p[j];
     Coords c = rowc;
     if (I.size() == 1) {
       c.push_back({p, rp.W > 1, true});
@@ -1121,6 +1143,24 @@ KernelSpec generate_pattern_kernel(const CompGraph& g, const std::vector<int>& v
   const bool long_rows = max_tpr >= 32 && !has_col;
   const bool single_row_body = long_rows && bodies.size() == 1;
   if (long_rows) block = std::min(1024, single_row_body ? std::max(256, 2 * max_tpr) : 2 * max_tpr);
+  if (single_row_body && max_tpr == 32) {
+    // pipelined rows with hoisted broadcasts: the CTA size that balances the
+    // prefetch registers against resident CTAs depends on how many tensors
+    // stream per row (B200 sweep, profiles/r01/row_hoist_ab.jsonl: LN with
+    // one stream 128 threads, residual+LN with two 512)
+    em.block = block;
+    em.out.str("");
+    em.clear_memo();
+    em.reduced.clear();
+    em.staged_hits.clear();
+    em.reset_wait();
+    emit_row(em, g, pat, bodies[0]);
+    em.reset_wait();
+    int streams = 0;
+    for (int v : em.staged_hits) streams += !pat.count(v) && g.node(v).shape.dtype == DType::F32;
+    if (streams == 1) block = 128;
+    if (streams == 2) block = 512;
+  }
   if (const int want = env_int("STITCH_ROW_BLOCK", 0); want > 0) {
     block = std::clamp((std::max(want, max_tpr) + max_tpr - 1) / max_tpr * max_tpr, 32, 1024);
   } else if (want < 0 && bodies.size() == 1 && bodies[0].kind == Kind::Row) {
@@ -1196,10 +1236,10 @@ KernelSpec generate_pattern_kernel(const CompGraph& g, const std::vector<int>& v
         std::vector<int> hits;
         for (int v : em.staged_hits)
           if (!pat.count(v) && g.node(v).shape.dtype == DType::F32) hits.push_back(v);
-        // one streamed tensor per team row: 2 x NJ float4 registers; with more
-        // the register pressure costs more than the prefetch hides
-        // (residual+LN, 2 streamed tensors: 7.08 -> 7.16 us pipelined)
-        const bool pipe_ok = hits.size() == 1 || env_int("STITCH_ROW_PIPE", 0) > 1;
+        // up to two streamed tensors per team row (2 x NJ float4 registers
+        // each); beyond that the register pressure costs more than the
+        // prefetch hides
+        const bool pipe_ok = hits.size() <= 2 || env_int("STITCH_ROW_PIPE", 0) > 1;
         if (!hits.empty() && !env_int("STITCH_STAGE", 0) && pipe_ok) {
           pipe[i] = hits;
           b.blocks = static_cast<int>(std::clamp<int64_t>((ntiles + pipe_rows - 1) / pipe_rows, 1,
