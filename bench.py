@@ -232,7 +232,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=50)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--steps-per-graph", type=int, default=64,
-                    help="steps captured per CUDA-graph launch (largest of 16/8/4/2/1 dividing --steps)")
+                    help="max steps captured per CUDA-graph launch (the largest count <= this dividing --steps)")
     ap.add_argument("--no-subgraphs", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--strong", action="store_true",
@@ -274,7 +274,8 @@ def main():
     sets = max(2, math.ceil(8 * L2_BYTES / per_set))
     # B consecutive steps per CUDA-graph launch (each step still reads its own
     # cold buffer set and writes its own outputs); B divides K exactly
-    spg = next(b for b in (args.steps_per_graph, 32, 16, 8, 4, 2, 1) if b >= 1 and args.steps % b == 0)
+    # the largest step count <= --steps-per-graph that divides K exactly
+    spg = next(b for b in range(max(1, min(args.steps_per_graph, args.steps)), 0, -1) if args.steps % b == 0)
     n_graphs = ex.prepare_batches(sets, spg)
     sets = max(sets, n_graphs * spg)
     # an explicit (non-default) stream: the graph replays AND the timing events
