@@ -115,9 +115,11 @@ bool Executor::ready() const {
 }
 
 void Executor::ensure_ready() {
+  // every entry point binds the executor's device first, so executors of
+  // several GPUs can be driven from one host thread
+  STC_RT(cudaSetDevice(dev_->ordinal));
   if (module_) return;
   if (!pending_.valid()) throw std::runtime_error("[exec] executor has no module");
-  STC_RT(cudaSetDevice(dev_->ordinal));
   finish_init(pending_.get());
 }
 
@@ -314,6 +316,7 @@ int Executor::capture_plan(int set, cudaStream_t origin, int prev) {
 }
 
 Executor::~Executor() {
+  if (dev_) cudaSetDevice(dev_->ordinal);
   for (auto ge : graphs_)
     if (ge) cudaGraphExecDestroy(ge);
   for (auto ge : batch_graphs_) cudaGraphExecDestroy(ge);
@@ -630,6 +633,7 @@ const Executor::Tensor* Executor::tensor(const std::string& name) const {
 }
 
 void Executor::upload(const void* const* in, int set) {
+  STC_RT(cudaSetDevice(dev_->ordinal));
   ensure_sets(set + 1);
   for (size_t i = 0; i < params_.size(); ++i) {
     const Tensor& t = tensors_.at(g_.node(params_[i]).name);
@@ -638,6 +642,7 @@ void Executor::upload(const void* const* in, int set) {
 }
 
 void Executor::download(void* const* out, int set) {
+  STC_RT(cudaSetDevice(dev_->ordinal));
   for (size_t i = 0; i < g_.outputs.size(); ++i) {
     const Tensor& t = tensors_.at(g_.node(g_.outputs[i]).name);
     STC_RT(cudaMemcpyAsync(out[i], t.dptr[static_cast<size_t>(set)], t.bytes, cudaMemcpyDeviceToHost, stream_));
@@ -656,7 +661,10 @@ void Executor::launch(cudaStream_t s, int set) {
   STC_RT(cudaGraphLaunch(graphs_[static_cast<size_t>(set)], s));
 }
 
-void Executor::sync() { STC_RT(cudaStreamSynchronize(stream_)); }
+void Executor::sync() {
+  STC_RT(cudaSetDevice(dev_->ordinal));
+  STC_RT(cudaStreamSynchronize(stream_));
+}
 
 void Executor::run_host(const void* const* in, void* const* out) {
   ensure_ready();
