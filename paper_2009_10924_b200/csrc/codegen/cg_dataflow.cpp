@@ -399,7 +399,19 @@ struct Body {
   std::vector<int> reductions;
   int64_t bytes = 0;
   int blocks = 1;
+  // original tensor axis of each position of dims_a ++ dims_b (empty:
+  // identity).  Reductions over middle / non-contiguous axes keep the row
+  // (last axis reduced) or column (last axis kept) mapping through it.
+  std::vector<int> perm;
 };
+
+// coordinates listed in dims_a ++ dims_b order -> tensor axis order
+Coords arrange(const Coords& ab, const std::vector<int>& perm) {
+  if (perm.empty()) return ab;
+  Coords out(ab.size());
+  for (size_t i = 0; i < ab.size(); ++i) out[static_cast<size_t>(perm[i])] = ab[i];
+  return out;
+}
 
 std::vector<int64_t> to64(const std::vector<int>& v) { return {v.begin(), v.end()}; }
 
@@ -749,9 +761,12 @@ void emit_row(Emitter& em, const CompGraph& g, const std::set<int>& pat, const B
       auto names = decompose(em, p, I, "i");
       for (size_t a = 0; a < I.size(); ++a) c.push_back({names[a], a + 1 == I.size() && rp.W > 1, true});
     }
+    c = arrange(c, b.perm);
     chunk_c[j] = c;
-    em.domain_off[coords_key(c)] = p;  // float offset inside this team's row of a staged tile
-    em.domain_chunk[coords_key(c)] = j;
+    if (b.perm.empty()) {  // contiguous rows only: offsets inside a staged / prefetched row
+      em.domain_off[coords_key(c)] = p;
+      em.domain_chunk[coords_key(c)] = j;
+    }
   }
   em.domain_dims = O;
   em.domain_dims.insert(em.domain_dims.end(), I.begin(), I.end());
@@ -939,6 +954,7 @@ void emit_column(Emitter& em, const CompGraph& g, const Body& b, const ColParams
     auto names = decompose(em, rr, P, "r");
     for (auto& n : names) c.push_back({n, false, true});
     c.insert(c.end(), colc.begin(), colc.end());
+    c = arrange(c, b.perm);
     for (size_t i = 0; i < nr; ++i) {
       const int r = b.reductions[i];
       const bool sum = g.node(r).kind == OpKind::ReduceSum;
@@ -1049,7 +1065,7 @@ KernelSpec generate_pattern_kernel(const CompGraph& g, const std::vector<int>& v
   std::vector<Body> bodies;
   auto add_body = [&](Body nb) {
     for (auto& b : bodies)
-      if (b.kind == nb.kind && b.dims_a == nb.dims_a && b.dims_b == nb.dims_b) {
+      if (b.kind == nb.kind && b.dims_a == nb.dims_a && b.dims_b == nb.dims_b && b.perm == nb.perm) {
         b.outputs.insert(b.outputs.end(), nb.outputs.begin(), nb.outputs.end());
         b.reductions.insert(b.reductions.end(), nb.reductions.begin(), nb.reductions.end());
         std::sort(b.reductions.begin(), b.reductions.end());
@@ -1062,37 +1078,40 @@ KernelSpec generate_pattern_kernel(const CompGraph& g, const std::vector<int>& v
       for (int o : comp.outputs) add_body({Kind::Local, dims_of(g.node(o).shape), {}, {o}, {}});
       continue;
     }
-    // common split of every reduction's operand shape
-    bool rows = true, cols = true;
-    std::vector<int> A, B, A2, B2;
+    // every reduction of the component must reduce the same axes of
+    // operands of the same shape; the last axis decides the mapping: reduced
+    // -> regional rows (contiguous along the last axis), kept -> global
+    // columns.  Suffix / prefix axis sets are the identity layouts.
+    std::vector<int> in0, axes0;
     for (size_t i = 0; i < comp.reductions.size(); ++i) {
       const OpNode& r = g.node(comp.reductions[i]);
       const auto in = dims_of(g.node(r.operands[0]).shape);
       std::set<int> ax(r.attrs.axes.begin(), r.attrs.axes.end());
-      const int m = static_cast<int>(ax.size()), n = static_cast<int>(in.size());
-      bool suffix = true, prefix = m < n;
-      for (int a = 0; a < n; ++a) {
-        suffix = suffix && (ax.count(a) > 0) == (a >= n - m);
-        prefix = prefix && (ax.count(a) > 0) == (a < m);
-      }
-      std::vector<int> o(in.begin(), in.end() - m), inn(in.end() - m, in.end());
-      std::vector<int> pp(in.begin(), in.begin() + std::min(m, n)), cc(in.begin() + std::min(m, n), in.end());
+      std::vector<int> axes(ax.begin(), ax.end());
       if (i == 0) {
-        A = o, B = inn, A2 = pp, B2 = cc;
+        in0 = in, axes0 = axes;
+      } else if (in != in0 || axes != axes0) {
+        throw TemplateMismatch("reductions of one component disagree on their split");
       }
-      rows = rows && suffix && o == A && inn == B;
-      cols = cols && prefix && pp == A2 && cc == B2;
     }
+    const int n = static_cast<int>(in0.size());
+    std::vector<int> kept, red;
+    for (int a = 0; a < n; ++a) (std::count(axes0.begin(), axes0.end(), a) ? red : kept).push_back(a);
+    const bool row_kind = n > 0 && std::count(axes0.begin(), axes0.end(), n - 1);
     Body body;
-    if (rows) {
-      body = {Kind::Row, A, B, {}, comp.reductions};
-    } else if (cols) {
-      body = {Kind::Column, A2, B2, {}, comp.reductions};
-    } else {
-      throw TemplateMismatch("reductions of one component disagree on their split");
-    }
-    std::vector<int> full = body.dims_a;
-    full.insert(full.end(), body.dims_b.begin(), body.dims_b.end());
+    body.kind = row_kind ? Kind::Row : Kind::Column;
+    body.reductions = comp.reductions;
+    const std::vector<int>& first = row_kind ? kept : red;
+    const std::vector<int>& second = row_kind ? red : kept;
+    for (int a : first) body.dims_a.push_back(in0[static_cast<size_t>(a)]);
+    for (int a : second) body.dims_b.push_back(in0[static_cast<size_t>(a)]);
+    body.perm = first;
+    body.perm.insert(body.perm.end(), second.begin(), second.end());
+    bool identity = true;
+    for (int a = 0; a < n; ++a) identity = identity && body.perm[static_cast<size_t>(a)] == a;
+    if (identity) body.perm.clear();
+    if (body.kind == Kind::Column && body.dims_b.empty()) throw TemplateMismatch("column body without kept axes");
+    const std::vector<int>& full = in0;  // operand shape, tensor axis order
     const std::vector<int>& unit = body.kind == Kind::Row ? body.dims_a : body.dims_b;
     for (int o : comp.outputs) {
       const auto od = dims_of(g.node(o).shape);

@@ -227,6 +227,14 @@ EDGE_SHAPES = {
     "softmax_cluster_16x8192": _softmax_text(16, 8192),
     "ln_cluster_4x40000": _ln_text(4, 40000),
     "softmax_cluster_ragged_5x9002": _softmax_text(5, 9002),
+    # reductions over middle / non-contiguous axes: regional rows when the
+    # last axis is reduced, global columns when it is kept (axis permutation)
+    "mid_axis_sum": "x = parameter : f32[8,512,64]\ne = exp(x)\ns = reduce_sum(e) axes=1\ny = mul(s, s)\noutput y\n",
+    "outer_inner_max": "x = parameter : f32[8,512,64]\nm = reduce_max(x) axes=[0,2]\ny = mul(m, m)\noutput y\n",
+    "outer_axis_ragged": "x = parameter : f32[7,33,10]\ns = reduce_sum(x) axes=[0,2]\noutput s\n",
+    "mid_axis_softmax": "x = parameter : f32[4,300,32]\nm = reduce_max(x) axes=1\nmb = broadcast(m) dims=[0,2] : "
+                        "f32[4,300,32]\nc = sub(x, mb)\ne = exp(c)\ns = reduce_sum(e) axes=1\nsb = broadcast(s) "
+                        "dims=[0,2] : f32[4,300,32]\ny = div(e, sb)\noutput y\n",
 }
 
 
