@@ -435,6 +435,10 @@ def main():
                 subs["bert_layer_model_tf32"] = time_subgraph(stitch, "bert_layer", gemm=True)
             except Exception as e:
                 subs["bert_layer_model_tf32"] = {"error": str(e)[:300]}
+            try:  # real-model deployment shape: refined plan + cuBLASLt GEMMs
+                subs["bert_layer_model_tf32_refined"] = time_subgraph(stitch, "bert_layer", gemm=True, refine=True)
+            except Exception as e:
+                subs["bert_layer_model_tf32_refined"] = {"error": str(e)[:300]}
             # non-parity plan refinement (HBM-bytes / launch cost terms)
             for name in ("bert_layer", "dien_T10"):
                 try:
