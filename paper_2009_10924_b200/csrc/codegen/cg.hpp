@@ -75,9 +75,15 @@ KernelSpec generate_program_kernel(const CompGraph& g, const StitchedProgram& pr
                                    const std::string& name, bool checked = false);
 
 // opaque_compute placeholder: mean of all operand elements, broadcast
-// (src/sim.cpp:215-226), one cooperative kernel.
+// (src/sim.cpp:215-226): one CTA for small operands, else a cooperative grid.
 KernelSpec generate_opaque_kernel(const CompGraph& g, int vertex, const std::string& name,
                                   int sm_count);
+
+// Several mutually independent small opaque placeholders in one launch, one
+// 1024-thread CTA per op (CTA j computes vertices[j]).  Every vertex must be
+// small enough for the single-CTA form (opaque_single).
+KernelSpec generate_opaque_pack(const CompGraph& g, const std::vector<int>& vertices, const std::string& name);
+bool opaque_single(const CompGraph& g, int vertex);
 
 // device helpers every module includes
 const std::string& device_prelude();

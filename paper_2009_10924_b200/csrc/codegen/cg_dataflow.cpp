@@ -1421,50 +1421,29 @@ KernelSpec generate_pattern_kernel(const CompGraph& g, const std::vector<int>& v
 // opaque_compute placeholder: mean of every operand element, broadcast
 // (src/sim.cpp:215-226).  Phase 1 per-CTA f64 partial sums, grid barrier,
 // every CTA folds the partials in the same order, then fills the output.
-KernelSpec generate_opaque_kernel(const CompGraph& g, int vertex, const std::string& name, int) {
+// Placeholder semantics of one opaque op (mean of every operand element,
+// broadcast; src/sim.cpp:215-226): the statements after the PDL wait.  The
+// enclosing code defines bid_ / nbid_ (this CTA's index and the CTA count
+// of the op) and, for the grid form, bar_ / part_.
+static std::string opaque_body(const CompGraph& g, int vertex, bool single, int grid, int block,
+                               const std::string& wait) {
   const OpNode& n = g.node(vertex);
-  std::set<int> ops(n.operands.begin(), n.operands.end());
   int64_t count = 0;
   for (int o : n.operands) count += g.node(o).shape.element_count();
-  const int64_t work = count + n.shape.element_count();
-  // small tensors (e.g. DIEN's [256,36] GEMM outputs): one 1024-thread CTA,
-  // no grid-wide barrier; large ones: cooperative grid with a barrier
-  const bool single = work <= (int64_t(1) << 20);
-  const int grid = single ? 1 : kSmCount * 4;  // cooperative: 4 co-resident 256-thread CTAs per SM
-  const int block = single ? 1024 : kBlock;
-  KernelSpec k;
-  k.name = name;
-  k.tmpl = single ? "opaque" : "opaque(grid)";
-  k.pattern_key = "op:" + n.name;
-  k.grid = grid;
-  k.block = block;
-  k.cooperative = !single;
   std::ostringstream s;
-  s << "extern \"C\" __global__ void __launch_bounds__(" << block << ", " << (single ? 1 : 4) << ") " << name << "(";
-  for (int o : ops) {
-    s << "const " << c_type(g.node(o).shape.dtype) << "* __restrict__ T_" << g.node(o).name << ", ";
-    k.inputs.push_back(g.node(o).name);
-  }
-  s << c_type(n.shape.dtype) << "* __restrict__ T_" << n.name;
-  if (!single) {
-    s << ", unsigned* __restrict__ bar_, double* __restrict__ part_";
-    k.scratch_bytes = 256 + int64_t(grid) * 8;
-  }
-  // trigger dependents as soon as our own prerequisites are met: a dependent
-  // then launches (and becomes resident) while we run, hiding its launch
-  // latency behind our body (STITCH_OPAQUE_EARLY=0: trigger at exit)
-  const bool early = env_int("STITCH_OPAQUE_EARLY", 1) != 0;
-  s << ") {\n" << (entry_trigger(grid) ? "  pdl_launch();\n" : "") << "  pdl_wait();\n"
-    << (early ? "  pdl_launch();\n" : "");
-  k.outputs.push_back(n.name);
   s << "  __shared__ double red_[" << block / 32 << "];\n  double acc = 0.0;\n";
   // an operand listed twice is counted twice, as upstream
   if (single) {
     // one CTA: issue every load of every operand first (128-bit where the
     // tensor allows), then fold -- one memory round trip instead of a chain
+    // Graph parameters are never written by a kernel: their loads go before
+    // the PDL wait (`wait`), kernel-produced operands after it
     int vi = 0;
     std::vector<std::pair<std::string, int>> regs;  // (array, lanes per element)
-    for (int o : n.operands) {
+    for (int pass = 0; pass < 2; ++pass) {
+     if (pass == 1) s << wait;
+     for (int o : n.operands) {
+      if ((g.node(o).kind == OpKind::Parameter) != (pass == 0)) continue;
       const TensorShape& sh = g.node(o).shape;
       const int64_t cnt = sh.element_count();
       const bool vec = sh.dtype == DType::F32 && cnt % 4 == 0;
@@ -1491,6 +1470,7 @@ KernelSpec generate_opaque_kernel(const CompGraph& g, int vertex, const std::str
           << " ? ldv(T_" << g.node(o).name << ", i) : 0.f; }\n";
         regs.push_back({a, 1});
       }
+     }
     }
     for (const auto& [a, lanes] : regs) {
       s << "  #pragma unroll\n  for (int k = 0; k < (int)(sizeof(" << a << ") / sizeof(" << a << "[0])); ++k) ";
@@ -1503,6 +1483,7 @@ KernelSpec generate_opaque_kernel(const CompGraph& g, int vertex, const std::str
   } else {
     // grid: 128-bit grid-stride loads, 4 independent accumulators per thread
     // so each thread keeps 4 loads in flight
+    s << wait;
     s << "  const i64 gt_ = (i64)blockIdx.x * blockDim.x + threadIdx.x, gs_ = (i64)gridDim.x * blockDim.x;\n"
       << "  double a0_ = 0.0, a1_ = 0.0, a2_ = 0.0, a3_ = 0.0;\n";
     for (int o : n.operands) {
@@ -1541,15 +1522,92 @@ KernelSpec generate_opaque_kernel(const CompGraph& g, int vertex, const std::str
   s << "  const float fill = (float)(" << (count ? "tot / " + std::to_string(count) + ".0" : "0.0") << ");\n";
   const int64_t nout = n.shape.element_count();
   if (n.shape.dtype == DType::F32 && nout % 4 == 0)  // 128-bit stores
-    s << "  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < " << nout / 4
-      << "; i += (i64)gridDim.x * blockDim.x) st4(T_" << n.name << " + 4 * i, fill, fill, fill, fill);\n";
+    s << "  for (i64 i = (i64)bid_ * blockDim.x + threadIdx.x; i < " << nout / 4
+      << "; i += (i64)nbid_ * blockDim.x) st4(T_" << n.name << " + 4 * i, fill, fill, fill, fill);\n";
   else
-    s << "  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < " << nout
-      << "; i += (i64)gridDim.x * blockDim.x) stv(T_" << n.name << ", i, fill);\n";
+    s << "  for (i64 i = (i64)bid_ * blockDim.x + threadIdx.x; i < " << nout
+      << "; i += (i64)nbid_ * blockDim.x) stv(T_" << n.name << ", i, fill);\n";
+  return s.str();
+}
+
+bool opaque_single(const CompGraph& g, int vertex) {
+  const OpNode& n = g.node(vertex);
+  int64_t work = n.shape.element_count();
+  for (int o : n.operands) work += g.node(o).shape.element_count();
+  return work <= (int64_t(1) << 20);
+}
+
+KernelSpec generate_opaque_kernel(const CompGraph& g, int vertex, const std::string& name, int) {
+  const OpNode& n = g.node(vertex);
+  std::set<int> ops(n.operands.begin(), n.operands.end());
+  // small tensors (e.g. DIEN's [256,36] GEMM outputs): one 1024-thread CTA,
+  // no grid-wide barrier; large ones: cooperative grid with a barrier
+  const bool single = opaque_single(g, vertex);
+  const int grid = single ? 1 : kSmCount * 4;  // cooperative: 4 co-resident 256-thread CTAs per SM
+  const int block = single ? 1024 : kBlock;
+  KernelSpec k;
+  k.name = name;
+  k.tmpl = single ? "opaque" : "opaque(grid)";
+  k.pattern_key = "op:" + n.name;
+  k.grid = grid;
+  k.block = block;
+  k.cooperative = !single;
+  std::ostringstream s;
+  s << "extern \"C\" __global__ void __launch_bounds__(" << block << ", " << (single ? 1 : 4) << ") " << name << "(";
+  for (int o : ops) {
+    s << "const " << c_type(g.node(o).shape.dtype) << "* __restrict__ T_" << g.node(o).name << ", ";
+    k.inputs.push_back(g.node(o).name);
+  }
+  s << c_type(n.shape.dtype) << "* __restrict__ T_" << n.name;
+  if (!single) {
+    s << ", unsigned* __restrict__ bar_, double* __restrict__ part_";
+    k.scratch_bytes = 256 + int64_t(grid) * 8;
+  }
+  // trigger dependents as soon as our own prerequisites are met: a dependent
+  // then launches (and becomes resident) while we run, hiding its launch
+  // latency behind our body (STITCH_OPAQUE_EARLY=0: trigger at exit)
+  const bool early = env_int("STITCH_OPAQUE_EARLY", 1) != 0;
+  s << ") {\n" << (entry_trigger(grid) ? "  pdl_launch();\n" : "");
+  k.outputs.push_back(n.name);
+  s << "  const int bid_ = blockIdx.x, nbid_ = gridDim.x;\n"
+    << opaque_body(g, vertex, single, grid, block, early ? "  pdl_wait();\n  pdl_launch();\n" : "  pdl_wait();\n");
   s << "  pdl_launch();\n}\n";
   k.source = s.str();
   int64_t bytes = n.shape.byte_size();
   for (int o : ops) bytes += g.node(o).shape.byte_size();
+  k.alg_bytes = bytes;
+  return k;
+}
+
+KernelSpec generate_opaque_pack(const CompGraph& g, const std::vector<int>& vertices, const std::string& name) {
+  KernelSpec k;
+  k.name = name;
+  k.tmpl = "opaque(pack" + std::to_string(vertices.size()) + ")";
+  k.grid = static_cast<int>(vertices.size());
+  k.block = 1024;
+  std::ostringstream sig, body;
+  std::set<std::string> seen;
+  int64_t bytes = 0;
+  sig << "extern \"C\" __global__ void __launch_bounds__(1024, 1) " << name << "(";
+  for (int v : vertices) {
+    if (!opaque_single(g, v)) throw std::invalid_argument("opaque pack: " + g.node(v).name + " needs the grid form");
+    k.pattern_key += std::string(k.pattern_key.empty() ? "" : "+") + "op:" + g.node(v).name;
+    for (int o : g.node(v).operands)
+      if (seen.insert(g.node(o).name).second) {
+        sig << "const " << c_type(g.node(o).shape.dtype) << "* __restrict__ T_" << g.node(o).name << ", ";
+        k.inputs.push_back(g.node(o).name);
+        bytes += g.node(o).shape.byte_size();
+      }
+  }
+  for (size_t j = 0; j < vertices.size(); ++j) {
+    const OpNode& n = g.node(vertices[j]);
+    sig << (j ? ", " : "") << c_type(n.shape.dtype) << "* __restrict__ T_" << n.name;
+    k.outputs.push_back(n.name);
+    bytes += n.shape.byte_size();
+    body << "  " << (j ? "} else " : "") << "if (blockIdx.x == " << j << ") {\n  const int bid_ = 0, nbid_ = 1;\n"
+         << opaque_body(g, vertices[j], true, 1, 1024, "  pdl_wait();\n");
+  }
+  k.source = sig.str() + ") {\n  pdl_launch();\n" + body.str() + "  }\n}\n";
   k.alg_bytes = bytes;
   return k;
 }

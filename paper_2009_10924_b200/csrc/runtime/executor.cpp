@@ -435,6 +435,7 @@ PlanKernels generate_plan_kernels(const CompGraph& g_, const FusionPlan& plan,
         const int w = unit_of[static_cast<size_t>(o)];
         if (w >= 0 && w != static_cast<int>(u) && deps[u].insert(w).second) users[static_cast<size_t>(w)].push_back(static_cast<int>(u));
       }
+  std::map<size_t, int> opaque_vertex;  // spec index -> vertex of a placeholder kernel
   std::set<std::pair<int, int>> ready;  // (fire position, unit)
   std::vector<size_t> pending(units.size());
   for (size_t u = 0; u < units.size(); ++u)
@@ -458,16 +459,63 @@ PlanKernels generate_plan_kernels(const CompGraph& g_, const FusionPlan& plan,
       k.alg_bytes = g_.node(n.operands[0]).shape.byte_size() + g_.node(n.operands[1]).shape.byte_size() +
                     n.shape.byte_size();
       specs_.push_back(std::move(k));
-    } else if (un.opaque)
+    } else if (un.opaque) {
       specs_.push_back(generate_opaque_kernel(g_, un.verts[0], "k" + std::to_string(idx++) + "_" +
                                                                    sanitize(g_.node(un.verts[0]).name),
                                               sm_count));
-    else
+      opaque_vertex[specs_.size() - 1] = un.verts[0];
+    } else
       add_pattern(un.verts, un.key);
     for (int w : users[static_cast<size_t>(u)])
       if (--pending[static_cast<size_t>(w)] == 0) ready.insert({units[static_cast<size_t>(w)].fire, w});
   }
   if (specs_.size() != units.size()) throw std::runtime_error("[exec] contracted plan graph has a cycle");
+  // Small opaque placeholders with the same producer kernels (DIEN's three
+  // gate GEMMs of a step read only the previous step's state; its per-step
+  // x.W GEMMs read only parameters) are mutually independent: launch each
+  // such set as ONE kernel, a CTA per op.  On the critical chain the set then
+  // follows its producer as a single same-lane PDL edge instead of forking
+  // lanes whose cross-lane edges only resolve at completion
+  // (profiles/r01/pdl_edge_probe.jsonl).  The plan (patterns, per-op
+  // semantics, outputs) is unchanged; STITCH_OPAQUE_PACK=0 launches one
+  // kernel per op.
+  const char* pack_env = std::getenv("STITCH_OPAQUE_PACK");
+  if (!(pack_env && *pack_env == '0') && !opaque_vertex.empty()) {
+    std::map<std::string, size_t> prod;
+    std::map<std::vector<size_t>, std::vector<size_t>> groups;  // producer set -> member specs
+    for (size_t i = 0; i < specs_.size(); ++i) {
+      std::set<size_t> d;
+      for (const auto& t : specs_[i].inputs)
+        if (auto it = prod.find(t); it != prod.end()) d.insert(it->second);
+      if (opaque_vertex.count(i) && opaque_single(g_, opaque_vertex[i]))
+        groups[std::vector<size_t>(d.begin(), d.end())].push_back(i);
+      for (const auto& t : specs_[i].outputs) prod[t] = i;
+    }
+    std::map<size_t, KernelSpec> packs;  // placed at the first member's position
+    std::set<size_t> drop;
+    for (auto& [d, members] : groups)
+      for (size_t at = 0; at + 1 < members.size(); at += 32) {  // <= 32 CTAs per pack
+        const size_t end = std::min(members.size(), at + 32);
+        if (end - at < 2) break;
+        std::vector<int> verts;
+        for (size_t j = at; j < end; ++j) {
+          verts.push_back(opaque_vertex[members[j]]);
+          drop.insert(members[j]);
+        }
+        packs[members[at]] = generate_opaque_pack(
+            g_, verts, "k" + std::to_string(idx++) + "_pack" + std::to_string(verts.size()) + "_" + sanitize(g_.node(verts[0]).name));
+      }
+    if (!packs.empty()) {
+      std::vector<KernelSpec> kept;
+      for (size_t i = 0; i < specs_.size(); ++i) {
+        if (auto it = packs.find(i); it != packs.end())
+          kept.push_back(std::move(it->second));
+        else if (!drop.count(i))
+          kept.push_back(std::move(specs_[i]));
+      }
+      specs_ = std::move(kept);
+    }
+  }
   // timeline hooks (no-ops unless compiled with -DSTITCH_TRACE, Executor::trace)
   for (size_t i = 0; i < specs_.size(); ++i) {
     auto& src = specs_[i].source;

@@ -152,6 +152,29 @@ def test_dag_capture_matches_linear_chain(monkeypatch):
             assert np.array_equal(dag[k], lin[k]), (name, k)
 
 
+def test_opaque_pack_matches_one_kernel_per_op(monkeypatch):
+    """packed opaque placeholders (one launch, a CTA per op) compute exactly
+    what one kernel per placeholder computes, and match the oracle"""
+    stitch = _stitch()
+    for name in ("dien_T10", "dien_T20"):
+        text = config_graph(name)
+        g = stitch.Graph(text)
+        plan = stitch.Plan(g, "b200")
+        inputs = stitch.random_inputs(g, 5)
+        ex = stitch.Executor(plan)
+        assert any(k["template"].startswith("opaque(pack") for k in ex.describe())
+        packed = ex.run(inputs)
+        monkeypatch.setenv("STITCH_OPAQUE_PACK", "0")
+        single = stitch.Executor(plan).run(inputs)
+        monkeypatch.delenv("STITCH_OPAQUE_PACK")
+        for k in single:
+            assert np.array_equal(packed[k], single[k]), (name, k)
+        og = no.parse_graph(text)
+        want = no.eval_reference(og, {k: v.astype(np.float64) for k, v in inputs.items()})
+        for k, tol in _tolerances(og).items():
+            assert stitch.compare({k: packed[k]}, {k: want[k]}, tol, 1e-5)["pass"], (name, k)
+
+
 @pytest.mark.parametrize("precision", ["fp32", "tf32"])
 def test_model_mode_gemm_bert_layer(monkeypatch, precision):
     """model mode (non-parity): the BERT FFN layer's
