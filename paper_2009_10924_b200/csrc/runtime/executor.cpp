@@ -239,6 +239,10 @@ int Executor::capture_plan(int set, cudaStream_t origin, int prev) {
   // path claims its producer's lane (a same-stream PDL edge) before its
   // siblings fork.
   int source_lane = -1;
+  // STITCH_SOURCE_LANE=0: producer-less kernels stay on the origin lane
+  // (captured first), so no consumer needs a cross-lane edge to them
+  const char* sl_env = std::getenv("STITCH_SOURCE_LANE");
+  const bool source_fork = !(sl_env && *sl_env == '0');
   std::vector<size_t> order;
   for (size_t i = 0; i < n; ++i)
     if (deps_[i].empty()) order.push_back(i);
@@ -271,6 +275,7 @@ int Executor::capture_plan(int set, cudaStream_t origin, int prev) {
   for (size_t i : order) {
     int best = -1;
     if (deps_[i].empty() && source_lane >= 0) best = source_lane;
+    if (deps_[i].empty() && !source_fork) best = 0;
     for (size_t l = 0; l < lanes.size() && !(deps_[i].empty() && source_lane >= 0); ++l) {  // the producer
       const int t = lanes[l].tail;                                                        // finishing last
       if (t >= 0 && std::count(deps_[i].begin(), deps_[i].end(), t) &&
@@ -306,6 +311,14 @@ int Executor::capture_plan(int set, cudaStream_t origin, int prev) {
     // stream capture then makes every incoming kernel edge programmatic,
     // including the cross-lane ones from event waits
     const int after = ln.tail >= 0 ? ln.tail : !deps_[i].empty() ? deps_[i].front() : (best == 0 ? prev : -1);
+    if (const char* dbg = std::getenv("STITCH_LANES"); dbg && *dbg == '1') {  // diagnostics: lane map
+      std::fprintf(stderr, "[lanes] %-22s lane %d after %s waits", specs_[i].name.c_str(), best,
+                   ln.tail >= 0 ? specs_[static_cast<size_t>(ln.tail)].name.c_str() : "-");
+      for (int d : deps_[i])
+        if (!(ln.tail >= 0 && (d == ln.tail || anc[static_cast<size_t>(ln.tail)][static_cast<size_t>(d)])))
+          std::fprintf(stderr, " %s", specs_[static_cast<size_t>(d)].name.c_str());
+      std::fprintf(stderr, "\n");
+    }
     launch_kernel(i, set, ln.s, after);
     STC_RT(cudaEventRecord(kernel_events_[i], ln.s));
     ln.tail = static_cast<int>(i);
@@ -436,6 +449,7 @@ PlanKernels generate_plan_kernels(const CompGraph& g_, const FusionPlan& plan,
         if (w >= 0 && w != static_cast<int>(u) && deps[u].insert(w).second) users[static_cast<size_t>(w)].push_back(static_cast<int>(u));
       }
   std::map<size_t, int> opaque_vertex;  // spec index -> vertex of a placeholder kernel
+  std::map<size_t, std::vector<int>> local_verts;  // spec index -> vertices of a local-template kernel
   std::set<std::pair<int, int>> ready;  // (fire position, unit)
   std::vector<size_t> pending(units.size());
   for (size_t u = 0; u < units.size(); ++u)
@@ -464,46 +478,78 @@ PlanKernels generate_plan_kernels(const CompGraph& g_, const FusionPlan& plan,
                                                                    sanitize(g_.node(un.verts[0]).name),
                                               sm_count));
       opaque_vertex[specs_.size() - 1] = un.verts[0];
-    } else
+    } else {
       add_pattern(un.verts, un.key);
+      if (specs_.back().tmpl == "local") local_verts[specs_.size() - 1] = un.verts;
+    }
     for (int w : users[static_cast<size_t>(u)])
       if (--pending[static_cast<size_t>(w)] == 0) ready.insert({units[static_cast<size_t>(w)].fire, w});
   }
   if (specs_.size() != units.size()) throw std::runtime_error("[exec] contracted plan graph has a cycle");
-  // Small opaque placeholders with the same producer kernels (DIEN's three
-  // gate GEMMs of a step read only the previous step's state; its per-step
-  // x.W GEMMs read only parameters) are mutually independent: launch each
-  // such set as ONE kernel, a CTA per op.  On the critical chain the set then
-  // follows its producer as a single same-lane PDL edge instead of forking
-  // lanes whose cross-lane edges only resolve at completion
-  // (profiles/r01/pdl_edge_probe.jsonl).  The plan (patterns, per-op
-  // semantics, outputs) is unchanged; STITCH_OPAQUE_PACK=0 launches one
-  // kernel per op.
+  // Horizontal packing.  Launch units with the same producer kernels are
+  // mutually independent; two kinds are packed into one launch each:
+  //  * small opaque placeholders (DIEN's three gate GEMMs of a step read only
+  //    the previous step's state; its per-step x.W GEMMs only parameters):
+  //    one 1024-thread CTA per op (generate_opaque_pack);
+  //  * local-template (elementwise) patterns: the independent template packs
+  //    their bodies into disjoint CTA ranges, each body the code it has alone.
+  // On a launch-bound chain a set then follows its producer as one same-lane
+  // PDL edge instead of fanning out over lanes whose cross-lane edges only
+  // resolve at completion (profiles/r01/pdl_edge_probe.jsonl).  The plan
+  // (patterns, per-op semantics, outputs) is unchanged;
+  // STITCH_OPAQUE_PACK=0 / STITCH_LOCAL_PACK=0 launch one kernel per unit.
   const char* pack_env = std::getenv("STITCH_OPAQUE_PACK");
-  if (!(pack_env && *pack_env == '0') && !opaque_vertex.empty()) {
+  const char* lpack_env = std::getenv("STITCH_LOCAL_PACK");
+  const bool pack_opaque = !(pack_env && *pack_env == '0');
+  const bool pack_local = !(lpack_env && *lpack_env == '0');
+  if ((pack_opaque && !opaque_vertex.empty()) || (pack_local && local_verts.size() > 1)) {
     std::map<std::string, size_t> prod;
-    std::map<std::vector<size_t>, std::vector<size_t>> groups;  // producer set -> member specs
+    // (kind, producer set) -> member specs; kind 0 opaque, 1 local
+    std::map<std::pair<int, std::vector<size_t>>, std::vector<size_t>> groups;
     for (size_t i = 0; i < specs_.size(); ++i) {
       std::set<size_t> d;
       for (const auto& t : specs_[i].inputs)
         if (auto it = prod.find(t); it != prod.end()) d.insert(it->second);
-      if (opaque_vertex.count(i) && opaque_single(g_, opaque_vertex[i]))
-        groups[std::vector<size_t>(d.begin(), d.end())].push_back(i);
+      const std::vector<size_t> dv(d.begin(), d.end());
+      if (pack_opaque && opaque_vertex.count(i) && opaque_single(g_, opaque_vertex[i])) groups[{0, dv}].push_back(i);
+      if (pack_local && local_verts.count(i)) groups[{1, dv}].push_back(i);
       for (const auto& t : specs_[i].outputs) prod[t] = i;
     }
     std::map<size_t, KernelSpec> packs;  // placed at the first member's position
     std::set<size_t> drop;
-    for (auto& [d, members] : groups)
-      for (size_t at = 0; at + 1 < members.size(); at += 32) {  // <= 32 CTAs per pack
+    for (auto& [kd, members] : groups)
+      for (size_t at = 0; at + 1 < members.size(); at += 32) {  // <= 32 units per pack
         const size_t end = std::min(members.size(), at + 32);
         if (end - at < 2) break;
-        std::vector<int> verts;
-        for (size_t j = at; j < end; ++j) {
-          verts.push_back(opaque_vertex[members[j]]);
-          drop.insert(members[j]);
+        if (kd.first == 0) {
+          std::vector<int> verts;
+          for (size_t j = at; j < end; ++j) verts.push_back(opaque_vertex[members[j]]);
+          packs[members[at]] = generate_opaque_pack(
+              g_, verts, "k" + std::to_string(idx++) + "_pack" + std::to_string(verts.size()) + "_" + sanitize(g_.node(verts[0]).name));
+        } else {
+          std::vector<int> verts;
+          std::vector<std::string> outs;
+          for (size_t j = at; j < end; ++j) {
+            verts.insert(verts.end(), local_verts[members[j]].begin(), local_verts[members[j]].end());
+            outs.insert(outs.end(), specs_[members[j]].outputs.begin(), specs_[members[j]].outputs.end());
+          }
+          std::sort(verts.begin(), verts.end());
+          KernelSpec k;
+          try {  // pattern_key below lists the packed units
+            k = generate_pattern_kernel(g_, verts, "k" + std::to_string(idx++) + "_pack" + std::to_string(end - at) + "_" +
+                                                       sanitize(g_.node(verts.front()).name), sm_count);
+          } catch (const TemplateMismatch&) {
+            continue;
+          }
+          auto ko = k.outputs;
+          std::sort(ko.begin(), ko.end());
+          std::sort(outs.begin(), outs.end());
+          if (ko != outs) continue;  // not a pure side-by-side packing: keep the units
+          k.pattern_key.clear();
+          for (size_t j = at; j < end; ++j) k.pattern_key += std::string(j == at ? "" : "+") + specs_[members[j]].pattern_key;
+          packs[members[at]] = std::move(k);
         }
-        packs[members[at]] = generate_opaque_pack(
-            g_, verts, "k" + std::to_string(idx++) + "_pack" + std::to_string(verts.size()) + "_" + sanitize(g_.node(verts[0]).name));
+        for (size_t j = at; j < end; ++j) drop.insert(members[j]);
       }
     if (!packs.empty()) {
       std::vector<KernelSpec> kept;

@@ -83,25 +83,31 @@ def test_dataflow_templates_chosen_for_fixtures():
         assert [k["template"].split("+")[0] for k in kernels] == [tmpl], name
 
 
-def test_opaque_placeholders_packed_per_producer_set(monkeypatch):
-    """small opaque placeholders with the same producer kernels launch as one
-    kernel, a CTA per op (executor-level; the plan is unchanged).  DIEN T=10:
-    the 13 parameter-only placeholders form one pack, each step's three gate
-    placeholders another -> 69 plan kernels in 39 launches"""
+def test_launch_units_packed_per_producer_set(monkeypatch):
+    """launch units with the same producer kernels share one launch
+    (executor-level; the plan is unchanged): small opaque placeholders a CTA
+    per op, local-template patterns side by side.  DIEN T=10: the 13
+    parameter-only placeholders form one pack, each step's three gate
+    placeholders another, the 10 parameter-only attention broadcasts one
+    local kernel -> 69 plan kernels in 30 launches"""
     stitch = _stitch()
     from tests.conftest import config_graph
     plan = stitch.Plan(stitch.Graph(config_graph("dien_T10")), "b200")
     _, packed = plan.codegen()
+    monkeypatch.setenv("STITCH_LOCAL_PACK", "0")
+    _, opaque_only = plan.codegen()
     monkeypatch.setenv("STITCH_OPAQUE_PACK", "0")
     _, single = plan.codegen()
     assert len(single) == plan.stats()["stitched_kernels"] == 69
-    assert len(packed) == 39
-    ops = lambda ks: sorted(p for k in ks if k["template"].startswith("opaque")
-                            for p in k["pattern"].split("+"))
-    assert ops(packed) == ops(single)  # every placeholder exactly once
-    packs = [k for k in packed if k["template"].startswith("opaque(pack")]
+    assert len(opaque_only) == 39
+    assert len(packed) == 30
+    units = lambda ks: sorted(p for k in ks for p in k["pattern"].split("+"))
+    assert units(packed) == units(opaque_only) == units(single)  # every unit exactly once
+    packs = [k for k in opaque_only if k["template"].startswith("opaque(pack")]
     assert sorted(k["grid"] for k in packs) == [3] * 9 + [13]
     assert all(k["grid"] == len(k["pattern"].split("+")) for k in packs)
+    outs = lambda ks: sorted(o for k in ks for o in k["outputs"])
+    assert outs(packed) == outs(single)
 
 
 def test_cubin_cache_warm_up(tmp_path, monkeypatch):

@@ -153,20 +153,23 @@ def test_dag_capture_matches_linear_chain(monkeypatch):
 
 
 def test_opaque_pack_matches_one_kernel_per_op(monkeypatch):
-    """packed opaque placeholders (one launch, a CTA per op) compute exactly
-    what one kernel per placeholder computes, and match the oracle"""
+    """packed launch units (opaque placeholders a CTA per op, local patterns
+    side by side) compute exactly what one kernel per unit computes, and
+    match the oracle"""
     stitch = _stitch()
-    for name in ("dien_T10", "dien_T20"):
+    for name in ("dien_T10", "dien_T20", "bert_layer"):
         text = config_graph(name)
         g = stitch.Graph(text)
         plan = stitch.Plan(g, "b200")
         inputs = stitch.random_inputs(g, 5)
         ex = stitch.Executor(plan)
-        assert any(k["template"].startswith("opaque(pack") for k in ex.describe())
+        assert len(ex.describe()) < plan.stats()["stitched_kernels"]
         packed = ex.run(inputs)
         monkeypatch.setenv("STITCH_OPAQUE_PACK", "0")
+        monkeypatch.setenv("STITCH_LOCAL_PACK", "0")
         single = stitch.Executor(plan).run(inputs)
         monkeypatch.delenv("STITCH_OPAQUE_PACK")
+        monkeypatch.delenv("STITCH_LOCAL_PACK")
         for k in single:
             assert np.array_equal(packed[k], single[k]), (name, k)
         og = no.parse_graph(text)

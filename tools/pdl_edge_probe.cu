@@ -86,8 +86,10 @@ int main() {
                          "A->C + cross-lane B->C, B without PDL", "A->C + B->C, B on same lane before A",
                          "chain A->A2->C (C waits on grand-parent)",
                          "A only on the other lane (cross-lane A->C, P->C same lane)",
-                         "fork P->{A, A2 on lane 2} -> C (join)"};
-  for (int variant = 0; variant < 7; ++variant) {
+                         "fork P->{A, A2 on lane 2} -> C (join)",
+                         "one lane A(8us)->A2->B->C: C three levels behind the running A",
+                         "one lane A(8us)->A2->C: C two levels behind the running A"};
+  for (int variant = 0; variant < 9; ++variant) {
     cudaGraph_t g;
     CK(cudaStreamBeginCapture(s1, cudaStreamCaptureModeThreadLocal));
     // slot 0: P (a predecessor so A itself launches from a PDL edge), 1: A, 2: B, 3: C, 4: A2
@@ -110,6 +112,8 @@ int main() {
       launch_spin(s1, true, ts, 1, 8000, 1);
     }
     if (variant == 4) launch_spin(s1, true, ts, 4, 3000, 1);
+    if (variant == 7 || variant == 8) launch_spin(s1, true, ts, 4, 300, 1);
+    if (variant == 7) launch_spin(s1, true, ts, 2, 300, 1);
     if (variant == 1 || variant == 2) CK(cudaStreamWaitEvent(s1, ev, 0));
     launch(probe, s1, true, ts, 3);
     CK(cudaStreamEndCapture(s1, &g));
@@ -130,6 +134,7 @@ int main() {
       CK(cudaStreamSynchronize(s1));
       unsigned long long h[16];
       CK(cudaMemcpy(h, ts, sizeof h, cudaMemcpyDeviceToHost));
+      // lead is measured against the running head A (slot 1) for 7/8
       const unsigned long long last_end = variant == 4 ? h[9] : h[3];
       if (r >= 3) {
         lead += (static_cast<double>(last_end) - static_cast<double>(h[6])) / 1e3;
