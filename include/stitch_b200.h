@@ -135,7 +135,9 @@ int stc_exec_run_host_zero_copy(stc_exec* e, const void* const* inputs, void* co
 /* In-graph kernel timeline of one replay (diagnostics; the exec must have been
  * created with STITCH_TRACE=1 in the environment): start_us[i] / end_us[i] =
  * first CTA entry / last CTA exit of kernel i (%globaltimer), us since the
- * earliest entry; -1 for library (GEMM) units.  Arrays of num_kernels. */
+ * earliest entry; -1 for library (GEMM) units.  Arrays of num_kernels
+ * entries -- for a plan run by the persistent template ("persistent(U)", one
+ * kernel) 1 + U: entry 1+u = unit u ready (producers counted) / done. */
 int stc_exec_trace(stc_exec* e, double* start_us, double* end_us);
 /* Pipelined host execution over chunks of DIFFERENT sizes: chunk k runs on
  * execs[exec_of_chunk[k]] (each exec built from a shard graph of the same

@@ -84,6 +84,16 @@ KernelSpec generate_opaque_kernel(const CompGraph& g, int vertex, const std::str
 // small enough for the single-CTA form (opaque_single).
 KernelSpec generate_opaque_pack(const CompGraph& g, const std::vector<int>& vertices, const std::string& name);
 bool opaque_single(const CompGraph& g, int vertex);
+int opaque_cluster(const CompGraph& g, int vertex);  // CTAs (one cluster) per small placeholder
+
+// Persistent template (cg_persist.cpp): the launch units of a launch-bound
+// plan inside one cooperative launch of <= max_ctas 1024-thread CTAs, unit
+// boundaries as completion counters instead of kernel boundaries.  nullopt
+// when some unit does not fit (library GEMM, scratch, dynamic smem,
+// clusters, a block size not dividing 1024, barriers in a sub-1024 unit, or
+// more than max_ctas CTAs).
+std::optional<KernelSpec> generate_persistent_kernel(const std::vector<KernelSpec>& units, const std::string& name,
+                                                     int max_ctas, const std::map<std::string, int64_t>& sizes);
 
 // device helpers every module includes
 const std::string& device_prelude();

@@ -552,14 +552,31 @@ int local_unroll(int64_t chunks, int block) {
   return 2;
 }
 
+// Launch-bound local bodies (domain <= STITCH_LOCAL_SMALL elements, default
+// 32768 -- less than one wave at one element per thread; e.g. DIEN's [256,36]
+// gates): one element per thread (DIEN T=10 81.5 -> 59.6 us,
+// profiles/r01/local_small_ab.jsonl).  Such a kernel is a
+// single partial wave whose time is one warp's instruction chain (loads,
+// then the dependent math, then stores), so fewer elements per thread -- no
+// 128-bit chunks, no unroll -- is shorter (ncu: ra1 at 2 x float4 per thread
+// issues 356 instructions per warp at ~20 cycles each).
+bool local_small(int64_t elements) { return elements <= env_int("STITCH_LOCAL_SMALL", 32768); }
+
+int local_width(const std::vector<int>& dims) {
+  if (dims.empty() || dims.back() % 4 != 0) return 1;
+  int64_t n = 1;
+  for (int d : dims) n *= d;
+  return local_small(n) ? 1 : 4;
+}
+
 // local: grid-stride over W-wide chunks of the domain, U chunks per thread
 void emit_local(Emitter& em, const CompGraph& g, const Body& b) {
   const std::vector<int>& D = b.dims_a;
   const int64_t N = prod(D);
-  em.W = (!D.empty() && D.back() % 4 == 0) ? 4 : 1;
+  em.W = local_width(D);
   const int64_t chunks = N / em.W;
   const int B = em.block;
-  const int U = local_unroll(chunks, B);
+  const int U = local_small(N) ? 1 : local_unroll(chunks, B);
   em.line("// local body: domain " + std::to_string(N) + " elements, vector " + std::to_string(em.W));
   em.open("for (i64 c0_ = (i64)vbid * " + std::to_string(B * U) + " + threadIdx.x; c0_ < " +
           std::to_string(chunks) + "; c0_ += (i64)vgrid * " + std::to_string(B * U) + ")");
@@ -1246,9 +1263,9 @@ KernelSpec generate_pattern_kernel(const CompGraph& g, const std::vector<int>& v
     Body& b = bodies[i];
     if (b.kind == Kind::Local) {
       const int64_t N = prod(b.dims_a);
-      const int w = (!b.dims_a.empty() && b.dims_a.back() % 4 == 0) ? 4 : 1;
+      const int w = local_width(b.dims_a);
       const int64_t chunks = N / w;
-      const int U = local_unroll(chunks, block);
+      const int U = local_small(N) ? 1 : local_unroll(chunks, block);
       b.blocks = static_cast<int>(std::clamp<int64_t>((chunks + int64_t(block) * U - 1) / (int64_t(block) * U), 1,
                                                       int64_t(kSmCount) * env_int("STITCH_LOCAL_CTAS", 32)));
     } else if (b.kind == Kind::Row && cluster > 1) {
@@ -1426,7 +1443,7 @@ KernelSpec generate_pattern_kernel(const CompGraph& g, const std::vector<int>& v
 // enclosing code defines bid_ / nbid_ (this CTA's index and the CTA count
 // of the op) and, for the grid form, bar_ / part_.
 static std::string opaque_body(const CompGraph& g, int vertex, bool single, int grid, int block,
-                               const std::string& wait) {
+                               const std::string& wait, int csize = 1) {
   const OpNode& n = g.node(vertex);
   int64_t count = 0;
   for (int o : n.operands) count += g.node(o).shape.element_count();
@@ -1448,25 +1465,26 @@ static std::string opaque_body(const CompGraph& g, int vertex, bool single, int 
       const int64_t cnt = sh.element_count();
       const bool vec = sh.dtype == DType::F32 && cnt % 4 == 0;
       const int64_t units = vec ? cnt / 4 : cnt;
-      const int64_t K = (units + block - 1) / block;
+      const int64_t span = int64_t(block) * csize;  // threads of the op (its cluster)
+      const int64_t K = (units + span - 1) / span;
       const std::string a = "v" + std::to_string(vi++) + "_";
       if (K > 8) {  // large operand: vectorised grid-stride loop
         if (vec)
-          s << "  for (i64 i = threadIdx.x; i < " << units << "; i += " << block << ") { const float4 q = ld4(T_"
+          s << "  for (i64 i = (i64)bid_ * " << block << " + threadIdx.x; i < " << units << "; i += " << span << ") { const float4 q = ld4(T_"
             << g.node(o).name << " + 4 * i); acc += ((double)q.x + (double)q.y) + ((double)q.z + (double)q.w); }\n";
         else
-          s << "  for (i64 i = threadIdx.x; i < " << units << "; i += " << block << ") acc += (double)ldv(T_"
+          s << "  for (i64 i = (i64)bid_ * " << block << " + threadIdx.x; i < " << units << "; i += " << span << ") acc += (double)ldv(T_"
             << g.node(o).name << ", i);\n";
         continue;
       }
       if (vec) {
         s << "  float4 " << a << "[" << K << "];\n  #pragma unroll\n  for (int k = 0; k < " << K
-          << "; ++k) { const i64 i = threadIdx.x + (i64)k * " << block << "; " << a << "[k] = i < " << units
+          << "; ++k) { const i64 i = (i64)bid_ * " << block << " + threadIdx.x + (i64)k * " << span << "; " << a << "[k] = i < " << units
           << " ? ld4(T_" << g.node(o).name << " + 4 * i) : make_float4(0.f, 0.f, 0.f, 0.f); }\n";
         regs.push_back({a, 4});
       } else {
         s << "  float " << a << "[" << K << "];\n  #pragma unroll\n  for (int k = 0; k < " << K
-          << "; ++k) { const i64 i = threadIdx.x + (i64)k * " << block << "; " << a << "[k] = i < " << units
+          << "; ++k) { const i64 i = (i64)bid_ * " << block << " + threadIdx.x + (i64)k * " << span << "; " << a << "[k] = i < " << units
           << " ? ldv(T_" << g.node(o).name << ", i) : 0.f; }\n";
         regs.push_back({a, 1});
       }
@@ -1513,6 +1531,9 @@ static std::string opaque_body(const CompGraph& g, int vertex, bool single, int 
     << "  __shared__ double tot_;\n  if (threadIdx.x < 32) {\n    double w_ = threadIdx.x < " << block / 32
     << " ? red_[threadIdx.x] : 0.0;\n    w_ = bfly_sum(w_, 32);\n    if (threadIdx.x == 0) tot_ = w_;\n  }\n"
     << "  __syncthreads();\n  double tot = tot_;\n";
+  if (single && csize > 1)  // the op's CTAs form one cluster: add their partials in rank order (DSMEM)
+    s << "  cluster_sync_all();\n  tot = 0.0;\n  #pragma unroll\n  for (unsigned r_ = 0; r_ < " << csize
+      << "u; ++r_) tot += ld_dsmem_f64(&tot_, r_);\n  cluster_sync_all();  // peers done reading our tot_\n";
   if (!single)
     s << "  if (threadIdx.x == 0) part_[blockIdx.x] = tot;\n  grid_sync(bar_, gridDim.x);\n"
       << "  __shared__ double all_;\n"
@@ -1530,6 +1551,22 @@ static std::string opaque_body(const CompGraph& g, int vertex, bool single, int 
   return s.str();
 }
 
+// CTAs (one thread-block cluster) per small placeholder.  Default 1: one
+// CTA per op.  STITCH_OPAQUE_CLUSTER=0 sizes a cluster so every thread moves
+// at most one 128-bit chunk of each operand and of the output (capped at 8):
+// shorter per-warp chains (one CTA: ~190 instructions per warp at ~29 cycles
+// each, ncu DIEN pack3) but the cluster launch and barriers cost more -- DIEN
+// T=20 121.8 (1) vs 129.2 (auto, 3) vs 141.0 us (8),
+// profiles/r01/opaque_cluster_ab.jsonl; =<n> forces n.
+int opaque_cluster(const CompGraph& g, int vertex) {
+  if (const int c = env_int("STITCH_OPAQUE_CLUSTER", 1); c > 0) return std::min(c, 8);
+  const OpNode& n = g.node(vertex);
+  int64_t units = n.shape.element_count();
+  for (int o : n.operands) units = std::max(units, g.node(o).shape.element_count());
+  units = (units + 3) / 4;
+  return static_cast<int>(std::clamp<int64_t>((units + 1023) / 1024, 1, 8));
+}
+
 bool opaque_single(const CompGraph& g, int vertex) {
   const OpNode& n = g.node(vertex);
   int64_t work = n.shape.element_count();
@@ -1543,7 +1580,8 @@ KernelSpec generate_opaque_kernel(const CompGraph& g, int vertex, const std::str
   // small tensors (e.g. DIEN's [256,36] GEMM outputs): one 1024-thread CTA,
   // no grid-wide barrier; large ones: cooperative grid with a barrier
   const bool single = opaque_single(g, vertex);
-  const int grid = single ? 1 : kSmCount * 4;  // cooperative: 4 co-resident 256-thread CTAs per SM
+  const int csize = single ? opaque_cluster(g, vertex) : 1;
+  const int grid = single ? csize : kSmCount * 4;  // cooperative: 4 co-resident 256-thread CTAs per SM
   const int block = single ? 1024 : kBlock;
   KernelSpec k;
   k.name = name;
@@ -1552,6 +1590,8 @@ KernelSpec generate_opaque_kernel(const CompGraph& g, int vertex, const std::str
   k.grid = grid;
   k.block = block;
   k.cooperative = !single;
+  k.cluster = csize;
+  if (csize > 1) k.tmpl += "-cluster" + std::to_string(csize);
   std::ostringstream s;
   s << "extern \"C\" __global__ void __launch_bounds__(" << block << ", " << (single ? 1 : 4) << ") " << name << "(";
   for (int o : ops) {
@@ -1570,7 +1610,8 @@ KernelSpec generate_opaque_kernel(const CompGraph& g, int vertex, const std::str
   s << ") {\n" << (entry_trigger(grid) ? "  pdl_launch();\n" : "");
   k.outputs.push_back(n.name);
   s << "  const int bid_ = blockIdx.x, nbid_ = gridDim.x;\n"
-    << opaque_body(g, vertex, single, grid, block, early ? "  pdl_wait();\n  pdl_launch();\n" : "  pdl_wait();\n");
+    << opaque_body(g, vertex, single, grid, block, early ? "  pdl_wait();\n  pdl_launch();\n" : "  pdl_wait();\n",
+                   csize);
   s << "  pdl_launch();\n}\n";
   k.source = s.str();
   int64_t bytes = n.shape.byte_size();
@@ -1582,9 +1623,12 @@ KernelSpec generate_opaque_kernel(const CompGraph& g, int vertex, const std::str
 KernelSpec generate_opaque_pack(const CompGraph& g, const std::vector<int>& vertices, const std::string& name) {
   KernelSpec k;
   k.name = name;
-  k.tmpl = "opaque(pack" + std::to_string(vertices.size()) + ")";
-  k.grid = static_cast<int>(vertices.size());
+  int csize = 1;  // one cluster per op, the largest op's size for all
+  for (int v : vertices) csize = std::max(csize, opaque_cluster(g, v));
+  k.tmpl = "opaque(pack" + std::to_string(vertices.size()) + (csize > 1 ? "x" + std::to_string(csize) : "") + ")";
+  k.grid = static_cast<int>(vertices.size()) * csize;
   k.block = 1024;
+  k.cluster = csize;
   std::ostringstream sig, body;
   std::set<std::string> seen;
   int64_t bytes = 0;
@@ -1604,8 +1648,9 @@ KernelSpec generate_opaque_pack(const CompGraph& g, const std::vector<int>& vert
     sig << (j ? ", " : "") << c_type(n.shape.dtype) << "* __restrict__ T_" << n.name;
     k.outputs.push_back(n.name);
     bytes += n.shape.byte_size();
-    body << "  " << (j ? "} else " : "") << "if (blockIdx.x == " << j << ") {\n  const int bid_ = 0, nbid_ = 1;\n"
-         << opaque_body(g, vertices[j], true, 1, 1024, "  pdl_wait();\n");
+    body << "  " << (j ? "} else " : "") << "if (blockIdx.x / " << csize << " == " << j << ") {\n  const int bid_ = blockIdx.x % "
+         << csize << ", nbid_ = " << csize << ";\n"
+         << opaque_body(g, vertices[j], true, csize, 1024, "  pdl_wait();\n", csize);
   }
   k.source = sig.str() + ") {\n  pdl_launch();\n" + body.str() + "  }\n}\n";
   k.alg_bytes = bytes;

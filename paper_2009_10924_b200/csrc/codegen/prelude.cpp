@@ -59,6 +59,38 @@ __device__ __forceinline__ float4 ld4h(const f16_t* p) {
   asm("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(a), "=r"(b) : "l"(p));
   return make_float4(h2f((f16_t)(a & 0xffffu)), h2f((f16_t)(a >> 16)), h2f((f16_t)(b & 0xffffu)), h2f((f16_t)(b >> 16)));
 }
+// coherent (L2, ld.global.cg) loads: the persistent template reads tensors
+// written earlier in the same launch by other CTAs, which the non-coherent
+// paths above may not
+__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" :: "l"(p)); }
+__device__ __forceinline__ void touch_l2(const void* p) {
+  unsigned v;
+  asm volatile("ld.global.cg.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+}
+// release-ordered add: the CTA's writes (ordered before it by a preceding
+// __syncthreads) become visible at gpu scope no later than the count
+__device__ __forceinline__ void red_release_add_u32(unsigned* p, unsigned v) {
+#ifdef STITCH_PERSIST_SC_FENCE
+  __threadfence();
+  atomicAdd(p, v);
+#else
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+#endif
+}
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ float ldv_l2(const float* p, i64 i) { return __ldcg(p + i); }
+__device__ __forceinline__ float ldv_l2(const f16_t* p, i64 i) { return h2f(__ldcg(p + i)); }
+__device__ __forceinline__ float ldv_l2(const int* p, i64 i) { return (float)__ldcg(p + i); }
+__device__ __forceinline__ float ldv_l2(const unsigned char* p, i64 i) { return __ldcg(p + i) ? 1.f : 0.f; }
+__device__ __forceinline__ float4 ld4_l2(const float* p) { return __ldcg(reinterpret_cast<const float4*>(p)); }
+__device__ __forceinline__ float4 ld4h_l2(const f16_t* p) {
+  const uint2 q = __ldcg(reinterpret_cast<const uint2*>(p));
+  return make_float4(h2f((f16_t)(q.x & 0xffffu)), h2f((f16_t)(q.x >> 16)), h2f((f16_t)(q.y & 0xffffu)), h2f((f16_t)(q.y >> 16)));
+}
 __device__ __forceinline__ void st4h(f16_t* p, float x, float y, float z, float w) {
   const unsigned a = (unsigned)f2h(x) | ((unsigned)f2h(y) << 16), b = (unsigned)f2h(z) | ((unsigned)f2h(w) << 16);
   asm volatile("st.global.cs.v2.u32 [%0], {%1,%2};" :: "l"(p), "r"(a), "r"(b) : "memory");
@@ -121,9 +153,11 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 #define STC_TRACE_BEGIN(k) do { if (threadIdx.x == 0) atomicMin(&stc_trace_[2 * (k)], gtimer()); } while (0)
 #define STC_TRACE_END(k) do { __syncthreads(); if (threadIdx.x == 0) atomicMax(&stc_trace_[2 * (k) + 1], gtimer()); } while (0)
+#define STC_TRACE_STAMP_END(k) do { if (threadIdx.x == 0) atomicMax(&stc_trace_[2 * (k) + 1], gtimer()); } while (0)
 #else
 #define STC_TRACE_BEGIN(k) do {} while (0)
 #define STC_TRACE_END(k) do {} while (0)
+#define STC_TRACE_STAMP_END(k) do {} while (0)
 #endif
 
 // programmatic dependent launch (PDL): no-ops unless launched with the

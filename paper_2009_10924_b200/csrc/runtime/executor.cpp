@@ -504,14 +504,16 @@ PlanKernels generate_plan_kernels(const CompGraph& g_, const FusionPlan& plan,
   const bool pack_local = !(lpack_env && *lpack_env == '0');
   if ((pack_opaque && !opaque_vertex.empty()) || (pack_local && local_verts.size() > 1)) {
     std::map<std::string, size_t> prod;
-    // (kind, producer set) -> member specs; kind 0 opaque, 1 local
+    // (kind, producer set) -> member specs; kind 0 opaque (+ its cluster size:
+    // a pack launches one uniform cluster per op), 1 local
     std::map<std::pair<int, std::vector<size_t>>, std::vector<size_t>> groups;
     for (size_t i = 0; i < specs_.size(); ++i) {
       std::set<size_t> d;
       for (const auto& t : specs_[i].inputs)
         if (auto it = prod.find(t); it != prod.end()) d.insert(it->second);
       const std::vector<size_t> dv(d.begin(), d.end());
-      if (pack_opaque && opaque_vertex.count(i) && opaque_single(g_, opaque_vertex[i])) groups[{0, dv}].push_back(i);
+      if (pack_opaque && opaque_vertex.count(i) && opaque_single(g_, opaque_vertex[i]))
+        groups[{-opaque_cluster(g_, opaque_vertex[i]), dv}].push_back(i);
       if (pack_local && local_verts.count(i)) groups[{1, dv}].push_back(i);
       for (const auto& t : specs_[i].outputs) prod[t] = i;
     }
@@ -521,7 +523,7 @@ PlanKernels generate_plan_kernels(const CompGraph& g_, const FusionPlan& plan,
       for (size_t at = 0; at + 1 < members.size(); at += 32) {  // <= 32 units per pack
         const size_t end = std::min(members.size(), at + 32);
         if (end - at < 2) break;
-        if (kd.first == 0) {
+        if (kd.first <= 0) {
           std::vector<int> verts;
           for (size_t j = at; j < end; ++j) verts.push_back(opaque_vertex[members[j]]);
           packs[members[at]] = generate_opaque_pack(
@@ -562,11 +564,22 @@ PlanKernels generate_plan_kernels(const CompGraph& g_, const FusionPlan& plan,
       specs_ = std::move(kept);
     }
   }
+  // Launch-bound plans (every unit small, e.g. DIEN): all units inside one
+  // cooperative launch (cg_persist.cpp), unit boundaries as L2 completion
+  // counters instead of kernel boundaries.  STITCH_PERSIST=1 enables it.
+  if (const char* pe = std::getenv("STITCH_PERSIST"); pe && *pe == '1' && mode != ExecMode::Program) {
+    const char* mc = std::getenv("STITCH_PERSIST_MAX_CTAS");
+    std::map<std::string, int64_t> sizes;
+    for (const auto& n : g_.nodes) sizes[n.name] = n.shape.byte_size();
+    if (auto pk = generate_persistent_kernel(specs_, "k" + std::to_string(idx++) + "_persistent",
+                                             mc && *mc ? std::atoi(mc) : 32, sizes))
+      specs_ = {std::move(*pk)};
+  }
   // timeline hooks (no-ops unless compiled with -DSTITCH_TRACE, Executor::trace)
   for (size_t i = 0; i < specs_.size(); ++i) {
     auto& src = specs_[i].source;
     if (specs_[i].is_gemm || src.empty()) continue;
-    const size_t open = src.find("{\n");
+    const size_t open = src.find("{\n", src.find("__global__"));
     const size_t close = src.rfind("}\n");
     if (open == std::string::npos || close == std::string::npos || close < open) continue;
     src.insert(close, "  STC_TRACE_END(" + std::to_string(i) + ");\n");
@@ -1035,7 +1048,9 @@ std::vector<std::pair<double, double>> Executor::trace(int set) {
   size_t bytes = 0;
   void* buf = module_->global("stc_trace_", &bytes);
   if (!buf) throw std::runtime_error("[exec] trace buffer missing from the module");
-  const size_t n = specs_.size();
+  // a persistent kernel also stamps each of its units (slots 1..U)
+  size_t n = specs_.size();
+  if (n == 1 && specs_[0].tmpl.rfind("persistent(", 0) == 0) n = 1 + std::stoul(specs_[0].tmpl.substr(11));
   std::vector<unsigned long long> init(2 * n);
   for (size_t i = 0; i < n; ++i) init[2 * i] = ~0ull, init[2 * i + 1] = 0ull;
   ensure_sets(set + 1);
@@ -1046,12 +1061,13 @@ std::vector<std::pair<double, double>> Executor::trace(int set) {
   STC_RT(cudaStreamSynchronize(stream_));
   std::vector<unsigned long long> t(2 * n);
   STC_RT(cudaMemcpy(t.data(), buf, t.size() * 8, cudaMemcpyDeviceToHost));
+  auto gemm = [&](size_t i) { return i < specs_.size() && specs_[i].is_gemm; };
   unsigned long long t0 = ~0ull;
   for (size_t i = 0; i < n; ++i)
-    if (!specs_[i].is_gemm) t0 = std::min(t0, t[2 * i]);
+    if (!gemm(i)) t0 = std::min(t0, t[2 * i]);
   std::vector<std::pair<double, double>> out(n, {-1.0, -1.0});
   for (size_t i = 0; i < n; ++i)
-    if (!specs_[i].is_gemm && t[2 * i + 1])
+    if (!gemm(i) && t[2 * i + 1])
       out[i] = {1e-3 * static_cast<double>(t[2 * i] - t0), 1e-3 * static_cast<double>(t[2 * i + 1] - t0)};
   return out;
 }

@@ -178,6 +178,26 @@ def test_opaque_pack_matches_one_kernel_per_op(monkeypatch):
             assert stitch.compare({k: packed[k]}, {k: want[k]}, tol, 1e-5)["pass"], (name, k)
 
 
+def test_persistent_template_matches_graph(monkeypatch):
+    """opt-in persistent template (STITCH_PERSIST=1: every launch unit of a
+    launch-bound plan in one cooperative launch, unit boundaries as L2
+    completion counters) computes exactly what the per-unit CUDA Graph
+    computes, over repeated launches (the counters' generation scheme)"""
+    stitch = _stitch()
+    text = config_graph("dien_T10")
+    g = stitch.Graph(text)
+    plan = stitch.Plan(g, "b200")
+    inputs = stitch.random_inputs(g, 7)
+    ref = stitch.Executor(plan).run(inputs)
+    monkeypatch.setenv("STITCH_PERSIST", "1")
+    ex = stitch.Executor(plan)
+    assert [k["template"] for k in ex.describe()] == ["persistent(30)"]
+    for _ in range(3):
+        got = ex.run(inputs)
+        for k in ref:
+            assert np.array_equal(got[k], ref[k]), k
+
+
 @pytest.mark.parametrize("precision", ["fp32", "tf32"])
 def test_model_mode_gemm_bert_layer(monkeypatch, precision):
     """model mode (non-parity): the BERT FFN layer's
@@ -264,10 +284,14 @@ EDGE_SHAPES = {
 }
 
 
+@pytest.mark.parametrize("small", ["default", "0"])
 @pytest.mark.parametrize("name", sorted(EDGE_SHAPES))
-def test_template_edge_shapes(name):
+def test_template_edge_shapes(name, small, monkeypatch):
     """template edge cases (ragged rows/columns, vector widths 1/2/4, team
-    sizes from 1 to 256 threads, single row / slab) under the B200 profile"""
+    sizes from 1 to 256 threads, single row / slab) under the B200 profile;
+    small="0" keeps 128-bit chunks for small local domains too"""
+    if small != "default":
+        monkeypatch.setenv("STITCH_LOCAL_SMALL", small)
     ex = _check(EDGE_SHAPES[name], "b200", "stitched", 5)
     assert all(k["template"] != "program" for k in ex.describe()), name
 
