@@ -110,6 +110,21 @@ def test_launch_units_packed_per_producer_set(monkeypatch):
     assert outs(packed) == outs(single)
 
 
+def test_persistent_template_codegen(monkeypatch):
+    """opt-in persistent template: a launch-bound plan becomes one cooperative
+    kernel whose unit bodies are shared between textually identical units
+    (DIEN's per-step kernels); plans with large kernels are left alone"""
+    stitch = _stitch()
+    from tests.conftest import config_graph
+    monkeypatch.setenv("STITCH_PERSIST", "1")
+    src, kernels = stitch.Plan(stitch.Graph(config_graph("dien_T10")), "b200").codegen()
+    assert [k["template"] for k in kernels] == ["persistent(30)"]
+    assert len(set(re.findall(r"\bunit\d+_\(", src))) == 6  # 30 units, 6 distinct bodies
+    assert re.fullmatch(r"[0-9a-f]{32}", stitch.compile_cuda(src))
+    _, big = stitch.Plan(stitch.Graph(config_graph("bert_layer")), "b200").codegen()
+    assert len(big) > 1 and not any(k["template"].startswith("persistent") for k in big)
+
+
 def test_cubin_cache_warm_up(tmp_path, monkeypatch):
     """stc_cache_warm: NVRTC-compiles plan modules into
     the persistent cache on host threads without a GPU; a second warm-up is
