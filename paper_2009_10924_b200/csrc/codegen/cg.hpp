@@ -33,7 +33,9 @@
 namespace stitch::gpu {
 
 struct KernelSpec {
-  std::string name;                  // __global__ symbol
+  std::string name;                  // __global__ symbol (unique per launch unit)
+  std::string symbol;                // function actually launched when it differs from name:
+                                     // units with identical code share one (executor dedup)
   std::string source;                // CUDA C++ (device code only; prelude separate)
   std::string tmpl;                  // local | regional | global | independent | program | opaque
   std::string pattern_key;           // FusionPattern::key() or "op:<name>"

@@ -6,6 +6,7 @@
 #include <chrono>
 #include <future>
 #include <cstdio>
+#include <regex>
 #include <cctype>
 #include <cstdlib>
 #include <cstring>
@@ -160,7 +161,7 @@ void Executor::finish_init(const std::string& cubin) {
       fns_.push_back(nullptr);
       continue;
     }
-    cudaKernel_t f = module_->fn(k.name);
+    cudaKernel_t f = module_->fn(k.symbol.empty() ? k.name : k.symbol);
     const void* fp = reinterpret_cast<const void*>(f);
     if (k.smem > 48 * 1024)
       STC_RT(cudaFuncSetAttribute(fp, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(k.smem)));
@@ -575,10 +576,33 @@ PlanKernels generate_plan_kernels(const CompGraph& g_, const FusionPlan& plan,
                                              mc && *mc ? std::atoi(mc) : 32, sizes))
       specs_ = {std::move(*pk)};
   }
+  // Units whose code differs only in the tensors they touch (DIEN's per-step
+  // kernels) share one function: canonical text = source with the kernel
+  // name and its tensor parameters renamed positionally.  Each launch still
+  // binds its own tensors.  The module then holds 6 instead of 30 functions
+  // for DIEN T=10 and a step's kernels find their code already cached by the
+  // previous step's (ncu: no_instruction stalls were ~20% of a tiny kernel's
+  // chain; T=10 59.6 -> 58.0 us, profiles/r01/dedup_ab.jsonl).  Off under STITCH_TRACE (the hooks carry the unit index) and
+  // with STITCH_DEDUP=0.
+  const char* tr_env = std::getenv("STITCH_TRACE");
+  const char* dd_env = std::getenv("STITCH_DEDUP");
+  if (!(tr_env && *tr_env == '1') && !(dd_env && *dd_env == '0')) {
+    std::map<std::string, std::string> owner;  // canonical source -> symbol
+    for (auto& k : specs_) {
+      if (k.is_gemm || k.source.empty()) continue;
+      std::string canon = std::regex_replace(k.source, std::regex("\\b" + k.name + "\\b"), "KNAME_");
+      int pi = 0;
+      for (const auto* list : {&k.inputs, &k.outputs})
+        for (const auto& t : *list)
+          canon = std::regex_replace(canon, std::regex("\\bT_" + t + "\\b"), "p" + std::to_string(pi++) + "_");
+      auto [it, fresh] = owner.emplace(canon, k.name);
+      if (!fresh) k.symbol = it->second;
+    }
+  }
   // timeline hooks (no-ops unless compiled with -DSTITCH_TRACE, Executor::trace)
   for (size_t i = 0; i < specs_.size(); ++i) {
     auto& src = specs_[i].source;
-    if (specs_[i].is_gemm || src.empty()) continue;
+    if (specs_[i].is_gemm || src.empty() || !specs_[i].symbol.empty()) continue;
     const size_t open = src.find("{\n", src.find("__global__"));
     const size_t close = src.rfind("}\n");
     if (open == std::string::npos || close == std::string::npos || close < open) continue;
@@ -588,7 +612,7 @@ PlanKernels generate_plan_kernels(const CompGraph& g_, const FusionPlan& plan,
   std::sort(params_.begin(), params_.end());
   out.source = device_prelude();
   for (const auto& k : specs_)
-    if (!k.is_gemm)
+    if (!k.is_gemm && k.symbol.empty())
       out.source += "\n// ---- " + k.name + " [" + k.tmpl + "] pattern " + k.pattern_key + "\n" + k.source;
   return out;
 }
@@ -1077,7 +1101,8 @@ std::string describe_specs(const std::vector<KernelSpec>& specs) {
   o << "[";
   for (size_t i = 0; i < specs.size(); ++i) {
     const auto& k = specs[i];
-    o << (i ? "," : "") << "{\"name\":\"" << k.name << "\",\"template\":\"" << json_escape(k.tmpl)
+    o << (i ? "," : "") << "{\"name\":\"" << k.name << "\",\"symbol\":\"" << (k.symbol.empty() ? k.name : k.symbol)
+      << "\",\"template\":\"" << json_escape(k.tmpl)
       << "\",\"pattern\":\"" << k.pattern_key << "\",\"grid\":" << k.grid << ",\"block\":" << k.block
       << ",\"smem\":" << k.smem << ",\"cooperative\":" << (k.cooperative ? "true" : "false")
       << ",\"cluster\":" << k.cluster

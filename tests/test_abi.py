@@ -108,6 +108,11 @@ def test_launch_units_packed_per_producer_set(monkeypatch):
     assert all(k["grid"] == len(k["pattern"].split("+")) for k in packs)
     outs = lambda ks: sorted(o for k in ks for o in k["outputs"])
     assert outs(packed) == outs(single)
+    # launches with identical code (modulo their tensors) share one function
+    assert len({k["symbol"] for k in packed}) == 6
+    monkeypatch.setenv("STITCH_DEDUP", "0")
+    _, nodedup = plan.codegen()
+    assert len({k["symbol"] for k in nodedup}) == 69
 
 
 def test_persistent_template_codegen(monkeypatch):
