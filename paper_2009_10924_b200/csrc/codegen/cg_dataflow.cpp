@@ -202,9 +202,13 @@ class Emitter {
         }
       }
     }
+    // graph parameters: non-coherent loads (immutable for the graph's
+    // lifetime); tensors of earlier kernels: coherent (prelude, ld4k)
+    const bool param = is_param(v);
+    const std::string LV = param ? "ldv(" : "ldvk(";
     if (nvary == 0 || W == 1) {
       const std::string t = fresh("t");
-      line("const float " + t + " = ldv(" + ptr + ", " + linear(v, c, 0) + ");");
+      line("const float " + t + " = " + LV + ptr + ", " + linear(v, c, 0) + ");");
       if (nvary == 0) return {{t}};
       return {{t}};
     }
@@ -213,20 +217,20 @@ class Emitter {
     Val r;
     if (contiguous && sh.dtype == DType::F16) {  // 4 halves, one 64-bit load
       const std::string q = fresh("q");
-      line("const float4 " + q + " = ld4h(" + ptr + " + " + linear(v, c, 0) + ");");
+      line("const float4 " + q + " = " + (param ? "ld4h(" : "ld4hk(") + ptr + " + " + linear(v, c, 0) + ");");
       for (const char* f : {".x", ".y", ".z", ".w"}) r.lanes.push_back(q + f);
       return r;
     }
     if (contiguous && sh.dtype == DType::F32) {
       const std::string q = fresh("q");
       const bool cached = cached_tensors.count(v) > 0;
-      line("const float4 " + q + " = " + (cached ? "ld4c(" : "ld4(") + ptr + " + " + linear(v, c, 0) + ");");
+      line("const float4 " + q + " = " + (!param ? "ld4k(" : cached ? "ld4c(" : "ld4(") + ptr + " + " + linear(v, c, 0) + ");");
       for (const char* f : {".x", ".y", ".z", ".w"}) r.lanes.push_back(q + f);
       return r;
     }
     for (int k = 0; k < W; ++k) {
       const std::string t = fresh("t");
-      line("const float " + t + " = ldv(" + ptr + ", " + linear(v, c, k) + ");");
+      line("const float " + t + " = " + LV + ptr + ", " + linear(v, c, k) + ");");
       r.lanes.push_back(t);
     }
     return r;
@@ -382,7 +386,8 @@ class Emitter {
           loaded.insert(data);
           if (!is_param(data)) ensure_wait();
           const std::string t = fresh("t");
-          line("const float " + t + " = ldv(T_" + g_.node(data).name + ", " + linear(data, dc, 0) + ");");
+          line("const float " + t + " = " + (is_param(data) ? "ldv(T_" : "ldvk(T_") + g_.node(data).name + ", " +
+               linear(data, dc, 0) + ");");
           r.lanes.push_back(t);
         }
         return r;
@@ -758,7 +763,7 @@ void emit_row(Emitter& em, const CompGraph& g, const std::set<int>& pat, const B
       for (int j = 0; j < rp.NJ; ++j) {
         const std::string nm = "pf_" + g.node(v).name + "_" + std::to_string(j);
         decl += std::string(decl == "float4" ? " " : ", ") + nm;
-        first += nm + " = ld4(T_" + g.node(v).name + " + r0_ * " + sL + " + " + off(j) + "); ";
+        first += nm + " = " + (em.is_param(v) ? "ld4(T_" : "ld4k(T_") + g.node(v).name + " + r0_ * " + sL + " + " + off(j) + "); ";
       }
     em.line(decl + ";");
     em.line("{ const i64 r0_ = min((i64)vbid * " + sRPB + " + team_, (i64)" + std::to_string(ROWS - 1) + "); " + first + "}");
@@ -768,7 +773,7 @@ void emit_row(Emitter& em, const CompGraph& g, const std::set<int>& pat, const B
       for (int j = 0; j < rp.NJ; ++j) {
         const std::string sfx = g.node(v).name + "_" + std::to_string(j);
         cur += std::string(cur == "float4" ? " " : ", ") + "cu_" + sfx + " = pf_" + sfx;
-        next += "pf_" + sfx + " = ld4(T_" + g.node(v).name + " + n_ * " + sL + " + " + off(j) + "); ";
+        next += "pf_" + sfx + " = " + (em.is_param(v) ? "ld4(T_" : "ld4k(T_") + g.node(v).name + " + n_ * " + sL + " + " + off(j) + "); ";
       }
     em.line("const " + cur + ";");
     em.line("{ const i64 n_ = rb_ + (i64)vgrid * " + sRPB + " + team_; if (n_ < " + sROWS + ") { " + next + "} }");
@@ -1457,10 +1462,21 @@ static std::string opaque_body(const CompGraph& g, int vertex, bool single, int 
     // the PDL wait (`wait`), kernel-produced operands after it
     int vi = 0;
     std::vector<std::pair<std::string, int>> regs;  // (array, lanes per element)
+    bool hoisted = false;
     for (int pass = 0; pass < 2; ++pass) {
+     // ptxas schedules griddepcontrol.wait (ACQBULK) above independent
+     // non-coherent loads of the same basic block, which would undo the
+     // hoisting; a CTA barrier between them keeps the loads in front
+     if (pass == 1 && hoisted && env_int("STITCH_OPAQUE_FENCE", 1) != 0) s << "  __syncthreads();\n";
      if (pass == 1) s << wait;
      for (int o : n.operands) {
       if ((g.node(o).kind == OpKind::Parameter) != (pass == 0)) continue;
+      hoisted = hoisted || pass == 0;
+      // pre-wait loads are coherent (ld.global, not .nc): ptxas keeps those
+      // in front of the barrier below, while it sinks .nc loads past it
+      const bool fence = pass == 0 && env_int("STITCH_OPAQUE_FENCE", 1) != 0;
+      const std::string L4 = pass == 1 ? "ld4k(" : fence ? "ld4p(" : "ld4(",
+                        LV = pass == 1 ? "ldvk(" : fence ? "ldvp(" : "ldv(";
       const TensorShape& sh = g.node(o).shape;
       const int64_t cnt = sh.element_count();
       const bool vec = sh.dtype == DType::F32 && cnt % 4 == 0;
@@ -1470,22 +1486,22 @@ static std::string opaque_body(const CompGraph& g, int vertex, bool single, int 
       const std::string a = "v" + std::to_string(vi++) + "_";
       if (K > 8) {  // large operand: vectorised grid-stride loop
         if (vec)
-          s << "  for (i64 i = (i64)bid_ * " << block << " + threadIdx.x; i < " << units << "; i += " << span << ") { const float4 q = ld4(T_"
+          s << "  for (i64 i = (i64)bid_ * " << block << " + threadIdx.x; i < " << units << "; i += " << span << ") { const float4 q = " << L4 << "T_"
             << g.node(o).name << " + 4 * i); acc += ((double)q.x + (double)q.y) + ((double)q.z + (double)q.w); }\n";
         else
-          s << "  for (i64 i = (i64)bid_ * " << block << " + threadIdx.x; i < " << units << "; i += " << span << ") acc += (double)ldv(T_"
+          s << "  for (i64 i = (i64)bid_ * " << block << " + threadIdx.x; i < " << units << "; i += " << span << ") acc += (double)" << LV << "T_"
             << g.node(o).name << ", i);\n";
         continue;
       }
       if (vec) {
         s << "  float4 " << a << "[" << K << "];\n  #pragma unroll\n  for (int k = 0; k < " << K
           << "; ++k) { const i64 i = (i64)bid_ * " << block << " + threadIdx.x + (i64)k * " << span << "; " << a << "[k] = i < " << units
-          << " ? ld4(T_" << g.node(o).name << " + 4 * i) : make_float4(0.f, 0.f, 0.f, 0.f); }\n";
+          << " ? " << L4 << "T_" << g.node(o).name << " + 4 * i) : make_float4(0.f, 0.f, 0.f, 0.f); }\n";
         regs.push_back({a, 4});
       } else {
         s << "  float " << a << "[" << K << "];\n  #pragma unroll\n  for (int k = 0; k < " << K
           << "; ++k) { const i64 i = (i64)bid_ * " << block << " + threadIdx.x + (i64)k * " << span << "; " << a << "[k] = i < " << units
-          << " ? ldv(T_" << g.node(o).name << ", i) : 0.f; }\n";
+          << " ? " << LV << "T_" << g.node(o).name << ", i) : 0.f; }\n";
         regs.push_back({a, 1});
       }
      }
@@ -1508,19 +1524,21 @@ static std::string opaque_body(const CompGraph& g, int vertex, bool single, int 
       const TensorShape& sh = g.node(o).shape;
       const int64_t cnt = sh.element_count();
       const std::string T = "T_" + g.node(o).name;
+      const bool param = g.node(o).kind == OpKind::Parameter;
+      const std::string L4 = param ? "ld4(" : "ld4k(", LV = param ? "ldv(" : "ldvk(";
       if (sh.dtype == DType::F32 && cnt % 4 == 0) {
         const std::string u = std::to_string(cnt / 4);
         s << "  for (i64 i = gt_; i < " << u << "; i += 4 * gs_) {\n"
-          << "    float4 q0 = ld4(" << T << " + 4 * i), q1 = make_float4(0.f, 0.f, 0.f, 0.f), q2 = q1, q3 = q1;\n"
-          << "    if (i + gs_ < " << u << ") q1 = ld4(" << T << " + 4 * (i + gs_));\n"
-          << "    if (i + 2 * gs_ < " << u << ") q2 = ld4(" << T << " + 4 * (i + 2 * gs_));\n"
-          << "    if (i + 3 * gs_ < " << u << ") q3 = ld4(" << T << " + 4 * (i + 3 * gs_));\n"
+          << "    float4 q0 = " << L4 << T << " + 4 * i), q1 = make_float4(0.f, 0.f, 0.f, 0.f), q2 = q1, q3 = q1;\n"
+          << "    if (i + gs_ < " << u << ") q1 = " << L4 << T << " + 4 * (i + gs_));\n"
+          << "    if (i + 2 * gs_ < " << u << ") q2 = " << L4 << T << " + 4 * (i + 2 * gs_));\n"
+          << "    if (i + 3 * gs_ < " << u << ") q3 = " << L4 << T << " + 4 * (i + 3 * gs_));\n"
           << "    a0_ += ((double)q0.x + (double)q0.y) + ((double)q0.z + (double)q0.w);\n"
           << "    a1_ += ((double)q1.x + (double)q1.y) + ((double)q1.z + (double)q1.w);\n"
           << "    a2_ += ((double)q2.x + (double)q2.y) + ((double)q2.z + (double)q2.w);\n"
           << "    a3_ += ((double)q3.x + (double)q3.y) + ((double)q3.z + (double)q3.w);\n  }\n";
       } else {
-        s << "  for (i64 i = gt_; i < " << cnt << "; i += gs_) a0_ += (double)ldv(" << T << ", i);\n";
+        s << "  for (i64 i = gt_; i < " << cnt << "; i += gs_) a0_ += (double)" << LV << T << ", i);\n";
       }
     }
     s << "  acc = (a0_ + a1_) + (a2_ + a3_);\n";

@@ -66,9 +66,9 @@ std::string as_unit_function(const KernelSpec& k, const std::string& fn) {
       {std::regex(R"(\bgridDim\.x\b)"), "vg_"},
       {std::regex(R"(\bthreadIdx\.x\b)"), "vt_"},
       {std::regex(R"(__restrict__)"), ""},
-      {std::regex(R"(\bld4c?\()"), "ld4_l2("},
-      {std::regex(R"(\bld4h\()"), "ld4h_l2("},
-      {std::regex(R"(\bldv\()"), "ldv_l2("},
+      {std::regex(R"(\bld4[ckp]?\()"), "ld4_l2("},
+      {std::regex(R"(\bld4hk?\()"), "ld4h_l2("},
+      {std::regex(R"(\bldv[kp]?\()"), "ldv_l2("},
       {std::regex(R"(\b__ldg\()"), "__ldcg("},
       {std::regex(R"(\bpdl_(wait|launch)\(\);)"), ""},
   };

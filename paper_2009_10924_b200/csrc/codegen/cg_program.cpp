@@ -191,12 +191,12 @@ class ProgramTranslator {
       case Stmt::FConst: return s.dst + " = " + c_double(s.cval) + ";";
       case Stmt::FMove: return s.dst + " = " + s.srcs[0] + ";";
       case Stmt::FOp: return fop(s);
-      case Stmt::GLoad:
+      case Stmt::GLoad:  // coherent loads: the tensor may come from an earlier kernel (prelude, ldvk)
         if (checked_)
           return "if (" + gd(s.guard) + ") { const i64 i_ = " + ex(s.idx) + "; if (i_ < 0 || i_ >= " +
                  std::to_string(count_of(s.tensor)) + "ll) { sim_fault(fault_, 2, i_); " + s.dst +
-                 " = 0.0; } else " + s.dst + " = (double)ldv(" + tname(s.tensor) + ", i_); } else " + s.dst + " = 0.0;";
-        return s.dst + " = " + gd(s.guard) + " ? (double)ldv(" + tname(s.tensor) + ", " + ex(s.idx) +
+                 " = 0.0; } else " + s.dst + " = (double)ldvk(" + tname(s.tensor) + ", i_); } else " + s.dst + " = 0.0;";
+        return s.dst + " = " + gd(s.guard) + " ? (double)ldvk(" + tname(s.tensor) + ", " + ex(s.idx) +
                ") : 0.0;";
       case Stmt::GStore: {
         if (checked_)

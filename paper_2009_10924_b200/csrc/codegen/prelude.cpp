@@ -20,10 +20,37 @@ __device__ __forceinline__ float h2f(f16_t h) { float f; asm("cvt.f32.f16 %0, %1
 __device__ __forceinline__ f16_t f2h(float f) { f16_t h; asm("cvt.rn.f16.f32 %0, %1;" : "=h"(h) : "f"(f)); return h; }
 
 // tensor element <-> f32 value (stitch::DType: f32 / f16 / i32 / bool)
-__device__ __forceinline__ float ldv(const float* p, i64 i) { return __ldg(p + i); }
-__device__ __forceinline__ float ldv(const f16_t* p, i64 i) { return h2f(__ldg(p + i)); }
-__device__ __forceinline__ float ldv(const int* p, i64 i) { return (float)__ldg(p + i); }
-__device__ __forceinline__ float ldv(const unsigned char* p, i64 i) { return __ldg(p + i) ? 1.f : 0.f; }
+// Global loads are volatile asm so they keep their place relative to
+// griddepcontrol.wait (also volatile): a kernel's graph-parameter loads are
+// emitted before its PDL wait to overlap the previous kernel's drain, and a
+// plain intrinsic / non-volatile asm load of read-only data may be sunk
+// below the wait by the compiler (SASS showed ACQBULK first in every DIEN
+// kernel).  STITCH_LD_FREE (an NVRTC define) restores free scheduling.
+#ifdef STITCH_LD_FREE
+#define STC_LD asm
+#else
+#define STC_LD asm volatile
+#endif
+__device__ __forceinline__ float ldv(const float* p, i64 i) {
+  float v;
+  STC_LD("ld.global.nc.f32 %0, [%1];" : "=f"(v) : "l"(p + i));
+  return v;
+}
+__device__ __forceinline__ float ldv(const f16_t* p, i64 i) {
+  unsigned short h;
+  STC_LD("ld.global.nc.u16 %0, [%1];" : "=h"(h) : "l"(p + i));
+  return h2f(h);
+}
+__device__ __forceinline__ float ldv(const int* p, i64 i) {
+  int v;
+  STC_LD("ld.global.nc.s32 %0, [%1];" : "=r"(v) : "l"(p + i));
+  return (float)v;
+}
+__device__ __forceinline__ float ldv(const unsigned char* p, i64 i) {
+  unsigned v;
+  STC_LD("ld.global.nc.u8 %0, [%1];" : "=r"(v) : "l"(p + i));
+  return (v & 0xffu) ? 1.f : 0.f;
+}
 __device__ __forceinline__ void stv(float* p, i64 i, float v) { p[i] = v; }
 __device__ __forceinline__ void stv(f16_t* p, i64 i, float v) { p[i] = f2h(v); }
 __device__ __forceinline__ void stv(int* p, i64 i, float v) { p[i] = (int)roundf(v); }
@@ -33,16 +60,62 @@ __device__ __forceinline__ void stv(unsigned char* p, i64 i, float v) { p[i] = v
 __device__ __forceinline__ float4 ld4(const float* p) {
   float4 r;
 #ifdef STITCH_L2_256B
-  asm("ld.global.nc.L1::no_allocate.L2::256B.v4.f32 {%0,%1,%2,%3}, [%4];"
+  STC_LD("ld.global.nc.L1::no_allocate.L2::256B.v4.f32 {%0,%1,%2,%3}, [%4];"
       : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
 #else
-  asm("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+  STC_LD("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
       : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
 #endif
   return r;
 }
 // 128-bit load through L1 (data re-read by many threads, e.g. gamma/beta rows)
-__device__ __forceinline__ float4 ld4c(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
+// Coherent loads (weak ld.global without .nc, no L1 allocation; =cg with
+// STITCH_LDK_CG).  Two uses:
+//  * tensors written by an EARLIER KERNEL of the graph (ld4k / ldvk /
+//    ld4hk): under programmatic dependent launch this kernel starts before
+//    its producer has finished, so such a tensor is not read-only for the
+//    kernel's lifetime and must not be read through ld.global.nc -- ptxas
+//    treats .nc loads as reads of immutable memory and may schedule them
+//    above griddepcontrol.wait (observed: opaque placeholders);
+//  * graph parameters that must be ISSUED before the PDL wait (ld4p /
+//    ldvp, opaque_body): ptxas keeps coherent loads in front of a CTA
+//    barrier, where it sinks .nc loads below the wait.
+#ifdef STITCH_LDK_CG
+#define STC_LDK "ld.global.cg"
+#else
+#define STC_LDK "ld.global.L1::no_allocate"
+#endif
+#define STC_LDK_V4(p, r) asm volatile(STC_LDK ".v4.f32 {%0,%1,%2,%3}, [%4];" \
+                                      : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p) : "memory")
+__device__ __forceinline__ float4 ld4k(const float* p) { float4 r; STC_LDK_V4(p, r); return r; }
+__device__ __forceinline__ float4 ld4p(const float* p) { float4 r; STC_LDK_V4(p, r); return r; }
+__device__ __forceinline__ float ldvk(const float* p, i64 i) {
+  float v;
+  asm volatile(STC_LDK ".f32 %0, [%1];" : "=f"(v) : "l"(p + i) : "memory");
+  return v;
+}
+__device__ __forceinline__ float ldvk(const f16_t* p, i64 i) {
+  unsigned short h;
+  asm volatile(STC_LDK ".u16 %0, [%1];" : "=h"(h) : "l"(p + i) : "memory");
+  return h2f(h);
+}
+__device__ __forceinline__ float ldvk(const int* p, i64 i) {
+  int v;
+  asm volatile(STC_LDK ".s32 %0, [%1];" : "=r"(v) : "l"(p + i) : "memory");
+  return (float)v;
+}
+__device__ __forceinline__ float ldvk(const unsigned char* p, i64 i) {
+  unsigned v;
+  asm volatile(STC_LDK ".u8 %0, [%1];" : "=r"(v) : "l"(p + i) : "memory");
+  return (v & 0xffu) ? 1.f : 0.f;
+}
+template <typename T>
+__device__ __forceinline__ float ldvp(const T* p, i64 i) { return ldvk(p, i); }
+__device__ __forceinline__ float4 ld4c(const float* p) {
+  float4 r;
+  STC_LD("ld.global.nc.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
+  return r;
+}
 // 128-bit streaming (evict-first) store: outputs are written once and not
 // re-read by this kernel (B200 A/B: profiles/r01/store_hint_sweep.jsonl)
 __device__ __forceinline__ void st4(float* p, float a, float b, float c, float d) {
@@ -56,7 +129,7 @@ __device__ __forceinline__ void st4(float* p, float a, float b, float c, float d
 // 4 halves as one 64-bit access (f16 tensors, 4-aligned element index)
 __device__ __forceinline__ float4 ld4h(const f16_t* p) {
   unsigned a, b;
-  asm("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(a), "=r"(b) : "l"(p));
+  STC_LD("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(a), "=r"(b) : "l"(p));
   return make_float4(h2f((f16_t)(a & 0xffffu)), h2f((f16_t)(a >> 16)), h2f((f16_t)(b & 0xffffu)), h2f((f16_t)(b >> 16)));
 }
 // coherent (L2, ld.global.cg) loads: the persistent template reads tensors
@@ -90,6 +163,11 @@ __device__ __forceinline__ float4 ld4_l2(const float* p) { return __ldcg(reinter
 __device__ __forceinline__ float4 ld4h_l2(const f16_t* p) {
   const uint2 q = __ldcg(reinterpret_cast<const uint2*>(p));
   return make_float4(h2f((f16_t)(q.x & 0xffffu)), h2f((f16_t)(q.x >> 16)), h2f((f16_t)(q.y & 0xffffu)), h2f((f16_t)(q.y >> 16)));
+}
+__device__ __forceinline__ float4 ld4hk(const f16_t* p) {
+  unsigned a, b;
+  asm volatile(STC_LDK ".v2.u32 {%0,%1}, [%2];" : "=r"(a), "=r"(b) : "l"(p) : "memory");
+  return make_float4(h2f((f16_t)(a & 0xffffu)), h2f((f16_t)(a >> 16)), h2f((f16_t)(b & 0xffffu)), h2f((f16_t)(b >> 16)));
 }
 __device__ __forceinline__ void st4h(f16_t* p, float x, float y, float z, float w) {
   const unsigned a = (unsigned)f2h(x) | ((unsigned)f2h(y) << 16), b = (unsigned)f2h(z) | ((unsigned)f2h(w) << 16);
