@@ -130,6 +130,24 @@ def test_persistent_template_codegen(monkeypatch):
     assert len(big) > 1 and not any(k["template"].startswith("persistent") for k in big)
 
 
+def test_kernel_produced_tensors_never_read_non_coherently():
+    """under programmatic dependent launch a tensor written by an earlier
+    kernel is not read-only for the consumer's lifetime: only graph
+    parameters may go through the ld.global.nc helpers (ld4 / ld4c / ld4h /
+    ldv); everything else must use the coherent ones (ld4k / ldvk / ld4hk),
+    which ptxas keeps below griddepcontrol.wait"""
+    stitch = _stitch()
+    from tests.conftest import config_graph, fixture_graphs
+    texts = [config_graph(n) for n in ("dien_T10", "bert_layer", "bert_cut")] + list(fixture_graphs().values())
+    for text in texts:
+        g = stitch.Graph(text)
+        params = {t.name for t in g.params}
+        for mode in ("stitched", "unfused"):
+            src, _ = stitch.Plan(g, "b200").codegen(mode)
+            for fn, t in re.findall(r"\b(ld4c?|ld4h|ldv)\(T_(\w+)", src):
+                assert t in params, (fn, t)
+
+
 def test_cubin_cache_warm_up(tmp_path, monkeypatch):
     """stc_cache_warm: NVRTC-compiles plan modules into
     the persistent cache on host threads without a GPU; a second warm-up is
