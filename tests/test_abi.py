@@ -4,6 +4,7 @@ and NVRTC sm_100a compilation work without a device."""
 import ctypes
 import os
 import re
+import shutil
 
 import pytest
 
@@ -146,6 +147,17 @@ def test_kernel_produced_tensors_never_read_non_coherently():
             src, _ = stitch.Plan(g, "b200").codegen(mode)
             for fn, t in re.findall(r"\b(ld4c?|ld4h|ldv)\(T_(\w+)", src):
                 assert t in params, (fn, t)
+
+
+@pytest.mark.skipif(shutil.which("cuobjdump") is None, reason="cuobjdump not on PATH")
+def test_sass_no_global_write_before_pdl_wait():
+    """SASS of the generated kernels (tools/sass_pdl_check.py): no global
+    store / reduction / atomic ahead of griddepcontrol.wait (ACQBULK) in any
+    kernel, and every kernel waits"""
+    from tools.sass_pdl_check import check
+    for name in ("dien_T10", "bert_layer", "attn_softmax", "colreduce", "bert_resln"):
+        for fn, r in check(name).items():
+            assert r["waited"] and r["writes_before_wait"] == 0, (name, fn, r)
 
 
 def test_cubin_cache_warm_up(tmp_path, monkeypatch):
