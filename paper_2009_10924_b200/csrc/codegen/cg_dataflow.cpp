@@ -1555,8 +1555,12 @@ static std::string opaque_body(const CompGraph& g, int vertex, bool single, int 
   if (!single)
     s << "  if (threadIdx.x == 0) part_[blockIdx.x] = tot;\n  grid_sync(bar_, gridDim.x);\n"
       << "  __shared__ double all_;\n"
-      << "  if (threadIdx.x < 32) {\n    double t = 0.0;\n    for (int b = threadIdx.x; b < " << grid
-      << "; b += 32) t += __ldcg(part_ + b);\n    t = bfly_sum(t, 32);\n    if (threadIdx.x == 0) all_ = t;\n  }\n"
+      // every partial load issued before the first add (one L2 round trip,
+      // not grid/32 dependent ones), then the same fixed-order fold
+      << "  if (threadIdx.x < 32) {\n    double pv_[" << (grid + 31) / 32 << "];\n    #pragma unroll\n    for (int k = 0; k < "
+      << (grid + 31) / 32 << "; ++k) { const int b = threadIdx.x + 32 * k; pv_[k] = b < " << grid
+      << " ? __ldcg(part_ + b) : 0.0; }\n    double t = 0.0;\n    #pragma unroll\n    for (int k = 0; k < " << (grid + 31) / 32
+      << "; ++k) t += pv_[k];\n    t = bfly_sum(t, 32);\n    if (threadIdx.x == 0) all_ = t;\n  }\n"
       << "  __syncthreads();\n  tot = all_;\n";
   s << "  const float fill = (float)(" << (count ? "tot / " + std::to_string(count) + ".0" : "0.0") << ");\n";
   const int64_t nout = n.shape.element_count();
