@@ -56,14 +56,22 @@ __device__ __forceinline__ void stv(f16_t* p, i64 i, float v) { p[i] = f2h(v); }
 __device__ __forceinline__ void stv(int* p, i64 i, float v) { p[i] = (int)roundf(v); }
 __device__ __forceinline__ void stv(unsigned char* p, i64 i, float v) { p[i] = v != 0.f; }
 
-// 128-bit streaming load that does not allocate in L1 (read-once data)
+// 128-bit streaming load of a graph parameter that does not allocate in L1
+// (read-once data)
 __device__ __forceinline__ float4 ld4(const float* p) {
   float4 r;
 #ifdef STITCH_L2_256B
   STC_LD("ld.global.nc.L1::no_allocate.L2::256B.v4.f32 {%0,%1,%2,%3}, [%4];"
       : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
 #else
+#ifdef STITCH_PARAM_NC
   STC_LD("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+#else
+  // weak coherent load: ptxas keeps it ahead of griddepcontrol.wait where it
+  // sinks .nc loads below it (bias+GELU 16.27 -> 15.70 us, others unchanged;
+  // profiles/r01/param_load_path_ab.jsonl); STITCH_PARAM_NC restores .nc
+  STC_LD("ld.global.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+#endif
       : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
 #endif
   return r;
