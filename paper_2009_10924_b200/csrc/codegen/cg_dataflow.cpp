@@ -1589,6 +1589,17 @@ int opaque_cluster(const CompGraph& g, int vertex) {
   return static_cast<int>(std::clamp<int64_t>((units + 1023) / 1024, 1, 8));
 }
 
+// threads of a single-CTA placeholder (STITCH_OPAQUE_BLOCK, 32..1024):
+// 512 balances the load/store chain per thread against the depth of the
+// block reduction (DIEN T=10 55.3 / 53.8 / 59.6 us at 1024 / 512 / 256,
+// profiles/r01/opaque_block_ab.jsonl)
+// (1024 under the opt-in persistent template, which runs barrier-using
+// units only as whole 1024-thread CTAs)
+int opaque_block() {
+  if (env_int("STITCH_PERSIST", 0) == 1) return 1024;
+  return std::clamp(env_int("STITCH_OPAQUE_BLOCK", 512) / 32 * 32, 32, 1024);
+}
+
 bool opaque_single(const CompGraph& g, int vertex) {
   const OpNode& n = g.node(vertex);
   int64_t work = n.shape.element_count();
@@ -1604,7 +1615,7 @@ KernelSpec generate_opaque_kernel(const CompGraph& g, int vertex, const std::str
   const bool single = opaque_single(g, vertex);
   const int csize = single ? opaque_cluster(g, vertex) : 1;
   const int grid = single ? csize : kSmCount * 4;  // cooperative: 4 co-resident 256-thread CTAs per SM
-  const int block = single ? 1024 : kBlock;
+  const int block = single ? opaque_block() : kBlock;
   KernelSpec k;
   k.name = name;
   k.tmpl = single ? "opaque" : "opaque(grid)";
@@ -1649,12 +1660,13 @@ KernelSpec generate_opaque_pack(const CompGraph& g, const std::vector<int>& vert
   for (int v : vertices) csize = std::max(csize, opaque_cluster(g, v));
   k.tmpl = "opaque(pack" + std::to_string(vertices.size()) + (csize > 1 ? "x" + std::to_string(csize) : "") + ")";
   k.grid = static_cast<int>(vertices.size()) * csize;
-  k.block = 1024;
+  const int ob = opaque_block();
+  k.block = ob;
   k.cluster = csize;
   std::ostringstream sig, body;
   std::set<std::string> seen;
   int64_t bytes = 0;
-  sig << "extern \"C\" __global__ void __launch_bounds__(1024, 1) " << name << "(";
+  sig << "extern \"C\" __global__ void __launch_bounds__(" << ob << ", 1) " << name << "(";
   for (int v : vertices) {
     if (!opaque_single(g, v)) throw std::invalid_argument("opaque pack: " + g.node(v).name + " needs the grid form");
     k.pattern_key += std::string(k.pattern_key.empty() ? "" : "+") + "op:" + g.node(v).name;
@@ -1672,7 +1684,7 @@ KernelSpec generate_opaque_pack(const CompGraph& g, const std::vector<int>& vert
     bytes += n.shape.byte_size();
     body << "  " << (j ? "} else " : "") << "if (blockIdx.x / " << csize << " == " << j << ") {\n  const int bid_ = blockIdx.x % "
          << csize << ", nbid_ = " << csize << ";\n"
-         << opaque_body(g, vertices[j], true, csize, 1024, "  pdl_wait();\n", csize);
+         << opaque_body(g, vertices[j], true, csize, ob, "  pdl_wait();\n", csize);
   }
   k.source = sig.str() + ") {\n  pdl_launch();\n" + body.str() + "  }\n}\n";
   k.alg_bytes = bytes;
