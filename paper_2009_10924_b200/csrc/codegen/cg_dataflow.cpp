@@ -39,7 +39,8 @@ namespace {
 constexpr int kSmCount = 148;
 
 // When a kernel triggers its dependents (griddepcontrol.launch_dependents).
-// Default (STITCH_PDL_TRIGGER=entry): first thing in the kernel, before its
+// For large grids (STITCH_PDL_TRIGGER=entry_large, the default; =entry for
+// all): first thing in the kernel, before its
 // own griddepcontrol.wait.  The hoisted prologue issues every graph-parameter
 // load before the wait, so triggering after the wait would hold the next
 // kernel back until this one's loads have landed; at entry the dependent
@@ -49,11 +50,16 @@ constexpr int kSmCount = 148;
 // wait returns only after its producers complete, and every kernel waits
 // before it exits, so completion is transitive along chains.  =wait: trigger
 // right after the wait; =entry_small: at entry only for grids of <= 148 CTAs.
+// Default =entry_large: at entry for grids of more than 148 CTAs, after the
+// wait for smaller ones -- a chain of one-wave kernels (DIEN) does better
+// when a dependent is not parked before its own producers have finished
+// (T=10 53.8 -> 52.5 us, T=20 108.8 -> 105.3 us; profiles/r01/pdl_trigger_ab.jsonl).
 bool entry_trigger(int grid) {
   const char* v = std::getenv("STITCH_PDL_TRIGGER");
-  const std::string mode = v && *v ? v : "entry";
+  const std::string mode = v && *v ? v : "entry_large";
   if (mode == "entry") return true;
   if (mode == "entry_small") return grid <= kSmCount;
+  if (mode == "entry_large") return grid > kSmCount;
   return false;
 }
 
