@@ -72,6 +72,11 @@ int stc_plan_kernel_text(const stc_plan* p, int i, char** out);
  * plan_kernel) and expressible by a stitching template.  The plan then no
  * longer equals the reference's; plan.json / kernel texts follow it. */
 int stc_plan_refine(stc_plan* p, int* merges, int64_t* bytes_saved);
+/* the last refinement's search effort: feasibility probes spent and whether
+ * the deterministic probe budget (STITCH_REFINE_MAX_PROBES, default 2000)
+ * stopped it before convergence (the refined plan is then a prefix of the
+ * converged one -- never host-speed dependent) */
+int stc_plan_refine_info(const stc_plan* p, int64_t* probes, int* budget_hit);
 int stc_plan_stats(const stc_plan* p, int* stitched_kernels, int* baseline_kernels,
                    int64_t* delta_evaluate_calls);
 /* stitch::plan_kernel on one vertex set -> program text; rc 1 = infeasible */

@@ -27,6 +27,8 @@ struct stc_plan {
   stitch::FusionPlan plan;
   std::map<std::string, stitch::KernelPlan> kernels;
   int stitched = 0, baseline = 0;
+  int64_t refine_probes = 0;   // last stc_plan_refine: feasibility probes spent
+  int refine_budget_hit = 0;   // ... and whether STITCH_REFINE_MAX_PROBES stopped it
 };
 
 namespace stc_abi {

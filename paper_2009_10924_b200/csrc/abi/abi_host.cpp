@@ -150,7 +150,15 @@ int stc_plan_refine(stc_plan* p, int* merges, int64_t* bytes_saved) {
     p->stitched = kernel_count(p->graph, p->plan);
     if (merges) *merges = st.merges;
     if (bytes_saved) *bytes_saved = st.bytes_saved;
+    p->refine_probes = st.probes;
+    p->refine_budget_hit = st.budget_hit ? 1 : 0;
   });
+}
+
+int stc_plan_refine_info(const stc_plan* p, int64_t* probes, int* budget_hit) {
+  if (probes) *probes = p->refine_probes;
+  if (budget_hit) *budget_hit = p->refine_budget_hit;
+  return 0;
 }
 
 int stc_plan_stats(const stc_plan* p, int* stitched, int* baseline, int64_t* calls) {

@@ -110,9 +110,33 @@ int64_t algorithmic_bytes(const CompGraph& g, const std::vector<int>& vertices);
 struct RefineStats {
   int merges = 0;
   int64_t bytes_saved = 0;
+  int64_t probes = 0;       // feasibility probes (plan_kernel + codegen) spent
+  bool budget_hit = false;  // stopped by STITCH_REFINE_MAX_PROBES, not by convergence
 };
 FusionPlan refine_plan(const CompGraph& g, const FusionPlan& plan, const MachineModel& model,
                        std::map<std::string, KernelPlan>& kernels, RefineStats* stats = nullptr);
+
+// C identifier of a tensor's kernel parameter.  Graph names may contain '.'
+// (the reference parser's identifier class, src/parser.cpp:50); names without
+// one keep the readable "T_<name>", dotted names become "TX_<escaped>" with
+// '_' -> "_U" and '.' -> "_D" -- injective: the prefixes differ, and inside
+// the dotted class the escape is reversible.
+inline std::string tensor_ident(const std::string& name) {
+  if (name.find('.') == std::string::npos) return "T_" + name;
+  std::string o = "TX_";
+  for (char c : name) o += c == '_' ? std::string("_U") : c == '.' ? std::string("_D") : std::string(1, c);
+  return o;
+}
+
+// `s` as a literal inside a std::regex (ECMAScript) pattern
+inline std::string regex_escape(const std::string& s) {
+  std::string o;
+  for (char c : s) {
+    if (std::string("\\^$.|?*+()[]{}").find(c) != std::string::npos) o += '\\';
+    o += c;
+  }
+  return o;
+}
 
 // small formatting helpers shared by the generators
 std::string c_float(double v);  // exact float literal of (float)v

@@ -36,7 +36,18 @@ namespace stitch::gpu {
 
 namespace {
 
-constexpr int kSmCount = 148;
+// SMs of the device the kernels are generated for (grid sizing, one-wave
+// tests): set per generator call from the executor's device attribute;
+// 148 (B200) for device-free code generation
+thread_local int tl_sm_count = 148;
+struct SmScope {
+  int old;
+  explicit SmScope(int sm) : old(tl_sm_count) {
+    if (sm > 0) tl_sm_count = sm;
+  }
+  ~SmScope() { tl_sm_count = old; }
+};
+inline int sm_now() { return tl_sm_count; }
 
 // When a kernel triggers its dependents (griddepcontrol.launch_dependents).
 // For large grids (STITCH_PDL_TRIGGER=entry_large, the default; =entry for
@@ -58,8 +69,8 @@ bool entry_trigger(int grid) {
   const char* v = std::getenv("STITCH_PDL_TRIGGER");
   const std::string mode = v && *v ? v : "entry_large";
   if (mode == "entry") return true;
-  if (mode == "entry_small") return grid <= kSmCount;
-  if (mode == "entry_large") return grid > kSmCount;
+  if (mode == "entry_small") return grid <= sm_now();
+  if (mode == "entry_large") return grid > sm_now();
   return false;
 }
 
@@ -183,7 +194,7 @@ class Emitter {
     loaded.insert(v);
     if (!is_param(v)) ensure_wait();
     const TensorShape& sh = g_.node(v).shape;
-    const std::string ptr = "T_" + g_.node(v).name;
+    const std::string ptr = tensor_ident(g_.node(v).name);
     int nvary = 0, last_vary = -1;
     for (size_t i = 0; i < c.size(); ++i)
       if (c[i].vary) ++nvary, last_vary = static_cast<int>(i);
@@ -194,7 +205,7 @@ class Emitter {
       if (it != domain_off.end() && dd == domain_dims) {
         staged_hits.insert(v);
         if (reg_staged.count(v)) {
-          const std::string q = "cu_" + g_.node(v).name + "_" + std::to_string(domain_chunk.at(it->first));
+          const std::string q = "cu_" + tensor_ident(g_.node(v).name) + "_" + std::to_string(domain_chunk.at(it->first));
           Val r;
           for (const char* f : {".x", ".y", ".z", ".w"}) r.lanes.push_back(q + f);
           return r;
@@ -392,7 +403,7 @@ class Emitter {
           loaded.insert(data);
           if (!is_param(data)) ensure_wait();
           const std::string t = fresh("t");
-          line("const float " + t + " = " + (is_param(data) ? "ldv(T_" : "ldvk(T_") + g_.node(data).name + ", " +
+          line("const float " + t + " = " + (is_param(data) ? "ldv(" : "ldvk(") + tensor_ident(g_.node(data).name) + ", " +
                linear(data, dc, 0) + ");");
           r.lanes.push_back(t);
         }
@@ -433,6 +444,12 @@ struct Body {
   // identity).  Reductions over middle / non-contiguous axes keep the row
   // (last axis reduced) or column (last axis kept) mapping through it.
   std::vector<int> perm;
+  // row bodies only: some reductions or outputs live on another trailing
+  // domain of the same rows (O ++ J, J != the primary inner dims), e.g. a
+  // softmax over a [B,T] score row feeding [B,H] gates of the same sequence;
+  // those run as team-strided scalar loops.  tpr > 0 overrides the team size.
+  bool multi = false;
+  int tpr = 0;
 };
 
 // coordinates listed in dims_a ++ dims_b order -> tensor axis order
@@ -535,7 +552,7 @@ std::vector<std::string> decompose(Emitter& em, const std::string& lin, const st
 void store_val(Emitter& em, const CompGraph& g, int v, const Coords& c, const Val& val,
                const std::string& guard) {
   const TensorShape& sh = g.node(v).shape;
-  const std::string ptr = "T_" + g.node(v).name;
+  const std::string ptr = tensor_ident(g.node(v).name);
   int nvary = 0;
   for (const auto& x : c) nvary += x.vary;
   const std::string pre = guard.empty() ? "" : "if (" + guard + ") ";
@@ -625,7 +642,7 @@ struct StageCfg {
 
 // block = 0: the team's natural CTA (max(256, TPR)); else the kernel's CTA
 // size, a multiple of TPR
-RowParams row_params(const std::vector<int>& inner, int block = 0) {
+RowParams row_params(const std::vector<int>& inner, int block = 0, int tpr = 0) {
   const int64_t L = prod(inner);
   RowParams p;
   p.W = inner.back() % 4 == 0 ? 4 : (inner.back() % 2 == 0 ? 2 : 1);
@@ -634,7 +651,7 @@ RowParams row_params(const std::vector<int>& inner, int block = 0) {
   // row and fewer registers (2 chunks); long rows keep ~8 chunks so a team
   // stays within one warp (B200 sweep, profiles/r01/row_chunk_sweep.jsonl)
   const int nj_target = std::max(1, env_int("STITCH_ROW_NJ", nch <= 64 ? 2 : 8));
-  p.TPR = static_cast<int>(std::clamp<int64_t>(pow2ceil((nch + nj_target - 1) / nj_target), 1, 1024));
+  p.TPR = tpr > 0 ? tpr : static_cast<int>(std::clamp<int64_t>(pow2ceil((nch + nj_target - 1) / nj_target), 1, 1024));
   p.NJ = static_cast<int>((nch + p.TPR - 1) / p.TPR);
   p.block = block > 0 ? block : std::max(kBlock, p.TPR);
   p.RPB = p.block / p.TPR;
@@ -662,7 +679,7 @@ void emit_row(Emitter& em, const CompGraph& g, const std::set<int>& pat, const B
   const std::vector<int>& O = b.dims_a;
   const std::vector<int>& I = b.dims_b;
   const int64_t ROWS = prod(O), L = prod(I);
-  const RowParams rp = cluster > 1 ? cluster_row_params(I, cluster, em.block) : row_params(I, em.block);
+  const RowParams rp = cluster > 1 ? cluster_row_params(I, cluster, em.block) : row_params(I, em.block, b.tpr);
   em.W = rp.W;
   const int64_t nch = L / rp.W;
   const bool partial = nch % rp.TPR != 0;
@@ -738,7 +755,7 @@ void emit_row(Emitter& em, const CompGraph& g, const std::set<int>& pat, const B
                         std::to_string(st->tensors.size()) + "u); ";
     for (size_t k = 0; k < st->tensors.size(); ++k)
       issue += "bulk_g2s(sbuf_ + (i64)s * " + std::to_string(st->tile_floats * static_cast<int64_t>(st->tensors.size())) +
-               " + " + std::to_string(static_cast<int64_t>(k) * st->tile_floats) + ", T_" + g.node(st->tensors[k]).name +
+               " + " + std::to_string(static_cast<int64_t>(k) * st->tile_floats) + ", " + tensor_ident(g.node(st->tensors[k]).name) +
                " + r0 * " + sL + ", nb, sbar_ + s); ";
     issue += "};";
     em.line(issue);
@@ -767,9 +784,9 @@ void emit_row(Emitter& em, const CompGraph& g, const std::set<int>& pat, const B
     std::string decl = "float4", first;
     for (int v : *pipe)
       for (int j = 0; j < rp.NJ; ++j) {
-        const std::string nm = "pf_" + g.node(v).name + "_" + std::to_string(j);
+        const std::string nm = "pf_" + tensor_ident(g.node(v).name) + "_" + std::to_string(j);
         decl += std::string(decl == "float4" ? " " : ", ") + nm;
-        first += nm + " = " + (em.is_param(v) ? "ld4(T_" : "ld4k(T_") + g.node(v).name + " + r0_ * " + sL + " + " + off(j) + "); ";
+        first += nm + " = " + (em.is_param(v) ? "ld4(" : "ld4k(") + tensor_ident(g.node(v).name) + " + r0_ * " + sL + " + " + off(j) + "); ";
       }
     em.line(decl + ";");
     em.line("{ const i64 r0_ = min((i64)vbid * " + sRPB + " + team_, (i64)" + std::to_string(ROWS - 1) + "); " + first + "}");
@@ -777,9 +794,9 @@ void emit_row(Emitter& em, const CompGraph& g, const std::set<int>& pat, const B
     std::string cur = "float4", next;
     for (int v : *pipe)
       for (int j = 0; j < rp.NJ; ++j) {
-        const std::string sfx = g.node(v).name + "_" + std::to_string(j);
+        const std::string sfx = tensor_ident(g.node(v).name) + "_" + std::to_string(j);
         cur += std::string(cur == "float4" ? " " : ", ") + "cu_" + sfx + " = pf_" + sfx;
-        next += "pf_" + sfx + " = " + (em.is_param(v) ? "ld4(T_" : "ld4k(T_") + g.node(v).name + " + n_ * " + sL + " + " + off(j) + "); ";
+        next += "pf_" + sfx + " = " + (em.is_param(v) ? "ld4(" : "ld4k(") + tensor_ident(g.node(v).name) + " + n_ * " + sL + " + " + off(j) + "); ";
       }
     em.line("const " + cur + ";");
     em.line("{ const i64 n_ = rb_ + (i64)vgrid * " + sRPB + " + team_; if (n_ < " + sROWS + ") { " + next + "} }");
@@ -817,6 +834,22 @@ void emit_row(Emitter& em, const CompGraph& g, const std::set<int>& pat, const B
   }
   em.domain_dims = O;
   em.domain_dims.insert(em.domain_dims.end(), I.begin(), I.end());
+  // multi-domain rows: reductions / outputs on another trailing domain J of
+  // the same row run as a team-strided scalar loop over J
+  auto secondary = [&](const TensorShape& sh) -> std::vector<int> {
+    if (!b.multi) return {};
+    const auto d = dims_of(sh);
+    if (d == em.domain_dims || d.size() <= O.size()) return {};
+    return std::vector<int>(d.begin() + static_cast<std::ptrdiff_t>(O.size()), d.end());
+  };
+  auto open_secondary = [&](const std::vector<int>& J) {
+    const std::string q = em.fresh("q");
+    em.open("for (int " + q + " = tl_; " + q + " < " + std::to_string(prod(J)) + "; " + q + " += " +
+            std::to_string(rp.TPR) + ")");
+    Coords c = rowc;
+    for (auto& n : decompose(em, q, J, "s")) c.push_back({n, false, true});
+    return c;
+  };
   for (auto& [lvl, rs] : levels) {
     // sums: compensated f32 partials per thread (kahan_add), folded to f64
     // for the cross-thread tree; max: exact in f32
@@ -831,9 +864,18 @@ void emit_row(Emitter& em, const CompGraph& g, const std::set<int>& pat, const B
       else
         em.line("float " + acc.back() + " = __int_as_float(0xff800000);");
     }
+    std::map<std::vector<int>, std::vector<size_t>> sec_groups;
+    for (size_t i = 0; i < rs.size(); ++i)
+      if (auto J = secondary(g.node(g.node(rs[i]).operands[0]).shape); !J.empty()) sec_groups[J].push_back(i);
+    auto is_sec = [&](size_t i) {
+      for (auto& [J, idx] : sec_groups)
+        if (std::count(idx.begin(), idx.end(), i)) return true;
+      return false;
+    };
     for (int j = 0; j < rp.NJ; ++j) {
       for (size_t i = 0; i < rs.size(); ++i) {
         const int r = rs[i];
+        if (is_sec(i)) continue;
         const bool sum = g.node(r).kind == OpKind::ReduceSum;
         const Val v = em.value(g.node(r).operands[0], chunk_c[j]);
         std::string upd;
@@ -847,6 +889,17 @@ void emit_row(Emitter& em, const CompGraph& g, const std::set<int>& pat, const B
         }
         em.line((partial ? "if (" + chunk_ok[j] + ") { " : "{ ") + upd + "}");
       }
+    }
+    for (auto& [J, idx] : sec_groups) {
+      const Coords c = open_secondary(J);
+      for (size_t i : idx) {
+        const Val v = em.value(g.node(rs[i]).operands[0], c);
+        if (g.node(rs[i]).kind == OpKind::ReduceSum)
+          em.line("kahan_add(" + ks[i] + ", " + kc[i] + ", " + v.at(0) + ");");
+        else
+          em.line(acc[i] + " = op_max(" + acc[i] + ", " + v.at(0) + ");");
+      }
+      em.close();
     }
     for (size_t i = 0; i < rs.size(); ++i)
       if (!ks[i].empty()) em.line("double " + acc[i] + " = (double)" + ks[i] + " - (double)" + kc[i] + ";");
@@ -898,18 +951,28 @@ void emit_row(Emitter& em, const CompGraph& g, const std::set<int>& pat, const B
     }
   }
   // outputs
+  std::map<std::vector<int>, std::vector<int>> sec_outputs;
   for (int o : b.outputs) {
     const auto& od = g.node(o).shape.dims;
     if (static_cast<int64_t>(od.size()) == static_cast<int64_t>(O.size())) {
       const Val v = em.value(o, rowc);
       em.ensure_wait();
-      em.line("if (row_ok && tl_ == 0) stv(T_" + g.node(o).name + ", " + em.linear(o, rowc, 0) + ", " + v.at(0) + ");");
+      em.line("if (row_ok && tl_ == 0) stv(" + tensor_ident(g.node(o).name) + ", " + em.linear(o, rowc, 0) + ", " + v.at(0) + ");");
+      continue;
+    }
+    if (auto J = secondary(g.node(o).shape); !J.empty()) {
+      sec_outputs[J].push_back(o);
       continue;
     }
     for (int j = 0; j < rp.NJ; ++j) {
       const Val v = em.value(o, chunk_c[j]);
       store_val(em, g, o, chunk_c[j], v, partial ? "row_ok && " + chunk_ok[j] : "row_ok");
     }
+  }
+  for (auto& [J, outs] : sec_outputs) {
+    const Coords c = open_secondary(J);
+    for (int o : outs) store_val(em, g, o, c, em.value(o, c), "row_ok");
+    em.close();
   }
   if (st) {  // every thread is done with stage s_: refill it with tile t_ + stages
     em.line("__syncthreads();");
@@ -959,7 +1022,7 @@ ColParams col_params(const std::vector<int>& P, const std::vector<int>& C, int t
 // runs the column consumers.  Deterministic, no co-residency requirement, no
 // CTA ever waits at a barrier.
 void emit_column(Emitter& em, const CompGraph& g, const Body& b, const ColParams& cp, int64_t partial_off,
-                 int64_t ctr_off) {
+                 int64_t ctr_off, int bar_slot = 0) {
   const std::vector<int>& P = b.dims_a;
   const std::vector<int>& C = b.dims_b;
   em.W = cp.W;
@@ -1050,7 +1113,10 @@ void emit_column(Emitter& em, const CompGraph& g, const Body& b, const ColParams
   const std::string last = em.fresh("last_");
   em.line("__shared__ unsigned " + last + ";");
   if (grid_sync_mode()) {
-    em.line("grid_sync(bar_, gridDim.x);");
+    // this body's own barrier words (the scratch header's first 64 words)
+    // and its own CTA count: in a packed kernel the other bodies' CTAs never
+    // arrive here
+    em.line("grid_sync(bar_ + " + std::to_string(2 * bar_slot) + ", (unsigned)vgrid);");
     em.line("if (threadIdx.x == 0) " + last + " = rbk_ == 0;");
   } else {
     em.line("__threadfence();");
@@ -1106,7 +1172,7 @@ void emit_column(Emitter& em, const CompGraph& g, const Body& b, const ColParams
 
 KernelSpec generate_pattern_kernel(const CompGraph& g, const std::vector<int>& verts,
                                    const std::string& name, int sm_count) {
-  (void)sm_count;
+  const SmScope sm_scope(sm_count);
   const std::set<int> pat(verts.begin(), verts.end());
   std::map<int, bool> dmemo;
   std::vector<Body> bodies;
@@ -1115,6 +1181,8 @@ KernelSpec generate_pattern_kernel(const CompGraph& g, const std::vector<int>& v
       if (b.kind == nb.kind && b.dims_a == nb.dims_a && b.dims_b == nb.dims_b && b.perm == nb.perm) {
         b.outputs.insert(b.outputs.end(), nb.outputs.begin(), nb.outputs.end());
         b.reductions.insert(b.reductions.end(), nb.reductions.begin(), nb.reductions.end());
+        b.multi = b.multi || nb.multi;
+        b.tpr = std::max(b.tpr, nb.tpr);
         std::sort(b.reductions.begin(), b.reductions.end());
         return;
       }
@@ -1130,6 +1198,7 @@ KernelSpec generate_pattern_kernel(const CompGraph& g, const std::vector<int>& v
     // -> regional rows (contiguous along the last axis), kept -> global
     // columns.  Suffix / prefix axis sets are the identity layouts.
     std::vector<int> in0, axes0;
+    bool multi = false;
     for (size_t i = 0; i < comp.reductions.size(); ++i) {
       const OpNode& r = g.node(comp.reductions[i]);
       const auto in = dims_of(g.node(r.operands[0]).shape);
@@ -1138,8 +1207,36 @@ KernelSpec generate_pattern_kernel(const CompGraph& g, const std::vector<int>& v
       if (i == 0) {
         in0 = in, axes0 = axes;
       } else if (in != in0 || axes != axes0) {
-        throw TemplateMismatch("reductions of one component disagree on their split");
+        multi = true;
       }
+    }
+    if (multi) {
+      // rows of one split, several trailing domains: every reduction must
+      // reduce a suffix of its operand's axes with the same kept prefix O;
+      // the largest trailing domain is the primary one
+      auto suffix_split = [&](int r, std::vector<int>& O, std::vector<int>& I) {
+        const OpNode& n = g.node(r);
+        const auto in = dims_of(g.node(n.operands[0]).shape);
+        std::set<int> ax(n.attrs.axes.begin(), n.attrs.axes.end());
+        const int k = static_cast<int>(in.size()) - static_cast<int>(ax.size());
+        for (int a = 0; a < static_cast<int>(in.size()); ++a)
+          if (ax.count(a) != (a >= k ? 1u : 0u)) return false;
+        O.assign(in.begin(), in.begin() + k);
+        I.assign(in.begin() + k, in.end());
+        return !I.empty();
+      };
+      std::vector<int> O0, Ibest;
+      for (size_t i = 0; i < comp.reductions.size(); ++i) {
+        std::vector<int> O, I;
+        if (!suffix_split(comp.reductions[i], O, I)) throw TemplateMismatch("reductions of one component disagree on their split");
+        if (i == 0) O0 = O;
+        if (O != O0) throw TemplateMismatch("reductions of one component disagree on their rows");
+        if (Ibest.empty() || prod(I) > prod(Ibest)) Ibest = I;
+      }
+      in0 = O0;
+      in0.insert(in0.end(), Ibest.begin(), Ibest.end());
+      axes0.clear();
+      for (size_t a = O0.size(); a < in0.size(); ++a) axes0.push_back(static_cast<int>(a));
     }
     const int n = static_cast<int>(in0.size());
     std::vector<int> kept, red;
@@ -1158,8 +1255,14 @@ KernelSpec generate_pattern_kernel(const CompGraph& g, const std::vector<int>& v
     for (int a = 0; a < n; ++a) identity = identity && body.perm[static_cast<size_t>(a)] == a;
     if (identity) body.perm.clear();
     if (body.kind == Kind::Column && body.dims_b.empty()) throw TemplateMismatch("column body without kept axes");
+    if (multi && !identity) throw TemplateMismatch("multi-domain rows need trailing reductions");
     const std::vector<int>& full = in0;  // operand shape, tensor axis order
     const std::vector<int>& unit = body.kind == Kind::Row ? body.dims_a : body.dims_b;
+    // row-aligned: dims = O ++ J for another trailing domain J of the same rows
+    auto row_aligned = [&](const std::vector<int>& od) {
+      return body.kind == Kind::Row && identity && od.size() > body.dims_a.size() &&
+             std::equal(body.dims_a.begin(), body.dims_a.end(), od.begin());
+    };
     for (int o : comp.outputs) {
       const auto od = dims_of(g.node(o).shape);
       const bool dep = downstream_of_reduction(g, pat, o, dmemo);
@@ -1169,9 +1272,26 @@ KernelSpec generate_pattern_kernel(const CompGraph& g, const std::vector<int>& v
         body.outputs.push_back(o);
       } else if (!dep) {
         add_body({Kind::Local, od, {}, {o}, {}});
+      } else if (row_aligned(od)) {
+        body.outputs.push_back(o);
+        multi = true;
       } else {
         throw TemplateMismatch("output " + g.node(o).name + " does not fit the reduction domain");
       }
+    }
+    if (multi) {
+      // team size: enough lanes for the widest domain (scalar elements on
+      // the secondary ones), within one warp so team reductions stay shuffles
+      const int64_t rows = std::max<int64_t>(1, prod(body.dims_a));
+      int64_t widest = prod(body.dims_b) / row_params(body.dims_b).W;
+      auto widen = [&](const TensorShape& sh) {
+        if (dims_of(sh) != full && dims_of(sh) != unit) widest = std::max<int64_t>(widest, sh.element_count() / rows);
+      };
+      for (int r : body.reductions) widen(g.node(g.node(r).operands[0]).shape);
+      for (int o : body.outputs) widen(g.node(o).shape);
+      body.multi = true;
+      body.tpr = static_cast<int>(std::clamp<int64_t>(pow2ceil(widest), row_params(body.dims_b).TPR, 32));
+      if (row_params(body.dims_b).TPR > 32) body.tpr = 0;
     }
     add_body(std::move(body));
   }
@@ -1195,7 +1315,7 @@ KernelSpec generate_pattern_kernel(const CompGraph& g, const std::vector<int>& v
   bool has_col = false;
   for (const auto& b : bodies) {
     has_col = has_col || b.kind == Kind::Column;
-    if (b.kind == Kind::Row) max_tpr = std::max(max_tpr, row_params(b.dims_b).TPR);
+    if (b.kind == Kind::Row) max_tpr = std::max(max_tpr, row_params(b.dims_b, 0, b.tpr).TPR);
   }
   block = std::max(block, max_tpr);
   // long rows (a warp or more per row) stream through a register pipeline
@@ -1206,7 +1326,9 @@ KernelSpec generate_pattern_kernel(const CompGraph& g, const std::vector<int>& v
   // (a kernel that packs other bodies keeps small 2-team CTAs and no
   // pipeline: its register allocation is shared with those bodies -- bias+GELU
   // packed with residual+LN runs 23 us that way vs 36 us pipelined)
-  const bool long_rows = max_tpr >= 32 && !has_col;
+  bool any_multi = false;
+  for (const auto& b : bodies) any_multi = any_multi || b.multi;
+  const bool long_rows = max_tpr >= 32 && !has_col && !any_multi;
   const bool single_row_body = long_rows && bodies.size() == 1;
   if (long_rows) block = std::min(1024, single_row_body ? std::max(256, 2 * max_tpr) : 2 * max_tpr);
   if (single_row_body && max_tpr == 32) {
@@ -1234,7 +1356,7 @@ KernelSpec generate_pattern_kernel(const CompGraph& g, const std::vector<int>& v
     // SM gets the same number of rows (+-1)
     const int64_t rows = prod(bodies[0].dims_a);
     for (int64_t k = 1; k <= 32; ++k) {
-      const int64_t rpc = (rows + kSmCount * k - 1) / (kSmCount * k);
+      const int64_t rpc = (rows + sm_now() * k - 1) / (sm_now() * k);
       if (rpc * max_tpr <= 1024) {
         block = static_cast<int>(std::max<int64_t>(32, rpc * max_tpr));
         break;
@@ -1246,13 +1368,13 @@ KernelSpec generate_pattern_kernel(const CompGraph& g, const std::vector<int>& v
   // thread-block cluster (<= 16 CTAs, DSMEM team reduction) so ROWS x C CTAs
   // share the row stream
   int cluster = 1;
-  if (bodies.size() == 1 && bodies[0].kind == Kind::Row && env_int("STITCH_ROW_CLUSTER", 1) != 0) {
-    const RowParams rp = row_params(bodies[0].dims_b, block);
+  if (bodies.size() == 1 && bodies[0].kind == Kind::Row && !bodies[0].multi && env_int("STITCH_ROW_CLUSTER", 1) != 0) {
+    const RowParams rp = row_params(bodies[0].dims_b, block, bodies[0].tpr);
     const int64_t rows = prod(bodies[0].dims_a), nch = prod(bodies[0].dims_b) / rp.W;
     const int64_t ntiles = (rows + rp.RPB - 1) / rp.RPB;
-    if (ntiles < kSmCount && nch >= 512) {
+    if (ntiles < sm_now() && nch >= 512) {
       int c = 2;
-      while (c < 16 && rows * c < 2 * kSmCount) c *= 2;
+      while (c < 16 && rows * c < 2 * sm_now()) c *= 2;
       const int b2 = static_cast<int>(std::clamp<int64_t>(pow2ceil((nch + int64_t(c) * 4 - 1) / (int64_t(c) * 4)), 128, 1024));
       if ((nch + int64_t(c) * b2 - 1) / (int64_t(c) * b2) <= 16 && int64_t(c) * b2 <= nch) {
         cluster = c;
@@ -1278,20 +1400,20 @@ KernelSpec generate_pattern_kernel(const CompGraph& g, const std::vector<int>& v
       const int64_t chunks = N / w;
       const int U = local_small(N) ? 1 : local_unroll(chunks, block);
       b.blocks = static_cast<int>(std::clamp<int64_t>((chunks + int64_t(block) * U - 1) / (int64_t(block) * U), 1,
-                                                      int64_t(kSmCount) * env_int("STITCH_LOCAL_CTAS", 32)));
+                                                      int64_t(sm_now()) * env_int("STITCH_LOCAL_CTAS", 32)));
     } else if (b.kind == Kind::Row && cluster > 1) {
       const int64_t rows = prod(b.dims_a);
-      b.blocks = static_cast<int>(std::min<int64_t>(rows, std::max<int64_t>(1, 4 * kSmCount / cluster)) * cluster);
+      b.blocks = static_cast<int>(std::min<int64_t>(rows, std::max<int64_t>(1, 4 * sm_now() / cluster)) * cluster);
     } else if (b.kind == Kind::Row) {
-      const RowParams rp = row_params(b.dims_b, block);
+      const RowParams rp = row_params(b.dims_b, block, b.tpr);
       const int64_t rows = prod(b.dims_a), L = prod(b.dims_b), ntiles = (rows + rp.RPB - 1) / rp.RPB;
-      b.blocks = static_cast<int>(std::clamp<int64_t>(ntiles, 1, int64_t(kSmCount) * env_int("STITCH_ROW_CTAS", 16)));
+      b.blocks = static_cast<int>(std::clamp<int64_t>(ntiles, 1, int64_t(sm_now()) * env_int("STITCH_ROW_CTAS", 16)));
       // dry run: which inputs does the body read at its own (row, chunk)
       // coordinates?  Those can be streamed a row ahead in registers
       // (default, STITCH_ROW_PIPE >= 2 rows per team) or through the opt-in
       // TMA pipeline (STITCH_STAGE=1: measured slower)
       const int pipe_rows = env_int("STITCH_ROW_PIPE", single_row_body ? 2 : 1);
-      if ((env_int("STITCH_STAGE", 0) || pipe_rows > 1) && rp.W == 4 && cluster == 1) {
+      if ((env_int("STITCH_STAGE", 0) || pipe_rows > 1) && rp.W == 4 && cluster == 1 && !b.multi) {
         em.out.str("");
         em.clear_memo();
         em.reduced.clear();
@@ -1309,7 +1431,7 @@ KernelSpec generate_pattern_kernel(const CompGraph& g, const std::vector<int>& v
         if (!hits.empty() && !env_int("STITCH_STAGE", 0) && pipe_ok) {
           pipe[i] = hits;
           b.blocks = static_cast<int>(std::clamp<int64_t>((ntiles + pipe_rows - 1) / pipe_rows, 1,
-                                                          int64_t(kSmCount) * env_int("STITCH_ROW_CTAS", 16)));
+                                                          int64_t(sm_now()) * env_int("STITCH_ROW_CTAS", 16)));
         } else if (!hits.empty() && env_int("STITCH_STAGE", 0)) {
           StageCfg& sc = stage[i];
           sc.tensors = hits;
@@ -1323,7 +1445,7 @@ KernelSpec generate_pattern_kernel(const CompGraph& g, const std::vector<int>& v
           sc.bytes = 128 + int64_t(sc.stages) * static_cast<int64_t>(hits.size()) * sc.tile_floats * 4;
           if (sc.bytes <= 200 * 1024) {
             const int64_t fit = std::clamp<int64_t>(int64_t(220 * 1024) / sc.bytes, 1, 2048 / rp.block);
-            b.blocks = static_cast<int>(std::min<int64_t>(ntiles, kSmCount * fit));
+            b.blocks = static_cast<int>(std::min<int64_t>(ntiles, sm_now() * fit));
             dyn_smem = std::max(dyn_smem, sc.bytes);
           } else {
             sc.tensors.clear();  // a tile set this large would starve occupancy: stay in registers
@@ -1331,7 +1453,7 @@ KernelSpec generate_pattern_kernel(const CompGraph& g, const std::vector<int>& v
         }
       }
     } else {
-      cps[i] = col_params(b.dims_a, b.dims_b, kSmCount * per_sm, block);
+      cps[i] = col_params(b.dims_a, b.dims_b, sm_now() * per_sm, block);
       b.blocks = cps[i].NCB * cps[i].RB;
       ctr_off[i] = ctr_words;
       ctr_words += cps[i].NCB;
@@ -1342,7 +1464,7 @@ KernelSpec generate_pattern_kernel(const CompGraph& g, const std::vector<int>& v
   const int64_t header = ((ctr_words * 4 + 255) / 256) * 256;
 
   std::ostringstream body_src;
-  int start = 0;
+  int start = 0, col_slot = 0;
   const bool interleave = bodies.size() > 1 && env_int("STITCH_INTERLEAVE", 0) != 0;
   for (size_t i = 0; i < bodies.size(); ++i) {
     const Body& b = bodies[i];
@@ -1355,7 +1477,7 @@ KernelSpec generate_pattern_kernel(const CompGraph& g, const std::vector<int>& v
     else if (b.kind == Kind::Row)
       emit_row(em, g, pat, b, stage[i].tensors.empty() ? nullptr : &stage[i], pipe[i].empty() ? nullptr : &pipe[i],
                cluster);
-    else emit_column(em, g, b, cps[i], part_off[i], ctr_off[i]);
+    else emit_column(em, g, b, cps[i], part_off[i], ctr_off[i], col_slot++);
     em.ensure_wait();  // every path waits before the CTA retires
     if (interleave) {
       body_src << "  " << (i ? "else " : "") << "if (body_ == " << i << ") {\n";
@@ -1420,12 +1542,12 @@ KernelSpec generate_pattern_kernel(const CompGraph& g, const std::vector<int>& v
       << ") " << name << "(";
   bool first = true;
   for (int v : em.loaded) {
-    sig << (first ? "" : ", ") << "const " << c_type(g.node(v).shape.dtype) << "* __restrict__ T_" << g.node(v).name;
+    sig << (first ? "" : ", ") << "const " << c_type(g.node(v).shape.dtype) << "* __restrict__ " << tensor_ident(g.node(v).name);
     first = false;
     k.inputs.push_back(g.node(v).name);
   }
   for (int v : outs) {
-    sig << (first ? "" : ", ") << c_type(g.node(v).shape.dtype) << "* __restrict__ T_" << g.node(v).name;
+    sig << (first ? "" : ", ") << c_type(g.node(v).shape.dtype) << "* __restrict__ " << tensor_ident(g.node(v).name);
     first = false;
     k.outputs.push_back(g.node(v).name);
   }
@@ -1492,22 +1614,22 @@ static std::string opaque_body(const CompGraph& g, int vertex, bool single, int 
       const std::string a = "v" + std::to_string(vi++) + "_";
       if (K > 8) {  // large operand: vectorised grid-stride loop
         if (vec)
-          s << "  for (i64 i = (i64)bid_ * " << block << " + threadIdx.x; i < " << units << "; i += " << span << ") { const float4 q = " << L4 << "T_"
-            << g.node(o).name << " + 4 * i); acc += ((double)q.x + (double)q.y) + ((double)q.z + (double)q.w); }\n";
+          s << "  for (i64 i = (i64)bid_ * " << block << " + threadIdx.x; i < " << units << "; i += " << span << ") { const float4 q = " << L4
+            << tensor_ident(g.node(o).name) << " + 4 * i); acc += ((double)q.x + (double)q.y) + ((double)q.z + (double)q.w); }\n";
         else
-          s << "  for (i64 i = (i64)bid_ * " << block << " + threadIdx.x; i < " << units << "; i += " << span << ") acc += (double)" << LV << "T_"
-            << g.node(o).name << ", i);\n";
+          s << "  for (i64 i = (i64)bid_ * " << block << " + threadIdx.x; i < " << units << "; i += " << span << ") acc += (double)" << LV
+            << tensor_ident(g.node(o).name) << ", i);\n";
         continue;
       }
       if (vec) {
         s << "  float4 " << a << "[" << K << "];\n  #pragma unroll\n  for (int k = 0; k < " << K
           << "; ++k) { const i64 i = (i64)bid_ * " << block << " + threadIdx.x + (i64)k * " << span << "; " << a << "[k] = i < " << units
-          << " ? " << L4 << "T_" << g.node(o).name << " + 4 * i) : make_float4(0.f, 0.f, 0.f, 0.f); }\n";
+          << " ? " << L4 << tensor_ident(g.node(o).name) << " + 4 * i) : make_float4(0.f, 0.f, 0.f, 0.f); }\n";
         regs.push_back({a, 4});
       } else {
         s << "  float " << a << "[" << K << "];\n  #pragma unroll\n  for (int k = 0; k < " << K
           << "; ++k) { const i64 i = (i64)bid_ * " << block << " + threadIdx.x + (i64)k * " << span << "; " << a << "[k] = i < " << units
-          << " ? " << LV << "T_" << g.node(o).name << ", i) : 0.f; }\n";
+          << " ? " << LV << tensor_ident(g.node(o).name) << ", i) : 0.f; }\n";
         regs.push_back({a, 1});
       }
      }
@@ -1529,7 +1651,7 @@ static std::string opaque_body(const CompGraph& g, int vertex, bool single, int 
     for (int o : n.operands) {
       const TensorShape& sh = g.node(o).shape;
       const int64_t cnt = sh.element_count();
-      const std::string T = "T_" + g.node(o).name;
+      const std::string T = tensor_ident(g.node(o).name);
       const bool param = g.node(o).kind == OpKind::Parameter;
       const std::string L4 = param ? "ld4(" : "ld4k(", LV = param ? "ldv(" : "ldvk(";
       if (sh.dtype == DType::F32 && cnt % 4 == 0) {
@@ -1572,10 +1694,10 @@ static std::string opaque_body(const CompGraph& g, int vertex, bool single, int 
   const int64_t nout = n.shape.element_count();
   if (n.shape.dtype == DType::F32 && nout % 4 == 0)  // 128-bit stores
     s << "  for (i64 i = (i64)bid_ * blockDim.x + threadIdx.x; i < " << nout / 4
-      << "; i += (i64)nbid_ * blockDim.x) st4(T_" << n.name << " + 4 * i, fill, fill, fill, fill);\n";
+      << "; i += (i64)nbid_ * blockDim.x) st4(" << tensor_ident(n.name) << " + 4 * i, fill, fill, fill, fill);\n";
   else
     s << "  for (i64 i = (i64)bid_ * blockDim.x + threadIdx.x; i < " << nout
-      << "; i += (i64)nbid_ * blockDim.x) stv(T_" << n.name << ", i, fill);\n";
+      << "; i += (i64)nbid_ * blockDim.x) stv(" << tensor_ident(n.name) << ", i, fill);\n";
   return s.str();
 }
 
@@ -1613,14 +1735,15 @@ bool opaque_single(const CompGraph& g, int vertex) {
   return work <= (int64_t(1) << 20);
 }
 
-KernelSpec generate_opaque_kernel(const CompGraph& g, int vertex, const std::string& name, int) {
+KernelSpec generate_opaque_kernel(const CompGraph& g, int vertex, const std::string& name, int sm_count) {
+  const SmScope sm_scope(sm_count);
   const OpNode& n = g.node(vertex);
   std::set<int> ops(n.operands.begin(), n.operands.end());
   // small tensors (e.g. DIEN's [256,36] GEMM outputs): one 1024-thread CTA,
   // no grid-wide barrier; large ones: cooperative grid with a barrier
   const bool single = opaque_single(g, vertex);
   const int csize = single ? opaque_cluster(g, vertex) : 1;
-  const int grid = single ? csize : kSmCount * 4;  // cooperative: 4 co-resident 256-thread CTAs per SM
+  const int grid = single ? csize : sm_now() * 4;  // cooperative: 4 co-resident 256-thread CTAs per SM
   const int block = single ? opaque_block() : kBlock;
   KernelSpec k;
   k.name = name;
@@ -1634,10 +1757,10 @@ KernelSpec generate_opaque_kernel(const CompGraph& g, int vertex, const std::str
   std::ostringstream s;
   s << "extern \"C\" __global__ void __launch_bounds__(" << block << ", " << (single ? 1 : 4) << ") " << name << "(";
   for (int o : ops) {
-    s << "const " << c_type(g.node(o).shape.dtype) << "* __restrict__ T_" << g.node(o).name << ", ";
+    s << "const " << c_type(g.node(o).shape.dtype) << "* __restrict__ " << tensor_ident(g.node(o).name) << ", ";
     k.inputs.push_back(g.node(o).name);
   }
-  s << c_type(n.shape.dtype) << "* __restrict__ T_" << n.name;
+  s << c_type(n.shape.dtype) << "* __restrict__ " << tensor_ident(n.name);
   if (!single) {
     s << ", unsigned* __restrict__ bar_, double* __restrict__ part_";
     k.scratch_bytes = 256 + int64_t(grid) * 8;
@@ -1669,6 +1792,7 @@ KernelSpec generate_opaque_pack(const CompGraph& g, const std::vector<int>& vert
   const int ob = opaque_block();
   k.block = ob;
   k.cluster = csize;
+  const bool early = env_int("STITCH_OPAQUE_EARLY", 1) != 0;
   std::ostringstream sig, body;
   std::set<std::string> seen;
   int64_t bytes = 0;
@@ -1678,21 +1802,25 @@ KernelSpec generate_opaque_pack(const CompGraph& g, const std::vector<int>& vert
     k.pattern_key += std::string(k.pattern_key.empty() ? "" : "+") + "op:" + g.node(v).name;
     for (int o : g.node(v).operands)
       if (seen.insert(g.node(o).name).second) {
-        sig << "const " << c_type(g.node(o).shape.dtype) << "* __restrict__ T_" << g.node(o).name << ", ";
+        sig << "const " << c_type(g.node(o).shape.dtype) << "* __restrict__ " << tensor_ident(g.node(o).name) << ", ";
         k.inputs.push_back(g.node(o).name);
         bytes += g.node(o).shape.byte_size();
       }
   }
   for (size_t j = 0; j < vertices.size(); ++j) {
     const OpNode& n = g.node(vertices[j]);
-    sig << (j ? ", " : "") << c_type(n.shape.dtype) << "* __restrict__ T_" << n.name;
+    sig << (j ? ", " : "") << c_type(n.shape.dtype) << "* __restrict__ " << tensor_ident(n.name);
     k.outputs.push_back(n.name);
     bytes += n.shape.byte_size();
     body << "  " << (j ? "} else " : "") << "if (blockIdx.x / " << csize << " == " << j << ") {\n  const int bid_ = blockIdx.x % "
          << csize << ", nbid_ = " << csize << ";\n"
-         << opaque_body(g, vertices[j], true, csize, ob, "  pdl_wait();\n", csize);
+         << opaque_body(g, vertices[j], true, csize, ob, early ? "  pdl_wait();\n  pdl_launch();\n" : "  pdl_wait();\n",
+                        csize);
   }
-  k.source = sig.str() + ") {\n  pdl_launch();\n" + body.str() + "  }\n}\n";
+  // dependents are triggered like a single placeholder's (entry_trigger:
+  // after the wait for a one-wave pack under the default entry_large)
+  k.source = sig.str() + ") {\n" + (entry_trigger(k.grid) ? "  pdl_launch();\n" : "") + body.str() +
+             "  }\n  pdl_launch();\n}\n";
   k.alg_bytes = bytes;
   return k;
 }

@@ -57,7 +57,7 @@ std::string as_unit_function(const KernelSpec& k, const std::string& fn) {
   int pi = 0;
   for (const auto* list : {&k.inputs, &k.outputs})
     for (const auto& t : *list)
-      body = std::regex_replace(body, std::regex("\\bT_" + t + "\\b"), "p" + std::to_string(pi++) + "_");
+      body = std::regex_replace(body, std::regex("\\b" + regex_escape(tensor_ident(t)) + "\\b"), "p" + std::to_string(pi++) + "_");
   const size_t close = body.find(") {\n");
   if (close == std::string::npos) throw std::invalid_argument("persistent: no signature end in " + k.name);
   body.insert(close, ", const int vb_, const int vg_, const int vt_");
@@ -120,7 +120,7 @@ std::optional<KernelSpec> generate_persistent_kernel(const std::vector<KernelSpe
   // parameter types come from the unit signatures ("const T* T_name")
   auto type_of = [&](const std::string& t) {
     for (const auto& k : units) {
-      const std::string key = "* __restrict__ T_" + t;
+      const std::string key = "* __restrict__ " + tensor_ident(t);
       for (size_t at = k.source.find(key); at != std::string::npos; at = k.source.find(key, at + 1)) {
         const char c = at + key.size() < k.source.size() ? k.source[at + key.size()] : ',';
         if (c != ',' && c != ')') continue;  // a longer name with this prefix
@@ -160,11 +160,11 @@ std::optional<KernelSpec> generate_persistent_kernel(const std::vector<KernelSpe
   s << "extern \"C\" __global__ void __launch_bounds__(1024, 1) " << name << "(";
   bool first = true;
   for (const auto& t : ins) {
-    s << (first ? "" : ", ") << "const " << type_of(t) << "* T_" << t;
+    s << (first ? "" : ", ") << "const " << type_of(t) << "* " << tensor_ident(t);
     first = false;
   }
   for (const auto& t : writes) {
-    s << (first ? "" : ", ") << type_of(t) << "* T_" << t;
+    s << (first ? "" : ", ") << type_of(t) << "* " << tensor_ident(t);
     first = false;
   }
   // CTA c takes part in unit u iff it owns one of u's virtual CTAs
@@ -194,7 +194,7 @@ std::optional<KernelSpec> generate_persistent_kernel(const std::vector<KernelSpe
       const int64_t bytes = tensor_bytes(t);
       s << "  for (i64 o_ = ((i64)blockIdx.x * 1024 + threadIdx.x) * 128; o_ < " << bytes
         << "; o_ += (i64)gridDim.x * 1024 * 128) "
-        << (touch ? "touch_l2((const char*)T_" : "prefetch_l2((const char*)T_") << t << " + o_);\n";
+        << (touch ? "touch_l2((const char*)" : "prefetch_l2((const char*)") << tensor_ident(t) << " + o_);\n";
     }
   }
   for (int u = 0; u < U; ++u) {
@@ -214,8 +214,8 @@ std::optional<KernelSpec> generate_persistent_kernel(const std::vector<KernelSpe
                                                        std::to_string(ku.block) + ")"
                                                  : "")
       << "; v < " << ku.grid << "; v += " << parts[static_cast<size_t>(u)] * per << ") " << fn[static_cast<size_t>(u)] << "(";
-    for (const auto& t : ku.inputs) s << "T_" << t << ", ";
-    for (const auto& t : ku.outputs) s << "T_" << t << ", ";
+    for (const auto& t : ku.inputs) s << tensor_ident(t) << ", ";
+    for (const auto& t : ku.outputs) s << tensor_ident(t) << ", ";
     s << "v, " << ku.grid << ", (int)(threadIdx.x" << (per > 1 ? " % " + std::to_string(ku.block) : "") << "));\n";
     s << "    __syncthreads();\n    STC_TRACE_STAMP_END(" << 1 + u << ");\n    if (threadIdx.x == 0) red_release_add_u32(bar_ + "
       << 1 + u << ", 1u);\n  }\n";

@@ -12,6 +12,7 @@
 #include <cmath>
 #include <cstdio>
 #include <map>
+#include <memory>
 #include <set>
 #include <sstream>
 
@@ -94,7 +95,7 @@ class ProgramTranslator {
   }
 
  private:
-  static std::string tname(const std::string& n) { return "T_" + n; }
+  static std::string tname(const std::string& n) { return tensor_ident(n); }
 
   int64_t count_of(const std::string& tensor) const {
     for (const auto& b : p_.inputs)
@@ -255,9 +256,64 @@ class ProgramTranslator {
 
 }  // namespace
 
+namespace {
+// Register names derived from graph names (buf_<vertex>) may contain '.'
+// (src/parser.cpp:50): rename them to C identifiers before translation.
+// Names with a '.' get the prefix "R_" (the planner's own register names are
+// t<N> / i<N> / acc<N> / buf_<name> / loop variables, none starting "R_")
+// and '_' -> "_U", '.' -> "_D", so the renaming is injective.
+std::string reg_ident(const std::string& n) {
+  if (n.find('.') == std::string::npos) return n;
+  std::string o = "R_";
+  for (char c : n) o += c == '_' ? std::string("_U") : c == '.' ? std::string("_D") : std::string(1, c);
+  return o;
+}
+
+ExprP rename_expr(const ExprP& e) {
+  if (!e) return e;
+  if ((e->kind == Expr::Var || e->kind == Expr::Reg) && e->name.find('.') == std::string::npos && !e->a && !e->b)
+    return e;
+  auto c = std::make_shared<Expr>(*e);
+  if (c->kind == Expr::Var || c->kind == Expr::Reg) c->name = reg_ident(c->name);
+  c->a = rename_expr(e->a);
+  c->b = rename_expr(e->b);
+  return c;
+}
+
+BExprP rename_bexpr(const BExprP& e) {
+  if (!e) return e;
+  auto c = std::make_shared<BExpr>(*e);
+  c->lhs = rename_expr(e->lhs);
+  c->rhs = rename_expr(e->rhs);
+  c->a = rename_bexpr(e->a);
+  c->b = rename_bexpr(e->b);
+  return c;
+}
+
+bool needs_rename(const StitchedProgram& p) {
+  for (const auto& s : p.stmts) {
+    if (s.dst.find('.') != std::string::npos || s.loop_var.find('.') != std::string::npos) return true;
+    for (const auto& x : s.srcs)
+      if (x.find('.') != std::string::npos) return true;
+  }
+  return false;
+}
+}  // namespace
+
 KernelSpec generate_program_kernel(const CompGraph& g, const StitchedProgram& prog,
                                    const std::string& name, bool checked) {
-  return ProgramTranslator(g, prog, checked).run(name);
+  if (!needs_rename(prog)) return ProgramTranslator(g, prog, checked).run(name);
+  StitchedProgram p = prog;
+  for (auto& s : p.stmts) {
+    s.dst = reg_ident(s.dst);
+    s.loop_var = reg_ident(s.loop_var);
+    for (auto& x : s.srcs) x = reg_ident(x);
+    s.dst_slot = rename_expr(s.dst_slot);
+    s.src_slot = rename_expr(s.src_slot);
+    s.idx = rename_expr(s.idx);
+    s.guard = rename_bexpr(s.guard);
+  }
+  return ProgramTranslator(g, p, checked).run(name);
 }
 
 }  // namespace stitch::gpu

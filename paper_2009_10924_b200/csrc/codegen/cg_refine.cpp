@@ -61,17 +61,17 @@ FusionPlan refine_plan(const CompGraph& g, const FusionPlan& plan, const Machine
   const auto cons = g.consumer_lists();
   std::map<std::vector<int>, bool> feasible_memo;
   // plan_kernel is the expensive part (the reference emitter on the merged
-  // pattern): bound the merged size and the total planning time
-  const char* bs = std::getenv("STITCH_REFINE_BUDGET_S");
-  const double budget_s = bs && *bs ? std::atof(bs) : 20.0;
+  // pattern): bound the merged size and the number of feasibility probes --
+  // a count, not a clock, so the refined plan never depends on host speed
+  const char* bs = std::getenv("STITCH_REFINE_MAX_PROBES");
+  const int64_t max_probes = bs && *bs ? std::atoll(bs) : 2000;
   const char* ms = std::getenv("STITCH_REFINE_MAX_VERTS");
   const int max_verts = std::min(model.search.max_pattern_size, ms && *ms ? std::atoi(ms) : 64);
-  const auto t0 = std::chrono::steady_clock::now();
-  auto out_of_time = [&] {
-    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > budget_s;
-  };
+  RefineStats st;
+  auto out_of_time = [&] { return st.probes >= max_probes; };
   auto feasible = [&](const std::vector<int>& verts) {
     if (auto it = feasible_memo.find(verts); it != feasible_memo.end()) return it->second;
+    ++st.probes;
     bool ok = static_cast<int>(verts.size()) <= max_verts;
     FusionPattern p;
     p.vertices = verts;
@@ -92,7 +92,6 @@ FusionPlan refine_plan(const CompGraph& g, const FusionPlan& plan, const Machine
     feasible_memo[verts] = ok;
     return ok;
   };
-  RefineStats st;
   while (!out_of_time()) {
     // candidate merges: (producer unit, consumer unit) pairs along graph edges
     struct Cand {
@@ -155,6 +154,7 @@ FusionPlan refine_plan(const CompGraph& g, const FusionPlan& plan, const Machine
   }
   std::sort(out.patterns.begin(), out.patterns.end(),
             [](const FusionPattern& x, const FusionPattern& y) { return x.vertices.front() < y.vertices.front(); });
+  st.budget_hit = out_of_time();
   if (stats) *stats = st;
   return out;
 }

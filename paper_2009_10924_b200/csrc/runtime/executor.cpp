@@ -481,7 +481,7 @@ PlanKernels generate_plan_kernels(const CompGraph& g_, const FusionPlan& plan,
       opaque_vertex[specs_.size() - 1] = un.verts[0];
     } else {
       add_pattern(un.verts, un.key);
-      if (specs_.back().tmpl == "local") local_verts[specs_.size() - 1] = un.verts;
+      if (specs_.back().tmpl == "local" || specs_.back().tmpl == "regional") local_verts[specs_.size() - 1] = un.verts;
     }
     for (int w : users[static_cast<size_t>(u)])
       if (--pending[static_cast<size_t>(w)] == 0) ready.insert({units[static_cast<size_t>(w)].fire, w});
@@ -492,8 +492,10 @@ PlanKernels generate_plan_kernels(const CompGraph& g_, const FusionPlan& plan,
   //  * small opaque placeholders (DIEN's three gate GEMMs of a step read only
   //    the previous step's state; its per-step x.W GEMMs only parameters):
   //    one 1024-thread CTA per op (generate_opaque_pack);
-  //  * local-template (elementwise) patterns: the independent template packs
-  //    their bodies into disjoint CTA ranges, each body the code it has alone.
+  //  * local- and regional-template patterns: the independent template packs
+  //    their bodies into disjoint CTA ranges (bodies over the same domain
+  //    merge, e.g. DIEN's per-step attention-column squeezes become one row
+  //    body with one reduction per step).
   // On a launch-bound chain a set then follows its producer as one same-lane
   // PDL edge instead of fanning out over lanes whose cross-lane edges only
   // resolve at completion (profiles/r01/pdl_edge_probe.jsonl).  The plan
@@ -503,7 +505,13 @@ PlanKernels generate_plan_kernels(const CompGraph& g_, const FusionPlan& plan,
   const char* lpack_env = std::getenv("STITCH_LOCAL_PACK");
   const bool pack_opaque = !(pack_env && *pack_env == '0');
   const bool pack_local = !(lpack_env && *lpack_env == '0');
-  if ((pack_opaque && !opaque_vertex.empty()) || (pack_local && local_verts.size() > 1)) {
+  // Packing repeats until nothing changes: once a set of units is one
+  // launch, their consumers may share that launch as their only producer
+  // (DIEN: the per-step attention-column slices pack first, then the
+  // squeezes that read them).
+  for (int round = 0; round < 8; ++round) {
+  if (!((pack_opaque && !opaque_vertex.empty()) || (pack_local && local_verts.size() > 1))) break;
+  {
     std::map<std::string, size_t> prod;
     // (kind, producer set) -> member specs; kind 0 opaque (+ its cluster size:
     // a pack launches one uniform cluster per op), 1 local
@@ -519,6 +527,7 @@ PlanKernels generate_plan_kernels(const CompGraph& g_, const FusionPlan& plan,
       for (const auto& t : specs_[i].outputs) prod[t] = i;
     }
     std::map<size_t, KernelSpec> packs;  // placed at the first member's position
+    std::map<size_t, std::vector<size_t>> pack_members;
     std::set<size_t> drop;
     for (auto& [kd, members] : groups)
       for (size_t at = 0; at + 1 < members.size(); at += 32) {  // <= 32 units per pack
@@ -552,18 +561,30 @@ PlanKernels generate_plan_kernels(const CompGraph& g_, const FusionPlan& plan,
           for (size_t j = at; j < end; ++j) k.pattern_key += std::string(j == at ? "" : "+") + specs_[members[j]].pattern_key;
           packs[members[at]] = std::move(k);
         }
-        for (size_t j = at; j < end; ++j) drop.insert(members[j]);
+        for (size_t j = at; j < end; ++j) drop.insert(members[j]), pack_members[members[at]].push_back(members[j]);
       }
-    if (!packs.empty()) {
-      std::vector<KernelSpec> kept;
-      for (size_t i = 0; i < specs_.size(); ++i) {
-        if (auto it = packs.find(i); it != packs.end())
-          kept.push_back(std::move(it->second));
-        else if (!drop.count(i))
-          kept.push_back(std::move(specs_[i]));
+    if (packs.empty()) break;
+    std::vector<KernelSpec> kept;
+    std::map<size_t, int> next_opaque;
+    std::map<size_t, std::vector<int>> next_local;
+    for (size_t i = 0; i < specs_.size(); ++i) {
+      if (auto it = packs.find(i); it != packs.end()) {
+        if (local_verts.count(i)) {  // a local/regional pack may pack again
+          std::vector<int> verts;
+          for (size_t j : pack_members[i]) verts.insert(verts.end(), local_verts[j].begin(), local_verts[j].end());
+          next_local[kept.size()] = verts;
+        }
+        kept.push_back(std::move(it->second));
+      } else if (!drop.count(i)) {
+        if (auto o = opaque_vertex.find(i); o != opaque_vertex.end()) next_opaque[kept.size()] = o->second;
+        if (auto l = local_verts.find(i); l != local_verts.end()) next_local[kept.size()] = l->second;
+        kept.push_back(std::move(specs_[i]));
       }
-      specs_ = std::move(kept);
     }
+    specs_ = std::move(kept);
+    opaque_vertex = std::move(next_opaque);
+    local_verts = std::move(next_local);
+  }
   }
   // Launch-bound plans (every unit small, e.g. DIEN): all units inside one
   // cooperative launch (cg_persist.cpp), unit boundaries as L2 completion
@@ -590,11 +611,11 @@ PlanKernels generate_plan_kernels(const CompGraph& g_, const FusionPlan& plan,
     std::map<std::string, std::string> owner;  // canonical source -> symbol
     for (auto& k : specs_) {
       if (k.is_gemm || k.source.empty()) continue;
-      std::string canon = std::regex_replace(k.source, std::regex("\\b" + k.name + "\\b"), "KNAME_");
+      std::string canon = std::regex_replace(k.source, std::regex("\\b" + regex_escape(k.name) + "\\b"), "KNAME_");
       int pi = 0;
       for (const auto* list : {&k.inputs, &k.outputs})
         for (const auto& t : *list)
-          canon = std::regex_replace(canon, std::regex("\\bT_" + t + "\\b"), "p" + std::to_string(pi++) + "_");
+          canon = std::regex_replace(canon, std::regex("\\b" + regex_escape(tensor_ident(t)) + "\\b"), "p" + std::to_string(pi++) + "_");
       auto [it, fresh] = owner.emplace(canon, k.name);
       if (!fresh) k.symbol = it->second;
     }

@@ -4,7 +4,8 @@
 
 bert_layer.graph   A.4: FFN GEMMs as opaque_compute + bias/GELU + bias/residual/LN
 bert_cut.graph     A.4-cut: GEMM outputs promoted to parameters, outputs gl and y
-dien_T<T>.graph    A.5: DIEN AUGRU recurrence, T steps, batch 256, hidden 36
+dien_T<T>.graph    A.5: DIEN AUGRU recurrence, T steps, batch 256, hidden 36, with the
+                   attention softmax over the time axis feeding every step
 dien_cut_T<T>.graph  A.5 with every opaque GEMM output promoted to a parameter
 """
 import os
@@ -53,18 +54,33 @@ def dien(T, cut, B=256, H=36):
           "bhb = broadcast(bh) dims=[1] : %s" % S,
           "c0 = constant value=0 : f32[]", "c1 = constant value=1 : f32[]",
           "c0b = broadcast(c0) : %s" % S, "c1b = broadcast(c1) : %s" % S]
+    # DIEN's attention: one score per (sequence, step) from the attention MLP
+    # over every interest state and the target ad (opaque GEMMs), softmax over
+    # the time axis (reduce_max / reduce_sum over T).  The IR has no reshape,
+    # so step t's weight column [B,1] is squeezed to [B] by a reduce_sum over
+    # its size-1 axis (exact: one term).
+    if cut:
+        L += ["sc = parameter : f32[%d,%d]" % (B, T)]
+    else:
+        L += ["x%d = parameter : %s" % (t, S) for t in range(T)]
+        L += ["tgt = parameter : %s" % S,
+              "sc = opaque_compute(%s, tgt) : f32[%d,%d]" % (", ".join("x%d" % t for t in range(T)), B, T)]
+    L += ["scm = reduce_max(sc) axes=1 : f32[%d]" % B,
+          "scmb = broadcast(scm) dims=[0] : f32[%d,%d]" % (B, T),
+          "scs = sub(sc, scmb)", "sce = exp(scs)",
+          "scz = reduce_sum(sce) axes=1 : f32[%d]" % B,
+          "sczb = broadcast(scz) dims=[0] : f32[%d,%d]" % (B, T),
+          "att = div(sce, sczb)"]
     h = "h0"
     for t in range(T):
         if cut:
             L += ["zu%d = parameter : %s" % (t, S), "zr%d = parameter : %s" % (t, S),
                   "uh%d = parameter : %s" % (t, S), "xh%d = parameter : %s" % (t, S)]
         else:
-            L += ["x%d = parameter : %s" % (t, S)]
             L += ["zu%d = opaque_compute(x%d, %s) : %s" % (t, t, h, S),
                   "zr%d = opaque_compute(x%d, %s) : %s" % (t, t, h, S),
                   "uh%d = opaque_compute(%s) : %s" % (t, h, S),
                   "xh%d = opaque_compute(x%d) : %s" % (t, t, S)]
-        L += ["att%d = parameter : f32[%d]" % (t, B)]
         for g, b in (("u", "bub"), ("r", "brb")):
             L += ["%sa%d = add(z%s%d, %s)" % (g, t, g, t, b),
                   "%sn%d = sub(c0b, %sa%d)" % (g, t, g, t),
@@ -75,6 +91,8 @@ def dien(T, cut, B=256, H=36):
               "hx%d = add(xh%d, rh%d)" % (t, t, t),
               "hb%d = add(hx%d, bhb)" % (t, t),
               "hc%d = tanh(hb%d)" % (t, t),
+              "ats%d = slice(att) starts=[0,%d] limits=[%d,%d]" % (t, t, B, t + 1),
+              "att%d = reduce_sum(ats%d) axes=1 : f32[%d]" % (t, t, B),
               "attb%d = broadcast(att%d) dims=[0] : %s" % (t, t, S),
               "au%d = mul(attb%d, u%d)" % (t, t, t),
               "om%d = sub(c1b, au%d)" % (t, t),

@@ -23,6 +23,7 @@ from __future__ import annotations
 
 import ctypes
 import json
+import warnings
 import os
 from typing import Dict, List, Optional, Sequence
 
@@ -77,7 +78,7 @@ def lib():
         "stc_plan_num_patterns": (ip, [vp]), "stc_plan_pattern": (ip, [vp, ip, P(ip), ip]),
         "stc_plan_kernel_text": (ip, [vp, ip, P(vp)]),
         "stc_plan_stats": (ip, [vp, P(ip), P(ip), P(i64)]),
-        "stc_plan_refine": (ip, [vp, P(ip), P(i64)]),
+        "stc_plan_refine": (ip, [vp, P(ip), P(i64)]), "stc_plan_refine_info": (ip, [vp, P(i64), P(ip)]),
         "stc_plan_kernel": (ip, [vp, cp, P(ip), ip, P(vp)]),
         "stc_codegen": (ip, [vp, ip, P(vp), P(vp)]),
         "stc_exec_create": (ip, [vp, ip, ip, P(vp)]), "stc_exec_destroy": (None, [vp]),
@@ -229,6 +230,12 @@ class Plan:
         (stc_plan_refine) -> (merges, bytes_saved)"""
         m, b = ctypes.c_int(), ctypes.c_int64()
         _check(lib().stc_plan_refine(self._h, ctypes.byref(m), ctypes.byref(b)))
+        pr, hit = ctypes.c_int64(), ctypes.c_int()
+        lib().stc_plan_refine_info(self._h, ctypes.byref(pr), ctypes.byref(hit))
+        self.refine_info = {"merges": m.value, "bytes_saved": b.value, "probes": pr.value,
+                            "budget_hit": bool(hit.value)}
+        if hit.value:
+            warnings.warn("plan refinement stopped by STITCH_REFINE_MAX_PROBES after %d probes" % pr.value)
         return m.value, b.value
 
     def json(self, seed: int = 0) -> str:

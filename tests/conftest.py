@@ -37,3 +37,14 @@ def golden_plan(name, cfg):
         return None
     with open(path) as f:
         return json.load(f)
+
+
+def dotted(text, prefix="layer."):
+    """the same graph with every node renamed to a dotted identifier (the
+    reference parser accepts '.' in names, src/parser.cpp:50), plus an
+    underscore so the escape of both characters is exercised"""
+    import re
+    names = [l.split("=")[0].strip() for l in text.splitlines() if "=" in l and not l.strip().startswith("#")]
+    for n in sorted(names, key=len, reverse=True):
+        text = re.sub(r"(?<![A-Za-z0-9_.])%s(?![A-Za-z0-9_.])" % re.escape(n), prefix + n + "_q", text)
+    return text

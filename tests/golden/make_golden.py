@@ -16,7 +16,7 @@ Writes, under tests/golden/:
                        plan.json bytes + sha256 of each program text
   numeric.json         sha256 of the reference's eval_reference outputs (f32
                        bytes) for fixtures x seeds 1..10 and config graphs x
-                       seed 1, plus the inputs' sha256 (random_inputs)
+                       seeds 1..3, plus the inputs' sha256 (random_inputs)
   numeric_small.npz    full eval_reference outputs, fixtures x seed 1
 """
 from __future__ import annotations
@@ -68,6 +68,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--skip-slow", action="store_true")
     ap.add_argument("--only", default="")
+    ap.add_argument("--numeric-only", action="store_true",
+                    help="only numeric.json / numeric_small.npz (fixtures x seeds 1..10, configs x seeds 1..3)")
     ap.add_argument("--shards", action="store_true",
                     help="per-shard plans (SURVEY §8e): <graph>@<n>__b200.json for n in 2,4,8")
     args = ap.parse_args()
@@ -99,7 +101,7 @@ def main():
     if args.only:
         graphs = {k: v for k, v in graphs.items() if k in args.only.split(",")}
 
-    for name, text in graphs.items():
+    for name, text in ({} if args.numeric_only else graphs).items():
         for cfg in CFGS:
             path = os.path.join(GOLD, "plans", "%s__%s.json" % (name, cfg))
             rec = plan_record(text, cfg)
@@ -112,7 +114,7 @@ def main():
 
     rnd = {}
     seed = 0
-    while len(rnd) < 100:
+    while len(rnd) < 100 and not args.numeric_only:
         seed += 1
         text = random_graph_text(seed, 10)
         if text is None:
@@ -123,16 +125,17 @@ def main():
             entry[cfg] = {"plan_json": pj, "summary": summ,
                           "programs_sha": {k: sha(v.encode()) for k, v in progs.items()}}
         rnd[str(seed)] = entry
-    with open(os.path.join(GOLD, "random_plans.json"), "w") as fh:
-        json.dump(rnd, fh, indent=1, sort_keys=True)
-    print("random plans done", flush=True)
+    if not args.numeric_only:
+        with open(os.path.join(GOLD, "random_plans.json"), "w") as fh:
+            json.dump(rnd, fh, indent=1, sort_keys=True)
+        print("random plans done", flush=True)
 
     numeric, small = {}, {}
     for name, text in graphs.items():
         g = no.parse_graph(text)
         ps = [(p.name, p.dims) for p in g.params()]
         outs = [g.nodes[o].dims for o in g.outputs]
-        seeds = range(1, 11) if name in fixtures else [1]
+        seeds = range(1, 11) if name in fixtures else range(1, 4)
         rec = {}
         for seed in seeds:
             ins = ref.random_inputs(text, ps, seed)

@@ -74,6 +74,29 @@ def test_codegen_and_nvrtc_compile_all_fixtures(mode):
         assert re.fullmatch(r"[0-9a-f]{32}", key)
 
 
+@pytest.mark.parametrize("persist", ["0", "1"])
+def test_dotted_tensor_names_compile(monkeypatch, persist):
+    """graph names with '.' (valid in the reference's parser) become C
+    identifiers through one injective escape in every generator (dataflow,
+    program, unfused, packed, deduplicated, persistent)"""
+    from tests.conftest import config_graph, dotted
+    monkeypatch.setenv("STITCH_PERSIST", persist)
+    stitch = _stitch()
+    texts = [dotted(t) for t in fixture_graphs().values()] + [dotted(config_graph("dien_T10"), "a.b_")]
+    for text in texts:
+        plan = stitch.Plan(stitch.Graph(text), "b200")
+        for mode in ("stitched", "program", "unfused"):
+            src, kernels = plan.codegen(mode)
+            assert "TX_" in src
+            assert not re.search(r"\bT_[A-Za-z0-9_]*\.", src)
+            assert re.fullmatch(r"[0-9a-f]{32}", stitch.compile_cuda(src))
+    # injective: 'a.b' and 'a_b' side by side stay distinct parameters
+    text = "a.b = parameter : f32[64]\na_b = parameter : f32[64]\ny = add(a.b, a_b)\noutput y\n"
+    src, kernels = stitch.Plan(stitch.Graph(text), "b200").codegen()
+    assert "TX_a_Db" in src and "T_a_b" in src
+    stitch.compile_cuda(src)
+
+
 def test_dataflow_templates_chosen_for_fixtures():
     stitch = _stitch()
     want = {"layernorm": "regional", "softmax": "regional", "variance": "regional",
@@ -89,8 +112,10 @@ def test_launch_units_packed_per_producer_set(monkeypatch):
     (executor-level; the plan is unchanged): small opaque placeholders a CTA
     per op, local-template patterns side by side.  DIEN T=10: the 13
     parameter-only placeholders form one pack, each step's three gate
-    placeholders another, the 10 parameter-only attention broadcasts one
-    local kernel -> 69 plan kernels in 30 launches"""
+    placeholders another; packing repeats over the packs, so the nine
+    attention-column slices, then their squeezes (regional), then the
+    attention broadcasts each become one launch -> 88 plan kernels in 33
+    launches"""
     stitch = _stitch()
     from tests.conftest import config_graph
     plan = stitch.Plan(stitch.Graph(config_graph("dien_T10")), "b200")
@@ -99,21 +124,21 @@ def test_launch_units_packed_per_producer_set(monkeypatch):
     _, opaque_only = plan.codegen()
     monkeypatch.setenv("STITCH_OPAQUE_PACK", "0")
     _, single = plan.codegen()
-    assert len(single) == plan.stats()["stitched_kernels"] == 69
-    assert len(opaque_only) == 39
-    assert len(packed) == 30
+    assert len(single) == plan.stats()["stitched_kernels"] == 88
+    assert len(opaque_only) == 57
+    assert len(packed) == 33
     units = lambda ks: sorted(p for k in ks for p in k["pattern"].split("+"))
     assert units(packed) == units(opaque_only) == units(single)  # every unit exactly once
     packs = [k for k in opaque_only if k["template"].startswith("opaque(pack")]
-    assert sorted(k["grid"] for k in packs) == [3] * 9 + [13]
+    assert sorted(k["grid"] for k in packs) == [3] * 9 + [14]
     assert all(k["grid"] == len(k["pattern"].split("+")) for k in packs)
     outs = lambda ks: sorted(o for k in ks for o in k["outputs"])
     assert outs(packed) == outs(single)
     # launches with identical code (modulo their tensors) share one function
-    assert len({k["symbol"] for k in packed}) == 6
+    assert len({k["symbol"] for k in packed}) == 9
     monkeypatch.setenv("STITCH_DEDUP", "0")
     _, nodedup = plan.codegen()
-    assert len({k["symbol"] for k in nodedup}) == 69
+    assert len({k["symbol"] for k in nodedup}) == 88
 
 
 def test_persistent_template_codegen(monkeypatch):
@@ -124,8 +149,8 @@ def test_persistent_template_codegen(monkeypatch):
     from tests.conftest import config_graph
     monkeypatch.setenv("STITCH_PERSIST", "1")
     src, kernels = stitch.Plan(stitch.Graph(config_graph("dien_T10")), "b200").codegen()
-    assert [k["template"] for k in kernels] == ["persistent(30)"]
-    assert len(set(re.findall(r"\bunit\d+_\(", src))) == 6  # 30 units, 6 distinct bodies
+    assert [k["template"] for k in kernels] == ["persistent(33)"]
+    assert len(set(re.findall(r"\bunit\d+_\(", src))) == 9  # 33 units, 9 distinct bodies
     assert re.fullmatch(r"[0-9a-f]{32}", stitch.compile_cuda(src))
     _, big = stitch.Plan(stitch.Graph(config_graph("bert_layer")), "b200").codegen()
     assert len(big) > 1 and not any(k["template"].startswith("persistent") for k in big)
