@@ -4,10 +4,16 @@ stitched-kernel HBM GB/s vs ~8 TB/s peak; subgraph us; kernels launched).
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
     torchrun --nproc-per-node N bench.py --gpus N ...
 
-Headline workload (N=1): BASELINE config C2, the BERT-base attention softmax
-chain (scale, mask-add, row-max, exp, row-sum, div) fp32 [32,12,128,128],
-planned by the bit-exact planner under the B200 device profile (1 stitched
-kernel), executed as an NVRTC sm_100a kernel in one CUDA Graph.
+Headline workload (N=1): BASELINE config C3, the largest single-GPU config:
+the BERT-base FFN memory-intensive subgraphs at batch 32 x seq 128 (4096 token
+rows) in their A.4-cut form -- bias+GELU(tanh) on
+ffn1 [4096,3072] and bias + residual + two-pass LayerNorm on ffn2/h [4096,768]
+-- planned by the bit-exact planner under the B200 device profile as ONE
+remote-packed stitched kernel (an `independent` launch whose CTAs run the local
+GELU body and the regional LayerNorm body), executed as an NVRTC sm_100a kernel
+in one CUDA Graph.  The other configs (C1, C2, C3a/b, C4, C5 T=10/20) are in
+`subgraphs`, each with its batched and single-launch time and roofline
+fraction and, where launch packing applies, its parity-mode launch count.
 
 One step = one replay of the plan's CUDA Graph over one batch.  `value` is
 algorithmic HBM bytes (unique inputs read once + outputs written once,
@@ -15,7 +21,10 @@ SURVEY.md §8d) x ranks / max-over-ranks time, inputs HBM-resident; timed with
 CUDA events on the stream the graph is launched on.  Between replays the
 executor rotates through independent buffer sets whose total exceeds L2 (cold
 inputs every step).  Multi-GPU: independent batch shards, one per rank, no
-collective on the data path (weak scaling).  `e2e` is the same metric through
+collective on the data path (weak scaling; --strong shards ONE batch).
+`python bench.py --gpus N` outside torchrun re-launches itself under
+torch.distributed.run with N ranks (gloo for the verification gather when the
+box has fewer GPUs than ranks, ranks then share devices).  `e2e` is the same metric through
 the C-ABI with pinned HOST buffers (H2D inputs + replay + D2H outputs per step).
 `--impl reference` times the reference's own CPU executor (oracle/_ref, the
 unmodified reference library) on all host threads on the same workload.
@@ -37,10 +46,14 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-WORKLOAD = "attn_softmax"
-WORKLOAD_DESC = "C2 BERT-base attention softmax chain fp32 [32,12,128,128] (+ key mask [32,128])"
-BATCH_TOKEN = "[32,"  # batch dim of every batched tensor in attn_softmax.graph
-SUBGRAPHS = ["ln_4096x768", "ln2pass_4096x768", "bert_gelu", "bert_resln", "colreduce", "dien_T10", "bert_layer"]
+WORKLOAD = "bert_cut"
+WORKLOAD_DESC = ("C3 BERT-base FFN memory-intensive subgraphs, batch 32 x seq 128: bias+GELU(tanh) on ffn1 "
+                 "[4096,3072] + bias+residual+two-pass LayerNorm on ffn2/h [4096,768], fp32 (A.4-cut)")
+ROWS = 4096      # token rows of the workload (= 32 sequences x 128)
+SEQ_ROWS = 128   # rows of one sequence (the verification sample)
+SUBGRAPHS = ["ln_4096x768", "ln2pass_4096x768", "attn_softmax", "bert_gelu", "bert_resln", "colreduce",
+             "dien_T10", "dien_T20", "bert_layer"]
+CPU_REPS = 5     # best of 5
 L2_BYTES = 126 * 1024 * 1024
 E2E_CHUNKS = int(os.environ.get("STITCH_E2E_CHUNKS", "4"))
 
@@ -60,13 +73,16 @@ def measured_peaks():
 
 
 def ncu_traffic(graph):
-    """dram bytes per launch of the dominant kernel from the committed ncu capture"""
+    """bytes per launch of the dominant kernel from the committed ncu capture
+    (profiles/ncu_summary.json): DRAM reads + SM->L2 writes.  One cold ncu
+    launch ends with its outputs still dirty in the 126 MB L2, so the DRAM
+    write counter undercounts; every byte the SMs write reaches HBM later."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
-            d = json.load(f)
-        return d.get(graph, {}).get("dram_bytes")
+            d = json.load(f).get(graph, {})
+        return (d["dram_read_bytes"] + d["sm_to_l2_write_bytes"]), d
     except Exception:
-        return None
+        return None, {}
 
 
 class ClockSampler:
@@ -129,12 +145,19 @@ class ClockSampler:
                                                                              "warm-up before it")}
 
 
-def cpu_reference_seconds(text, threads, reps):
-    """wall seconds of the unmodified reference eval_reference over the full
-    workload split into `threads` batch shards on `threads` host threads"""
+def _rule():
+    from paper_2009_10924_b200 import shard
+    return shard.RULES[WORKLOAD]
+
+
+def cpu_reference_seconds(text, threads, reps, rows=ROWS):
+    """best-of-reps wall seconds of the unmodified reference eval_reference over
+    `rows` token rows of the workload, split into `shards` batch shards run on
+    as many host threads (shards = the largest power of two <= threads that
+    divides rows; one shard = the reference's own single-threaded executor)"""
     from oracle import ref
-    shards = max(d for d in range(1, threads + 1) if 32 % d == 0)
-    shard_text = text.replace(BATCH_TOKEN, "[%d," % (32 // shards))
+    shards = max(d for d in range(1, threads + 1) if rows % d == 0 and (d & (d - 1)) == 0)
+    shard_text = _rule().extent_text(text, rows // shards)
     return ref.time_eval([shard_text] * shards, seed=1, reps=reps), shards
 
 
@@ -149,28 +172,30 @@ def run_reference(args):
         return
     text = read_graph(WORKLOAD)
     threads = os.cpu_count() or 1
-    # each step is a bounded sample of the workload: all 32 sequences, `heads`
-    # of the 12 attention heads, so that warm-up + K steps end in ~2 minutes
+    # each step is a bounded sample of the workload: `rows` of the 4096 token
+    # rows (whole sequences), sized so that warm-up + K steps end in ~2 minutes
     t_full, shards = cpu_reference_seconds(text, threads, 1)
     budget_s = float(os.environ.get("STITCH_REF_BUDGET_S", "120"))
-    heads = max(1, min(12, int(12 * budget_s / max(1e-9, (args.steps + args.warmup) * t_full))))
-    sample = text.replace("[32,12,", "[32,%d," % heads)
-    og = no.parse_graph(sample)
+    seqs = max(1, min(ROWS // SEQ_ROWS, int(ROWS // SEQ_ROWS * budget_s / max(1e-9, (args.steps + args.warmup) * t_full))))
+    while (ROWS // SEQ_ROWS) % seqs:
+        seqs -= 1
+    rows = seqs * SEQ_ROWS
+    og = no.parse_graph(_rule().extent_text(text, rows))
     bytes_step = no.algorithmic_bytes(og, [[n.id for n in og.nodes if n.kind not in ("parameter", "constant")]])
     times = []
     for i in range(args.warmup + args.steps):
-        s, shards = cpu_reference_seconds(sample, threads, 1)
+        s, shards = cpu_reference_seconds(text, threads, 1, rows)
         if i >= args.warmup:
             times.append(s)
     t = statistics.mean(times)
     val = bytes_step / t / 1e9
-    desc = ("C2 softmax chain, %d of 12 heads x 32 sequences per step (%d batch shards on %d host threads, "
-            "unmodified reference eval_reference from oracle/_ref)" % (heads, shards, shards))
+    desc = ("C3 A.4-cut, %d of 32 sequences (%d token rows) per step as %d batch shards on %d host threads, "
+            "unmodified reference eval_reference from oracle/_ref" % (seqs, rows, shards, shards))
     line = {"metric": "stitched-subgraph HBM GB/s (algorithmic bytes / time)", "value": round(val, 4),
             "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(t * 1e3, 3), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic: reference random_inputs(seed=1)",
-            "config": {"workload": WORKLOAD_DESC, "graph": WORKLOAD, "sample_heads": heads,
+            "config": {"workload": WORKLOAD_DESC, "graph": WORKLOAD, "sample_rows": rows,
                        "bytes_per_step": bytes_step}, "impl": "reference",
             "cpu_baseline": {"value": round(val, 4), "unit": "GB/s", "cores": shards, "kind": "reference",
                              "sample": desc},
@@ -181,48 +206,94 @@ def run_reference(args):
 def cpu_reference_subgraph(name, threads):
     """wall seconds of the unmodified reference eval_reference on the whole
     config graph, as `shards` independent shard graphs on as many host threads
-    (best of 3); shards = the largest divisor of the sharded extent <= threads"""
+    (best of 5); shards = the largest divisor of the sharded extent <= threads"""
     from oracle import ref
     from paper_2009_10924_b200 import shard
     text = read_graph(name)
     rule = shard.RULES.get(name)
     if rule is None:
-        return ref.time_eval([text], seed=1, reps=3), 1
+        return ref.time_eval([text], seed=1, reps=CPU_REPS), 1
     n = max(d for d in range(1, threads + 1) if rule.full % d == 0)
-    return ref.time_eval([rule.graph_text(text, n)] * n, seed=1, reps=3), n
+    return ref.time_eval([rule.graph_text(text, n)] * n, seed=1, reps=CPU_REPS), n
 
 
-def time_subgraph(stitch, name, gemm=False, refine=False):
-    g = stitch.Graph(read_graph(name))
-    plan = stitch.Plan(g, "b200")
-    if refine:
-        plan.refine()
+def _exec_timing(stitch, plan, g, gemm=False):
     ex = stitch.Executor(plan, gemm=gemm)
     ex.upload(stitch.random_inputs(g, 1))
-    desc = ex.describe()
     per_set = sum(t.nbytes for t in g.params) + sum(t.nbytes for t in g.outputs)
     sets = min(256, max(2, math.ceil(8 * L2_BYTES / max(per_set, 1))))
     us1, kus = ex.time(iters=200, warmup=20, sets=sets, per_kernel=True)
     us = ex.time_batched(steps=256, warmup=64, sets=sets, steps_per_graph=64)
+    return ex, us, us1, kus
+
+
+def time_subgraph(stitch, name, gemm=False, refine=False):
+    """one BASELINE config: `us` = back-to-back steps (64 per graph launch,
+    PDL overlap between steps), `us_one_launch_per_step` = one graph launch per
+    step (no cross-step overlap), each with its roofline fraction; when the
+    default launch packing merges plan kernels, `parity_mode` is the same plan
+    with packing off (launches == plan.json stitched_kernels)"""
+    g = stitch.Graph(read_graph(name))
+    plan = stitch.Plan(g, "b200")
+    if refine:
+        plan.refine()
+    ex, us, us1, kus = _exec_timing(stitch, plan, g, gemm)
+    desc = ex.describe()
     alg = sum(k["bytes"] for k in desc)
     top = max(range(len(desc)), key=lambda i: kus[i])
     peak, _ = measured_peaks()
+    plan_kernels = plan.stats()["stitched_kernels"]
     cpu = None
     if not gemm and not refine:
         try:
             from oracle import ref
             if ref.available():
                 s, n = cpu_reference_subgraph(name, os.cpu_count() or 1)
-                cpu = {"us": round(s * 1e6, 1), "threads": n, "kind": "reference",
+                cpu = {"us": round(s * 1e6, 1), "threads": n, "kind": "reference", "reps": CPU_REPS,
                        "gpu_speedup": round(s * 1e6 / us, 1)}
         except Exception as e:  # reported, never fatal
             cpu = {"error": str(e)[:200]}
-    return {"us": round(us, 3), "GBps": round(alg / us / 1e3, 1), "frac_of_measured_peak": round(alg / us / 1e3 / peak, 4),
-            "kernels": len(desc), "plan_kernels": plan.stats()["stitched_kernels"], "cpu_reference": cpu,
-            "us_one_launch_per_step": round(us1, 3),
-            "templates": sorted({k["template"] for k in desc}), "bytes": alg,
-            "dominant": {"name": desc[top]["name"], "template": desc[top]["template"],
-                         "us_event": round(kus[top], 3)}}
+    out = {"us": round(us, 3), "GBps": round(alg / us / 1e3, 1), "frac_of_measured_peak": round(alg / us / 1e3 / peak, 4),
+           "us_one_launch_per_step": round(us1, 3), "frac_one_launch": round(alg / us1 / 1e3 / peak, 4),
+           "kernels": len(desc), "plan_kernels": plan_kernels, "cpu_reference": cpu,
+           "templates": sorted({k["template"] for k in desc}), "bytes": alg,
+           "dominant": {"name": desc[top]["name"], "template": desc[top]["template"],
+                        "us_event": round(kus[top], 3), "bytes": desc[top]["bytes"],
+                        "frac_event": round(desc[top]["bytes"] / kus[top] / 1e3 / peak, 4)}}
+    del ex
+    if len(desc) != plan_kernels and not refine:
+        saved = {k: os.environ.get(k) for k in ("STITCH_OPAQUE_PACK", "STITCH_LOCAL_PACK")}
+        os.environ["STITCH_OPAQUE_PACK"] = os.environ["STITCH_LOCAL_PACK"] = "0"
+        try:
+            pex, pus, pus1, _ = _exec_timing(stitch, plan, g, gemm)
+            out["parity_mode"] = {"launches": pex.num_kernels, "us": round(pus, 3),
+                                  "us_one_launch_per_step": round(pus1, 3),
+                                  "note": "STITCH_OPAQUE_PACK=0 STITCH_LOCAL_PACK=0: one launch per plan kernel"}
+            del pex
+        finally:
+            for k, v in saved.items():
+                if v is None:
+                    os.environ.pop(k, None)
+                else:
+                    os.environ[k] = v
+    return out
+
+
+def spawn_ranks(args):
+    """`python bench.py --gpus N` (N>1) outside torchrun: re-launch under
+    torch.distributed.run with N ranks on this node (127.0.0.1); the ranks
+    share GPUs (gloo for the verification gather) when the box has fewer"""
+    import socket
+    import torch
+    env = dict(os.environ)
+    if torch.cuda.device_count() < args.gpus:
+        env.setdefault("STITCH_DIST_BACKEND", "gloo")
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(args.gpus),
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
 
 
 def main():
@@ -238,6 +309,8 @@ def main():
     ap.add_argument("--strong", action="store_true",
                     help="strong scaling: the 32-sequence batch is sharded over the ranks (32/N each, per-shard plans)")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args))
     if args.impl == "reference":
         return run_reference(args)
 
@@ -260,9 +333,8 @@ def main():
 
     from paper_2009_10924_b200 import stitch
     text = read_graph(WORKLOAD)
-    if args.strong and world > 1:  # this rank's shard of ONE 32-sequence batch, re-planned for its shape
-        from paper_2009_10924_b200 import shard as _shard
-        text = _shard.RULES[WORKLOAD].graph_text(text, world)
+    if args.strong and world > 1:  # this rank's shard of ONE 4096-row batch, re-planned for its shape
+        text = _rule().graph_text(text, world)
     g = stitch.Graph(text)
     plan = stitch.Plan(g, "b200")
     ex = stitch.Executor(plan, device=local)
@@ -337,6 +409,7 @@ def main():
     dom_us = ms_step * 1e3 * (kus[top] / sum(kus)) if len(desc) > 1 else ms_step * 1e3
     peak, peak_kind = measured_peaks()
     achieved = desc[top]["bytes"] / (dom_us * 1e-6) / 1e9
+    traffic, traffic_raw = ncu_traffic(WORKLOAD)
 
     # e2e through the C-ABI with pinned host buffers (inputs and outputs)
     pin_in = {t.name: torch.from_numpy(inputs[t.name]).pin_memory().numpy() for t in g.params}
@@ -346,11 +419,11 @@ def main():
     # pipelined: the batch as E2E_CHUNKS chunk plans, H2D / graph / D2H of
     # consecutive chunks overlapped (stc_exec_run_host_chunked)
     from paper_2009_10924_b200 import shard
-    rule = shard.RULES[WORKLOAD]
+    rule = _rule()
     if args.strong and world > 1:  # chunk this rank's shard
-        rule = shard.ShardRule(32 // world, r"\[%d," % (32 // world), rule.axis_of)
-    cx = stitch.ChunkedExecutor(text, rule, max(d for d in range(1, E2E_CHUNKS + 1) if rule.full % d == 0),
-                                device=local)
+        rule = shard.ShardRule(ROWS // world, r"\[%d[,\]]" % (ROWS // world), rule.axis_of)
+    cx_chunks = max(d for d in range(1, E2E_CHUNKS + 1) if rule.full % d == 0)
+    cx = stitch.ChunkedExecutor(text, rule, cx_chunks, device=local)
     e2e_steps = max(5, min(50, args.steps // 20))
 
     def host_loop(fn, n):
@@ -372,12 +445,12 @@ def main():
     e2e_val = alg_bytes * world / e2e_s / 1e9
 
     # verification outside every timed region: each rank's sequence-0 outputs
-    # (set 0 holds this rank's inputs) are gathered to rank 0 over NCCL and
-    # checked against the numpy oracle on the same inputs
+    # (token rows 0..127; set 0 holds this rank's inputs) are gathered to rank
+    # 0 over NCCL and checked against the numpy oracle on the same inputs
     ex.launch(sp, 0)
     torch.cuda.synchronize()
     outs = ex.download()
-    seq0 = {t.name: np.ascontiguousarray(outs[t.name][0:1]) for t in g.outputs}
+    seq0 = {t.name: np.ascontiguousarray(outs[t.name][0:SEQ_ROWS]) for t in g.outputs}
     gathered = {}
     for name_, a in seq0.items():
         tt = torch.from_numpy(a).to(coll_dev)
@@ -390,12 +463,12 @@ def main():
     verification = None
     if rank == 0:
         from oracle import numpy_oracle as no
-        from paper_2009_10924_b200 import shard as _sh
-        one = no.parse_graph(_sh.RULES[WORKLOAD].extent_text(read_graph(WORKLOAD), 1))
+        one = no.parse_graph(_rule().extent_text(read_graph(WORKLOAD), SEQ_ROWS))
         ok, worst = True, 0.0
         for r in range(world):
             full_in = stitch.random_inputs(g, seed=1 + r)
-            want = no.eval_reference(one, {k: v[0:1].astype(np.float64) for k, v in full_in.items()})
+            seq_in = _rule().slice_inputs(full_in, ROWS // SEQ_ROWS, 0) if g.params[0].dims[0] >= SEQ_ROWS else full_in
+            want = no.eval_reference(one, {k: v.astype(np.float64) for k, v in seq_in.items()})
             rep = stitch.compare({k: gathered[k][r] for k in want}, want, 1e-4, 1e-5)
             ok, worst = ok and rep["pass"], max(worst, rep["max_rel"])
         verification = {"pass": ok, "ranks": world, "max_rel": worst,
@@ -410,16 +483,20 @@ def main():
                 from oracle import ref
                 if ref.available():
                     threads = os.cpu_count() or 1
-                    s, shards = cpu_reference_seconds(text, threads, 3)
+                    s, shards = cpu_reference_seconds(text, threads, CPU_REPS)
+                    # the reference executor is single-threaded by design: one core, whole batch
+                    s1 = ref.time_eval([text], seed=1, reps=CPU_REPS)
                     cpu = {"value": round(alg_bytes / s / 1e9, 4), "unit": "GB/s", "cores": shards,
                            "kind": "reference",
-                           "sample": "full C2 batch as %d batch shards on %d host threads, unmodified "
-                                     "reference eval_reference (oracle/_ref), best of 3: %.3f s"
-                                     % (shards, shards, s)}
-                    # the reference executor is single-threaded by design: one core, whole batch
-                    s1 = ref.time_eval([text], seed=1, reps=2)
-                    cpu["single_core"] = {"value": round(alg_bytes / s1 / 1e9, 4), "seconds": round(s1, 3),
-                                          "sample": "full C2 batch, one thread, best of 2"}
+                           "sample": "full C3 batch (4096 token rows) as %d batch shards on %d host threads, "
+                                     "unmodified reference eval_reference (oracle/_ref), best of %d: %.3f s"
+                                     % (shards, shards, CPU_REPS, s),
+                           "all_cores": {"value": round(alg_bytes / s / 1e9, 4), "seconds": round(s, 4),
+                                         "cores": shards, "us_per_subgraph": round(s * 1e6, 1)},
+                           "single_core": {"value": round(alg_bytes / s1 / 1e9, 4), "seconds": round(s1, 4),
+                                           "cores": 1, "us_per_subgraph": round(s1 * 1e6, 1),
+                                           "sample": "full C3 batch, one thread, best of %d" % CPU_REPS},
+                           "protocol": "BASELINE.md §3: best of %d, 1-core and all-core" % CPU_REPS}
             except Exception as e:  # reported, never fatal
                 cpu = {"value": None, "unit": "GB/s", "cores": 0, "kind": "reference", "sample": "failed: %s" % e}
         subs = {}
@@ -463,16 +540,26 @@ def main():
                        "bytes_per_step_per_gpu": alg_bytes,
                        "l2": "inputs larger than L2: %d rotating buffer sets x %.1f MB = %.0f MB (>= 8x the 126 MB L2)"
                              % (sets, per_set / 1e6, sets * per_set / 1e6),
-                       "global_batch": 32 if args.strong else 32 * world,
+                       "global_batch": "%d sequences x 128 tokens" % (32 if args.strong else 32 * world),
+                       "ranks_per_device": max(1, world // max(1, torch.cuda.device_count())),
                        "parallelism": "independent batch shards, %d rank(s), no collective" % world},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "peak_source": peak_kind + " (MEASURED_PEAKS.json hbm_gbs)"
                          if peak_kind == "measured" else "fallback 6650 GB/s",
-                         "traffic": ncu_traffic(WORKLOAD),
-                         "traffic_note": "ncu dram__bytes_read+write during one cold launch (profiles/ncu_summary.json); "
-                                         "equals the algorithmic READ bytes -- the outputs are still dirty in the "
-                                         "126 MB L2 when the kernel ends and are written back later", "kernel": desc[top]["name"],
+                         "traffic": traffic,
+                         "traffic_ratio": round(traffic / desc[top]["bytes"], 4) if traffic else None,
+                         "traffic_note": "ncu, one cold launch (profiles/ncu_summary.json): dram__bytes_read.sum + "
+                                         "SM->L2 write bytes (lts__t_sectors_srcunit_tex_op_write); the DRAM write "
+                                         "counter of a single cold launch misses the outputs still dirty in the 126 MB "
+                                         "L2, which are written back after the kernel ends (raw: %s)"
+                                         % json.dumps({k: v for k, v in traffic_raw.items() if k != "report"}),
+                         "kernel": desc[top]["name"],
                          "kernel_us": round(dom_us, 3), "kernel_bytes": desc[top]["bytes"],
+                         "kernel_us_one_launch": round(kus[top], 3),
+                         "frac_one_launch": round(desc[top]["bytes"] / (kus[top] * 1e-6) / 1e9 / peak, 4),
+                         "one_launch_note": "the same kernel timed with one CUDA-graph launch per step (CUDA events "
+                                            "around the kernel, cold rotated inputs, no cross-step PDL overlap): "
+                                            "the latency of one subgraph call",
                          "frac_of_8TBps": round(achieved / 8000.0, 4),
                          "peak_note": "the measured peak is a plain copy kernel timed launch by launch; back-to-back "
                                       "steps with programmatic dependent launch overlap one step's drain with the next "
@@ -480,10 +567,10 @@ def main():
             "cpu_baseline": cpu,
             "e2e": {"value": round(e2e_val, 3), "unit": "GB/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "us_per_step": round(e2e_s * 1e6, 1),
-                    "path": "stc_exec_run_host_chunked: pinned host -> %d batch chunks (chunk plans re-planned "
-                            "for batch %d); H2D of chunk k+1 on the copy engine overlaps the stitched kernels of "
-                            "chunk k, which write their outputs straight into the mapped pinned host buffer"
-                            % (E2E_CHUNKS, 32 // E2E_CHUNKS),
+                    "path": "stc_exec_run_host_chunked: pinned host -> %d row chunks (chunk plans re-planned "
+                            "for %d token rows); H2D of chunk k+1 on the copy engine overlaps the stitched kernels "
+                            "of chunk k, which write their outputs straight into the mapped pinned host buffer"
+                            % (cx_chunks, rule.full // cx_chunks),
                     "unpipelined": {"value": round(alg_bytes * world / e2e_plain_s / 1e9, 3),
                                     "us_per_step": round(e2e_plain_s * 1e6, 1),
                                     "path": "stc_exec_run_host: H2D all -> graph -> D2H all"}},

@@ -79,6 +79,8 @@ def main():
                 kname = rec["kernel"]
                 summ[g] = {"kernel": kname, "report": os.path.relpath(dest, ROOT),
                            "dram_bytes": int((rec.get("dram_read_MB", 0) + rec.get("dram_write_MB", 0)) * 1e6),
+                           "dram_read_bytes": int(rec.get("dram_read_MB", 0) * 1e6),
+                           "dram_write_bytes": int(rec.get("dram_write_MB", 0) * 1e6),
                            "sm_to_l2_write_bytes": int(rec.get("sm_to_l2_write_MB", 0) * 1e6),
                            "duration_us_cold": rec.get("duration_us")}
                 break

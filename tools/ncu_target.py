@@ -4,7 +4,7 @@ import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2009_10924_b200 import stitch
 
-names = sys.argv[1:] or ["ln_4096x768", "attn_softmax", "colreduce", "bert_gelu", "bert_resln", "ln2pass_4096x768"]
+names = sys.argv[1:] or ["bert_cut", "ln_4096x768", "attn_softmax", "colreduce", "bert_gelu", "bert_resln", "ln2pass_4096x768"]
 for name in names:
     g = stitch.Graph.from_file(os.path.join(stitch.GRAPHS, name + ".graph"))
     ex = stitch.Executor(stitch.Plan(g, "b200"), graph=False)
