@@ -542,6 +542,10 @@ def main():
                              % (sets, per_set / 1e6, sets * per_set / 1e6),
                        "global_batch": "%d sequences x 128 tokens" % (32 if args.strong else 32 * world),
                        "ranks_per_device": max(1, world // max(1, torch.cuda.device_count())),
+                       **({"shared_device_note": "logic run: %d ranks share %d GPU(s) as time-sliced contexts, so a "
+                                                 "rank's timed region can fall inside its own time slice; the value "
+                                                 "is not a multi-GPU throughput" % (world, torch.cuda.device_count())}
+                          if world > torch.cuda.device_count() else {}),
                        "parallelism": "independent batch shards, %d rank(s), no collective" % world},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "peak_source": peak_kind + " (MEASURED_PEAKS.json hbm_gbs)"

@@ -1575,6 +1575,23 @@ KernelSpec generate_pattern_kernel(const CompGraph& g, const std::vector<int>& v
 // broadcast; src/sim.cpp:215-226): the statements after the PDL wait.  The
 // enclosing code defines bid_ / nbid_ (this CTA's index and the CTA count
 // of the op) and, for the grid form, bar_ / part_.
+int opaque_block();
+
+// 128-bit operand chunks one thread of a single-CTA placeholder holds in
+// registers before it folds them (the single path issues every load first)
+constexpr int kOpaqueRegChunks = 12;
+
+static int64_t opaque_chunks_per_thread(const CompGraph& g, int vertex, int64_t span) {
+  int64_t k = 0;
+  for (int o : g.node(vertex).operands) {
+    const TensorShape& sh = g.node(o).shape;
+    const int64_t cnt = sh.element_count();
+    const int64_t units = sh.dtype == DType::F32 && cnt % 4 == 0 ? cnt / 4 : cnt;
+    k += (units + span - 1) / span;
+  }
+  return k;
+}
+
 static std::string opaque_body(const CompGraph& g, int vertex, bool single, int grid, int block,
                                const std::string& wait, int csize = 1) {
   const OpNode& n = g.node(vertex);
@@ -1590,6 +1607,19 @@ static std::string opaque_body(const CompGraph& g, int vertex, bool single, int 
     // the PDL wait (`wait`), kernel-produced operands after it
     int vi = 0;
     std::vector<std::pair<std::string, int>> regs;  // (array, lanes per element)
+    int64_t held = 0;  // chunks in registers not yet folded
+    auto fold = [&]() {
+      for (const auto& [a, lanes] : regs) {
+        s << "  #pragma unroll\n  for (int k = 0; k < (int)(sizeof(" << a << ") / sizeof(" << a << "[0])); ++k) ";
+        if (lanes == 4)
+          s << "acc += ((double)" << a << "[k].x + (double)" << a << "[k].y) + ((double)" << a << "[k].z + (double)" << a
+            << "[k].w);\n";
+        else
+          s << "acc += (double)" << a << "[k];\n";
+      }
+      regs.clear();
+      held = 0;
+    };
     bool hoisted = false;
     for (int pass = 0; pass < 2; ++pass) {
      // ptxas schedules griddepcontrol.wait (ACQBULK) above independent
@@ -1621,6 +1651,9 @@ static std::string opaque_body(const CompGraph& g, int vertex, bool single, int 
             << tensor_ident(g.node(o).name) << ", i);\n";
         continue;
       }
+      // beyond the register budget: fold what is held before loading more
+      if (held > 0 && held + K > kOpaqueRegChunks) fold();
+      held += K;
       if (vec) {
         s << "  float4 " << a << "[" << K << "];\n  #pragma unroll\n  for (int k = 0; k < " << K
           << "; ++k) { const i64 i = (i64)bid_ * " << block << " + threadIdx.x + (i64)k * " << span << "; " << a << "[k] = i < " << units
@@ -1634,14 +1667,7 @@ static std::string opaque_body(const CompGraph& g, int vertex, bool single, int 
       }
      }
     }
-    for (const auto& [a, lanes] : regs) {
-      s << "  #pragma unroll\n  for (int k = 0; k < (int)(sizeof(" << a << ") / sizeof(" << a << "[0])); ++k) ";
-      if (lanes == 4)
-        s << "acc += ((double)" << a << "[k].x + (double)" << a << "[k].y) + ((double)" << a << "[k].z + (double)" << a
-          << "[k].w);\n";
-      else
-        s << "acc += (double)" << a << "[k];\n";
-    }
+    fold();
   } else {
     // grid: 128-bit grid-stride loads, 4 independent accumulators per thread
     // so each thread keeps 4 loads in flight
@@ -1701,15 +1727,25 @@ static std::string opaque_body(const CompGraph& g, int vertex, bool single, int 
   return s.str();
 }
 
-// CTAs (one thread-block cluster) per small placeholder.  Default 1: one
-// CTA per op.  STITCH_OPAQUE_CLUSTER=0 sizes a cluster so every thread moves
-// at most one 128-bit chunk of each operand and of the output (capped at 8):
-// shorter per-warp chains (one CTA: ~190 instructions per warp at ~29 cycles
-// each, ncu DIEN pack3) but the cluster launch and barriers cost more -- DIEN
-// T=20 121.8 (1) vs 129.2 (auto, 3) vs 141.0 us (8),
-// profiles/r01/opaque_cluster_ab.jsonl; =<n> forces n.
+// CTAs (one thread-block cluster) per small placeholder.  Default: the
+// fewest CTAs (<= 8) whose threads hold every operand chunk in at most
+// kOpaqueRegChunks float4 registers -- 1 for DIEN's per-step gate GEMMs
+// (2 x [256,36] operands: 10 chunks per thread), 5 for the attention-score
+// GEMM over all T interest states (11 operands: 55 chunks per thread in one
+// CTA, which spilled 1.3 KB/thread and ran 20.8 us).  A cluster costs a
+// launch + barriers, so small ops stay single-CTA (DIEN T=20 121.8 (1) vs
+// 129.2 (3) vs 141.0 us (8) for the gate GEMMs,
+// profiles/r01/opaque_cluster_ab.jsonl).  STITCH_OPAQUE_CLUSTER=0 is the
+// older auto rule (one 128-bit chunk per thread of the largest tensor),
+// =<n> forces n.
 int opaque_cluster(const CompGraph& g, int vertex) {
-  if (const int c = env_int("STITCH_OPAQUE_CLUSTER", 1); c > 0) return std::min(c, 8);
+  const int c = env_int("STITCH_OPAQUE_CLUSTER", -1);
+  if (c > 0) return std::min(c, 8);
+  if (c < 0) {
+    for (int k = 1; k <= 8; ++k)
+      if (opaque_chunks_per_thread(g, vertex, int64_t(opaque_block()) * k) <= kOpaqueRegChunks) return k;
+    return 8;
+  }
   const OpNode& n = g.node(vertex);
   int64_t units = n.shape.element_count();
   for (int o : n.operands) units = std::max(units, g.node(o).shape.element_count());
