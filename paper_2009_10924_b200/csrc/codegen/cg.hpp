@@ -97,6 +97,32 @@ int opaque_cluster(const CompGraph& g, int vertex);  // CTAs (one cluster) per s
 std::optional<KernelSpec> generate_persistent_kernel(const std::vector<KernelSpec>& units, const std::string& name,
                                                      int max_ctas, const std::map<std::string, int64_t>& sizes);
 
+// While alive, generate_pattern_kernel emits every pattern for CTAs of
+// exactly `block` threads (the resident template's physical CTA): no
+// thread-block clusters, no PDL hooks.  TemplateMismatch if a row team needs
+// more threads.
+struct ForcedBlockScope {
+  int old;
+  explicit ForcedBlockScope(int block);
+  ~ForcedBlockScope();
+};
+
+// Resident template (cg_resident.cpp): a launch-bound plan whose tensors
+// all share a leading batch axis (every non-opaque op row-local) runs as ONE
+// thread-block cluster; CTA r owns batch rows [r*R, (r+1)*R).  Plan kernels
+// become phases separated by CTA barriers, their boundary tensors live in
+// the CTA's shared memory, and opaque placeholders (means over whole
+// operands) combine per-CTA partial sums through distributed shared memory
+// behind one cluster barrier.  `units` = the plan's launch units in
+// execution order (vertex sets; opaque = a single opaque_compute vertex).
+// nullopt when the graph is not row-shardable or does not fit.
+struct ResidentUnit {
+  std::vector<int> verts;
+  bool opaque = false;
+};
+std::optional<KernelSpec> generate_resident_kernel(const CompGraph& g, const std::vector<ResidentUnit>& units,
+                                                   const std::string& name, std::string* why = nullptr);
+
 // device helpers every module includes
 const std::string& device_prelude();
 

@@ -49,6 +49,10 @@ struct SmScope {
 };
 inline int sm_now() { return tl_sm_count; }
 
+// Resident generation (cg_resident.cpp): every pattern kernel is emitted for
+// one 1024-thread CTA that is also the physical CTA -- no clusters, no PDL
+thread_local int tl_force_block = 0;
+
 // When a kernel triggers its dependents (griddepcontrol.launch_dependents).
 // For large grids (STITCH_PDL_TRIGGER=entry_large, the default; =entry for
 // all): first thing in the kernel, before its
@@ -1382,8 +1386,15 @@ KernelSpec generate_pattern_kernel(const CompGraph& g, const std::vector<int>& v
       }
     }
   }
+  if (tl_force_block > 0) {
+    for (const auto& b : bodies)
+      if (b.kind == Kind::Row && row_params(b.dims_b, 0, b.tpr).TPR > tl_force_block)
+        throw TemplateMismatch("resident: row team wider than the CTA");
+    block = tl_force_block;
+    cluster = 1;
+  }
   em.block = block;
-  em.hoist = env_int("STITCH_PDL", 1) != 0 && env_int("STITCH_PDL_HOIST", 1) != 0;
+  em.hoist = tl_force_block == 0 && env_int("STITCH_PDL", 1) != 0 && env_int("STITCH_PDL_HOIST", 1) != 0;
   const int per_sm = std::max(1, std::min(env_int("STITCH_COL_CTAS", 3), 2048 / block));
 
   // CTA budget per body; scratch = [256 B reserved][strip arrival counters][f64 partials]
@@ -1561,7 +1572,7 @@ KernelSpec generate_pattern_kernel(const CompGraph& g, const std::vector<int>& v
   // programmatic dependent launch: hoisted prologue (parameter loads before
   // griddepcontrol.wait, Emitter::ensure_wait) unless STITCH_PDL_HOIST=0,
   // which waits at entry and triggers dependents at exit
-  const bool pdl = env_int("STITCH_PDL", 1) != 0;
+  const bool pdl = tl_force_block == 0 && env_int("STITCH_PDL", 1) != 0;
   const bool hoist = pdl && env_int("STITCH_PDL_HOIST", 1) != 0;
   k.source = sig.str() + (pdl && entry_trigger(k.grid) ? "  pdl_launch();\n" : "") +
              (pdl && !hoist ? "  pdl_wait();\n" : "") + body_src.str() + (pdl ? "  pdl_launch();\n" : "") + "}\n";
@@ -1860,5 +1871,8 @@ KernelSpec generate_opaque_pack(const CompGraph& g, const std::vector<int>& vert
   k.alg_bytes = bytes;
   return k;
 }
+
+ForcedBlockScope::ForcedBlockScope(int block) : old(tl_force_block) { tl_force_block = block; }
+ForcedBlockScope::~ForcedBlockScope() { tl_force_block = old; }
 
 }  // namespace stitch::gpu

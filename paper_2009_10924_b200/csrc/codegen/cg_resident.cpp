@@ -1,0 +1,534 @@
+// Resident template: a launch-bound plan as ONE thread-block cluster.
+//
+// Why.  On DIEN-like graphs (hundreds of [256,36] ops) every plan kernel is a
+// few hundred bytes of work per SM, so a CUDA Graph of kernels costs one
+// dependent-launch + L2 round trip per kernel boundary (~1.5-2.6 us per DIEN
+// unit, profiles/r02/dien_T10_timeline.txt), and the persistent template's
+// L2 completion counters cost about the same (profiles/r01/persistent_*).
+// The values themselves would fit on chip: a [256,36] f32 tensor is 36 KB.
+//
+// How.  Every tensor of the graph either carries the batch as its leading
+// axis ("sharded") or does not depend on the batch row at all
+// ("replicated"), and every non-opaque op is row-local: elementwise ops,
+// broadcasts that keep axis 0, reductions / slices / transposes that do not
+// touch axis 0.  CTA r of a cluster of C CTAs then owns batch rows
+// [r*R, (r+1)*R) of every sharded tensor and computes them alone:
+//   * each plan kernel (pattern / singleton / materialised constant) is the
+//     dataflow template generated for the SHARD graph (batch R instead of B,
+//     same node ids) with one 1024-thread CTA, called as a device function;
+//   * tensors that cross plan-kernel boundaries live in the CTA's shared
+//     memory (liveness-reused slots), graph parameters and outputs in their
+//     global buffers at the CTA's row offset; all accesses are generic
+//     loads/stores, ordered by CTA barriers only where a unit reads what an
+//     earlier unit since the last barrier wrote;
+//   * opaque placeholders (mean of every operand element, broadcast --
+//     src/sim.cpp:215-226) are the only cross-row ops: each CTA reduces its
+//     rows in f64, the partials meet through distributed shared memory behind
+//     ONE cluster barrier per group of independent placeholders, and every
+//     CTA folds the C partials in rank order (identical result everywhere).
+// The plan (patterns, per-op f32 rounding, the opaque semantics) is the one
+// the graph executor runs; only the kernel boundaries stay on chip.
+#include <algorithm>
+#include <cstdlib>
+#include <map>
+#include <optional>
+#include <regex>
+#include <set>
+#include <sstream>
+
+#include "codegen/cg.hpp"
+
+namespace stitch::gpu {
+
+namespace {
+
+int64_t prod_from(const std::vector<int64_t>& d, size_t from) {
+  int64_t p = 1;
+  for (size_t i = from; i < d.size(); ++i) p *= d[i];
+  return p;
+}
+
+bool is_elementwise(OpKind k) {
+  switch (k) {
+    case OpKind::Add: case OpKind::Sub: case OpKind::Mul: case OpKind::Div: case OpKind::Max: case OpKind::Min:
+    case OpKind::Exp: case OpKind::Tanh: case OpKind::Log: case OpKind::Rsqrt: case OpKind::Power:
+      return true;
+    default:
+      return false;
+  }
+}
+
+// batch extent: the leading dimension shared by most rank>=1 parameters
+int64_t batch_extent(const CompGraph& g) {
+  std::map<int64_t, int> votes;
+  for (const auto& n : g.nodes)
+    if (n.kind == OpKind::Parameter && n.shape.rank() >= 1) ++votes[n.shape.dims[0]];
+  int64_t best = 0;
+  int bv = 0;
+  for (auto [b, v] : votes)
+    if (v > bv || (v == bv && b > best)) best = b, bv = v;
+  return best;
+}
+
+// sharded[v]: v's leading axis is the batch row.  False + *why when some op
+// would mix rows (the graph is not row-shardable).
+bool analyse_rows(const CompGraph& g, int64_t B, std::vector<char>& sharded, std::string* why) {
+  auto fail = [&](const OpNode& n, const std::string& m) {
+    if (why) *why = "op " + n.name + ": " + m;
+    return false;
+  };
+  sharded.assign(g.nodes.size(), 0);
+  for (const auto& n : g.nodes) {
+    const bool lead_b = n.shape.rank() >= 1 && n.shape.dims[0] == B;
+    auto sh = [&](int o) { return sharded[static_cast<size_t>(o)] != 0; };
+    char& s = sharded[static_cast<size_t>(n.id)];
+    if (n.kind == OpKind::Parameter || n.kind == OpKind::Constant || n.kind == OpKind::OpaqueCompute) {
+      s = lead_b;
+    } else if (is_elementwise(n.kind)) {
+      for (int o : n.operands)
+        if (sh(o) != sh(n.operands[0])) return fail(n, "mixes batch-row and replicated operands");
+      s = sh(n.operands[0]);
+    } else if (n.kind == OpKind::Broadcast) {
+      const int x = n.operands[0];
+      const auto& d = n.attrs.dims;
+      if (sh(x)) {
+        if (d.empty() || d[0] != 0 || !lead_b) return fail(n, "broadcast moves the batch axis");
+        s = 1;
+      } else {
+        // replicated data: sharded only when axis 0 is pure replication
+        s = lead_b && std::find(d.begin(), d.end(), 0) == d.end();
+      }
+    } else if (n.kind == OpKind::ReduceSum || n.kind == OpKind::ReduceMax) {
+      if (sh(n.operands[0])) {
+        if (std::count(n.attrs.axes.begin(), n.attrs.axes.end(), 0)) return fail(n, "reduces over the batch axis");
+        s = 1;
+      }
+    } else if (n.kind == OpKind::Slice) {
+      if (sh(n.operands[0])) {
+        if (n.attrs.starts.empty() || n.attrs.starts[0] != 0 || n.attrs.limits[0] != B)
+          return fail(n, "slices the batch axis");
+        s = 1;
+      }
+    } else if (n.kind == OpKind::Transpose) {
+      if (sh(n.operands[0])) {
+        if (n.attrs.perm.empty() || n.attrs.perm[0] != 0) return fail(n, "transposes the batch axis");
+        s = 1;
+      }
+    } else {
+      for (int o : n.operands)
+        if (sh(o)) return fail(n, "gathers across batch rows");
+    }
+  }
+  return true;
+}
+
+// the pattern kernel's source as __device__ FN_(tensors..., vb_, vg_):
+// tensor params renamed positionally, every global access generic
+std::string as_resident_function(const KernelSpec& k) {
+  const std::string& src = k.source;
+  const size_t at = src.find(k.name + "(");
+  if (src.compare(0, 10, "extern \"C\"") != 0 || at == std::string::npos)
+    throw std::invalid_argument("resident: unexpected kernel header in " + k.name);
+  std::string body = "__device__ __forceinline__ void FN_(" + src.substr(at + k.name.size() + 1);
+  int pi = 0;
+  for (const auto* list : {&k.inputs, &k.outputs})
+    for (const auto& t : *list)
+      body = std::regex_replace(body, std::regex("\\b" + regex_escape(tensor_ident(t)) + "\\b"), "p" + std::to_string(pi++) + "_");
+  const size_t close = body.find(") {\n");
+  if (close == std::string::npos) throw std::invalid_argument("resident: no signature end in " + k.name);
+  body.insert(close, ", const int vb_, const int vg_");
+  static const std::vector<std::pair<std::regex, std::string>> rewrites = {
+      {std::regex(R"(\bblockIdx\.x\b)"), "vb_"},
+      {std::regex(R"(\bgridDim\.x\b)"), "vg_"},
+      {std::regex(R"(__restrict__)"), ""},
+      {std::regex(R"(\bld4[ckp]?\()"), "ld4_g("},
+      {std::regex(R"(\bld4hk?\()"), "ld4h_g("},
+      {std::regex(R"(\bldv[kp]?\()"), "ldv_g("},
+      {std::regex(R"(\b__ldg\()"), "ldg_g("},
+      {std::regex(R"(\bst4\()"), "st4_g("},
+      {std::regex(R"(\bst4h\()"), "st4h_g("},
+      {std::regex(R"(\bpdl_(wait|launch)\(\);)"), ""},
+      {std::regex(R"(\bSTC_TRACE_[A-Z_]+\([^)]*\);)"), ""},
+  };
+  for (const auto& [re, to] : rewrites) body = std::regex_replace(body, re, to);
+  return std::regex_replace(body, std::regex(R"(\bblockDim\.x\b)"), std::to_string(k.block));
+}
+
+struct Slot {
+  int64_t off = 0, bytes = 0;
+};
+
+}  // namespace
+
+std::optional<KernelSpec> generate_resident_kernel(const CompGraph& g, const std::vector<ResidentUnit>& units,
+                                                   const std::string& name, std::string* why) {
+  auto no = [&](const std::string& m) -> std::optional<KernelSpec> {
+    if (why) *why = m;
+    return std::nullopt;
+  };
+  if (units.size() < 2) return no("fewer than two launch units");
+  const int64_t B = batch_extent(g);
+  if (B < 1) return no("no batch axis");
+  std::vector<char> sharded;
+  if (!analyse_rows(g, B, sharded, why)) return std::nullopt;
+  // cluster size: the most CTAs (<= 16) with a whole number of rows each,
+  // a multiple of 4 (16-byte aligned row blocks for 128-bit accesses)
+  int C = 1;
+  for (int c : {16, 8, 4, 2})
+    if (B % c == 0 && (B / c) % 4 == 0) {
+      C = c;
+      break;
+    }
+  const int64_t R = B / C;
+  CompGraph gs = g;  // the shard graph: batch R, same node ids
+  for (auto& n : gs.nodes) {
+    if (!sharded[static_cast<size_t>(n.id)]) continue;
+    n.shape.dims[0] = R;
+    if (n.kind == OpKind::Slice) n.attrs.limits[0] = static_cast<int>(R);
+  }
+  auto local_elems = [&](int v) {
+    const auto& sh = g.node(v).shape;
+    return sharded[static_cast<size_t>(v)] ? R * prod_from(sh.dims, 1) : sh.element_count();
+  };
+  auto local_bytes = [&](int v) { return local_elems(v) * dtype_bytes(g.node(v).shape.dtype); };
+
+  // per unit: generated code (patterns) or the opaque vertex
+  struct U {
+    std::vector<int> verts;
+    bool opaque = false;
+    KernelSpec spec;  // patterns
+    std::vector<int> ins, outs;  // tensor vertex ids
+    std::set<size_t> deps;
+  };
+  std::vector<U> us(units.size());
+  std::map<int, size_t> producer;  // tensor vertex -> unit
+  for (size_t i = 0; i < units.size(); ++i) {
+    U& u = us[i];
+    u.verts = units[i].verts;
+    u.opaque = units[i].opaque;
+    if (u.opaque) {
+      if (u.verts.size() != 1) return no("opaque unit with several vertices");
+      const OpNode& n = g.node(u.verts[0]);
+      std::set<int> seen;
+      for (int o : n.operands)
+        if (seen.insert(o).second) u.ins.push_back(o);
+      u.outs = {n.id};
+    } else {
+      try {
+        const ForcedBlockScope fb(1024);
+        u.spec = generate_pattern_kernel(gs, u.verts, "RK_", 1);
+      } catch (const std::exception& e) {
+        return no(std::string("unit ") + g.node(u.verts.front()).name + ": " + e.what());
+      }
+      if (u.spec.scratch_bytes > 0 || u.spec.cooperative || u.spec.cluster > 1 || u.spec.smem > 0 || u.spec.block != 1024)
+        return no("unit " + g.node(u.verts.front()).name + " needs a grid-wide template (" + u.spec.tmpl + ")");
+      for (const auto& t : u.spec.inputs) u.ins.push_back(g.by_name.at(t));
+      for (const auto& t : u.spec.outputs) u.outs.push_back(g.by_name.at(t));
+    }
+    for (int t : u.outs) producer[t] = i;
+  }
+  std::vector<std::vector<size_t>> users(us.size());
+  for (size_t i = 0; i < us.size(); ++i)
+    for (int t : us[i].ins) {
+      if (auto it = producer.find(t); it != producer.end()) {
+        if (it->second != i && us[i].deps.insert(it->second).second) users[it->second].push_back(i);
+      } else if (g.node(t).kind != OpKind::Parameter) {
+        return no("tensor " + g.node(t).name + " is read but produced by no unit");
+      }
+    }
+
+  // schedule: CTA-local units as soon as they are ready; ready placeholders
+  // wait until nothing else is, then run together behind one cluster barrier
+  std::vector<std::vector<size_t>> steps;  // one unit, or a group of placeholders
+  {
+    std::vector<size_t> pending(us.size());
+    std::set<size_t> ready;
+    for (size_t i = 0; i < us.size(); ++i)
+      if (!(pending[i] = us[i].deps.size())) ready.insert(i);
+    size_t done = 0;
+    auto finish = [&](size_t i) {
+      ++done;
+      for (size_t w : users[i])
+        if (--pending[w] == 0) ready.insert(w);
+    };
+    while (!ready.empty()) {
+      auto it = std::find_if(ready.begin(), ready.end(), [&](size_t i) { return !us[i].opaque; });
+      if (it != ready.end()) {
+        const size_t i = *it;
+        ready.erase(it);
+        steps.push_back({i});
+        finish(i);
+        continue;
+      }
+      std::vector<size_t> grp(ready.begin(), ready.end());
+      ready.clear();
+      steps.push_back(grp);
+      for (size_t i : grp) finish(i);
+    }
+    if (done != us.size()) return no("unit dependency cycle");
+  }
+
+  // placement: graph parameters / outputs in global memory, everything else
+  // crossing a unit boundary in a shared-memory slot (reused after the
+  // barrier that follows its last reader)
+  std::set<int> graph_out(g.outputs.begin(), g.outputs.end());
+  std::map<int, size_t> last_step;
+  for (size_t s = 0; s < steps.size(); ++s)
+    for (size_t i : steps[s])
+      for (int t : us[i].ins) last_step[t] = s;
+  std::map<int, Slot> slot;
+  std::vector<Slot> free_list, pending_free;
+  int64_t smem_top = 0;
+  constexpr int64_t kSmemCap = 200 * 1024;
+  auto alloc = [&](int64_t bytes) {
+    bytes = (bytes + 127) / 128 * 128;
+    std::sort(free_list.begin(), free_list.end(), [](const Slot& a, const Slot& b) { return a.off < b.off; });
+    for (size_t i = 0; i < free_list.size(); ++i)
+      if (free_list[i].bytes >= bytes) {
+        Slot s{free_list[i].off, bytes};
+        free_list[i].off += bytes;
+        free_list[i].bytes -= bytes;
+        if (free_list[i].bytes == 0) free_list.erase(free_list.begin() + static_cast<long>(i));
+        return s;
+      }
+    Slot s{smem_top, bytes};
+    smem_top += bytes;
+    return s;
+  };
+
+  std::ostringstream fns, body;
+  std::map<std::string, std::string> fn_of;  // canonical unit source -> function name
+  auto ptr = [&](int t) -> std::string {
+    const OpNode& n = g.node(t);
+    const std::string ty = c_type(n.shape.dtype);
+    if (auto it = slot.find(t); it != slot.end())
+      return "reinterpret_cast<" + ty + "*>(rs_smem_ + " + std::to_string(it->second.off) + ")";
+    const std::string off = sharded[static_cast<size_t>(t)] ? " + (i64)rk_ * " + std::to_string(local_elems(t)) : "";
+    return "(" + tensor_ident(n.name) + off + ")";
+  };
+  std::set<size_t> since_barrier;  // units executed after the last CTA barrier
+  std::set<int> params_used, outs_written;
+  int opaque_slots = 0, max_group = 1, n_barriers = 0, n_cluster = 0;
+  auto barrier = [&]() {
+    body << "  __syncthreads();\n";
+    ++n_barriers;
+    since_barrier.clear();
+    free_list.insert(free_list.end(), pending_free.begin(), pending_free.end());
+    pending_free.clear();
+  };
+  auto place_outputs = [&](size_t i) {
+    for (int t : us[i].outs) {
+      if (graph_out.count(t)) {
+        outs_written.insert(t);
+        continue;
+      }
+      if (slot.count(t)) continue;
+      slot[t] = alloc(local_bytes(t));
+    }
+  };
+  std::set<int> retired;  // a tensor read by several members of a group is freed once
+  auto retire_inputs = [&](size_t s) {
+    for (size_t i : steps[s])
+      for (int t : us[i].ins)
+        if (last_step[t] == s && slot.count(t) && !graph_out.count(t) && retired.insert(t).second)
+          pending_free.push_back(slot[t]);
+  };
+  // graph parameters: staged whole into shared memory at kernel entry by
+  // the TMA engine (one cp.async.bulk per parameter slice -- a sharded
+  // slice is R contiguous rows -- completing on one mbarrier), so every unit
+  // reads them on chip; slots are reused after their last reader like any
+  // other.  STITCH_RESIDENT_STAGE=0 reads them from global memory instead.
+  std::vector<int> staged;
+  int64_t staged_bytes = 0;
+  {
+    const char* st = std::getenv("STITCH_RESIDENT_STAGE");
+    const bool stage = !(st && *st == '0');
+    std::set<int> ps;
+    for (const auto& u : us)
+      for (int t : u.ins)
+        if (g.node(t).kind == OpKind::Parameter) ps.insert(t);
+    for (int t : ps)
+      if (stage && local_bytes(t) % 16 == 0 && local_bytes(t) > 0) {
+        slot[t] = alloc(local_bytes(t));
+        staged.push_back(t);
+        staged_bytes += local_bytes(t);
+      }
+  }
+  const std::set<int> staged_set(staged.begin(), staged.end());
+  bool staged_ready = staged.empty();
+  for (size_t s = 0; s < steps.size(); ++s) {
+    if (!staged_ready) {
+      bool reads = false;
+      for (size_t i : steps[s])
+        for (int t : us[i].ins) reads = reads || staged_set.count(t);
+      if (reads) {
+        body << "  mbar_wait(&rs_mbar_, 0u);  // staged parameters have landed\n";
+        staged_ready = true;
+      }
+    }
+    bool need = false;
+    for (size_t i : steps[s])
+      for (size_t d : us[i].deps) need = need || since_barrier.count(d);
+    if (need) barrier();
+    // diagnostics (STITCH_TRACE builds): slot 1+s = [first CTA entering step
+    // s, last CTA leaving it]
+    if (s) body << "  STC_TRACE_STAMP_END(" << s << ");\n";
+    body << "  STC_TRACE_BEGIN(" << 1 + s << ");\n";
+    for (size_t i : steps[s])
+      for (int t : us[i].ins)
+        if (g.node(t).kind == OpKind::Parameter) params_used.insert(t);
+    if (!us[steps[s][0]].opaque) {
+      const size_t i = steps[s][0];
+      place_outputs(i);
+      const std::string canon = as_resident_function(us[i].spec);
+      auto it = fn_of.find(canon);
+      if (it == fn_of.end()) {
+        it = fn_of.emplace(canon, "ru" + std::to_string(fn_of.size()) + "_").first;
+        fns << std::regex_replace(canon, std::regex("\\bFN_\\("), it->second + "(") << "\n";
+      }
+      body << "  // unit " << i << ": " << us[i].spec.tmpl << " {" << g.node(us[i].verts.front()).name
+           << (us[i].verts.size() > 1 ? ", ..." : "") << "} grid " << us[i].spec.grid << "\n";
+      body << "  for (int v_ = 0; v_ < " << us[i].spec.grid << "; ++v_) " << it->second << "(";
+      for (const auto& tn : us[i].spec.inputs) body << ptr(g.by_name.at(tn)) << ", ";
+      for (const auto& tn : us[i].spec.outputs) body << ptr(g.by_name.at(tn)) << ", ";
+      body << "v_, " << us[i].spec.grid << ");\n";
+      since_barrier.insert(i);
+      retire_inputs(s);
+      // a unit with its own shared scratch (cross-warp team reductions):
+      // the next call of the same function must not overwrite it early
+      if (canon.find("__shared__") != std::string::npos) barrier();
+      continue;
+    }
+    // a group of opaque placeholders: f64 partials of this CTA's rows,
+    // block fold, one cluster barrier, rank-ordered fold of the C partials
+    const auto& grp = steps[s];
+    max_group = std::max<int>(max_group, static_cast<int>(grp.size()));
+    body << "  {  // placeholder group:";
+    for (size_t i : grp) body << " " << g.node(us[i].verts[0]).name;
+    body << "\n";
+    // one f64 partial per DISTINCT operand slice (the group's placeholders
+    // share operands: x_t and h_t), then each member adds the partials of
+    // its operand list -- an operand listed twice counts twice (opaque_body)
+    std::map<int, int> dk;  // operand vertex -> partial index
+    for (size_t j : grp)
+      for (int o : g.node(us[j].verts[0]).operands) dk.emplace(o, static_cast<int>(dk.size()));
+    for (auto [o, k] : dk) {
+      const TensorShape& sh = g.node(o).shape;
+      const int64_t cnt = local_elems(o);
+      const std::string guard = !sharded[static_cast<size_t>(o)] ? "if (rk_ == 0) " : "";
+      body << "    double d" << k << "_ = 0.0;\n";
+      if (sh.dtype == DType::F32 && cnt % 4 == 0)
+        body << "    " << guard << "for (int i = threadIdx.x; i < " << cnt / 4 << "; i += 1024) { const float4 q = ld4_g("
+             << ptr(o) << " + 4 * i); d" << k << "_ += ((double)q.x + (double)q.y) + ((double)q.z + (double)q.w); }\n";
+      else
+        body << "    " << guard << "for (int i = threadIdx.x; i < " << cnt << "; i += 1024) d" << k << "_ += (double)ldv_g("
+             << ptr(o) << ", i);\n";
+    }
+    for (size_t j = 0; j < grp.size(); ++j) {
+      body << "    { double a_ = 0.0";
+      for (int o : g.node(us[grp[j]].verts[0]).operands) body << " + d" << dk[o] << "_";
+      body << ";\n      a_ = bfly_sum(a_, 32);\n      if ((threadIdx.x & 31) == 0) rs_red_[" << j * 32
+           << " + (threadIdx.x >> 5)] = a_; }\n";
+    }
+    // warp j folds member j's 32 warp sums into this CTA's partial
+    body << "    __syncthreads();\n    {\n      const int w_ = threadIdx.x >> 5, l_ = threadIdx.x & 31;\n";
+    for (size_t j = 0; j < grp.size(); ++j)
+      body << "      if (w_ == " << j % 32 << ") { const double v_ = bfly_sum(rs_red_[" << j * 32
+           << " + l_], 32); if (l_ == 0) rs_part_[" << opaque_slots + static_cast<int>(j) << "] = v_; }\n";
+    body << "    }\n    cluster_sync_all();\n";
+    ++n_cluster;
+    // warp j: lane r reads rank r's partial of member j (DSMEM, all in
+    // flight at once); a butterfly folds them in the same order in every CTA
+    body << "    {\n      const int w_ = threadIdx.x >> 5, l_ = threadIdx.x & 31;\n";
+    for (size_t j = 0; j < grp.size(); ++j) {
+      const OpNode& n = g.node(us[grp[j]].verts[0]);
+      int64_t count = 0;
+      for (int o : n.operands) count += g.node(o).shape.element_count();
+      body << "      if (w_ == " << j % 32 << ") { double t_ = l_ < " << C << " ? ld_dsmem_f64(&rs_part_["
+           << opaque_slots + static_cast<int>(j) << "], (unsigned)l_) : 0.0; t_ = bfly_sum(t_, 32); if (l_ == 0) rs_fill_["
+           << j << "] = (float)(" << (count ? "t_ / " + std::to_string(count) + ".0" : "0.0") << "); }\n";
+    }
+    body << "    }\n    __syncthreads();\n";
+    for (size_t i : grp) place_outputs(i);
+    for (size_t j = 0; j < grp.size(); ++j) {
+      const OpNode& n = g.node(us[grp[j]].verts[0]);
+      const int64_t nout = local_elems(n.id);
+      const bool rep_out = !sharded[static_cast<size_t>(n.id)] && graph_out.count(n.id);
+      const std::string guard = rep_out ? "if (rk_ == 0) " : "";
+      body << "    { const float fill = rs_fill_[" << j << "];\n";
+      if (n.shape.dtype == DType::F32 && nout % 4 == 0)
+        body << "      " << guard << "for (int i = threadIdx.x; i < " << nout / 4 << "; i += 1024) st4_g(" << ptr(n.id)
+             << " + 4 * i, fill, fill, fill, fill); }\n";
+      else
+        body << "      " << guard << "for (int i = threadIdx.x; i < " << nout << "; i += 1024) stv(" << ptr(n.id)
+             << ", i, fill); }\n";
+    }
+    body << "  }\n";
+    opaque_slots += static_cast<int>(grp.size());
+    // the cluster barrier ordered everything before it
+    since_barrier.clear();
+    free_list.insert(free_list.end(), pending_free.begin(), pending_free.end());
+    pending_free.clear();
+    for (size_t i : grp) since_barrier.insert(i);
+    retire_inputs(s);
+  }
+  body << "  STC_TRACE_STAMP_END(" << steps.size() << ");\n";
+  if (smem_top > kSmemCap)
+    return no("boundary tensors need " + std::to_string(smem_top) + " B of shared memory per CTA");
+
+  KernelSpec k;
+  k.name = name;
+  k.tmpl = "resident(" + std::to_string(us.size()) + " units, " + std::to_string(steps.size()) + " steps, cluster " +
+           std::to_string(C) + ")";
+  k.grid = C;
+  k.block = 1024;
+  k.cluster = C;
+  k.smem = std::max<int64_t>(smem_top, 16);
+  std::ostringstream s;
+  s << fns.str();
+  s << "extern \"C\" __global__ void __launch_bounds__(1024, 1) " << name << "(";
+  bool first = true;
+  for (int t : params_used) {
+    s << (first ? "" : ", ") << "const " << c_type(g.node(t).shape.dtype) << "* " << tensor_ident(g.node(t).name);
+    k.inputs.push_back(g.node(t).name);
+    first = false;
+  }
+  for (int t : outs_written) {
+    s << (first ? "" : ", ") << c_type(g.node(t).shape.dtype) << "* " << tensor_ident(g.node(t).name);
+    k.outputs.push_back(g.node(t).name);
+    first = false;
+  }
+  s << ") {\n"
+    << "  // " << B << " batch rows, " << R << " per CTA; " << us.size() << " plan units in " << steps.size()
+    << " steps, " << n_barriers << " CTA barriers, " << n_cluster << " cluster barriers; " << smem_top
+    << " B of boundary tensors per CTA\n"
+    << "  extern __shared__ __align__(128) unsigned char rs_smem_[];\n"
+    << "  __shared__ double rs_red_[" << 32 * max_group << "];\n"
+    << "  __shared__ double rs_part_[" << std::max(1, opaque_slots) << "];\n"
+    << "  __shared__ float rs_fill_[" << max_group << "];\n"
+    << "  const int rk_ = (int)cluster_ctarank();\n  (void)rk_;\n";
+  if (!staged.empty()) {
+    s << "  __shared__ __align__(8) unsigned long long rs_mbar_;\n"
+      << "  if (threadIdx.x == 0) {\n    mbar_init(&rs_mbar_, 1);\n    mbar_fence_init();\n"
+      << "    mbar_expect_tx(&rs_mbar_, " << staged_bytes << "u);\n";
+    for (int t : staged) {
+      const std::string off = sharded[static_cast<size_t>(t)] ? " + (i64)rk_ * " + std::to_string(local_elems(t)) : "";
+      s << "    bulk_g2s(rs_smem_ + " << slot[t].off << ", " << tensor_ident(g.node(t).name) << off << ", "
+        << local_bytes(t) << "u, &rs_mbar_);\n";
+    }
+    s << "  }\n  __syncthreads();  // the mbarrier is initialised before anyone waits on it\n";
+  }
+  s << body.str()
+    << "  cluster_sync_all();  // peers may still read rs_part_ through DSMEM\n}\n";
+  k.source = s.str();
+  for (const auto& u : us) k.alg_bytes += u.opaque ? 0 : u.spec.alg_bytes;
+  for (const auto& u : us)
+    if (u.opaque) {
+      const OpNode& n = g.node(u.verts[0]);
+      k.alg_bytes += n.shape.byte_size();
+      for (int o : u.ins) k.alg_bytes += g.node(o).shape.byte_size();
+    }
+  return k;
+}
+
+}  // namespace stitch::gpu

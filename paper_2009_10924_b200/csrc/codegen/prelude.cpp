@@ -182,6 +182,27 @@ __device__ __forceinline__ void st4h(f16_t* p, float x, float y, float z, float 
   asm volatile("st.global.cs.v2.u32 [%0], {%1,%2};" :: "l"(p), "r"(a), "r"(b) : "memory");
 }
 
+// generic-address loads/stores (resident template): a unit's tensors may be
+// graph buffers in global memory or slots in the CTA's shared memory, and
+// every value read was written by this CTA before a CTA barrier
+__device__ __forceinline__ float ldv_g(const float* p, i64 i) { return p[i]; }
+__device__ __forceinline__ float ldv_g(const f16_t* p, i64 i) { return h2f(p[i]); }
+__device__ __forceinline__ float ldv_g(const int* p, i64 i) { return (float)p[i]; }
+__device__ __forceinline__ float ldv_g(const unsigned char* p, i64 i) { return p[i] ? 1.f : 0.f; }
+__device__ __forceinline__ float4 ld4_g(const float* p) { return *reinterpret_cast<const float4*>(p); }
+__device__ __forceinline__ float4 ld4h_g(const f16_t* p) {
+  const uint2 q = *reinterpret_cast<const uint2*>(p);
+  return make_float4(h2f((f16_t)(q.x & 0xffffu)), h2f((f16_t)(q.x >> 16)), h2f((f16_t)(q.y & 0xffffu)), h2f((f16_t)(q.y >> 16)));
+}
+__device__ __forceinline__ void st4_g(float* p, float a, float b, float c, float d) {
+  *reinterpret_cast<float4*>(p) = make_float4(a, b, c, d);
+}
+__device__ __forceinline__ void st4h_g(f16_t* p, float x, float y, float z, float w) {
+  *reinterpret_cast<uint2*>(p) = make_uint2((unsigned)f2h(x) | ((unsigned)f2h(y) << 16), (unsigned)f2h(z) | ((unsigned)f2h(w) << 16));
+}
+template <typename T>
+__device__ __forceinline__ T ldg_g(const T* p) { return *p; }
+
 // e^x as 2^(x log2 e): one FMUL + MUFU.EX2.  Relative error <= |x| 2^-24
 // (rounding of the product) + 2^-22 (ex2.approx) < 5.5e-6 for every finite
 // result (|x| < 88.7) -- inside the 1e-5 elementwise band; results below

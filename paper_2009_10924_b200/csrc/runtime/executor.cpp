@@ -449,6 +449,7 @@ PlanKernels generate_plan_kernels(const CompGraph& g_, const FusionPlan& plan,
         const int w = unit_of[static_cast<size_t>(o)];
         if (w >= 0 && w != static_cast<int>(u) && deps[u].insert(w).second) users[static_cast<size_t>(w)].push_back(static_cast<int>(u));
       }
+  std::vector<ResidentUnit> runits;      // spec index -> its vertices (resident template)
   std::map<size_t, int> opaque_vertex;  // spec index -> vertex of a placeholder kernel
   std::map<size_t, std::vector<int>> local_verts;  // spec index -> vertices of a local-template kernel
   std::set<std::pair<int, int>> ready;  // (fire position, unit)
@@ -483,10 +484,26 @@ PlanKernels generate_plan_kernels(const CompGraph& g_, const FusionPlan& plan,
       add_pattern(un.verts, un.key);
       if (specs_.back().tmpl == "local" || specs_.back().tmpl == "regional") local_verts[specs_.size() - 1] = un.verts;
     }
+    runits.push_back({un.verts, un.opaque});
     for (int w : users[static_cast<size_t>(u)])
       if (--pending[static_cast<size_t>(w)] == 0) ready.insert({units[static_cast<size_t>(w)].fire, w});
   }
   if (specs_.size() != units.size()) throw std::runtime_error("[exec] contracted plan graph has a cycle");
+  // Resident template (cg_resident.cpp, STITCH_RESIDENT=1): a row-shardable
+  // launch-bound plan runs as one thread-block cluster, plan-kernel
+  // boundaries kept in shared memory.  Falls back to the launch graph below
+  // when the plan does not fit (reason on stderr with STITCH_RESIDENT_LOG=1).
+  if (const char* rv = std::getenv("STITCH_RESIDENT");
+      rv && *rv == '1' && mode == ExecMode::Stitched && !gemm_opaque) {
+    std::string why;
+    if (auto rk = generate_resident_kernel(g_, runits, "k" + std::to_string(idx++) + "_resident", &why)) {
+      specs_ = {std::move(*rk)};
+      opaque_vertex.clear();
+      local_verts.clear();
+    }
+    if (const char* lg = std::getenv("STITCH_RESIDENT_LOG"); lg && *lg == '1')
+      std::fprintf(stderr, "[exec] resident template not used: %s\n", why.c_str());
+  }
   // Horizontal packing.  Launch units with the same producer kernels are
   // mutually independent; two kinds are packed into one launch each:
   //  * small opaque placeholders (DIEN's three gate GEMMs of a step read only
@@ -589,7 +606,7 @@ PlanKernels generate_plan_kernels(const CompGraph& g_, const FusionPlan& plan,
   // Launch-bound plans (every unit small, e.g. DIEN): all units inside one
   // cooperative launch (cg_persist.cpp), unit boundaries as L2 completion
   // counters instead of kernel boundaries.  STITCH_PERSIST=1 enables it.
-  if (const char* pe = std::getenv("STITCH_PERSIST"); pe && *pe == '1' && mode != ExecMode::Program) {
+  if (const char* pe = std::getenv("STITCH_PERSIST"); pe && *pe == '1' && mode != ExecMode::Program && specs_.size() > 1) {
     const char* mc = std::getenv("STITCH_PERSIST_MAX_CTAS");
     std::map<std::string, int64_t> sizes;
     for (const auto& n : g_.nodes) sizes[n.name] = n.shape.byte_size();
@@ -1096,6 +1113,9 @@ std::vector<std::pair<double, double>> Executor::trace(int set) {
   // a persistent kernel also stamps each of its units (slots 1..U)
   size_t n = specs_.size();
   if (n == 1 && specs_[0].tmpl.rfind("persistent(", 0) == 0) n = 1 + std::stoul(specs_[0].tmpl.substr(11));
+  // ... and a resident kernel each of its steps
+  if (std::smatch m; n == 1 && std::regex_search(specs_[0].tmpl, m, std::regex(R"(^resident\(.* (\d+) steps)")))
+    n = 1 + std::stoul(m[1].str());
   std::vector<unsigned long long> init(2 * n);
   for (size_t i = 0; i < n; ++i) init[2 * i] = ~0ull, init[2 * i + 1] = 0ull;
   ensure_sets(set + 1);
