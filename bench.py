@@ -262,20 +262,27 @@ def time_subgraph(stitch, name, gemm=False, refine=False):
                         "frac_event": round(desc[top]["bytes"] / kus[top] / 1e3 / peak, 4)}}
     del ex
     if len(desc) != plan_kernels and not refine:
-        saved = {k: os.environ.get(k) for k in ("STITCH_OPAQUE_PACK", "STITCH_LOCAL_PACK")}
-        os.environ["STITCH_OPAQUE_PACK"] = os.environ["STITCH_LOCAL_PACK"] = "0"
-        try:
-            pex, pus, pus1, _ = _exec_timing(stitch, plan, g, gemm)
-            out["parity_mode"] = {"launches": pex.num_kernels, "us": round(pus, 3),
-                                  "us_one_launch_per_step": round(pus1, 3),
-                                  "note": "STITCH_OPAQUE_PACK=0 STITCH_LOCAL_PACK=0: one launch per plan kernel"}
-            del pex
-        finally:
-            for k, v in saved.items():
-                if v is None:
-                    os.environ.pop(k, None)
-                else:
-                    os.environ[k] = v
+        # the same plan as a launch graph: packed (default packing), and in
+        # parity mode (one launch per plan kernel)
+        variants = [("launch_graph", {"STITCH_RESIDENT": "0"},
+                     "STITCH_RESIDENT=0: the plan's CUDA Graph of kernels (launch packing on)")] \
+            if desc[0]["template"].startswith("resident(") else []
+        variants.append(("parity_mode", {"STITCH_RESIDENT": "0", "STITCH_OPAQUE_PACK": "0", "STITCH_LOCAL_PACK": "0"},
+                         "STITCH_RESIDENT=0 STITCH_OPAQUE_PACK=0 STITCH_LOCAL_PACK=0: one launch per plan kernel"))
+        for key, env, note in variants:
+            saved = {k: os.environ.get(k) for k in env}
+            os.environ.update(env)
+            try:
+                pex, pus, pus1, _ = _exec_timing(stitch, plan, g, gemm)
+                out[key] = {"launches": pex.num_kernels, "us": round(pus, 3), "us_one_launch_per_step": round(pus1, 3),
+                            "note": note}
+                del pex
+            finally:
+                for k, v in saved.items():
+                    if v is None:
+                        os.environ.pop(k, None)
+                    else:
+                        os.environ[k] = v
     return out
 
 

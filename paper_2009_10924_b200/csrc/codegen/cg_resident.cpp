@@ -355,6 +355,28 @@ std::optional<KernelSpec> generate_resident_kernel(const CompGraph& g, const std
       }
   }
   const std::set<int> staged_set(staged.begin(), staged.end());
+  // every CTA writes its rows of each placeholder output with the folded mean
+  auto emit_fills = [&](const std::vector<size_t>& grp) {
+    for (size_t i : grp) place_outputs(i);
+    for (size_t j = 0; j < grp.size(); ++j) {
+      const OpNode& n = g.node(us[grp[j]].verts[0]);
+      const int64_t nout = local_elems(n.id);
+      const bool rep_out = !sharded[static_cast<size_t>(n.id)] && graph_out.count(n.id);
+      const std::string guard = rep_out ? "if (rk_ == 0) " : "";
+      body << "    { const float fill = rs_fill_[" << j << "];\n";
+      if (n.shape.dtype == DType::F32 && nout % 4 == 0)
+        body << "      " << guard << "for (int i = threadIdx.x; i < " << nout / 4 << "; i += 1024) st4_g(" << ptr(n.id)
+             << " + 4 * i, fill, fill, fill, fill); }\n";
+      else
+        body << "      " << guard << "for (int i = threadIdx.x; i < " << nout << "; i += 1024) stv(" << ptr(n.id)
+             << ", i, fill); }\n";
+    }
+  };
+  // STITCH_RESIDENT_PUSH=0: placeholder partials meet behind a cluster
+  // barrier (DSMEM pull) instead of st.async pushes + per-group mbarriers
+  const char* pv = std::getenv("STITCH_RESIDENT_PUSH");
+  const bool push = C > 1 && !(pv && *pv == '0');
+  int n_push = 0;
   bool staged_ready = staged.empty();
   for (size_t s = 0; s < steps.size(); ++s) {
     if (!staged_ready) {
@@ -412,29 +434,94 @@ std::optional<KernelSpec> generate_resident_kernel(const CompGraph& g, const std
     std::map<int, int> dk;  // operand vertex -> partial index
     for (size_t j : grp)
       for (int o : g.node(us[j].verts[0]).operands) dk.emplace(o, static_cast<int>(dk.size()));
-    for (auto [o, k] : dk) {
-      const TensorShape& sh = g.node(o).shape;
-      const int64_t cnt = local_elems(o);
-      const std::string guard = !sharded[static_cast<size_t>(o)] ? "if (rk_ == 0) " : "";
-      body << "    double d" << k << "_ = 0.0;\n";
-      if (sh.dtype == DType::F32 && cnt % 4 == 0)
-        body << "    " << guard << "for (int i = threadIdx.x; i < " << cnt / 4 << "; i += 1024) { const float4 q = ld4_g("
-             << ptr(o) << " + 4 * i); d" << k << "_ += ((double)q.x + (double)q.y) + ((double)q.z + (double)q.w); }\n";
-      else
-        body << "    " << guard << "for (int i = threadIdx.x; i < " << cnt << "; i += 1024) d" << k << "_ += (double)ldv_g("
-             << ptr(o) << ", i);\n";
+    // small slices (every DIEN operand: 144 float4 per CTA): warp k folds
+    // operand k on its own (strided 128-bit loads + one butterfly), all
+    // operands in parallel, then thread j adds member j's operand partials;
+    // larger ones: block-wide per-thread partials + two-level fold
+    bool warp_path = dk.size() <= 32;
+    for (auto [o, k] : dk) warp_path = warp_path && local_elems(o) <= 16384;
+    if (warp_path) {
+      body << "    {\n      const int w_ = threadIdx.x >> 5, l_ = threadIdx.x & 31;\n";
+      for (auto [o, k] : dk) {
+        const TensorShape& sh = g.node(o).shape;
+        const int64_t cnt = local_elems(o);
+        const std::string guard = !sharded[static_cast<size_t>(o)] ? " && rk_ == 0" : "";
+        body << "      if (w_ == " << k << ") { double d_ = 0.0;\n        if (true" << guard << ") ";
+        if (sh.dtype == DType::F32 && cnt % 4 == 0)
+          body << "for (int i = l_; i < " << cnt / 4 << "; i += 32) { const float4 q = ld4_g(" << ptr(o)
+               << " + 4 * i); d_ += ((double)q.x + (double)q.y) + ((double)q.z + (double)q.w); }\n";
+        else
+          body << "for (int i = l_; i < " << cnt << "; i += 32) d_ += (double)ldv_g(" << ptr(o) << ", i);\n";
+        body << "        d_ = bfly_sum(d_, 32); if (l_ == 0) rs_red_[" << k << "] = d_; }\n";
+      }
+      body << "    }\n    __syncthreads();\n";
+      if (push && static_cast<int64_t>(grp.size()) * C <= 1024) {
+        // push: thread (j, r) sends member j's partial to rank r's inbox
+        // (st.async, completing on rank r's mbarrier of this group); every
+        // CTA waits only for the C x G partials addressed to it
+        body << "    if (threadIdx.x < " << grp.size() * C << ") {\n      const int j_ = threadIdx.x / " << C
+             << ", r_ = threadIdx.x % " << C << ";\n      double v_ = 0.0;\n";
+        for (size_t j = 0; j < grp.size(); ++j) {
+          body << "      " << (j ? "else " : "") << "if (j_ == " << j << ") v_ = 0.0";
+          for (int o : g.node(us[grp[j]].verts[0]).operands) body << " + rs_red_[" << dk[o] << "]";
+          body << ";\n";
+        }
+        body << "      st_async_f64(&rs_inbox_[(" << opaque_slots << " + j_) * " << C << " + rk_], v_, &rs_gbar_["
+             << n_push << "], (unsigned)r_);\n    }\n"
+             << "    if (threadIdx.x == 0) mbar_expect_tx(&rs_gbar_[" << n_push << "], " << grp.size() * C * 8 << "u);\n"
+             << "    mbar_wait_cluster(&rs_gbar_[" << n_push << "], 0u);\n";
+        ++n_push;
+        body << "    {\n      const int w_ = threadIdx.x >> 5, l_ = threadIdx.x & 31;\n";
+        for (size_t j = 0; j < grp.size(); ++j) {
+          const OpNode& n = g.node(us[grp[j]].verts[0]);
+          int64_t count = 0;
+          for (int o : n.operands) count += g.node(o).shape.element_count();
+          body << "      if (w_ == " << j % 32 << ") { double t_ = l_ < " << C << " ? rs_inbox_[("
+               << opaque_slots + static_cast<int>(j) << ") * " << C << " + l_] : 0.0; t_ = bfly_sum(t_, 32); if (l_ == 0) rs_fill_["
+               << j << "] = (float)(" << (count ? "t_ / " + std::to_string(count) + ".0" : "0.0") << "); }\n";
+        }
+        body << "    }\n    __syncthreads();\n";
+        emit_fills(grp);
+        opaque_slots += static_cast<int>(grp.size());
+        body << "  }\n";
+        since_barrier.clear();
+        free_list.insert(free_list.end(), pending_free.begin(), pending_free.end());
+        pending_free.clear();
+        for (size_t i : grp) since_barrier.insert(i);
+        retire_inputs(s);
+        continue;
+      }
+      for (size_t j = 0; j < grp.size(); ++j) {
+        body << "    if (threadIdx.x == " << j << ") rs_part_[" << opaque_slots + static_cast<int>(j) << "] = 0.0";
+        for (int o : g.node(us[grp[j]].verts[0]).operands) body << " + rs_red_[" << dk[o] << "]";
+        body << ";\n";
+      }
+      body << "    {\n";
+    } else {
+      for (auto [o, k] : dk) {
+        const TensorShape& sh = g.node(o).shape;
+        const int64_t cnt = local_elems(o);
+        const std::string guard = !sharded[static_cast<size_t>(o)] ? "if (rk_ == 0) " : "";
+        body << "    double d" << k << "_ = 0.0;\n";
+        if (sh.dtype == DType::F32 && cnt % 4 == 0)
+          body << "    " << guard << "for (int i = threadIdx.x; i < " << cnt / 4 << "; i += 1024) { const float4 q = ld4_g("
+               << ptr(o) << " + 4 * i); d" << k << "_ += ((double)q.x + (double)q.y) + ((double)q.z + (double)q.w); }\n";
+        else
+          body << "    " << guard << "for (int i = threadIdx.x; i < " << cnt << "; i += 1024) d" << k << "_ += (double)ldv_g("
+               << ptr(o) << ", i);\n";
+      }
+      for (size_t j = 0; j < grp.size(); ++j) {
+        body << "    { double a_ = 0.0";
+        for (int o : g.node(us[grp[j]].verts[0]).operands) body << " + d" << dk[o] << "_";
+        body << ";\n      a_ = bfly_sum(a_, 32);\n      if ((threadIdx.x & 31) == 0) rs_red_[" << j * 32
+             << " + (threadIdx.x >> 5)] = a_; }\n";
+      }
+      // warp j folds member j's 32 warp sums into this CTA's partial
+      body << "    __syncthreads();\n    {\n      const int w_ = threadIdx.x >> 5, l_ = threadIdx.x & 31;\n";
+      for (size_t j = 0; j < grp.size(); ++j)
+        body << "      if (w_ == " << j % 32 << ") { const double v_ = bfly_sum(rs_red_[" << j * 32
+             << " + l_], 32); if (l_ == 0) rs_part_[" << opaque_slots + static_cast<int>(j) << "] = v_; }\n";
     }
-    for (size_t j = 0; j < grp.size(); ++j) {
-      body << "    { double a_ = 0.0";
-      for (int o : g.node(us[grp[j]].verts[0]).operands) body << " + d" << dk[o] << "_";
-      body << ";\n      a_ = bfly_sum(a_, 32);\n      if ((threadIdx.x & 31) == 0) rs_red_[" << j * 32
-           << " + (threadIdx.x >> 5)] = a_; }\n";
-    }
-    // warp j folds member j's 32 warp sums into this CTA's partial
-    body << "    __syncthreads();\n    {\n      const int w_ = threadIdx.x >> 5, l_ = threadIdx.x & 31;\n";
-    for (size_t j = 0; j < grp.size(); ++j)
-      body << "      if (w_ == " << j % 32 << ") { const double v_ = bfly_sum(rs_red_[" << j * 32
-           << " + l_], 32); if (l_ == 0) rs_part_[" << opaque_slots + static_cast<int>(j) << "] = v_; }\n";
     body << "    }\n    cluster_sync_all();\n";
     ++n_cluster;
     // warp j: lane r reads rank r's partial of member j (DSMEM, all in
@@ -449,20 +536,7 @@ std::optional<KernelSpec> generate_resident_kernel(const CompGraph& g, const std
            << j << "] = (float)(" << (count ? "t_ / " + std::to_string(count) + ".0" : "0.0") << "); }\n";
     }
     body << "    }\n    __syncthreads();\n";
-    for (size_t i : grp) place_outputs(i);
-    for (size_t j = 0; j < grp.size(); ++j) {
-      const OpNode& n = g.node(us[grp[j]].verts[0]);
-      const int64_t nout = local_elems(n.id);
-      const bool rep_out = !sharded[static_cast<size_t>(n.id)] && graph_out.count(n.id);
-      const std::string guard = rep_out ? "if (rk_ == 0) " : "";
-      body << "    { const float fill = rs_fill_[" << j << "];\n";
-      if (n.shape.dtype == DType::F32 && nout % 4 == 0)
-        body << "      " << guard << "for (int i = threadIdx.x; i < " << nout / 4 << "; i += 1024) st4_g(" << ptr(n.id)
-             << " + 4 * i, fill, fill, fill, fill); }\n";
-      else
-        body << "      " << guard << "for (int i = threadIdx.x; i < " << nout << "; i += 1024) stv(" << ptr(n.id)
-             << ", i, fill); }\n";
-    }
+    emit_fills(grp);
     body << "  }\n";
     opaque_slots += static_cast<int>(grp.size());
     // the cluster barrier ordered everything before it
@@ -506,7 +580,13 @@ std::optional<KernelSpec> generate_resident_kernel(const CompGraph& g, const std
     << "  __shared__ double rs_red_[" << 32 * max_group << "];\n"
     << "  __shared__ double rs_part_[" << std::max(1, opaque_slots) << "];\n"
     << "  __shared__ float rs_fill_[" << max_group << "];\n"
+    << (n_push ? "  __shared__ double rs_inbox_[" + std::to_string(opaque_slots * C) + "];\n"
+                 "  __shared__ __align__(8) unsigned long long rs_gbar_[" + std::to_string(n_push) + "];\n" : std::string())
     << "  const int rk_ = (int)cluster_ctarank();\n  (void)rk_;\n";
+  if (n_push) {  // peers push into our inbox only after every mbarrier of the cluster is initialised
+    s << "  if (threadIdx.x < " << n_push << ") mbar_init(&rs_gbar_[threadIdx.x], 1);\n"
+      << "  if (threadIdx.x == 0) mbar_fence_init();\n  cluster_sync_all();\n";
+  }
   if (!staged.empty()) {
     s << "  __shared__ __align__(8) unsigned long long rs_mbar_;\n"
       << "  if (threadIdx.x == 0) {\n    mbar_init(&rs_mbar_, 1);\n    mbar_fence_init();\n"

@@ -313,6 +313,22 @@ __device__ __forceinline__ double ld_dsmem_f64(const double* p, unsigned rank) {
   return v;
 }
 
+// remote push (resident template): the f64 `v` into cluster CTA `rank`'s
+// shared memory at (our address of) `dst`, completing `bytes` on that CTA's
+// mbarrier `b` -- a one-way signal instead of a cluster-wide barrier
+__device__ __forceinline__ void st_async_f64(double* dst, double v, unsigned long long* b, unsigned rank) {
+  unsigned rd, rb;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rd) : "r"(smem_addr(dst)), "r"(rank));
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(smem_addr(b)), "r"(rank));
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" :: "r"(rd), "d"(v), "r"(rb)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(unsigned long long* b, unsigned parity) {
+  asm volatile("{\n .reg .pred P1;\n LAB_WAITC:\n"
+               " mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n"
+               " @P1 bra DONEC;\n bra LAB_WAITC;\n DONEC:\n}" :: "r"(smem_addr(b)), "r"(parity) : "memory");
+}
+
 // run_program fault report: first fault wins (code 1 race, 2 global OOB, 3 shared OOB)
 __device__ __forceinline__ void sim_fault(unsigned* f, unsigned code, i64 where) {
   if (atomicCAS(f, 0u, code) == 0u) {

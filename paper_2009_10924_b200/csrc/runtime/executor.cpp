@@ -489,12 +489,16 @@ PlanKernels generate_plan_kernels(const CompGraph& g_, const FusionPlan& plan,
       if (--pending[static_cast<size_t>(w)] == 0) ready.insert({units[static_cast<size_t>(w)].fire, w});
   }
   if (specs_.size() != units.size()) throw std::runtime_error("[exec] contracted plan graph has a cycle");
-  // Resident template (cg_resident.cpp, STITCH_RESIDENT=1): a row-shardable
-  // launch-bound plan runs as one thread-block cluster, plan-kernel
-  // boundaries kept in shared memory.  Falls back to the launch graph below
-  // when the plan does not fit (reason on stderr with STITCH_RESIDENT_LOG=1).
-  if (const char* rv = std::getenv("STITCH_RESIDENT");
-      rv && *rv == '1' && mode == ExecMode::Stitched && !gemm_opaque) {
+  // Resident template (cg_resident.cpp): a row-shardable launch-bound plan
+  // runs as one thread-block cluster, plan-kernel boundaries kept in shared
+  // memory.  Default: tried for plans of >= 16 launch units (DIEN: 88 / 178;
+  // the fixtures and single-kernel configs keep their launch graph);
+  // STITCH_RESIDENT=1 tries every plan, =0 never.  Falls back to the launch
+  // graph below when the plan does not fit (reason on stderr with
+  // STITCH_RESIDENT_LOG=1).
+  const char* rv = std::getenv("STITCH_RESIDENT");
+  const bool try_resident = rv && *rv ? *rv == '1' : units.size() >= 16;
+  if (try_resident && mode == ExecMode::Stitched && !gemm_opaque) {
     std::string why;
     if (auto rk = generate_resident_kernel(g_, runits, "k" + std::to_string(idx++) + "_resident", &why)) {
       specs_ = {std::move(*rk)};

@@ -23,6 +23,7 @@ from __future__ import annotations
 
 import ctypes
 import json
+import re
 import warnings
 import os
 from typing import Dict, List, Optional, Sequence
@@ -471,6 +472,8 @@ class Executor:
         d = self.describe()
         if n == 1 and d[0]["template"].startswith("persistent("):  # + one entry per unit
             n = 1 + int(d[0]["template"][11:-1])
+        if n == 1 and d[0]["template"].startswith("resident("):  # + one entry per step
+            n = 1 + int(re.search(r" (\d+) steps", d[0]["template"]).group(1))
         a, b = (ctypes.c_double * max(1, n))(), (ctypes.c_double * max(1, n))()
         _check(lib().stc_exec_trace(self._h, a, b))
         return list(zip(a[:n], b[:n]))

@@ -114,8 +114,10 @@ def test_launch_units_packed_per_producer_set(monkeypatch):
     parameter-only placeholders form one pack, each step's three gate
     placeholders another; packing repeats over the packs, so the nine
     attention-column slices, then their squeezes (regional), then the
-    attention broadcasts each become one launch -> 88 plan kernels in 33
-    launches"""
+    attention broadcasts each become one launch -> 88 plan kernels in 34
+    launches (the attention-score placeholder over all T states is a
+    5-CTA cluster of its own).  Launch graph only: STITCH_RESIDENT=0"""
+    monkeypatch.setenv("STITCH_RESIDENT", "0")
     stitch = _stitch()
     from tests.conftest import config_graph
     plan = stitch.Plan(stitch.Graph(config_graph("dien_T10")), "b200")
@@ -125,17 +127,17 @@ def test_launch_units_packed_per_producer_set(monkeypatch):
     monkeypatch.setenv("STITCH_OPAQUE_PACK", "0")
     _, single = plan.codegen()
     assert len(single) == plan.stats()["stitched_kernels"] == 88
-    assert len(opaque_only) == 57
-    assert len(packed) == 33
+    assert len(opaque_only) == 58
+    assert len(packed) == 34
     units = lambda ks: sorted(p for k in ks for p in k["pattern"].split("+"))
     assert units(packed) == units(opaque_only) == units(single)  # every unit exactly once
     packs = [k for k in opaque_only if k["template"].startswith("opaque(pack")]
-    assert sorted(k["grid"] for k in packs) == [3] * 9 + [14]
+    assert sorted(k["grid"] for k in packs) == [3] * 9 + [13]
     assert all(k["grid"] == len(k["pattern"].split("+")) for k in packs)
     outs = lambda ks: sorted(o for k in ks for o in k["outputs"])
     assert outs(packed) == outs(single)
     # launches with identical code (modulo their tensors) share one function
-    assert len({k["symbol"] for k in packed}) == 9
+    assert len({k["symbol"] for k in packed}) == 10
     monkeypatch.setenv("STITCH_DEDUP", "0")
     _, nodedup = plan.codegen()
     assert len({k["symbol"] for k in nodedup}) == 88
@@ -148,6 +150,8 @@ def test_persistent_template_codegen(monkeypatch):
     stitch = _stitch()
     from tests.conftest import config_graph
     monkeypatch.setenv("STITCH_PERSIST", "1")
+    monkeypatch.setenv("STITCH_RESIDENT", "0")
+    monkeypatch.setenv("STITCH_OPAQUE_CLUSTER", "1")  # the persistent template takes no clusters
     src, kernels = stitch.Plan(stitch.Graph(config_graph("dien_T10")), "b200").codegen()
     assert [k["template"] for k in kernels] == ["persistent(33)"]
     assert len(set(re.findall(r"\bunit\d+_\(", src))) == 9  # 33 units, 9 distinct bodies
@@ -156,12 +160,13 @@ def test_persistent_template_codegen(monkeypatch):
     assert len(big) > 1 and not any(k["template"].startswith("persistent") for k in big)
 
 
-def test_kernel_produced_tensors_never_read_non_coherently():
+def test_kernel_produced_tensors_never_read_non_coherently(monkeypatch):
     """under programmatic dependent launch a tensor written by an earlier
     kernel is not read-only for the consumer's lifetime: only graph
     parameters may go through the ld.global.nc helpers (ld4 / ld4c / ld4h /
     ldv); everything else must use the coherent ones (ld4k / ldvk / ld4hk),
     which ptxas keeps below griddepcontrol.wait"""
+    monkeypatch.setenv("STITCH_RESIDENT", "0")  # the launch graph's kernels (resident units read generically)
     stitch = _stitch()
     from tests.conftest import config_graph, fixture_graphs
     texts = [config_graph(n) for n in ("dien_T10", "bert_layer", "bert_cut")] + list(fixture_graphs().values())
@@ -175,10 +180,11 @@ def test_kernel_produced_tensors_never_read_non_coherently():
 
 
 @pytest.mark.skipif(shutil.which("cuobjdump") is None, reason="cuobjdump not on PATH")
-def test_sass_no_global_write_before_pdl_wait():
+def test_sass_no_global_write_before_pdl_wait(monkeypatch):
     """SASS of the generated kernels (tools/sass_pdl_check.py): no global
     store / reduction / atomic ahead of griddepcontrol.wait (ACQBULK) in any
     kernel, and every kernel waits"""
+    monkeypatch.setenv("STITCH_RESIDENT", "0")  # launch-graph kernels (the resident kernel has no PDL)
     from tools.sass_pdl_check import check
     for name in ("dien_T10", "bert_layer", "attn_softmax", "colreduce", "bert_resln"):
         for fn, r in check(name).items():

@@ -103,7 +103,8 @@ def test_parity_mode_launches_equal_plan_kernels(name, monkeypatch):
     """launch count is a parity observable (reference pipeline.cpp:144-146,
     kernel_count): with launch packing off, the CUDA Graph holds exactly the
     plan's stitched_kernels launches; the packed default launches fewer and
-    computes the same bits"""
+    computes the same bits (launch graph: STITCH_RESIDENT=0)"""
+    monkeypatch.setenv("STITCH_RESIDENT", "0")
     stitch = _stitch()
     text = config_graph(name)
     g = stitch.Graph(text)
@@ -201,6 +202,7 @@ def test_chunked_host_run_matches_full_plan(name, nchunks):
 def test_dag_capture_matches_linear_chain(monkeypatch):
     """the plan's CUDA Graph captured as a DAG (independent kernels on forked
     streams) computes exactly what the linear chain computes"""
+    monkeypatch.setenv("STITCH_RESIDENT", "0")
     stitch = _stitch()
     for name in ("dien_T10", "bert_layer"):
         text = config_graph(name)
@@ -219,6 +221,7 @@ def test_opaque_pack_matches_one_kernel_per_op(monkeypatch):
     """packed launch units (opaque placeholders a CTA per op, local patterns
     side by side) compute exactly what one kernel per unit computes, and
     match the oracle"""
+    monkeypatch.setenv("STITCH_RESIDENT", "0")
     stitch = _stitch()
     for name in ("dien_T10", "dien_T20", "bert_layer"):
         text = config_graph(name)
@@ -248,6 +251,7 @@ def test_persistent_template_matches_graph(monkeypatch):
     computes, over repeated launches (the counters' generation scheme)"""
     stitch = _stitch()
     monkeypatch.setenv("STITCH_OPAQUE_CLUSTER", "1")  # the persistent template takes no clusters
+    monkeypatch.setenv("STITCH_RESIDENT", "0")
     text = config_graph("dien_T10")
     g = stitch.Graph(text)
     plan = stitch.Plan(g, "b200")
@@ -662,6 +666,7 @@ def test_resident_template_matches_oracle(name, monkeypatch):
     g = stitch.Graph(text)
     plan = stitch.Plan(g, "b200")
     og = no.parse_graph(text)
+    monkeypatch.setenv("STITCH_RESIDENT", "0")
     graph_ex = stitch.Executor(plan)
     monkeypatch.setenv("STITCH_RESIDENT", "1")
     ex = stitch.Executor(plan)
