@@ -222,15 +222,54 @@ def _exec_timing(stitch, plan, g, gemm=False):
     ex.upload(stitch.random_inputs(g, 1))
     per_set = sum(t.nbytes for t in g.params) + sum(t.nbytes for t in g.outputs)
     sets = min(256, max(2, math.ceil(8 * L2_BYTES / max(per_set, 1))))
-    us1, kus = ex.time(iters=200, warmup=20, sets=sets, per_kernel=True)
+    us1, _ = ex.time(iters=200, warmup=20, sets=sets)
+    usc, kus = ex.time_call(iters=200, warmup=20, sets=sets, per_kernel=True)
     us = ex.time_batched(steps=256, warmup=64, sets=sets, steps_per_graph=64)
-    return ex, us, us1, kus
+    return ex, us, (us1, usc, serial_us(stitch, plan, g, sets, gemm)), kus
+
+
+def serial_us(stitch, plan, g, sets, gemm=False, steps=256, spg=64, device=0):
+    """us per step of back-to-back steps with programmatic dependent launch
+    off (STITCH_PDL=0): every step's kernels start after the previous step
+    completed -- one subgraph's fill, stream and drain without the launch
+    latency of a call or any cross-step overlap"""
+    saved = os.environ.get("STITCH_PDL")
+    os.environ["STITCH_PDL"] = "0"
+    try:
+        ex = stitch.Executor(plan, device=device, gemm=gemm)
+        ex.upload(stitch.random_inputs(g, 1))
+        us = ex.time_batched(steps=steps, warmup=32, sets=sets, steps_per_graph=spg)
+        del ex
+        return us
+    finally:
+        if saved is None:
+            os.environ.pop("STITCH_PDL", None)
+        else:
+            os.environ["STITCH_PDL"] = saved
+
+
+def call_floor(stitch):
+    """the fixed cost of one call: a 4-element graph, one launch queued
+    behind a spinning warp (us_one_call), and back to back without PDL
+    (us_serial)"""
+    g = stitch.Graph("x = parameter : f32[4]\ny = parameter : f32[4]\nz = add(x, y)\noutput z\n")
+    plan = stitch.Plan(g, "b200")
+    ex = stitch.Executor(plan)
+    ex.upload(stitch.random_inputs(g, 1))
+    usc, _ = ex.time_call(iters=200, warmup=20, sets=2)
+    del ex
+    return {"graph": "z = x + y, f32[4]", "us_one_call": round(usc, 3), "us_serial": round(serial_us(stitch, plan, g, 2), 3),
+            "note": "a call's launch-to-completion floor on an idle device (us_one_call) and a step's floor when "
+                    "steps are queued back to back without PDL (us_serial); the subgraphs' us_one_call and us_serial "
+                    "are these plus their data time"}
 
 
 def time_subgraph(stitch, name, gemm=False, refine=False):
     """one BASELINE config: `us` = back-to-back steps (64 per graph launch,
     PDL overlap between steps), `us_one_launch_per_step` = one graph launch per
-    step (no cross-step overlap), each with its roofline fraction; when the
+    step back to back (no cross-step overlap; host submission rate included),
+    `us_one_call` = one call's launch-to-completion on the device (replay
+    queued behind a spinning warp), each with its roofline fraction; when the
     default launch packing merges plan kernels, `parity_mode` is the same plan
     with packing off (launches == plan.json stitched_kernels)"""
     g = stitch.Graph(read_graph(name))
@@ -254,7 +293,9 @@ def time_subgraph(stitch, name, gemm=False, refine=False):
         except Exception as e:  # reported, never fatal
             cpu = {"error": str(e)[:200]}
     out = {"us": round(us, 3), "GBps": round(alg / us / 1e3, 1), "frac_of_measured_peak": round(alg / us / 1e3 / peak, 4),
-           "us_one_launch_per_step": round(us1, 3), "frac_one_launch": round(alg / us1 / 1e3 / peak, 4),
+           "us_one_launch_per_step": round(us1[0], 3), "frac_one_launch": round(alg / us1[0] / 1e3 / peak, 4),
+           "us_one_call": round(us1[1], 3), "frac_one_call": round(alg / us1[1] / 1e3 / peak, 4),
+           "us_serial": round(us1[2], 3), "frac_serial": round(alg / us1[2] / 1e3 / peak, 4),
            "kernels": len(desc), "plan_kernels": plan_kernels, "cpu_reference": cpu,
            "templates": sorted({k["template"] for k in desc}), "bytes": alg,
            "dominant": {"name": desc[top]["name"], "template": desc[top]["template"],
@@ -274,7 +315,8 @@ def time_subgraph(stitch, name, gemm=False, refine=False):
             os.environ.update(env)
             try:
                 pex, pus, pus1, _ = _exec_timing(stitch, plan, g, gemm)
-                out[key] = {"launches": pex.num_kernels, "us": round(pus, 3), "us_one_launch_per_step": round(pus1, 3),
+                out[key] = {"launches": pex.num_kernels, "us": round(pus, 3), "us_one_launch_per_step": round(pus1[0], 3),
+                            "us_one_call": round(pus1[1], 3), "us_serial": round(pus1[2], 3),
                             "note": note}
                 del pex
             finally:
@@ -410,7 +452,12 @@ def main():
 
     # per-kernel device time (events around each kernel, same rotation) for the
     # roofline, and the step time with one graph launch per step for reference
-    us_single, kus = ex.time(iters=200, warmup=10, sets=sets, per_kernel=True)
+    us_single, _ = ex.time(iters=200, warmup=10, sets=sets)
+    # latency of one call: each replay queued behind a spinning warp so the
+    # events time the device (launch to completion), not the host submission
+    us_call, kus = ex.time_call(iters=200, warmup=10, sets=sets, per_kernel=True)
+    us_ser = serial_us(stitch, plan, g, sets, steps=512, spg=spg, device=local)
+    floor = call_floor(stitch) if rank == 0 else None
     top = max(range(len(desc)), key=lambda i: kus[i])
     # dominant kernel's time inside the graph: its share of the step (1-kernel plan -> the step)
     dom_us = ms_step * 1e3 * (kus[top] / sum(kus)) if len(desc) > 1 else ms_step * 1e3
@@ -544,6 +591,9 @@ def main():
                                  "previous step drains (us_per_subgraph_one_launch_per_step: one graph launch per "
                                  "step, no cross-step overlap)" % spg,
                        "us_per_subgraph_one_launch_per_step": round(us_single, 3),
+                       "us_per_subgraph_one_call": round(us_call, 3),
+                       "us_per_subgraph_serial": round(us_ser, 3),
+                       "call_floor": floor,
                        "bytes_per_step_per_gpu": alg_bytes,
                        "l2": "inputs larger than L2: %d rotating buffer sets x %.1f MB = %.0f MB (>= 8x the 126 MB L2)"
                              % (sets, per_set / 1e6, sets * per_set / 1e6),
@@ -566,11 +616,18 @@ def main():
                                          % json.dumps({k: v for k, v in traffic_raw.items() if k != "report"}),
                          "kernel": desc[top]["name"],
                          "kernel_us": round(dom_us, 3), "kernel_bytes": desc[top]["bytes"],
-                         "kernel_us_one_launch": round(kus[top], 3),
-                         "frac_one_launch": round(desc[top]["bytes"] / (kus[top] * 1e-6) / 1e9 / peak, 4),
-                         "one_launch_note": "the same kernel timed with one CUDA-graph launch per step (CUDA events "
-                                            "around the kernel, cold rotated inputs, no cross-step PDL overlap): "
-                                            "the latency of one subgraph call",
+                         "kernel_us_serial": round(us_ser * (kus[top] / sum(kus)) if len(desc) > 1 else us_ser, 3),
+                         "frac_serial": round(desc[top]["bytes"] / ((us_ser * (kus[top] / sum(kus)) if len(desc) > 1
+                                                                     else us_ser) * 1e-6) / 1e9 / peak, 4),
+                         "serial_note": "steps back to back with programmatic dependent launch off: each step starts "
+                                        "after the previous one completed (the kernel's fill, stream and drain; no "
+                                        "launch latency, no cross-step overlap)",
+                         "kernel_us_one_call": round(kus[top], 3),
+                         "frac_one_call": round(desc[top]["bytes"] / (kus[top] * 1e-6) / 1e9 / peak, 4),
+                         "one_call_note": "the same kernel launched on its own between CUDA events, queued behind a "
+                                          "warp spinning on the global timer so the events bracket launch-to-completion "
+                                          "on the device and not the host's submission; cold rotated inputs, no "
+                                          "cross-step PDL overlap: the latency of one subgraph call",
                          "frac_of_8TBps": round(achieved / 8000.0, 4),
                          "peak_note": "the measured peak is a plain copy kernel timed launch by launch; back-to-back "
                                       "steps with programmatic dependent launch overlap one step's drain with the next "

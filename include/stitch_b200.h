@@ -172,6 +172,15 @@ int stc_exec_tensor(const stc_exec* e, const char* name, void** dptr, size_t* by
  * num_kernels) = average duration of kernel i measured by per-kernel events. */
 int stc_exec_time(stc_exec* e, int iters, int warmup, int sets, double* us_per_run,
                   double* kernel_us);
+/* Latency of ONE call on the device: each replay (set rotated as above) is
+ * queued behind a warp spinning on the global timer, so the events around it
+ * bracket the replay's device time -- launch-to-completion of an idle device
+ * -- and not the host's submission of the launch.  us_per_call = average
+ * over iters; kernel_us[i] (optional) = kernel i launched on its own between
+ * events (same spin prelude).  No equivalent in the reference (it has no
+ * device path); the figure behind the bench's single-call roofline. */
+int stc_exec_time_call(stc_exec* e, int iters, int warmup, int sets, double* us_per_call,
+                       double* kernel_us);
 /* Batched replay: `steps_per_graph` consecutive steps (rotating buffer sets)
  * captured into ONE CUDA Graph so the graph-launch cost is paid once per
  * batch (the paper's launch-overhead argument applied across batches).

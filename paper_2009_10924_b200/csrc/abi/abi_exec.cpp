@@ -187,6 +187,16 @@ int stc_exec_time(stc_exec* e, int iters, int warmup, int sets, double* us_per_r
   });
 }
 
+int stc_exec_time_call(stc_exec* e, int iters, int warmup, int sets, double* us_per_call, double* kernel_us) {
+  return guarded([&] {
+    std::vector<double> per;
+    const double us = e->ex->time_call(iters, warmup, sets, kernel_us ? &per : nullptr);
+    if (us_per_call) *us_per_call = us;
+    if (kernel_us)
+      for (size_t i = 0; i < per.size(); ++i) kernel_us[i] = per[i];
+  });
+}
+
 int stc_exec_prepare_batches(stc_exec* e, int sets, int steps_per_graph, int* n_graphs) {
   return guarded([&] {
     const int n = e->ex->prepare_batches(sets, steps_per_graph);

@@ -131,6 +131,9 @@ class Emitter {
   // current row lives in registers cu_<name>_<chunk> (prefetched a row ahead)
   std::map<std::string, int> domain_chunk;
   std::set<int> reg_staged;
+  // row-invariant [L] operands copied once per CTA into shared memory:
+  // tensor -> smem array (loads at a chunk offset read it instead of global)
+  std::map<int, std::string> smem_bcast;
 
   const std::string& ix() const { return ix_; }
   std::string fresh(const char* p) { return p + std::to_string(counter_++); }
@@ -202,6 +205,13 @@ class Emitter {
     int nvary = 0, last_vary = -1;
     for (size_t i = 0; i < c.size(); ++i)
       if (c[i].vary) ++nvary, last_vary = static_cast<int>(i);
+    if (auto sb = smem_bcast.find(v); sb != smem_bcast.end() && W == 4 && c.size() == 1 && c[0].vary) {
+      const std::string q = fresh("q");
+      line("const float4 " + q + " = lds4(" + sb->second + " + " + c[0].base + ");");
+      Val r;
+      for (const char* f : {".x", ".y", ".z", ".w"}) r.lanes.push_back(q + f);
+      return r;
+    }
     if (W == 4 && sh.dtype == DType::F32 && !domain_off.empty()) {
       auto it = domain_off.find(coords_key(c));
       std::vector<int> dd;
@@ -726,17 +736,40 @@ void emit_row(Emitter& em, const CompGraph& g, const std::set<int>& pat, const B
   // rows (the register pipeline): with one row per team it just costs
   // registers (residual+LN 7.09 -> 8.11 us; LN 4.69 -> 4.27 us pipelined,
   // profiles/r01/row_hoist_ab.jsonl)
+  // With two or more streamed tensors the prefetch registers (2 x streams x
+  // NJ float4) plus the hoisted operands exceed the 128-register cap of a
+  // 512-thread CTA (residual+LN spilled 160 B/thread): there the operands go
+  // to shared memory instead (STITCH_ROW_HOIST_BCAST: 1 registers, 2 shared
+  // memory, 0 off; default 2 for >= 2 streams, else 1)
   const bool multi_row = pipe && !pipe->empty() && rp.W == 4;
-  if (I.size() == 1 && multi_row && env_int("STITCH_ROW_HOIST_BCAST", 1))
+  const int hoist_mode = env_int("STITCH_ROW_HOIST_BCAST", pipe && pipe->size() >= 2 ? 2 : 1);
+  if (I.size() == 1 && multi_row && hoist_mode) {
+    std::set<int> srcs;
     for (int v : pat) {
       const OpNode& n = g.node(v);
       if (n.kind != OpKind::Broadcast || pat.count(n.operands[0])) continue;
       const OpNode& src = g.node(n.operands[0]);
       if (src.kind == OpKind::Constant || src.shape.rank() != 1 || src.shape.dims[0] != L) continue;
+      if (src.shape.dtype != DType::F32 || L % 4 != 0) continue;
       if (n.attrs.dims.size() != 1 || n.attrs.dims[0] != static_cast<int>(O.size())) continue;
       if (n.shape.rank() != static_cast<int>(O.size() + 1)) continue;
-      for (int j = 0; j < rp.NJ; ++j) em.value(src.id, Coords{{chunk_p[j], rp.W > 1, true}});
+      srcs.insert(src.id);
     }
+    for (int sid : srcs) {
+      if (hoist_mode == 2) {
+        if (!em.is_param(sid)) em.ensure_wait();
+        const std::string nm = "sb_" + tensor_ident(g.node(sid).name);
+        em.line("__shared__ __align__(16) float " + nm + "[" + sL + "];");
+        em.line("for (int i_ = threadIdx.x; i_ < " + std::to_string(L / 4) + "; i_ += " + std::to_string(rp.block) +
+                ") reinterpret_cast<float4*>(" + nm + ")[i_] = " + (em.is_param(sid) ? "ld4c(" : "ld4k(") +
+                tensor_ident(g.node(sid).name) + " + i_ * 4);");
+        em.smem_bcast[sid] = nm;
+      } else {
+        for (int j = 0; j < rp.NJ; ++j) em.value(sid, Coords{{chunk_p[j], rp.W > 1, true}});
+      }
+    }
+    if (hoist_mode == 2 && !srcs.empty()) em.line("__syncthreads();");
+  }
   if (st) {
     // TMA-staged inputs that a kernel produces must wait; graph parameters
     // are streamed before the wait (hoisted prologue)
@@ -988,6 +1021,7 @@ void emit_row(Emitter& em, const CompGraph& g, const std::set<int>& pat, const B
   em.domain_chunk.clear();
   em.staged_ptr.clear();
   em.reg_staged.clear();
+  em.smem_bcast.clear();
 }
 
 bool grid_sync_mode() {
@@ -1350,8 +1384,22 @@ KernelSpec generate_pattern_kernel(const CompGraph& g, const std::vector<int>& v
     em.reset_wait();
     int streams = 0;
     for (int v : em.staged_hits) streams += !pat.count(v) && g.node(v).shape.dtype == DType::F32;
-    if (streams == 1) block = 128;
-    if (streams == 2) block = 512;
+    // balanced: k CTAs per SM (STITCH_ROW_CTAS_PER_SM, default 2) sized so
+    // the grid covers every SM with the same number of row teams (+-1): for
+    // 4096 rows, 2 rows per team, 7 teams = 224 threads x 293 CTAs instead
+    // of 128 x 512 (3 or 4 CTAs per SM) or 512 x 128 (20 SMs idle).  The
+    // prefetch registers cap a CTA at 512 threads (128 registers each).
+    // =0: the earlier fixed sizes (one stream 128, two streams 512)
+    const int k_sm = env_int("STITCH_ROW_CTAS_PER_SM", 2);
+    if (k_sm > 0) {
+      const int64_t rows = prod(bodies[0].dims_a);
+      const int64_t teams = (rows + 1) / 2;  // the register pipeline's 2 rows per team
+      const int64_t per_cta = (teams + int64_t(sm_now()) * k_sm - 1) / (int64_t(sm_now()) * k_sm);
+      block = static_cast<int>(std::clamp<int64_t>(per_cta * max_tpr, std::max(64, max_tpr), std::max(512, max_tpr)));
+    } else {
+      if (streams == 1) block = 128;
+      if (streams == 2) block = 512;
+    }
   }
   if (const int want = env_int("STITCH_ROW_BLOCK", 0); want > 0) {
     block = std::clamp((std::max(want, max_tpr) + max_tpr - 1) / max_tpr * max_tpr, 32, 1024);

@@ -57,5 +57,7 @@ class Module {
 
 // fixed kernels compiled by nvcc into this library (csrc/kernels/util.cu)
 void launch_l2_flush(void* buf, size_t bytes, cudaStream_t s);
+// one warp spinning for `ns` nanoseconds of device time (timing prelude)
+void launch_spin(unsigned long long ns, cudaStream_t s);
 
 }  // namespace stitch::gpu

@@ -1108,6 +1108,56 @@ double Executor::time(int iters, int warmup, int sets, std::vector<double>* per_
   return us;
 }
 
+double Executor::time_call(int iters, int warmup, int sets, std::vector<double>* per_kernel) {
+  ensure_ready();
+  sets = std::max(1, sets);
+  iters = std::max(1, iters);
+  prepare_sets(sets);
+  for (int w = 0; w < warmup; ++w) launch(stream_, w % sets);
+  STC_RT(cudaStreamSynchronize(stream_));
+  // the spin outlasts the host submitting the events and the launch(es)
+  // queued behind it (a few us per launch)
+  const unsigned long long spin_ns = 30000ull + 5000ull * specs_.size();
+  cudaEvent_t e0, e1;
+  STC_RT(cudaEventCreate(&e0));
+  STC_RT(cudaEventCreate(&e1));
+  double total = 0.0;
+  for (int it = 0; it < iters; ++it) {
+    launch_spin(spin_ns, stream_);
+    STC_RT(cudaEventRecord(e0, stream_));
+    launch(stream_, it % sets);
+    STC_RT(cudaEventRecord(e1, stream_));
+    STC_RT(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    STC_RT(cudaEventElapsedTime(&ms, e0, e1));
+    total += 1000.0 * ms;
+  }
+  if (per_kernel) {
+    per_kernel->assign(specs_.size(), 0.0);
+    std::vector<cudaEvent_t> ev(specs_.size() + 1);
+    for (auto& e : ev) STC_RT(cudaEventCreate(&e));
+    for (int it = 0; it < iters; ++it) {
+      const int s = it % sets;
+      launch_spin(spin_ns, stream_);
+      STC_RT(cudaEventRecord(ev[0], stream_));
+      for (size_t i = 0; i < specs_.size(); ++i) {
+        launch_kernel(i, s, stream_);
+        STC_RT(cudaEventRecord(ev[i + 1], stream_));
+      }
+      STC_RT(cudaEventSynchronize(ev.back()));
+      for (size_t i = 0; i < specs_.size(); ++i) {
+        float kms = 0.f;
+        STC_RT(cudaEventElapsedTime(&kms, ev[i], ev[i + 1]));
+        (*per_kernel)[i] += 1000.0 * kms / iters;
+      }
+    }
+    for (auto& e : ev) cudaEventDestroy(e);
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return total / iters;
+}
+
 std::vector<std::pair<double, double>> Executor::trace(int set) {
   ensure_ready();
   if (!tracing_) throw std::runtime_error("[exec] trace() needs an executor built with STITCH_TRACE=1");

@@ -112,6 +112,10 @@ class Executor {
 
   // CUDA-event timing (see stc_exec_time in include/stitch_b200.h)
   double time(int iters, int warmup, int sets, std::vector<double>* per_kernel_us, int batch = 1);
+  // Latency of one call on the device (see stc_exec_time_call): every
+  // replay is queued behind a spinning warp so its bracketing events time
+  // the replay, not the host's submission of it
+  double time_call(int iters, int warmup, int sets, std::vector<double>* per_kernel_us);
 
   std::string describe_json() const;
   // one replay of set `set` with the in-graph timeline: per kernel (first CTA

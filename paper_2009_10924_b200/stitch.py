@@ -97,6 +97,7 @@ def lib():
         "stc_exec_sync": (ip, [vp]),
         "stc_exec_tensor": (ip, [vp, cp, P(vp), P(ctypes.c_size_t)]),
         "stc_exec_time": (ip, [vp, ip, ip, ip, P(ctypes.c_double), P(ctypes.c_double)]),
+        "stc_exec_time_call": (ip, [vp, ip, ip, ip, P(ctypes.c_double), P(ctypes.c_double)]),
         "stc_exec_prepare_batches": (ip, [vp, ip, ip, P(ip)]),
         "stc_exec_launch_batch": (ip, [vp, vp, ip]),
         "stc_exec_time_batched": (ip, [vp, ip, ip, ip, ip, P(ctypes.c_double)]),
@@ -509,6 +510,14 @@ class Executor:
         us = ctypes.c_double()
         kus = (ctypes.c_double * max(1, self.num_kernels))() if per_kernel else None
         _check(lib().stc_exec_time(self._h, iters, warmup, sets, ctypes.byref(us), kus))
+        return us.value, (list(kus[: self.num_kernels]) if per_kernel else None)
+
+    def time_call(self, iters: int = 100, warmup: int = 10, sets: int = 1, per_kernel: bool = False):
+        """(us per call, [us per kernel] or None): each replay queued behind a
+        spinning warp so the events time the device, not the host submission"""
+        us = ctypes.c_double()
+        kus = (ctypes.c_double * max(1, self.num_kernels))() if per_kernel else None
+        _check(lib().stc_exec_time_call(self._h, iters, warmup, sets, ctypes.byref(us), kus))
         return us.value, (list(kus[: self.num_kernels]) if per_kernel else None)
 
     def prepare_batches(self, sets: int, steps_per_graph: int) -> int:

@@ -1,6 +1,8 @@
 """Sweep codegen knobs (env vars) for one graph: us per subgraph (batched
-graph replays, inputs rotated past L2), us with one graph launch per step
-(plus per-kernel event times), grid, block.
+graph replays, inputs rotated past L2), us_serial (the same with STITCH_PDL=0:
+no cross-step overlap), us with one graph launch per step
+(host submission rate included), us of one call on the device
+(replay queued behind a spinning warp; plus per-kernel event times), grid, block.
 
     python tools/sweep_env.py <graph> 'VAR=a,b VAR2=c,d' ...
 """
@@ -16,9 +18,18 @@ if os.environ.get("SWEEP_CHILD"):
     per_set = sum(t.nbytes for t in g.params) + sum(t.nbytes for t in g.outputs)
     sets = min(128, max(2, math.ceil(8 * 126 * 2**20 / per_set)))
     us = ex.time_batched(steps=256, warmup=32, sets=sets, steps_per_graph=16)
-    us1, kus = ex.time(iters=200, warmup=20, sets=sets, per_kernel=True)
+    us1, _ = ex.time(iters=200, warmup=20, sets=sets)
+    usc, kus = ex.time_call(iters=200, warmup=20, sets=sets, per_kernel=True)
+    del ex
+    # serial: the same batched replay with STITCH_PDL=0 -- each step starts
+    # after the previous completed (fill + stream + drain, no launch latency)
+    os.environ["STITCH_PDL"] = "0"
+    exs = stitch.Executor(stitch.Plan(g, os.environ.get("SWEEP_CFG", "b200")))
+    exs.upload(stitch.random_inputs(g, 1))
+    uss = exs.time_batched(steps=256, warmup=32, sets=sets, steps_per_graph=16)
     print(json.dumps({"us": round(us, 3), "GBps": round(sum(k["bytes"] for k in d) / us / 1e3, 1),
-                      "us_one_launch": round(us1, 3), "kernel_us_one_launch": [round(x, 3) for x in kus],
+                      "us_serial": round(uss, 3), "us_one_launch": round(us1, 3), "us_one_call": round(usc, 3),
+                      "kernel_us_one_call": [round(x, 3) for x in kus],
                       "grid": [k["grid"] for k in d], "block": [k["block"] for k in d]}))
     sys.exit(0)
 name = sys.argv[1]
