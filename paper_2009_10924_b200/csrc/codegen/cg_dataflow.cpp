@@ -1445,6 +1445,15 @@ KernelSpec generate_pattern_kernel(const CompGraph& g, const std::vector<int>& v
   em.hoist = tl_force_block == 0 && env_int("STITCH_PDL", 1) != 0 && env_int("STITCH_PDL_HOIST", 1) != 0;
   const int per_sm = std::max(1, std::min(env_int("STITCH_COL_CTAS", 3), 2048 / block));
 
+  // local CTAs per SM: 32 (every grid-stride CTA resident at 64 registers x
+  // 32 threads); packed beside a row body the kernel's 64-thread CTAs carry
+  // the row body's ~55 registers, so 18 fit per SM and a grid of 18 per SM
+  // takes its passes without a partial second wave of local CTAs (bert_cut
+  // 22.80 -> 22.56 us batched, 23.56 -> 23.27 us serial,
+  // profiles/r02/rows/bert_cut_sweep.jsonl)
+  bool has_row = false;
+  for (const auto& b : bodies) has_row = has_row || b.kind == Kind::Row;
+  const int local_ctas = bodies.size() > 1 && has_row && block == 64 ? 18 : 32;
   // CTA budget per body; scratch = [256 B reserved][strip arrival counters][f64 partials]
   int64_t part_words = 0, ctr_words = 64, dyn_smem = 0;
   std::vector<StageCfg> stage(bodies.size());
@@ -1459,7 +1468,7 @@ KernelSpec generate_pattern_kernel(const CompGraph& g, const std::vector<int>& v
       const int64_t chunks = N / w;
       const int U = local_small(N) ? 1 : local_unroll(chunks, block);
       b.blocks = static_cast<int>(std::clamp<int64_t>((chunks + int64_t(block) * U - 1) / (int64_t(block) * U), 1,
-                                                      int64_t(sm_now()) * env_int("STITCH_LOCAL_CTAS", 32)));
+                                                      int64_t(sm_now()) * env_int("STITCH_LOCAL_CTAS", local_ctas)));
     } else if (b.kind == Kind::Row && cluster > 1) {
       const int64_t rows = prod(b.dims_a);
       b.blocks = static_cast<int>(std::min<int64_t>(rows, std::max<int64_t>(1, 4 * sm_now() / cluster)) * cluster);
