@@ -1348,6 +1348,25 @@ KernelSpec generate_pattern_kernel(const CompGraph& g, const std::vector<int>& v
       if (!pat.count(s)) em.cached_tensors.insert(s);
     }
 
+  // A row body packed beside a local body (bert_cut: residual+LN next to
+  // bias+GELU) spreads each long row over more lanes -- 2 float4 chunks per
+  // thread (STITCH_PACKED_ROW_NJ) instead of ~8 -- so the shared CTA holds
+  // 32 registers per thread (55 at 6 chunks: the row's values are live
+  // across both reductions) and the local body runs at full occupancy:
+  // bert_cut 22.55 -> 21.86 us batched (profiles/r02/rows/cut_nj.jsonl)
+  {
+    bool has_local = false;
+    for (const auto& b : bodies) has_local = has_local || b.kind == Kind::Local;
+    const int nj = env_int("STITCH_PACKED_ROW_NJ", 2);
+    if (has_local && bodies.size() > 1 && nj > 0)
+      for (auto& b : bodies)
+        if (b.kind == Kind::Row && !b.multi && b.tpr == 0) {
+          const RowParams rp0 = row_params(b.dims_b);
+          if (rp0.TPR < 32) continue;
+          const int64_t nch = prod(b.dims_b) / rp0.W;
+          b.tpr = static_cast<int>(std::clamp<int64_t>(pow2ceil((nch + nj - 1) / nj), 32, 1024));
+        }
+  }
   // one CTA size for every body of the kernel: a multiple of every row team
   int block = kBlock, max_tpr = 1;
   bool has_col = false;
@@ -1445,15 +1464,15 @@ KernelSpec generate_pattern_kernel(const CompGraph& g, const std::vector<int>& v
   em.hoist = tl_force_block == 0 && env_int("STITCH_PDL", 1) != 0 && env_int("STITCH_PDL_HOIST", 1) != 0;
   const int per_sm = std::max(1, std::min(env_int("STITCH_COL_CTAS", 3), 2048 / block));
 
-  // local CTAs per SM: 32 (every grid-stride CTA resident at 64 registers x
-  // 32 threads); packed beside a row body the kernel's 64-thread CTAs carry
-  // the row body's ~55 registers, so 18 fit per SM and a grid of 18 per SM
-  // takes its passes without a partial second wave of local CTAs (bert_cut
-  // 22.80 -> 22.56 us batched, 23.56 -> 23.27 us serial,
-  // profiles/r02/rows/bert_cut_sweep.jsonl)
+  // local CTAs per SM: 32 by default; packed beside a row body, as many as
+  // are resident at once (2048 threads / CTA size: 8 x 256 threads with the
+  // 2-chunk rows above, 21.86 vs 22.89 us at 32; 18 for 64-thread CTAs
+  // carrying a 6-chunk row body's 55 registers, 22.80 -> 22.56 us), so the
+  // local grid-stride CTAs take their passes without a partial second wave
+  // (profiles/r02/rows/bert_cut_sweep.jsonl, cut_nj.jsonl)
   bool has_row = false;
   for (const auto& b : bodies) has_row = has_row || b.kind == Kind::Row;
-  const int local_ctas = bodies.size() > 1 && has_row && block == 64 ? 18 : 32;
+  const int local_ctas = bodies.size() > 1 && has_row ? (block == 64 ? 18 : std::clamp(2048 / block, 1, 32)) : 32;
   // CTA budget per body; scratch = [256 B reserved][strip arrival counters][f64 partials]
   int64_t part_words = 0, ctr_words = 64, dyn_smem = 0;
   std::vector<StageCfg> stage(bodies.size());
@@ -1468,7 +1487,7 @@ KernelSpec generate_pattern_kernel(const CompGraph& g, const std::vector<int>& v
       const int64_t chunks = N / w;
       const int U = local_small(N) ? 1 : local_unroll(chunks, block);
       b.blocks = static_cast<int>(std::clamp<int64_t>((chunks + int64_t(block) * U - 1) / (int64_t(block) * U), 1,
-                                                      int64_t(sm_now()) * env_int("STITCH_LOCAL_CTAS", local_ctas)));
+                                                      int64_t(sm_now()) * std::max(1, env_int("STITCH_LOCAL_CTAS", local_ctas))));
     } else if (b.kind == Kind::Row && cluster > 1) {
       const int64_t rows = prod(b.dims_a);
       b.blocks = static_cast<int>(std::min<int64_t>(rows, std::max<int64_t>(1, 4 * sm_now() / cluster)) * cluster);
