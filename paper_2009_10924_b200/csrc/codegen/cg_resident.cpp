@@ -173,9 +173,12 @@ std::optional<KernelSpec> generate_resident_kernel(const CompGraph& g, const std
   if (!analyse_rows(g, B, sharded, why)) return std::nullopt;
   // cluster size: the most CTAs (<= 16) with a whole number of rows each,
   // a multiple of 4 (16-byte aligned row blocks for 128-bit accesses)
+  // (STITCH_RESIDENT_CLUSTER caps it)
   int C = 1;
+  const char* cv = std::getenv("STITCH_RESIDENT_CLUSTER");
+  const int cmax = cv && *cv ? std::atoi(cv) : 16;
   for (int c : {16, 8, 4, 2})
-    if (B % c == 0 && (B / c) % 4 == 0) {
+    if (c <= cmax && B % c == 0 && (B / c) % 4 == 0) {
       C = c;
       break;
     }

@@ -48,3 +48,18 @@ def dotted(text, prefix="layer."):
     for n in sorted(names, key=len, reverse=True):
         text = re.sub(r"(?<![A-Za-z0-9_.])%s(?![A-Za-z0-9_.])" % re.escape(n), prefix + n + "_q", text)
     return text
+
+
+_PLANS = {}
+
+
+def cached_plan(text, cfg):
+    """one stitch.Plan per (graph text, cfg) per test session: plans are
+    immutable after construction and planning DIEN takes ~40 s on this host
+    (the reference: ~100 s).  Tests about planning itself construct fresh ones
+    where they check the search (test_plan_parity.test_random_graphs)."""
+    from paper_2009_10924_b200 import stitch
+    key = (text, cfg)
+    if key not in _PLANS:
+        _PLANS[key] = stitch.Plan(stitch.Graph(text), cfg)
+    return _PLANS[key]

@@ -8,7 +8,7 @@ import shutil
 
 import pytest
 
-from tests.conftest import ROOT, fixture_graphs
+from tests.conftest import ROOT, cached_plan, config_graph, fixture_graphs
 
 HEADER = os.path.join(ROOT, "include", "stitch_b200.h")
 
@@ -84,7 +84,7 @@ def test_dotted_tensor_names_compile(monkeypatch, persist):
     stitch = _stitch()
     texts = [dotted(t) for t in fixture_graphs().values()] + [dotted(config_graph("dien_T10"), "a.b_")]
     for text in texts:
-        plan = stitch.Plan(stitch.Graph(text), "b200")
+        plan = cached_plan(text, "b200")
         for mode in ("stitched", "program", "unfused"):
             src, kernels = plan.codegen(mode)
             assert "TX_" in src
@@ -120,7 +120,7 @@ def test_launch_units_packed_per_producer_set(monkeypatch):
     monkeypatch.setenv("STITCH_RESIDENT", "0")
     stitch = _stitch()
     from tests.conftest import config_graph
-    plan = stitch.Plan(stitch.Graph(config_graph("dien_T10")), "b200")
+    plan = cached_plan(config_graph("dien_T10"), "b200")
     _, packed = plan.codegen()
     monkeypatch.setenv("STITCH_LOCAL_PACK", "0")
     _, opaque_only = plan.codegen()
@@ -152,11 +152,11 @@ def test_persistent_template_codegen(monkeypatch):
     monkeypatch.setenv("STITCH_PERSIST", "1")
     monkeypatch.setenv("STITCH_RESIDENT", "0")
     monkeypatch.setenv("STITCH_OPAQUE_CLUSTER", "1")  # the persistent template takes no clusters
-    src, kernels = stitch.Plan(stitch.Graph(config_graph("dien_T10")), "b200").codegen()
+    src, kernels = cached_plan(config_graph("dien_T10"), "b200").codegen()
     assert [k["template"] for k in kernels] == ["persistent(33)"]
     assert len(set(re.findall(r"\bunit\d+_\(", src))) == 9  # 33 units, 9 distinct bodies
     assert re.fullmatch(r"[0-9a-f]{32}", stitch.compile_cuda(src))
-    _, big = stitch.Plan(stitch.Graph(config_graph("bert_layer")), "b200").codegen()
+    _, big = cached_plan(config_graph("bert_layer"), "b200").codegen()
     assert len(big) > 1 and not any(k["template"].startswith("persistent") for k in big)
 
 
@@ -171,10 +171,10 @@ def test_kernel_produced_tensors_never_read_non_coherently(monkeypatch):
     from tests.conftest import config_graph, fixture_graphs
     texts = [config_graph(n) for n in ("dien_T10", "bert_layer", "bert_cut")] + list(fixture_graphs().values())
     for text in texts:
-        g = stitch.Graph(text)
-        params = {t.name for t in g.params}
+        plan = cached_plan(text, "b200")
+        params = {t.name for t in plan.graph.params}
         for mode in ("stitched", "unfused"):
-            src, _ = stitch.Plan(g, "b200").codegen(mode)
+            src, _ = plan.codegen(mode)
             for fn, t in re.findall(r"\b(ld4c?|ld4h|ldv)\(T_(\w+)", src):
                 assert t in params, (fn, t)
 
@@ -187,7 +187,7 @@ def test_sass_no_global_write_before_pdl_wait(monkeypatch):
     monkeypatch.setenv("STITCH_RESIDENT", "0")  # launch-graph kernels (the resident kernel has no PDL)
     from tools.sass_pdl_check import check
     for name in ("dien_T10", "bert_layer", "attn_softmax", "colreduce", "bert_resln"):
-        for fn, r in check(name).items():
+        for fn, r in check(name, plan=cached_plan(config_graph(name), "b200")).items():
             assert r["waited"] and r["writes_before_wait"] == 0, (name, fn, r)
 
 

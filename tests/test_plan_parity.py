@@ -9,7 +9,7 @@ import os
 
 import pytest
 
-from tests.conftest import GOLD, golden_plan, graph_text
+from tests.conftest import GOLD, cached_plan, golden_plan, graph_text
 
 PLAN_FILES = sorted(f[:-5] for f in os.listdir(os.path.join(GOLD, "plans")) if f.endswith(".json"))
 SLOW = {"bert_cut", "dien_T20"}  # reference planner: 172 s / 14 s
@@ -26,9 +26,8 @@ def test_plan_bytes(case):
     name, cfg = case.split("__")
     rec = golden_plan(name, cfg)
     # per-shard plans carry their shard graph text
-    g = stitch.Graph(rec["graph_text"] if "graph_text" in rec else graph_text(name))
-    assert g.serialize() == rec["serialized"]
-    plan = stitch.Plan(g, cfg)
+    plan = cached_plan(rec["graph_text"] if "graph_text" in rec else graph_text(name), cfg)
+    assert plan.graph.serialize() == rec["serialized"]
     pj = plan.json()
     assert pj == rec["plan_json"]
     keys = [p["key"] for p in json.loads(pj)["patterns"]]

@@ -4,14 +4,13 @@ import re
 
 import pytest
 
-from tests.conftest import config_graph
+from tests.conftest import cached_plan, config_graph
 
 
 def _codegen(name, monkeypatch, resident=True):
     from paper_2009_10924_b200 import stitch
     monkeypatch.setenv("STITCH_RESIDENT", "1" if resident else "0")
-    g = stitch.Graph(config_graph(name))
-    return stitch.Plan(g, "b200").codegen()
+    return cached_plan(config_graph(name), "b200").codegen()
 
 
 @pytest.mark.parametrize("name,rows", [("dien_T10", 16), ("dien_T20", 16)])

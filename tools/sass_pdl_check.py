@@ -18,10 +18,11 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 
-def check(name, cfg="b200"):
+def check(name, cfg="b200", plan=None):
     from paper_2009_10924_b200 import stitch
-    g = stitch.Graph.from_file(os.path.join(stitch.GRAPHS, name + ".graph"))
-    src, _ = stitch.Plan(g, cfg).codegen()
+    if plan is None:
+        plan = stitch.Plan(stitch.Graph.from_file(os.path.join(stitch.GRAPHS, name + ".graph")), cfg)
+    src, _ = plan.codegen()
     key = stitch.compile_cuda(src)
     cache = os.environ.get("STITCH_CACHE_DIR", os.path.join(os.path.dirname(stitch.__file__), "lib", "cubin_cache"))
     sass = subprocess.run(["cuobjdump", "-sass", os.path.join(cache, key + ".cubin")], capture_output=True,
