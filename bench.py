@@ -257,11 +257,14 @@ def call_floor(stitch):
     ex = stitch.Executor(plan)
     ex.upload(stitch.random_inputs(g, 1))
     usc, _ = ex.time_call(iters=200, warmup=20, sets=2)
+    us1, _ = ex.time(iters=200, warmup=20, sets=2)
     del ex
     return {"graph": "z = x + y, f32[4]", "us_one_call": round(usc, 3), "us_serial": round(serial_us(stitch, plan, g, 2), 3),
-            "note": "a call's launch-to-completion floor on an idle device (us_one_call) and a step's floor when "
-                    "steps are queued back to back without PDL (us_serial); the subgraphs' us_one_call and us_serial "
-                    "are these plus their data time"}
+            "us_one_launch_per_step": round(us1, 3),
+            "note": "a call's launch-to-completion floor on an idle device (us_one_call), a step's floor when "
+                    "steps are queued back to back without PDL (us_serial) and when every step is its own graph "
+                    "launch (us_one_launch_per_step); the subgraphs' us_one_call, us_serial and "
+                    "us_one_launch_per_step are these plus their data time"}
 
 
 def time_subgraph(stitch, name, gemm=False, refine=False):

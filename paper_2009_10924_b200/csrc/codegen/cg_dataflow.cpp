@@ -741,8 +741,11 @@ void emit_row(Emitter& em, const CompGraph& g, const std::set<int>& pat, const B
   // 512-thread CTA (residual+LN spilled 160 B/thread): there the operands go
   // to shared memory instead (STITCH_ROW_HOIST_BCAST: 1 registers, 2 shared
   // memory, 0 off; default 2 for >= 2 streams, else 1)
-  const bool multi_row = pipe && !pipe->empty() && rp.W == 4;
-  const int hoist_mode = env_int("STITCH_ROW_HOIST_BCAST", pipe && pipe->size() >= 2 ? 2 : 1);
+  // The TMA-staged rows (st) hoist them into shared memory as well: re-read
+  // per row they were the second-largest stall in the staged LN kernel
+  // (ncu source page, profiles/r02/tma/)
+  const bool multi_row = (pipe && !pipe->empty() && rp.W == 4) || (st && rp.W == 4);
+  const int hoist_mode = env_int("STITCH_ROW_HOIST_BCAST", st || (pipe && pipe->size() >= 2) ? 2 : 1);
   if (I.size() == 1 && multi_row && hoist_mode) {
     std::set<int> srcs;
     for (int v : pat) {
@@ -1531,7 +1534,8 @@ KernelSpec generate_pattern_kernel(const CompGraph& g, const std::vector<int>& v
             --sc.stages;
           sc.bytes = 128 + int64_t(sc.stages) * static_cast<int64_t>(hits.size()) * sc.tile_floats * 4;
           if (sc.bytes <= 200 * 1024) {
-            const int64_t fit = std::clamp<int64_t>(int64_t(220 * 1024) / sc.bytes, 1, 2048 / rp.block);
+            // (less the row-invariant operands hoisted into static smem, ~2 rows)
+            const int64_t fit = std::clamp<int64_t>((int64_t(220 * 1024) - 2 * L * 4) / sc.bytes, 1, 2048 / rp.block);
             b.blocks = static_cast<int>(std::min<int64_t>(ntiles, sm_now() * fit));
             dyn_smem = std::max(dyn_smem, sc.bytes);
           } else {
@@ -1755,9 +1759,9 @@ static std::string opaque_body(const CompGraph& g, int vertex, bool single, int 
      }
     }
     fold();
-  } else {
-    // grid: 128-bit grid-stride loads, 4 independent accumulators per thread
-    // so each thread keeps 4 loads in flight
+  } else if (env_int("STITCH_OPAQUE_GRID_BATCH", 8) <= 0) {
+    // grid (the round-1 form): 128-bit grid-stride loads, 4 independent
+    // accumulators per thread, everything after the PDL wait
     s << wait;
     s << "  const i64 gt_ = (i64)blockIdx.x * blockDim.x + threadIdx.x, gs_ = (i64)gridDim.x * blockDim.x;\n"
       << "  double a0_ = 0.0, a1_ = 0.0, a2_ = 0.0, a3_ = 0.0;\n";
@@ -1783,6 +1787,85 @@ static std::string opaque_body(const CompGraph& g, int vertex, bool single, int 
       }
     }
     s << "  acc = (a0_ + a1_) + (a2_ + a3_);\n";
+  } else {
+    // grid: each thread's chunks of every operand are issued as batches of
+    // up to STITCH_OPAQUE_GRID_BATCH 128-bit loads into registers before any
+    // is folded (one memory round trip per batch instead of one per 4
+    // chunks); graph parameters are loaded before the PDL wait (coherent
+    // loads + a CTA barrier keep ptxas from sinking them below it), so they
+    // stream while the producer drains.  64 registers per thread at
+    // 4 CTAs x 256 threads per SM: 8 float4 in flight per thread
+    const int B = std::clamp(env_int("STITCH_OPAQUE_GRID_BATCH", 8), 1, 16);
+    const int64_t span = int64_t(grid) * block;
+    s << "  const i64 gt_ = (i64)blockIdx.x * " << block << " + threadIdx.x;\n";
+    int vi = 0;
+    int64_t held = 0;
+    std::vector<std::pair<std::string, int>> regs;
+    auto fold = [&]() {
+      for (const auto& [a, lanes] : regs) {
+        s << "  #pragma unroll\n  for (int k = 0; k < (int)(sizeof(" << a << ") / sizeof(" << a << "[0])); ++k) ";
+        if (lanes == 4)
+          s << "acc += ((double)" << a << "[k].x + (double)" << a << "[k].y) + ((double)" << a << "[k].z + (double)" << a
+            << "[k].w);\n";
+        else
+          s << "acc += (double)" << a << "[k];\n";
+      }
+      regs.clear();
+      held = 0;
+    };
+    bool hoisted = false;
+    for (int pass = 0; pass < 2; ++pass) {
+      if (pass == 1) {
+        fold();
+        if (hoisted && env_int("STITCH_OPAQUE_FENCE", 1) != 0) s << "  __syncthreads();\n";
+        s << wait;
+      }
+      for (int o : n.operands) {
+        if ((g.node(o).kind == OpKind::Parameter) != (pass == 0)) continue;
+        hoisted = hoisted || pass == 0;
+        const bool fence = pass == 0 && env_int("STITCH_OPAQUE_FENCE", 1) != 0;
+        const std::string L4 = pass == 1 ? "ld4k(" : fence ? "ld4p(" : "ld4(",
+                          LV = pass == 1 ? "ldvk(" : fence ? "ldvp(" : "ldv(";
+        const TensorShape& sh = g.node(o).shape;
+        const int64_t cnt = sh.element_count();
+        const bool vec = sh.dtype == DType::F32 && cnt % 4 == 0;
+        const int64_t units = vec ? cnt / 4 : cnt;
+        const int64_t K = (units + span - 1) / span;
+        const std::string T = tensor_ident(g.node(o).name);
+        if (K > B) {  // large operand: loop over batches of B chunks, each folded when it lands
+          fold();
+          const std::string a = "v" + std::to_string(vi++) + "_";
+          s << "  for (i64 b_ = gt_; b_ < " << units << "; b_ += " << B * span << ") {\n";
+          if (vec)
+            s << "    float4 " << a << "[" << B << "];\n    #pragma unroll\n    for (int k = 0; k < " << B
+              << "; ++k) { const i64 i = b_ + (i64)k * " << span << "; " << a << "[k] = i < " << units << " ? " << L4
+              << T << " + 4 * i) : make_float4(0.f, 0.f, 0.f, 0.f); }\n    #pragma unroll\n    for (int k = 0; k < " << B
+              << "; ++k) acc += ((double)" << a << "[k].x + (double)" << a << "[k].y) + ((double)" << a << "[k].z + (double)"
+              << a << "[k].w);\n  }\n";
+          else
+            s << "    float " << a << "[" << B << "];\n    #pragma unroll\n    for (int k = 0; k < " << B
+              << "; ++k) { const i64 i = b_ + (i64)k * " << span << "; " << a << "[k] = i < " << units << " ? " << LV << T
+              << ", i) : 0.f; }\n    #pragma unroll\n    for (int k = 0; k < " << B << "; ++k) acc += (double)" << a
+              << "[k];\n  }\n";
+          continue;
+        }
+        if (held > 0 && held + K > B) fold();
+        held += K;
+        const std::string a = "v" + std::to_string(vi++) + "_";
+        if (vec) {
+          s << "  float4 " << a << "[" << K << "];\n  #pragma unroll\n  for (int k = 0; k < " << K
+            << "; ++k) { const i64 i = gt_ + (i64)k * " << span << "; " << a << "[k] = i < " << units << " ? " << L4 << T
+            << " + 4 * i) : make_float4(0.f, 0.f, 0.f, 0.f); }\n";
+          regs.push_back({a, 4});
+        } else {
+          s << "  float " << a << "[" << K << "];\n  #pragma unroll\n  for (int k = 0; k < " << K
+            << "; ++k) { const i64 i = gt_ + (i64)k * " << span << "; " << a << "[k] = i < " << units << " ? " << LV << T
+            << ", i) : 0.f; }\n";
+          regs.push_back({a, 1});
+        }
+      }
+    }
+    fold();
   }
   // warp sums -> warp 0 folds them with one butterfly (fixed order,
   // deterministic) -> broadcast through shared memory

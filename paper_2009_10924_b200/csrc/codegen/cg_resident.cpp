@@ -23,9 +23,11 @@
 //     earlier unit since the last barrier wrote;
 //   * opaque placeholders (mean of every operand element, broadcast --
 //     src/sim.cpp:215-226) are the only cross-row ops: each CTA reduces its
-//     rows in f64, the partials meet through distributed shared memory behind
-//     ONE cluster barrier per group of independent placeholders, and every
-//     CTA folds the C partials in rank order (identical result everywhere).
+//     rows in f64, pushes the partials of a group of independent placeholders
+//     to every peer's shared memory (st.async, completing on the peer's
+//     mbarrier of that group; STITCH_RESIDENT_PUSH=0: one cluster barrier
+//     per group and DSMEM loads), and every CTA folds the C partials in rank
+//     order (identical result everywhere).
 // The plan (patterns, per-op f32 rounding, the opaque semantics) is the one
 // the graph executor runs; only the kernel boundaries stay on chip.
 #include <algorithm>
@@ -240,9 +242,36 @@ std::optional<KernelSpec> generate_resident_kernel(const CompGraph& g, const std
       }
     }
 
+  // placeholder groups whose partials meet by st.async pushes can be split:
+  // phase A (local fold + push) and phase B (wait for the peers' partials,
+  // fold, fill), with up to STITCH_RESIDENT_FILL ready CTA-local units that do
+  // not depend on the group run in between -- they hide the DSMEM exchange
+  // (DIEN: the attention-column units, one triple per recurrent step)
+  const char* pv = std::getenv("STITCH_RESIDENT_PUSH");
+  const bool push = C > 1 && !(pv && *pv == '0');
+  const char* fv = std::getenv("STITCH_RESIDENT_FILL");
+  const int fill_units = fv && *fv ? std::max(0, std::atoi(fv)) : 3;
+  auto group_partials = [&](const std::vector<size_t>& grp) {
+    std::map<int, int> dk;  // operand vertex -> partial index
+    for (size_t j : grp)
+      for (int o : g.node(us[j].verts[0]).operands) dk.emplace(o, static_cast<int>(dk.size()));
+    return dk;
+  };
+  auto warp_path_of = [&](const std::map<int, int>& dk) {
+    bool ok = dk.size() <= 32;
+    for (auto [o, k] : dk) ok = ok && local_elems(o) <= 16384;
+    return ok;
+  };
+  auto pushed = [&](const std::vector<size_t>& grp) {
+    return push && warp_path_of(group_partials(grp)) && static_cast<int64_t>(grp.size()) * C <= 1024;
+  };
+
   // schedule: CTA-local units as soon as they are ready; ready placeholders
-  // wait until nothing else is, then run together behind one cluster barrier
+  // wait until nothing else is, then run together as one group -- or, with
+  // split groups, as soon as they are ready, with fillers inside the group
+  enum Phase { kUnit = 0, kGroupA = 1, kGroupB = 2, kGroup = 3 };
   std::vector<std::vector<size_t>> steps;  // one unit, or a group of placeholders
+  std::vector<int> phase;
   {
     std::vector<size_t> pending(us.size());
     std::set<size_t> ready;
@@ -254,18 +283,44 @@ std::optional<KernelSpec> generate_resident_kernel(const CompGraph& g, const std
       for (size_t w : users[i])
         if (--pending[w] == 0) ready.insert(w);
     };
+    auto next_local = [&]() {
+      return std::find_if(ready.begin(), ready.end(), [&](size_t i) { return !us[i].opaque; });
+    };
     while (!ready.empty()) {
-      auto it = std::find_if(ready.begin(), ready.end(), [&](size_t i) { return !us[i].opaque; });
+      std::vector<size_t> ops;
+      for (size_t i : ready)
+        if (us[i].opaque) ops.push_back(i);
+      if (fill_units > 0 && !ops.empty() && pushed(ops)) {
+        for (size_t i : ops) ready.erase(i);
+        steps.push_back(ops);
+        phase.push_back(kGroupA);
+        for (int f = 0; f < fill_units; ++f) {
+          auto it = next_local();
+          if (it == ready.end()) break;
+          const size_t i = *it;
+          ready.erase(it);
+          steps.push_back({i});
+          phase.push_back(kUnit);
+          finish(i);
+        }
+        steps.push_back(ops);
+        phase.push_back(kGroupB);
+        for (size_t i : ops) finish(i);
+        continue;
+      }
+      auto it = next_local();
       if (it != ready.end()) {
         const size_t i = *it;
         ready.erase(it);
         steps.push_back({i});
+        phase.push_back(kUnit);
         finish(i);
         continue;
       }
       std::vector<size_t> grp(ready.begin(), ready.end());
       ready.clear();
       steps.push_back(grp);
+      phase.push_back(kGroup);
       for (size_t i : grp) finish(i);
     }
     if (done != us.size()) return no("unit dependency cycle");
@@ -277,8 +332,9 @@ std::optional<KernelSpec> generate_resident_kernel(const CompGraph& g, const std
   std::set<int> graph_out(g.outputs.begin(), g.outputs.end());
   std::map<int, size_t> last_step;
   for (size_t s = 0; s < steps.size(); ++s)
-    for (size_t i : steps[s])
-      for (int t : us[i].ins) last_step[t] = s;
+    if (phase[s] != kGroupB)  // phase B only writes the group's outputs
+      for (size_t i : steps[s])
+        for (int t : us[i].ins) last_step[t] = s;
   std::map<int, Slot> slot;
   std::vector<Slot> free_list, pending_free;
   int64_t smem_top = 0;
@@ -377,11 +433,38 @@ std::optional<KernelSpec> generate_resident_kernel(const CompGraph& g, const std
   };
   // STITCH_RESIDENT_PUSH=0: placeholder partials meet behind a cluster
   // barrier (DSMEM pull) instead of st.async pushes + per-group mbarriers
-  const char* pv = std::getenv("STITCH_RESIDENT_PUSH");
-  const bool push = C > 1 && !(pv && *pv == '0');
   int n_push = 0;
+  std::map<size_t, std::pair<int, int>> split_of;  // group's first unit -> (mbarrier, inbox slot base)
   bool staged_ready = staged.empty();
   for (size_t s = 0; s < steps.size(); ++s) {
+    if (phase[s] == kGroupB) {
+      // the peers' partials: wait, fold in rank order, fill (the barrier
+      // inside orders the fillers run since phase A as well)
+      const auto& grp = steps[s];
+      const auto [bar, base] = split_of.at(grp[0]);
+      body << "  STC_TRACE_STAMP_END(" << s << ");\n  STC_TRACE_BEGIN(" << 1 + s << ");\n";
+      body << "  {  // placeholder group (wait):";
+      for (size_t i : grp) body << " " << g.node(us[i].verts[0]).name;
+      body << "\n    mbar_wait_cluster(&rs_gbar_[" << bar << "], 0u);\n";
+      body << "    {\n      const int w_ = threadIdx.x >> 5, l_ = threadIdx.x & 31;\n";
+      for (size_t j = 0; j < grp.size(); ++j) {
+        const OpNode& n = g.node(us[grp[j]].verts[0]);
+        int64_t count = 0;
+        for (int o : n.operands) count += g.node(o).shape.element_count();
+        body << "      if (w_ == " << j % 32 << ") { double t_ = l_ < " << C << " ? rs_inbox_[(" << base + static_cast<int>(j)
+             << ") * " << C << " + l_] : 0.0; t_ = bfly_sum(t_, 32); if (l_ == 0) rs_fill_[" << j << "] = (float)("
+             << (count ? "t_ / " + std::to_string(count) + ".0" : "0.0") << "); }\n";
+      }
+      body << "    }\n    __syncthreads();\n";
+      ++n_barriers;
+      since_barrier.clear();
+      free_list.insert(free_list.end(), pending_free.begin(), pending_free.end());
+      pending_free.clear();
+      emit_fills(grp);
+      body << "  }\n";
+      for (size_t i : grp) since_barrier.insert(i);
+      continue;
+    }
     if (!staged_ready) {
       bool reads = false;
       for (size_t i : steps[s])
@@ -458,7 +541,7 @@ std::optional<KernelSpec> generate_resident_kernel(const CompGraph& g, const std
         body << "        d_ = bfly_sum(d_, 32); if (l_ == 0) rs_red_[" << k << "] = d_; }\n";
       }
       body << "    }\n    __syncthreads();\n";
-      if (push && static_cast<int64_t>(grp.size()) * C <= 1024) {
+      if (pushed(grp)) {
         // push: thread (j, r) sends member j's partial to rank r's inbox
         // (st.async, completing on rank r's mbarrier of this group); every
         // CTA waits only for the C x G partials addressed to it
@@ -471,8 +554,20 @@ std::optional<KernelSpec> generate_resident_kernel(const CompGraph& g, const std
         }
         body << "      st_async_f64(&rs_inbox_[(" << opaque_slots << " + j_) * " << C << " + rk_], v_, &rs_gbar_["
              << n_push << "], (unsigned)r_);\n    }\n"
-             << "    if (threadIdx.x == 0) mbar_expect_tx(&rs_gbar_[" << n_push << "], " << grp.size() * C * 8 << "u);\n"
-             << "    mbar_wait_cluster(&rs_gbar_[" << n_push << "], 0u);\n";
+             << "    if (threadIdx.x == 0) mbar_expect_tx(&rs_gbar_[" << n_push << "], " << grp.size() * C * 8 << "u);\n";
+        if (phase[s] == kGroupA) {  // phase B waits, after the fillers
+          split_of[grp[0]] = {n_push, opaque_slots};
+          ++n_push;
+          opaque_slots += static_cast<int>(grp.size());
+          body << "  }\n";
+          // the barrier after the local fold ordered everything before it
+          since_barrier.clear();
+          free_list.insert(free_list.end(), pending_free.begin(), pending_free.end());
+          pending_free.clear();
+          retire_inputs(s);
+          continue;
+        }
+        body << "    mbar_wait_cluster(&rs_gbar_[" << n_push << "], 0u);\n";
         ++n_push;
         body << "    {\n      const int w_ = threadIdx.x >> 5, l_ = threadIdx.x & 31;\n";
         for (size_t j = 0; j < grp.size(); ++j) {
@@ -586,10 +681,8 @@ std::optional<KernelSpec> generate_resident_kernel(const CompGraph& g, const std
     << (n_push ? "  __shared__ double rs_inbox_[" + std::to_string(opaque_slots * C) + "];\n"
                  "  __shared__ __align__(8) unsigned long long rs_gbar_[" + std::to_string(n_push) + "];\n" : std::string())
     << "  const int rk_ = (int)cluster_ctarank();\n  (void)rk_;\n";
-  if (n_push) {  // peers push into our inbox only after every mbarrier of the cluster is initialised
-    s << "  if (threadIdx.x < " << n_push << ") mbar_init(&rs_gbar_[threadIdx.x], 1);\n"
-      << "  if (threadIdx.x == 0) mbar_fence_init();\n  cluster_sync_all();\n";
-  }
+  // the parameter staging is issued first: its HBM round trip then overlaps
+  // the cluster barrier that publishes the inbox mbarriers below
   if (!staged.empty()) {
     s << "  __shared__ __align__(8) unsigned long long rs_mbar_;\n"
       << "  if (threadIdx.x == 0) {\n    mbar_init(&rs_mbar_, 1);\n    mbar_fence_init();\n"
@@ -599,7 +692,12 @@ std::optional<KernelSpec> generate_resident_kernel(const CompGraph& g, const std
       s << "    bulk_g2s(rs_smem_ + " << slot[t].off << ", " << tensor_ident(g.node(t).name) << off << ", "
         << local_bytes(t) << "u, &rs_mbar_);\n";
     }
-    s << "  }\n  __syncthreads();  // the mbarrier is initialised before anyone waits on it\n";
+    s << "  }\n";
+    if (!n_push) s << "  __syncthreads();  // the mbarrier is initialised before anyone waits on it\n";
+  }
+  if (n_push) {  // peers push into our inbox only after every mbarrier of the cluster is initialised
+    s << "  if (threadIdx.x < " << n_push << ") mbar_init(&rs_gbar_[threadIdx.x], 1);\n"
+      << "  if (threadIdx.x == 0) mbar_fence_init();\n  cluster_sync_all();  // also orders rs_mbar_'s init before any wait\n";
   }
   s << body.str()
     << "  cluster_sync_all();  // peers may still read rs_part_ through DSMEM\n}\n";

@@ -163,7 +163,10 @@ void Executor::finish_init(const std::string& cubin) {
     }
     cudaKernel_t f = module_->fn(k.symbol.empty() ? k.name : k.symbol);
     const void* fp = reinterpret_cast<const void*>(f);
-    if (k.smem > 48 * 1024)
+    // opt in whenever there is dynamic shared memory: static + dynamic above
+    // 48 KB needs it even when the dynamic part alone is below (TMA-staged
+    // rows with their row-invariant operands hoisted into static smem)
+    if (k.smem > 0)
       STC_RT(cudaFuncSetAttribute(fp, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(k.smem)));
     if (k.cluster > 8) STC_RT(cudaFuncSetAttribute(fp, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     if (k.cooperative) {

@@ -532,12 +532,15 @@ def _variant_text(name):
     return EDGE_SHAPES[name] if name in EDGE_SHAPES else config_graph(name)
 
 
+@pytest.mark.parametrize("stages", ["2", "3"])
 @pytest.mark.parametrize("name", STAGE_CASES)
-def test_tma_staged_regional_matches_oracle(name, monkeypatch):
+def test_tma_staged_regional_matches_oracle(name, stages, monkeypatch):
     """STITCH_STAGE=1: regional rows streamed into shared memory by
     cp.async.bulk (TMA bulk copies completing on an mbarrier, multi-stage
     ring per CTA) instead of registers -- same bits as the register path,
-    within tolerance of the oracle, over repeated launches (ring phases)"""
+    within tolerance of the oracle, over repeated launches (ring phases).
+    2 stages: dynamic smem below 48 KB plus the hoisted row-invariant
+    operands in static smem above it (the launch needs the opt-in)"""
     stitch = _stitch()
     text = _variant_text(name)
     g = stitch.Graph(text)
@@ -545,6 +548,7 @@ def test_tma_staged_regional_matches_oracle(name, monkeypatch):
     inputs = stitch.random_inputs(g, 4)
     ref = stitch.Executor(plan).run(inputs)
     monkeypatch.setenv("STITCH_STAGE", "1")
+    monkeypatch.setenv("STITCH_STAGES", stages)
     ex = stitch.Executor(plan)
     kinds = [k["template"] for k in ex.describe()]
     if name in ("ln_4096x768", "ln2pass_4096x768", "bert_resln", "bert_cut"):
