@@ -149,14 +149,58 @@ void Executor::finish_init(const std::string& cubin) {
       STC_LT(cublasLtMatmulPreferenceCreate(&pref));
       STC_LT(cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES, &gemm_->ws_bytes,
                                                   sizeof(gemm_->ws_bytes)));
-      cublasLtMatmulHeuristicResult_t res{};
+      // STITCH_GEMM_TUNE=n > 1: the heuristic's top n candidates are timed
+      // once on scratch operands of this shape (best of 3 after a warm-up)
+      // and the fastest kept.  Default 1, the heuristic's first choice: on
+      // the BERT layer tuning over 8 candidates changed nothing (94.7 vs
+      // 94.8 us) and over 16 picked a slower one in the graph (98.6 us;
+      // profiles/r02/gemm/gemm_tune.jsonl)
+      const char* tv = std::getenv("STITCH_GEMM_TUNE");
+      const int want = std::clamp(tv && *tv ? std::atoi(tv) : 1, 1, 32);
+      std::vector<cublasLtMatmulHeuristicResult_t> res(static_cast<size_t>(want));
       int found = 0;
       const cublasStatus_t hs =
-          cublasLtMatmulAlgoGetHeuristic(gemm_->lt, u.op, u.b, u.a, u.c, u.c, pref, 1, &res, &found);
+          cublasLtMatmulAlgoGetHeuristic(gemm_->lt, u.op, u.b, u.a, u.c, u.c, pref, want, res.data(), &found);
       cublasLtMatmulPreferenceDestroy(pref);
       if (hs != CUBLAS_STATUS_SUCCESS || found < 1)
         throw std::runtime_error("[cublasLt] no algorithm for GEMM " + k.name);
-      u.algo = res.algo;
+      int best = 0;
+      if (found > 1) {
+        void *da = nullptr, *db = nullptr, *dc = nullptr;
+        STC_RT(cudaMalloc(&da, M * K * sizeof(float)));
+        STC_RT(cudaMalloc(&db, K * N * sizeof(float)));
+        STC_RT(cudaMalloc(&dc, M * N * sizeof(float)));
+        STC_RT(cudaMemset(da, 0x3c, M * K * sizeof(float)));
+        STC_RT(cudaMemset(db, 0x3c, K * N * sizeof(float)));
+        cudaEvent_t e0, e1;
+        STC_RT(cudaEventCreate(&e0));
+        STC_RT(cudaEventCreate(&e1));
+        const float alpha = 1.f, beta = 0.f;
+        float best_ms = 0.f;
+        for (int c = 0; c < found; ++c) {
+          float t = -1.f;
+          for (int rep = 0; rep < 4; ++rep) {
+            STC_RT(cudaEventRecord(e0, stream_));
+            if (cublasLtMatmul(gemm_->lt, u.op, &alpha, db, u.b, da, u.a, &beta, dc, u.c, dc, u.c, &res[c].algo,
+                               gemm_->workspace, gemm_->ws_bytes, stream_) != CUBLAS_STATUS_SUCCESS) {
+              t = -1.f;
+              break;
+            }
+            STC_RT(cudaEventRecord(e1, stream_));
+            STC_RT(cudaEventSynchronize(e1));
+            float ms = 0.f;
+            STC_RT(cudaEventElapsedTime(&ms, e0, e1));
+            if (rep > 0 && (t < 0.f || ms < t)) t = ms;
+          }
+          if (t > 0.f && (best_ms == 0.f || t < best_ms)) best_ms = t, best = c;
+        }
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        cudaFree(da);
+        cudaFree(db);
+        cudaFree(dc);
+      }
+      u.algo = res[static_cast<size_t>(best)].algo;
       gemm_->units[ki] = u;
       fns_.push_back(nullptr);
       continue;
