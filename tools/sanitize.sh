@@ -20,4 +20,12 @@ timeout 1500 compute-sanitizer --tool racecheck --print-limit 10 python -m pytes
   -k "tma_staged or grid_barrier" > gpurun_out/racecheck_variants.log 2>&1
 timeout 1500 compute-sanitizer --tool synccheck --print-limit 10 python -m pytest tests/test_gpu_exec.py -q -x \
   -k "tma_staged or grid_barrier" > gpurun_out/synccheck_variants.log 2>&1
+# resident template (one cluster kernel: DSMEM st.async pushes, mbarriers,
+# cp.async.bulk parameter staging, split placeholder groups)
+timeout 1500 compute-sanitizer --tool memcheck --print-limit 20 python -m pytest tests/test_gpu_exec.py -q -x \
+  -k "resident" > gpurun_out/memcheck_resident.log 2>&1
+timeout 1500 compute-sanitizer --tool racecheck --print-limit 10 python -m pytest tests/test_gpu_exec.py -q -x \
+  -k "resident_template_matches" > gpurun_out/racecheck_resident.log 2>&1
+timeout 1500 compute-sanitizer --tool synccheck --print-limit 10 python -m pytest tests/test_gpu_exec.py -q -x \
+  -k "resident_template_matches" > gpurun_out/synccheck_resident.log 2>&1
 tail -n 2 gpurun_out/memcheck*.log gpurun_out/racecheck*.log gpurun_out/synccheck*.log
