@@ -31,6 +31,7 @@
 // The plan (patterns, per-op f32 rounding, the opaque semantics) is the one
 // the graph executor runs; only the kernel boundaries stay on chip.
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <map>
 #include <optional>
@@ -185,6 +186,18 @@ std::optional<KernelSpec> generate_resident_kernel(const CompGraph& g, const std
       break;
     }
   const int64_t R = B / C;
+  // folding the C partials: a butterfly over the next power of two lanes;
+  // the mean as a product with the correctly rounded reciprocal of the
+  // count (a double division is a ~100-cycle subroutine on the step's
+  // critical path; the f32 mean it rounds to is the quotient's)
+  int fold_w = 1;
+  while (fold_w < C) fold_w *= 2;
+  fold_w = std::max(fold_w, 2);
+  auto inv_count = [](int64_t count) {
+    char buf[64];
+    std::snprintf(buf, sizeof buf, "%.17g", 1.0 / static_cast<double>(count));
+    return std::string(buf);
+  };
   CompGraph gs = g;  // the shard graph: batch R, same node ids
   for (auto& n : gs.nodes) {
     if (!sharded[static_cast<size_t>(n.id)]) continue;
@@ -452,8 +465,8 @@ std::optional<KernelSpec> generate_resident_kernel(const CompGraph& g, const std
         int64_t count = 0;
         for (int o : n.operands) count += g.node(o).shape.element_count();
         body << "      if (w_ == " << j % 32 << ") { double t_ = l_ < " << C << " ? rs_inbox_[(" << base + static_cast<int>(j)
-             << ") * " << C << " + l_] : 0.0; t_ = bfly_sum(t_, 32); if (l_ == 0) rs_fill_[" << j << "] = (float)("
-             << (count ? "t_ / " + std::to_string(count) + ".0" : "0.0") << "); }\n";
+             << ") * " << C << " + l_] : 0.0; t_ = bfly_sum(t_, " << fold_w << "); if (l_ == 0) rs_fill_[" << j << "] = (float)("
+             << (count ? "t_ * " + inv_count(count) : "0.0") << "); }\n";
       }
       body << "    }\n    __syncthreads();\n";
       ++n_barriers;
@@ -526,19 +539,42 @@ std::optional<KernelSpec> generate_resident_kernel(const CompGraph& g, const std
     // larger ones: block-wide per-thread partials + two-level fold
     bool warp_path = dk.size() <= 32;
     for (auto [o, k] : dk) warp_path = warp_path && local_elems(o) <= 16384;
+    // W warps per operand (32 / operands, at most one chunk per lane each):
+    // warp k*W + j folds chunks j*32 + lane, step W*32, of operand k; the
+    // operand's partial is then the W warp sums added in j order
+    // (STITCH_RESIDENT_WARPS caps W; 1 = one warp per operand, the round-2
+    // first form: 0.65 us per DIEN step fold, profiles/r02/resident/)
+    int W = 1;
+    if (warp_path) {
+      int64_t most = 1;
+      for (auto [o, k] : dk) {
+        const int64_t cnt = local_elems(o);
+        most = std::max<int64_t>(most, g.node(o).shape.dtype == DType::F32 && cnt % 4 == 0 ? cnt / 4 : cnt);
+      }
+      const char* wv = std::getenv("STITCH_RESIDENT_WARPS");
+      const int wcap = wv && *wv ? std::max(1, std::atoi(wv)) : 32;
+      W = static_cast<int>(std::clamp<int64_t>((most + 31) / 32, 1, std::min<int64_t>(wcap, 32 / std::max<size_t>(1, dk.size()))));
+    }
+    auto operand_partial = [&](int k) {
+      std::string e = "rs_red_[" + std::to_string(k * W) + "]";
+      for (int j = 1; j < W; ++j) e = "(" + e + " + rs_red_[" + std::to_string(k * W + j) + "])";
+      return e;
+    };
     if (warp_path) {
       body << "    {\n      const int w_ = threadIdx.x >> 5, l_ = threadIdx.x & 31;\n";
       for (auto [o, k] : dk) {
         const TensorShape& sh = g.node(o).shape;
         const int64_t cnt = local_elems(o);
         const std::string guard = !sharded[static_cast<size_t>(o)] ? " && rk_ == 0" : "";
-        body << "      if (w_ == " << k << ") { double d_ = 0.0;\n        if (true" << guard << ") ";
+        body << "      if (w_ >= " << k * W << " && w_ < " << (k + 1) * W << ") { const int j_ = w_ - " << k * W
+             << "; double d_ = 0.0;\n        if (true" << guard << ") ";
         if (sh.dtype == DType::F32 && cnt % 4 == 0)
-          body << "for (int i = l_; i < " << cnt / 4 << "; i += 32) { const float4 q = ld4_g(" << ptr(o)
+          body << "for (int i = j_ * 32 + l_; i < " << cnt / 4 << "; i += " << 32 * W << ") { const float4 q = ld4_g(" << ptr(o)
                << " + 4 * i); d_ += ((double)q.x + (double)q.y) + ((double)q.z + (double)q.w); }\n";
         else
-          body << "for (int i = l_; i < " << cnt << "; i += 32) d_ += (double)ldv_g(" << ptr(o) << ", i);\n";
-        body << "        d_ = bfly_sum(d_, 32); if (l_ == 0) rs_red_[" << k << "] = d_; }\n";
+          body << "for (int i = j_ * 32 + l_; i < " << cnt << "; i += " << 32 * W << ") d_ += (double)ldv_g(" << ptr(o)
+               << ", i);\n";
+        body << "        d_ = bfly_sum(d_, 32); if (l_ == 0) rs_red_[" << k * W << " + j_] = d_; }\n";
       }
       body << "    }\n    __syncthreads();\n";
       if (pushed(grp)) {
@@ -549,7 +585,7 @@ std::optional<KernelSpec> generate_resident_kernel(const CompGraph& g, const std
              << ", r_ = threadIdx.x % " << C << ";\n      double v_ = 0.0;\n";
         for (size_t j = 0; j < grp.size(); ++j) {
           body << "      " << (j ? "else " : "") << "if (j_ == " << j << ") v_ = 0.0";
-          for (int o : g.node(us[grp[j]].verts[0]).operands) body << " + rs_red_[" << dk[o] << "]";
+          for (int o : g.node(us[grp[j]].verts[0]).operands) body << " + " << operand_partial(dk[o]);
           body << ";\n";
         }
         body << "      st_async_f64(&rs_inbox_[(" << opaque_slots << " + j_) * " << C << " + rk_], v_, &rs_gbar_["
@@ -575,8 +611,8 @@ std::optional<KernelSpec> generate_resident_kernel(const CompGraph& g, const std
           int64_t count = 0;
           for (int o : n.operands) count += g.node(o).shape.element_count();
           body << "      if (w_ == " << j % 32 << ") { double t_ = l_ < " << C << " ? rs_inbox_[("
-               << opaque_slots + static_cast<int>(j) << ") * " << C << " + l_] : 0.0; t_ = bfly_sum(t_, 32); if (l_ == 0) rs_fill_["
-               << j << "] = (float)(" << (count ? "t_ / " + std::to_string(count) + ".0" : "0.0") << "); }\n";
+               << opaque_slots + static_cast<int>(j) << ") * " << C << " + l_] : 0.0; t_ = bfly_sum(t_, " << fold_w << "); if (l_ == 0) rs_fill_["
+               << j << "] = (float)(" << (count ? "t_ * " + inv_count(count) : "0.0") << "); }\n";
         }
         body << "    }\n    __syncthreads();\n";
         emit_fills(grp);
@@ -591,7 +627,7 @@ std::optional<KernelSpec> generate_resident_kernel(const CompGraph& g, const std
       }
       for (size_t j = 0; j < grp.size(); ++j) {
         body << "    if (threadIdx.x == " << j << ") rs_part_[" << opaque_slots + static_cast<int>(j) << "] = 0.0";
-        for (int o : g.node(us[grp[j]].verts[0]).operands) body << " + rs_red_[" << dk[o] << "]";
+        for (int o : g.node(us[grp[j]].verts[0]).operands) body << " + " << operand_partial(dk[o]);
         body << ";\n";
       }
       body << "    {\n";
@@ -630,8 +666,8 @@ std::optional<KernelSpec> generate_resident_kernel(const CompGraph& g, const std
       int64_t count = 0;
       for (int o : n.operands) count += g.node(o).shape.element_count();
       body << "      if (w_ == " << j % 32 << ") { double t_ = l_ < " << C << " ? ld_dsmem_f64(&rs_part_["
-           << opaque_slots + static_cast<int>(j) << "], (unsigned)l_) : 0.0; t_ = bfly_sum(t_, 32); if (l_ == 0) rs_fill_["
-           << j << "] = (float)(" << (count ? "t_ / " + std::to_string(count) + ".0" : "0.0") << "); }\n";
+           << opaque_slots + static_cast<int>(j) << "], (unsigned)l_) : 0.0; t_ = bfly_sum(t_, " << fold_w << "); if (l_ == 0) rs_fill_["
+           << j << "] = (float)(" << (count ? "t_ * " + inv_count(count) : "0.0") << "); }\n";
     }
     body << "    }\n    __syncthreads();\n";
     emit_fills(grp);

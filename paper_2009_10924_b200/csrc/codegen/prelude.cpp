@@ -258,9 +258,14 @@ __device__ __forceinline__ unsigned long long gtimer() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
-#define STC_TRACE_BEGIN(k) do { if (threadIdx.x == 0) atomicMin(&stc_trace_[2 * (k)], gtimer()); } while (0)
-#define STC_TRACE_END(k) do { __syncthreads(); if (threadIdx.x == 0) atomicMax(&stc_trace_[2 * (k) + 1], gtimer()); } while (0)
-#define STC_TRACE_STAMP_END(k) do { if (threadIdx.x == 0) atomicMax(&stc_trace_[2 * (k) + 1], gtimer()); } while (0)
+#ifdef STITCH_TRACE_CTAS  // per-CTA slots: k * CTAS + CTA (CTAs past CTAS fold into CTA 0's)
+#define STC_SLOT(k) ((k) * STITCH_TRACE_CTAS + (blockIdx.x < STITCH_TRACE_CTAS ? blockIdx.x : 0))
+#else
+#define STC_SLOT(k) (k)
+#endif
+#define STC_TRACE_BEGIN(k) do { if (threadIdx.x == 0) atomicMin(&stc_trace_[2 * STC_SLOT(k)], gtimer()); } while (0)
+#define STC_TRACE_END(k) do { __syncthreads(); if (threadIdx.x == 0) atomicMax(&stc_trace_[2 * STC_SLOT(k) + 1], gtimer()); } while (0)
+#define STC_TRACE_STAMP_END(k) do { if (threadIdx.x == 0) atomicMax(&stc_trace_[2 * STC_SLOT(k) + 1], gtimer()); } while (0)
 #else
 #define STC_TRACE_BEGIN(k) do {} while (0)
 #define STC_TRACE_END(k) do {} while (0)

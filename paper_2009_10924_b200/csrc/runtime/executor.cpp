@@ -99,6 +99,12 @@ Executor::Executor(const CompGraph& g, const FusionPlan& plan,
   if (const char* t = std::getenv("STITCH_TRACE"); t && *t == '1') {
     opts.push_back("-DSTITCH_TRACE");
     tracing_ = true;
+    // STITCH_TRACE_CTAS=c: slot k of CTA b < c is recorded on its own
+    // (slot k*c + b), so per-CTA step times come back without cross-CTA skew
+    if (const char* c = std::getenv("STITCH_TRACE_CTAS"); c && std::atoi(c) > 0) {
+      trace_ctas_ = std::atoi(c);
+      opts.push_back("-DSTITCH_TRACE_CTAS=" + std::to_string(trace_ctas_));
+    }
   }
   ensure_sets(1);
   if (async_compile) {
@@ -1217,6 +1223,7 @@ std::vector<std::pair<double, double>> Executor::trace(int set) {
   // ... and a resident kernel each of its steps
   if (std::smatch m; n == 1 && std::regex_search(specs_[0].tmpl, m, std::regex(R"(^resident\(.* (\d+) steps)")))
     n = 1 + std::stoul(m[1].str());
+  n *= static_cast<size_t>(std::max(1, trace_ctas_));
   std::vector<unsigned long long> init(2 * n);
   for (size_t i = 0; i < n; ++i) init[2 * i] = ~0ull, init[2 * i + 1] = 0ull;
   ensure_sets(set + 1);

@@ -161,6 +161,7 @@ class Executor {
   bool coop_in_graph_ = true;
   bool pdl_ = true;  // STITCH_PDL=0 disables programmatic dependent launch
   bool tracing_ = false;
+  int trace_ctas_ = 0;  // STITCH_TRACE_CTAS: per-CTA trace slots
   bool dag_ = true;  // STITCH_DAG=0 captures the plan as one linear chain
   bool sources_only_ = false;  // STITCH_DAG=2: fork only producer-less kernels
   std::vector<std::vector<int>> deps_;       // [kernel] -> producer kernels

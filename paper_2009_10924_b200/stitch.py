@@ -475,6 +475,7 @@ class Executor:
             n = 1 + int(d[0]["template"][11:-1])
         if n == 1 and d[0]["template"].startswith("resident("):  # + one entry per step
             n = 1 + int(re.search(r" (\d+) steps", d[0]["template"]).group(1))
+        n *= max(1, int(os.environ.get("STITCH_TRACE_CTAS", "0") or 0))  # per-CTA slots: k * CTAS + CTA
         a, b = (ctypes.c_double * max(1, n))(), (ctypes.c_double * max(1, n))()
         _check(lib().stc_exec_trace(self._h, a, b))
         return list(zip(a[:n], b[:n]))
