@@ -458,7 +458,10 @@ std::optional<KernelSpec> generate_resident_kernel(const CompGraph& g, const std
       body << "  STC_TRACE_STAMP_END(" << s << ");\n  STC_TRACE_BEGIN(" << 1 + s << ");\n";
       body << "  {  // placeholder group (wait):";
       for (size_t i : grp) body << " " << g.node(us[i].verts[0]).name;
-      body << "\n    mbar_wait_cluster(&rs_gbar_[" << bar << "], 0u);\n";
+      // only the folding warps read the inbox: they alone wait on it (a
+      // cluster-scope acquire per thread); the barrier below holds the rest
+      body << "\n    if (threadIdx.x < " << 32 * std::min<size_t>(grp.size(), 32)
+           << ") mbar_wait_cluster(&rs_gbar_[" << bar << "], 0u);\n";
       body << "    {\n      const int w_ = threadIdx.x >> 5, l_ = threadIdx.x & 31;\n";
       for (size_t j = 0; j < grp.size(); ++j) {
         const OpNode& n = g.node(us[grp[j]].verts[0]);
@@ -603,7 +606,8 @@ std::optional<KernelSpec> generate_resident_kernel(const CompGraph& g, const std
           retire_inputs(s);
           continue;
         }
-        body << "    mbar_wait_cluster(&rs_gbar_[" << n_push << "], 0u);\n";
+        body << "    if (threadIdx.x < " << 32 * std::min<size_t>(grp.size(), 32) << ") mbar_wait_cluster(&rs_gbar_["
+             << n_push << "], 0u);\n";
         ++n_push;
         body << "    {\n      const int w_ = threadIdx.x >> 5, l_ = threadIdx.x & 31;\n";
         for (size_t j = 0; j < grp.size(); ++j) {
