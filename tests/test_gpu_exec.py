@@ -698,3 +698,32 @@ def test_resident_request_on_any_graph_is_correct(name, monkeypatch):
     monkeypatch.setenv("STITCH_RESIDENT", "1")
     text = fixture_graphs()[name] if name in FIXTURES else config_graph(name)
     _check(text, "b200", "stitched", 2, bitwise=name in LIGHT_ONLY)
+
+
+SHARD_CASES = [(name, n) for name in ["attn_softmax", "ln_4096x768", "ln2pass_4096x768", "bert_gelu", "bert_resln",
+                                      "bert_cut", "colreduce"] for n in (2, 4, 8)]
+
+
+@pytest.mark.parametrize("name,n", SHARD_CASES)
+def test_shard_plans_reassemble_full_graph_on_gpu(name, n):
+    """multi-GPU path, one shard after another on this GPU: each
+    of the n shards runs its OWN plan (shard shapes re-plan; golden per-shard
+    plans in tests/golden/plans/*@n__b200.json) on the CUDA executor, and the
+    gathered outputs equal the FULL graph's oracle at the north-star
+    tolerances -- what n GPUs running one shard each produce"""
+    from paper_2009_10924_b200.shard import RULES
+    stitch = _stitch()
+    rule = RULES[name]
+    text = config_graph(name)
+    g_full = stitch.Graph(text)
+    inputs = stitch.random_inputs(g_full, 1)
+    shard_text = rule.graph_text(text, n)
+    ex = stitch.Executor(stitch.Plan(stitch.Graph(shard_text), "b200"))
+    parts = [ex.run(rule.slice_inputs(inputs, n, r)) for r in range(n)]
+    got = rule.concat_outputs(parts)
+    og = no.parse_graph(text)
+    want = no.eval_reference(og, {k: v.astype(np.float64) for k, v in inputs.items()})
+    for k, tol in _tolerances(og).items():
+        assert got[k].shape == want[k].shape, k
+        rep = stitch.compare({k: got[k]}, {k: want[k]}, tol, _abs_floor(og, k))
+        assert rep["pass"], "%s@%d %s: %s" % (name, n, k, rep["message"])
