@@ -458,6 +458,49 @@ std::optional<KernelSpec> generate_resident_kernel(const CompGraph& g, const std
       body << "  STC_TRACE_STAMP_END(" << s << ");\n  STC_TRACE_BEGIN(" << 1 + s << ");\n";
       body << "  {  // placeholder group (wait):";
       for (size_t i : grp) body << " " << g.node(us[i].verts[0]).name;
+      // small groups (DIEN's three gates per step): every filling thread
+      // folds the C partials itself, in rank order, and writes its share of
+      // the fills -- no butterfly, no rs_fill_ round trip, no barrier here
+      // (the next reader of the fills barriers as usual).  The group's
+      // output slots come only from barrier-protected free slots: the
+      // fillers since phase A may still be reading theirs
+      // (STITCH_RESIDENT_DIRECT_FOLD=0: butterfly fold + barrier + fill)
+      const char* dfv = std::getenv("STITCH_RESIDENT_DIRECT_FOLD");
+      if (!(dfv && *dfv == '0') && grp.size() <= 4) {
+        for (size_t i : grp) place_outputs(i);
+        int64_t most = 1;
+        for (size_t i : grp) {
+          const OpNode& n = g.node(us[i].verts[0]);
+          const int64_t nout = local_elems(n.id);
+          most = std::max<int64_t>(most, n.shape.dtype == DType::F32 && nout % 4 == 0 ? nout / 4 : nout);
+        }
+        const int T = static_cast<int>(std::min<int64_t>(1024, (most + 31) / 32 * 32));
+        body << "\n    if (threadIdx.x < " << T << ") {\n      mbar_wait_cluster(&rs_gbar_[" << bar << "], 0u);\n";
+        for (size_t j = 0; j < grp.size(); ++j) body << "      double t" << j << "_ = 0.0;\n";
+        body << "      #pragma unroll\n      for (int r_ = 0; r_ < " << C << "; ++r_) {";
+        for (size_t j = 0; j < grp.size(); ++j)
+          body << " t" << j << "_ += rs_inbox_[(" << base + static_cast<int>(j) << ") * " << C << " + r_];";
+        body << " }\n";
+        for (size_t j = 0; j < grp.size(); ++j) {
+          const OpNode& n = g.node(us[grp[j]].verts[0]);
+          int64_t count = 0;
+          for (int o : n.operands) count += g.node(o).shape.element_count();
+          const int64_t nout = local_elems(n.id);
+          const bool rep_out = !sharded[static_cast<size_t>(n.id)] && graph_out.count(n.id);
+          const std::string guard = rep_out ? "if (rk_ == 0) " : "";
+          body << "      { const float fill = (float)(" << (count ? "t" + std::to_string(j) + "_ * " + inv_count(count) : "0.0")
+               << ");\n";
+          if (n.shape.dtype == DType::F32 && nout % 4 == 0)
+            body << "        " << guard << "for (int i = threadIdx.x; i < " << nout / 4 << "; i += " << T << ") st4_g("
+                 << ptr(n.id) << " + 4 * i, fill, fill, fill, fill); }\n";
+          else
+            body << "        " << guard << "for (int i = threadIdx.x; i < " << nout << "; i += " << T << ") stv(" << ptr(n.id)
+                 << ", i, fill); }\n";
+        }
+        body << "    }\n  }\n";
+        for (size_t i : grp) since_barrier.insert(i);
+        continue;
+      }
       // only the folding warps read the inbox: they alone wait on it (a
       // cluster-scope acquire per thread); the barrier below holds the rest
       body << "\n    if (threadIdx.x < " << 32 * std::min<size_t>(grp.size(), 32)
