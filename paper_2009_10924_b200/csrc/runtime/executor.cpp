@@ -146,6 +146,15 @@ void Executor::finish_init(const std::string& cubin) {
       const cublasComputeType_t ct = fp32 && *fp32 == '1' ? CUBLAS_COMPUTE_32F : CUBLAS_COMPUTE_32F_FAST_TF32;
       GemmState::Unit u;
       STC_LT(cublasLtMatmulDescCreate(&u.op, ct, CUDA_R_32F));
+      // a plain GEMM: no epilogue and no bias pointer, set explicitly (the
+      // fp32 SIMT kernels cuBLASLt picks carry a bias/relu epilogue variant;
+      // under compute-sanitizer memcheck they read the bias pointer)
+      {
+        const cublasLtEpilogue_t epi = CUBLASLT_EPILOGUE_DEFAULT;
+        const void* no_bias = nullptr;
+        STC_LT(cublasLtMatmulDescSetAttribute(u.op, CUBLASLT_MATMUL_DESC_EPILOGUE, &epi, sizeof(epi)));
+        STC_LT(cublasLtMatmulDescSetAttribute(u.op, CUBLASLT_MATMUL_DESC_BIAS_POINTER, &no_bias, sizeof(no_bias)));
+      }
       const uint64_t M = static_cast<uint64_t>(k.gemm_m), N = static_cast<uint64_t>(k.gemm_n),
                      K = static_cast<uint64_t>(k.gemm_k);
       STC_LT(cublasLtMatrixLayoutCreate(&u.b, CUDA_R_32F, N, K, static_cast<int64_t>(N)));

@@ -28,4 +28,7 @@ timeout 1500 compute-sanitizer --tool racecheck --print-limit 10 python -m pytes
   -k "resident_template_matches" > gpurun_out/racecheck_resident.log 2>&1
 timeout 1500 compute-sanitizer --tool synccheck --print-limit 10 python -m pytest tests/test_gpu_exec.py -q -x \
   -k "resident_template_matches" > gpurun_out/synccheck_resident.log 2>&1
+# model mode (cuBLASLt GEMMs in the graph), BERT layer, shard plans, host paths
+timeout 2000 compute-sanitizer --tool memcheck --print-limit 20 python -m pytest tests/test_gpu_exec.py -q -x \
+  -k "bert_layer or shard_plans or refined or model_mode or two_rank or chunked" > gpurun_out/memcheck_layer_shards.log 2>&1
 tail -n 2 gpurun_out/memcheck*.log gpurun_out/racecheck*.log gpurun_out/synccheck*.log
