@@ -141,6 +141,8 @@ void Executor::finish_init(const std::string& cubin) {
         gemm_ = std::make_unique<GemmState>();
         STC_LT(cublasLtCreate(&gemm_->lt));
         STC_RT(cudaMalloc(&gemm_->workspace, gemm_->ws_bytes));
+        // zeroed once (hygiene; 32 MB at executor creation)
+        STC_RT(cudaMemset(gemm_->workspace, 0, gemm_->ws_bytes));
       }
       const char* fp32 = std::getenv("STITCH_GEMM_FP32");
       const cublasComputeType_t ct = fp32 && *fp32 == '1' ? CUBLAS_COMPUTE_32F : CUBLAS_COMPUTE_32F_FAST_TF32;
