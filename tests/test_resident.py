@@ -55,3 +55,28 @@ def test_shared_memory_slots_never_alias_live_tensors(name, monkeypatch):
         # a unit binds each of its (distinct) tensors once: distinct slots
         offs = re.findall(r"rs_smem_ \+ (\d+)\)", args)
         assert len(set(offs)) == len(offs), args
+
+
+@pytest.mark.parametrize("name", ["dien_T10", "dien_T20"])
+def test_split_groups_fill_no_slot_a_filler_binds(name, monkeypatch):
+    """split placeholder groups (phase A push, fillers, phase B fold + fill):
+    the fillers run without a barrier before phase B's fills, so no fill may
+    land in a shared-memory slot any filler between the two phases binds,
+    and every filler is independent of its group (it reads none of the
+    group's outputs)"""
+    src, _ = _codegen(name, monkeypatch)
+    body = src[src.index("// ---- "):]
+    parts = re.split(r"\n  \{  // placeholder group", body)
+    splits = 0
+    for i, part in enumerate(parts[1:], 1):
+        if not part.startswith(" (wait):"):
+            continue
+        splits += 1
+        fills = set(re.findall(r"st4_g\(reinterpret_cast<float\*>\(rs_smem_ \+ (\d+)\)", part.split("\n  }\n")[0]))
+        assert fills, part[:200]
+        fillers = parts[i - 1].split("\n  }\n", 1)[1] if "\n  }\n" in parts[i - 1] else ""
+        bound = set()
+        for args in re.findall(r"\bru\d+_\((.*), v_, \d+\);", fillers):
+            bound |= set(re.findall(r"rs_smem_ \+ (\d+)\)", args))
+        assert not (fills & bound), (sorted(fills & bound), part[:120])
+    assert splits >= (9 if name == "dien_T10" else 19)
