@@ -132,7 +132,17 @@ std::string as_resident_function(const KernelSpec& k) {
   const size_t at = src.find(k.name + "(");
   if (src.compare(0, 10, "extern \"C\"") != 0 || at == std::string::npos)
     throw std::invalid_argument("resident: unexpected kernel header in " + k.name);
-  std::string body = "__device__ __forceinline__ void FN_(" + src.substr(at + k.name.size() + 1);
+  // every call inlined: the pointers are then known shared-memory slots
+  // (LDS/STS).  STITCH_RESIDENT_INLINE=0 keeps one copy of each unit
+  // function, so DIEN's per-step calls would reuse code already in the
+  // instruction cache (the inlined kernel's top ncu stall is
+  // no_instructions, 34% of samples).  Measured slower, because the calls
+  // then address generic pointers and lose constant propagation: T=10
+  // 20.1 -> 25.9 us, T=20 36.9 -> 49.6 us (profiles/r02/resident/resident_inline.jsonl)
+  const char* iv = std::getenv("STITCH_RESIDENT_INLINE");
+  const bool inl = !(iv && *iv == '0');
+  std::string body = std::string(inl ? "__device__ __forceinline__" : "__device__ __noinline__") + " void FN_(" +
+                     src.substr(at + k.name.size() + 1);
   int pi = 0;
   for (const auto* list : {&k.inputs, &k.outputs})
     for (const auto& t : *list)
