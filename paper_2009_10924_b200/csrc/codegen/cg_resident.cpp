@@ -31,6 +31,7 @@
 // The plan (patterns, per-op f32 rounding, the opaque semantics) is the one
 // the graph executor runs; only the kernel boundaries stay on chip.
 #include <algorithm>
+#include <cctype>
 #include <cstdio>
 #include <cstdlib>
 #include <map>
@@ -170,6 +171,106 @@ std::string as_resident_function(const KernelSpec& k) {
 struct Slot {
   int64_t off = 0, bytes = 0;
 };
+
+// Recurrent plans (DIEN) emit the same step block once per time step, equal
+// up to integer literals (slot offsets, inbox / mbarrier indices, trace
+// slots): ~700 SASS instructions per step, so the straight-line kernel is
+// ~8.8k instructions, each fetched cold once per launch (ncu: no_instructions
+// is the top stall, 34% of samples).  The longest run of >= 3 consecutive
+// blocks (split at placeholder-group markers) that agree outside their
+// integer literals becomes ONE loop body; the literals that differ between
+// iterations come from a __constant__ table.  A differing literal that
+// touches an identifier, a suffix or a float literal aborts the rewrite.
+std::string loop_recurrence(const std::string& body, const std::string& tab, std::string* tab_decl, int* iters) {
+  static const std::regex marker(R"(\n  \{  // placeholder group: )");
+  std::vector<size_t> at;
+  for (auto it = std::sregex_iterator(body.begin(), body.end(), marker); it != std::sregex_iterator(); ++it)
+    at.push_back(static_cast<size_t>(it->position()));
+  if (at.size() < 4) return body;
+  static const std::regex digits(R"(\d+)"), comment(R"(//[^\n]*)");
+  // blocks without their comments (unit / group labels name the step)
+  auto block = [&](size_t i) { return std::regex_replace(body.substr(at[i], at[i + 1] - at[i]), comment, ""); };
+  auto shape = [&](size_t i) { return std::regex_replace(block(i), digits, "#"); };
+  size_t best_lo = 0, best_n = 0;
+  for (size_t lo = 0; lo + 1 < at.size();) {
+    const std::string s0 = shape(lo);
+    size_t n = 1;
+    while (lo + n + 1 < at.size() && shape(lo + n) == s0) ++n;
+    if (n > best_n) best_n = n, best_lo = lo;
+    lo += n;
+  }
+  if (best_n < 3) return body;
+  struct Tok {
+    size_t pos, len;
+    std::string val;
+  };
+  std::vector<std::vector<Tok>> toks(best_n);
+  for (size_t b = 0; b < best_n; ++b) {
+    const std::string blk = block(best_lo + b);
+    for (auto it = std::sregex_iterator(blk.begin(), blk.end(), digits); it != std::sregex_iterator(); ++it)
+      toks[b].push_back({static_cast<size_t>(it->position()), static_cast<size_t>(it->length()), it->str()});
+  }
+  const std::string first = block(best_lo);
+  auto ident = [](char c) { return std::isalnum(static_cast<unsigned char>(c)) || c == '_' || c == '.'; };
+  std::vector<size_t> var;
+  std::set<size_t> fn_var;  // the N of a unit call "ruN_(" differs (e.g. DIEN's per-step column slices)
+  for (size_t k = 0; k < toks[0].size(); ++k) {
+    bool differs = false;
+    for (size_t b = 1; b < best_n; ++b) differs = differs || toks[b][k].val != toks[0][k].val;
+    if (!differs) continue;
+    const Tok& t = toks[0][k];
+    const bool unit_fn = t.pos >= 2 && first.compare(t.pos - 2, 2, "ru") == 0 && (t.pos < 3 || !ident(first[t.pos - 3])) &&
+                         first.compare(t.pos + t.len, 2, "_(") == 0;
+    if (unit_fn) {
+      fn_var.insert(var.size());
+    } else if ((t.pos > 0 && ident(first[t.pos - 1])) ||
+               (t.pos + t.len < first.size() && ident(first[t.pos + t.len]))) {
+      return body;  // part of a name, a suffix or a float literal: not a plain integer
+    }
+    const size_t line = first.rfind('\n', t.pos);
+    if (first.find("#pragma", line == std::string::npos ? 0 : line) < t.pos) return body;
+    var.push_back(k);
+  }
+  const std::string V = std::to_string(var.size());
+  auto entry = [&](size_t v) { return tab + "[it_ * " + V + " + " + std::to_string(v) + "]"; };
+  std::string tmpl;
+  size_t cur = 0;
+  for (size_t v = 0; v < var.size(); ++v) {
+    const Tok& t = toks[0][var[v]];
+    tmpl += first.substr(cur, t.pos - cur) + (fn_var.count(v) ? "@F" + std::to_string(v) + "@" : entry(v));
+    cur = t.pos + t.len;
+  }
+  tmpl += first.substr(cur);
+  // a unit call whose function differs per step: dispatch on the table entry
+  // (one case per distinct function; the arguments are the loop template's)
+  for (size_t v : fn_var) {
+    const std::string mark = "@F" + std::to_string(v) + "@";
+    const size_t m = tmpl.find(mark);
+    const size_t ls = tmpl.rfind('\n', m) + 1, le = tmpl.find('\n', m);
+    const std::string line = tmpl.substr(ls, le - ls);
+    std::set<std::string> names;
+    for (size_t b = 0; b < best_n; ++b) names.insert(toks[b][var[v]].val);
+    std::string sw = "  switch (" + entry(v) + ") {";
+    for (const auto& nm : names) {
+      std::string l = line;
+      l.replace(l.find(mark), mark.size(), nm);
+      sw += "\n  case " + nm + ": " + l.substr(l.find_first_not_of(' ')) + " break;";
+    }
+    sw += "\n  default: __trap();\n  }";
+    tmpl.replace(ls, le - ls, sw);
+  }
+  if (tmpl.find("@F") != std::string::npos) return body;
+  std::ostringstream d;
+  d << "__constant__ int " << tab << "[" << std::max<size_t>(1, best_n * var.size()) << "] = {";
+  for (size_t b = 0; b < best_n; ++b)
+    for (size_t k : var) d << toks[b][k].val << ",";
+  d << "};\n";
+  *tab_decl = d.str();
+  *iters = static_cast<int>(best_n);
+  return body.substr(0, at[best_lo]) + "\n  // " + std::to_string(best_n) +
+         " recurrent steps as one loop (literals per step in " + tab + ")\n  #pragma unroll 1\n  for (int it_ = 0; it_ < " +
+         std::to_string(best_n) + "; ++it_) {" + tmpl + "\n  }" + body.substr(at[best_lo + best_n]);
+}
 
 }  // namespace
 
@@ -749,8 +850,19 @@ std::optional<KernelSpec> generate_resident_kernel(const CompGraph& g, const std
   k.block = 1024;
   k.cluster = C;
   k.smem = std::max<int64_t>(smem_top, 16);
+  // STITCH_RESIDENT_LOOP=1 rolls the recurrent steps into one loop.  Off by
+  // default: it removes most instruction-fetch stalls of a cold launch (ncu:
+  // no_instructions 67 -> 17 samples, 28.7 -> 26.3 us) but back-to-back
+  // launches find the straight-line code warm in L2, and the loop's table
+  // loads and switch add 15% instructions: T=10 20.1 -> 22.7 us, T=20
+  // 36.8 -> 42.8 us (profiles/r02/resident/resident_loop.jsonl)
+  std::string body_src = body.str(), tab_decl;
+  int loop_iters = 0;
+  if (const char* lv = std::getenv("STITCH_RESIDENT_LOOP"); lv && *lv == '1')
+    body_src = loop_recurrence(body_src, "rs_tab_" + name, &tab_decl, &loop_iters);
+  if (loop_iters) k.tmpl += ", loop " + std::to_string(loop_iters);
   std::ostringstream s;
-  s << fns.str();
+  s << fns.str() << tab_decl;
   s << "extern \"C\" __global__ void __launch_bounds__(1024, 1) " << name << "(";
   bool first = true;
   for (int t : params_used) {
@@ -792,7 +904,7 @@ std::optional<KernelSpec> generate_resident_kernel(const CompGraph& g, const std
     s << "  if (threadIdx.x < " << n_push << ") mbar_init(&rs_gbar_[threadIdx.x], 1);\n"
       << "  if (threadIdx.x == 0) mbar_fence_init();\n  cluster_sync_all();  // also orders rs_mbar_'s init before any wait\n";
   }
-  s << body.str()
+  s << body_src
     << "  cluster_sync_all();  // peers may still read rs_part_ through DSMEM\n}\n";
   k.source = s.str();
   for (const auto& u : us) k.alg_bytes += u.opaque ? 0 : u.spec.alg_bytes;

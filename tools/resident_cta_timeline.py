@@ -15,7 +15,15 @@ C = int(os.environ["STITCH_TRACE_CTAS"])
 name = sys.argv[1]
 g = stitch.Graph.from_file(os.path.join(stitch.GRAPHS, name + ".graph"))
 plan = stitch.Plan(g, "b200")
+# step labels from the straight-line source (the recurrent-step loop drops
+# them; its steps keep their trace slot numbers)
+_loop = os.environ.get("STITCH_RESIDENT_LOOP")
+os.environ["STITCH_RESIDENT_LOOP"] = "0"
 src, _ = plan.codegen()
+if _loop is None:
+    os.environ.pop("STITCH_RESIDENT_LOOP")
+else:
+    os.environ["STITCH_RESIDENT_LOOP"] = _loop
 labels = [l.strip() for l in src.splitlines() if l.startswith("  // unit ") or l.startswith("  {  // placeholder group")]
 ex = stitch.Executor(plan)
 ex.upload(stitch.random_inputs(g, 1))
