@@ -727,3 +727,24 @@ def test_shard_plans_reassemble_full_graph_on_gpu(name, n):
         assert got[k].shape == want[k].shape, k
         rep = stitch.compare({k: got[k]}, {k: want[k]}, tol, _abs_floor(og, k))
         assert rep["pass"], "%s@%d %s: %s" % (name, n, k, rep["message"])
+
+
+@pytest.mark.parametrize("name", ["dien_T10", "dien_T20"])
+def test_resident_recurrence_loop_matches_straight_line(name, monkeypatch):
+    """opt-in STITCH_RESIDENT_LOOP=1: the recurrent steps rolled into one loop
+    (per-step literals from a __constant__ table, per-step unit functions
+    dispatched by a switch) compute the same bits as the straight-line
+    resident kernel"""
+    stitch = _stitch()
+    g = stitch.Graph(config_graph(name))
+    plan = stitch.Plan(g, "b200")
+    monkeypatch.setenv("STITCH_RESIDENT", "1")
+    straight = stitch.Executor(plan)
+    monkeypatch.setenv("STITCH_RESIDENT_LOOP", "1")
+    looped = stitch.Executor(plan)
+    assert ", loop " in looped.describe()[0]["template"], looped.describe()[0]["template"]
+    for seed in (1, 2):
+        inputs = stitch.random_inputs(g, seed)
+        a, b = straight.run(inputs), looped.run(inputs)
+        for k in a:
+            assert np.array_equal(a[k], b[k]), (name, seed, k)
