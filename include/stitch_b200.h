@@ -142,7 +142,11 @@ int stc_exec_run_host_zero_copy(stc_exec* e, const void* const* inputs, void* co
  * first CTA entry / last CTA exit of kernel i (%globaltimer), us since the
  * earliest entry; -1 for library (GEMM) units.  Arrays of num_kernels
  * entries -- for a plan run by the persistent template ("persistent(U)", one
- * kernel) 1 + U: entry 1+u = unit u ready (producers counted) / done. */
+ * kernel) 1 + U: entry 1+u = unit u ready (producers counted) / done; for the
+ * resident template ("resident(U units, S steps, cluster C)", one kernel)
+ * 1 + S: entry 1+s = step s (first CTA entering / last CTA leaving).  With
+ * STITCH_TRACE_CTAS=c as well, every entry k is recorded per CTA b < c at
+ * index k*c + b (arrays c times longer). */
 int stc_exec_trace(stc_exec* e, double* start_us, double* end_us);
 /* Pipelined host execution over chunks of DIFFERENT sizes: chunk k runs on
  * execs[exec_of_chunk[k]] (each exec built from a shard graph of the same
