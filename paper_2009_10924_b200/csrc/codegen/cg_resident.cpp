@@ -274,8 +274,29 @@ std::string loop_recurrence(const std::string& body, const std::string& tab, std
 
 }  // namespace
 
+namespace {
+thread_local bool tl_no_handoff = false;  // retry without barrier elision
+}
+
+std::optional<KernelSpec> generate_resident_kernel_once(const CompGraph& g, const std::vector<ResidentUnit>& units,
+                                                        const std::string& name, std::string* why, bool* smem_bound);
+
+// Eliding barriers delays when freed slots return to the allocator (they are
+// reused only after a barrier), so a plan near the shared-memory cap may only
+// fit with every barrier kept: retry that way before giving up
 std::optional<KernelSpec> generate_resident_kernel(const CompGraph& g, const std::vector<ResidentUnit>& units,
                                                    const std::string& name, std::string* why) {
+  bool smem_bound = false;
+  auto k = generate_resident_kernel_once(g, units, name, why, &smem_bound);
+  if (k || !smem_bound) return k;
+  tl_no_handoff = true;
+  k = generate_resident_kernel_once(g, units, name, why, &smem_bound);
+  tl_no_handoff = false;
+  return k;
+}
+
+std::optional<KernelSpec> generate_resident_kernel_once(const CompGraph& g, const std::vector<ResidentUnit>& units,
+                                                        const std::string& name, std::string* why, bool* smem_bound) {
   auto no = [&](const std::string& m) -> std::optional<KernelSpec> {
     if (why) *why = m;
     return std::nullopt;
@@ -560,6 +581,44 @@ std::optional<KernelSpec> generate_resident_kernel(const CompGraph& g, const std
   int n_push = 0;
   std::map<size_t, std::pair<int, int>> split_of;  // group's first unit -> (mbarrier, inbox slot base)
   bool staged_ready = staged.empty();
+  // A local unit consuming another local unit's output needs no barrier
+  // when every element reaches it through the thread that wrote it: both
+  // are single local bodies over the same domain and vector width, with the
+  // same virtual grid (same element-to-thread map: c = v * 1024 + tid,
+  // grid-stride), and in the consumer the handed-over tensors (shape = the
+  // domain) feed only elementwise ops of that shape (identity coordinates).
+  // DIEN: each step's reset-gate unit -> update unit.
+  // STITCH_RESIDENT_HANDOFF=0 keeps every barrier.
+  const char* hv = std::getenv("STITCH_RESIDENT_HANDOFF");
+  const bool handoff = !(hv && *hv == '0') && !tl_no_handoff;
+  static const std::regex local_sig(R"(// local body: domain (\d+) elements, vector (\d+))");
+  auto local_domain = [&](size_t i) -> std::string {
+    if (us[i].opaque || us[i].spec.tmpl != "local") return "";
+    const std::string& src = us[i].spec.source;
+    auto it = std::sregex_iterator(src.begin(), src.end(), local_sig);
+    if (it == std::sregex_iterator()) return "";
+    const std::string sig = it->str(1) + "x" + it->str(2) + "g" + std::to_string(us[i].spec.grid);
+    return ++it == std::sregex_iterator() ? sig : "";  // exactly one local body
+  };
+  auto same_thread_handoff = [&](size_t i, size_t d) {
+    if (!handoff) return false;
+    const std::string di = local_domain(i), dd = local_domain(d);
+    if (di.empty() || di != dd) return false;
+    const int64_t n = std::stoll(di.substr(0, di.find('x')));
+    bool any = false;
+    for (int t : us[d].outs) {
+      if (std::find(us[i].ins.begin(), us[i].ins.end(), t) == us[i].ins.end()) continue;
+      any = true;
+      const TensorShape& ts = gs.node(t).shape;
+      if (ts.element_count() != n) return false;
+      for (int v : us[i].verts) {
+        const OpNode& c = gs.node(v);
+        if (std::find(c.operands.begin(), c.operands.end(), t) == c.operands.end()) continue;
+        if (!is_elementwise(c.kind) || c.shape.dims != ts.dims) return false;
+      }
+    }
+    return any;
+  };
   for (size_t s = 0; s < steps.size(); ++s) {
     if (phase[s] == kGroupB) {
       // the peers' partials: wait, fold in rank order, fill (the barrier
@@ -646,7 +705,7 @@ std::optional<KernelSpec> generate_resident_kernel(const CompGraph& g, const std
     }
     bool need = false;
     for (size_t i : steps[s])
-      for (size_t d : us[i].deps) need = need || since_barrier.count(d);
+      for (size_t d : us[i].deps) need = need || (since_barrier.count(d) && !same_thread_handoff(i, d));
     if (need) barrier();
     // diagnostics (STITCH_TRACE builds): slot 1+s = [first CTA entering step
     // s, last CTA leaving it]
@@ -839,8 +898,10 @@ std::optional<KernelSpec> generate_resident_kernel(const CompGraph& g, const std
     retire_inputs(s);
   }
   body << "  STC_TRACE_STAMP_END(" << steps.size() << ");\n";
-  if (smem_top > kSmemCap)
+  if (smem_top > kSmemCap) {
+    *smem_bound = true;
     return no("boundary tensors need " + std::to_string(smem_top) + " B of shared memory per CTA");
+  }
 
   KernelSpec k;
   k.name = name;
