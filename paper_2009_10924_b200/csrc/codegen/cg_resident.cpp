@@ -592,8 +592,15 @@ std::optional<KernelSpec> generate_resident_kernel_once(const CompGraph& g, cons
   const char* hv = std::getenv("STITCH_RESIDENT_HANDOFF");
   const bool handoff = !(hv && *hv == '0') && !tl_no_handoff;
   static const std::regex local_sig(R"(// local body: domain (\d+) elements, vector (\d+))");
+  // placeholder members filled "one element per thread" (direct fold below)
+  // hand over like a local unit with vector 1 and grid 1
+  std::map<size_t, std::string> fill_sig;
   auto local_domain = [&](size_t i) -> std::string {
-    if (us[i].opaque || us[i].spec.tmpl != "local") return "";
+    if (us[i].opaque) {
+      auto it = fill_sig.find(i);
+      return it == fill_sig.end() ? "" : it->second;
+    }
+    if (us[i].spec.tmpl != "local") return "";
     const std::string& src = us[i].spec.source;
     auto it = std::sregex_iterator(src.begin(), src.end(), local_sig);
     if (it == std::sregex_iterator()) return "";
@@ -644,6 +651,22 @@ std::optional<KernelSpec> generate_resident_kernel_once(const CompGraph& g, cons
           const int64_t nout = local_elems(n.id);
           most = std::max<int64_t>(most, n.shape.dtype == DType::F32 && nout % 4 == 0 ? nout / 4 : nout);
         }
+        // STITCH_RESIDENT_SCALAR_FILL=1 (every member a sharded [<= 1024
+        // elements] f32 tensor inside the kernel): thread t folds and writes
+        // element t of each -- the map a vector-1 local unit reads with, so
+        // that consumer needs no barrier.  Measured slower (576 threads each
+        // folding the peers' partials: T=10 19.4 -> 21.8 us,
+        // profiles/r02/resident/resident_scalar_fill.jsonl)
+        const char* sfv = std::getenv("STITCH_RESIDENT_SCALAR_FILL");
+        bool scalar_map = handoff && sfv && *sfv == '1';
+        int64_t most_el = 1;
+        for (size_t i : grp) {
+          const OpNode& n = g.node(us[i].verts[0]);
+          most_el = std::max<int64_t>(most_el, local_elems(n.id));
+          scalar_map = scalar_map && sharded[static_cast<size_t>(n.id)] && !graph_out.count(n.id) &&
+                       n.shape.dtype == DType::F32 && local_elems(n.id) <= 1024;
+        }
+        if (scalar_map) most = most_el;
         const int T = static_cast<int>(std::min<int64_t>(1024, (most + 31) / 32 * 32));
         body << "\n    if (threadIdx.x < " << T << ") {\n      mbar_wait_cluster(&rs_gbar_[" << bar << "], 0u);\n";
         for (size_t j = 0; j < grp.size(); ++j) body << "      double t" << j << "_ = 0.0;\n";
@@ -660,7 +683,10 @@ std::optional<KernelSpec> generate_resident_kernel_once(const CompGraph& g, cons
           const std::string guard = rep_out ? "if (rk_ == 0) " : "";
           body << "      { const float fill = (float)(" << (count ? "t" + std::to_string(j) + "_ * " + inv_count(count) : "0.0")
                << ");\n";
-          if (n.shape.dtype == DType::F32 && nout % 4 == 0)
+          if (scalar_map) {
+            body << "        if (threadIdx.x < " << nout << ") " << ptr(n.id) << "[threadIdx.x] = fill; }\n";
+            fill_sig[grp[j]] = std::to_string(nout) + "x1g1";
+          } else if (n.shape.dtype == DType::F32 && nout % 4 == 0)
             body << "        " << guard << "for (int i = threadIdx.x; i < " << nout / 4 << "; i += " << T << ") st4_g("
                  << ptr(n.id) << " + 4 * i, fill, fill, fill, fill); }\n";
           else
