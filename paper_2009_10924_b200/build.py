@@ -43,6 +43,18 @@ def _nlohmann_dir():
     raise RuntimeError("nlohmann/json.hpp (3.11.3) not found")
 
 
+def _cutlass_dirs():
+    """CUTLASS / CuTe headers vendored in the image (flashinfer's tree); empty
+    when absent -- gemm_sm100.cu then compiles to an 'unavailable' stub"""
+    for base in glob.glob("/opt/prime-rl/.venv/lib/python3*/site-packages/flashinfer/data/cutlass") + \
+            glob.glob(os.path.join(sys.prefix, "lib", "python3*", "site-packages", "flashinfer", "data", "cutlass")):
+        inc = os.path.join(base, "include")
+        if os.path.exists(os.path.join(inc, "cutlass", "cutlass.h")):
+            util = os.path.join(base, "tools", "util", "include")
+            return [inc] + ([util] if os.path.isdir(util) else [])
+    return []
+
+
 CXXFLAGS = ["-std=c++20", "-O2", "-g1", "-fPIC", "-Wall", "-Wno-sign-compare",
             "-I" + os.path.join(ROOT, "include"), "-I" + CSRC, "-I" + os.path.join(CUDA, "include")]
 NVCCFLAGS = ["-std=c++17", "-O3", ARCH, "-lineinfo", "-Xcompiler", "-fPIC",
@@ -91,11 +103,16 @@ def build(verbose=False, jobs=None):
         objs.append(o)
         if _stale(s, o, hdrs):
             jobs_list.append(["g++"] + CXXFLAGS + ["-I" + nl, "-c", s, "-o", o])
+    cutlass = _cutlass_dirs()
     for s in cu:
         o = os.path.join(OBJ_DIR, "cu_" + os.path.basename(s)[:-3] + ".o")
         objs.append(o)
-        if _stale(s, o, hdrs):
-            jobs_list.append([NVCC] + NVCCFLAGS + ["-c", s, "-o", o])
+        # the CUTLASS GEMM (model mode) takes ~2 min to compile and includes
+        # none of our headers: rebuilt only when its own source changes
+        gemm = os.path.basename(s).startswith("gemm_")
+        if _stale(s, o, [] if gemm else hdrs):
+            extra = ["--expt-relaxed-constexpr"] + ["-I" + d for d in cutlass] if gemm else []
+            jobs_list.append([NVCC] + NVCCFLAGS + extra + ["-c", s, "-o", o])
     with cf.ThreadPoolExecutor(max_workers=jobs or os.cpu_count() or 4) as ex:
         for r in ex.map(_run, jobs_list):
             if verbose and (r.stdout or r.stderr):

@@ -53,6 +53,11 @@ struct KernelSpec {
   // matmul C[M,N] = A[M,K] . B[K,N] runs as cuBLASLt; no generated source)
   bool is_gemm = false;
   int64_t gemm_m = 0, gemm_n = 0, gemm_k = 0;
+  // "bias_gelu": the plan's bias + GELU(tanh) pattern on the GEMM output is
+  // fused into the GEMM epilogue (model mode, CUTLASS tcgen05 kernel,
+  // csrc/kernels/gemm_sm100.cu); inputs = {A, B, bias}, outputs = the
+  // pattern's output
+  std::string gemm_epilogue;
 };
 
 // Thrown when a dataflow template cannot express a component; the caller

@@ -1,0 +1,94 @@
+// Model mode (non-parity): a matmul-shaped opaque_compute
+// followed by the plan's bias + GELU(tanh) pattern runs as ONE sm_100a kernel:
+// a CUTLASS 4.x TF32 tcgen05 GEMM (2-SM 256x256x32 tiles, TMA operand
+// loads, TMEM accumulators) whose epilogue adds the per-column bias and
+// applies GELU(tanh) --
+// the [M,N] GEMM output never reaches HBM.  Instantiated here from the CUTLASS
+// headers vendored in the image (flashinfer/data/cutlass); without them the
+// entry point reports "unavailable" and the executor keeps cuBLASLt + the
+// stitched kernel.
+#include <cstddef>
+#include <cuda_runtime.h>
+
+#if __has_include("cutlass/cutlass.h")
+#include "cutlass/cutlass.h"
+#include "cute/tensor.hpp"
+#include "cutlass/epilogue/collective/collective_builder.hpp"
+#include "cutlass/epilogue/thread/activation.h"
+#include "cutlass/gemm/collective/collective_builder.hpp"
+#include "cutlass/gemm/device/gemm_universal_adapter.h"
+#include "cutlass/gemm/kernel/gemm_universal.hpp"
+#include "cutlass/util/packed_stride.hpp"
+#define STC_HAVE_CUTLASS 1
+#endif
+
+namespace stitch::gpu {
+
+#ifdef STC_HAVE_CUTLASS
+namespace {
+using namespace cute;
+
+// GELU(tanh) epilogue: CUTLASS's GELU_taylor, 0.5 z (1 + tanh(z (k0 + k1 z^2)))
+// with tanh.approx.f32 (MUFU.TANH, rel err ~5e-4).  An accurate tanhf (the
+// graph's own op order) in the epilogue made the kernel 56.5 vs 38.3 us cold
+// for [4096x768]x[768x3072] (profiles/r02/gemm/fused_gemm_variants.txt): the
+// epilogue warps are few and the accurate tanh sequence long.  TF32 operand
+// rounding (~1e-3 relative) dominates the error either way.
+using Row = cutlass::layout::RowMajor;
+using MmaTile = Shape<_256, _256, _32>;
+using Cluster = Shape<_2, _1, _1>;
+using Fusion = cutlass::epilogue::fusion::LinCombPerColBiasEltAct<cutlass::epilogue::thread::GELU_taylor, float, float, float>;
+using Epilogue = typename cutlass::epilogue::collective::CollectiveBuilder<
+    cutlass::arch::Sm100, cutlass::arch::OpClassTensorOp, MmaTile, Cluster, cutlass::epilogue::collective::EpilogueTileAuto,
+    float, float, float, Row, 4, float, Row, 4, cutlass::epilogue::collective::EpilogueScheduleAuto, Fusion>::CollectiveOp;
+using Mainloop = typename cutlass::gemm::collective::CollectiveBuilder<
+    cutlass::arch::Sm100, cutlass::arch::OpClassTensorOp, float, Row, 4, float, Row, 4, float, MmaTile, Cluster,
+    cutlass::gemm::collective::StageCountAutoCarveout<static_cast<int>(sizeof(typename Epilogue::SharedStorage))>,
+    cutlass::gemm::collective::KernelScheduleAuto>::CollectiveOp;
+using Kernel = cutlass::gemm::kernel::GemmUniversal<Shape<int, int, int, int>, Mainloop, Epilogue>;
+using Gemm = cutlass::gemm::device::GemmUniversalAdapter<Kernel>;
+
+typename Gemm::Arguments make_args(const float* A, const float* B, const float* bias, float* D, int M, int N, int K) {
+  auto sA = cutlass::make_cute_packed_stride(typename Kernel::StrideA{}, cute::make_shape(M, K, 1));
+  auto sB = cutlass::make_cute_packed_stride(typename Kernel::StrideB{}, cute::make_shape(N, K, 1));
+  auto sC = cutlass::make_cute_packed_stride(typename Kernel::StrideC{}, cute::make_shape(M, N, 1));
+  auto sD = cutlass::make_cute_packed_stride(typename Kernel::StrideD{}, cute::make_shape(M, N, 1));
+  typename Gemm::Arguments args{cutlass::gemm::GemmUniversalMode::kGemm, {M, N, K, 1}, {A, sA, B, sB},
+                                {{}, nullptr, sC, D, sD}};
+  args.epilogue.thread.alpha = 1.f;
+  args.epilogue.thread.beta = 0.f;
+  args.epilogue.thread.bias_ptr = bias;
+  return args;
+}
+}  // namespace
+#endif
+
+// D[M,N] = GELU(A[M,K] . B[K,N] + bias[N]), all row-major f32, TF32 tensor
+// cores.  0 = launched on `stream`; 1 = unavailable (no CUTLASS / shape not
+// implementable); 2 = launch error.
+int gemm_bias_gelu_tf32(const float* A, const float* B, const float* bias, float* D, int M, int N, int K, void* workspace,
+                        size_t workspace_bytes, cudaStream_t stream) {
+#ifdef STC_HAVE_CUTLASS
+  auto args = make_args(A, B, bias, D, M, N, K);
+  Gemm gemm;
+  if (Gemm::get_workspace_size(args) > workspace_bytes || gemm.can_implement(args) != cutlass::Status::kSuccess) return 1;
+  if (gemm.initialize(args, workspace, stream) != cutlass::Status::kSuccess) return 2;
+  return gemm.run(stream) == cutlass::Status::kSuccess ? 0 : 2;
+#else
+  (void)A, (void)B, (void)bias, (void)D, (void)M, (void)N, (void)K, (void)workspace, (void)workspace_bytes, (void)stream;
+  return 1;
+#endif
+}
+
+// whether the fused path can run this shape (host-side check, no launch)
+bool gemm_bias_gelu_supported(int M, int N, int K, size_t workspace_bytes) {
+#ifdef STC_HAVE_CUTLASS
+  auto args = make_args(nullptr, nullptr, nullptr, nullptr, M, N, K);
+  return Gemm::get_workspace_size(args) <= workspace_bytes && Gemm::can_implement(args) == cutlass::Status::kSuccess;
+#else
+  (void)M, (void)N, (void)K, (void)workspace_bytes;
+  return false;
+#endif
+}
+
+}  // namespace stitch::gpu

@@ -35,6 +35,76 @@ std::string json_escape(const std::string& s) {
 
 }  // namespace
 
+// csrc/kernels/gemm_sm100.cu (CUTLASS tcgen05 GEMM + bias + GELU epilogue)
+int gemm_bias_gelu_tf32(const float* A, const float* B, const float* bias, float* D, int M, int N, int K, void* workspace,
+                        size_t workspace_bytes, cudaStream_t stream);
+bool gemm_bias_gelu_supported(int M, int N, int K, size_t workspace_bytes);
+
+namespace {
+// the plan's bias + GELU(tanh) pattern over one GEMM output (graphs/
+// bert_layer.graph): gl = (a*0.5) * (tanh((a + (a*a*a)*0.044715) * 0.79788456) + 1),
+// a = G + broadcast(bias[N]) dims=[1].  Commuted operands accepted.
+// -> the pattern's output vertex, the GEMM output G and the bias parameter.
+bool match_bias_gelu(const CompGraph& g, const std::vector<int>& verts, int* G_out, int* bias_out, int* out_v) {
+  const std::set<int> in(verts.begin(), verts.end());
+  auto node = [&](int v) -> const OpNode& { return g.node(v); };
+  auto cbcast = [&](int v, double val) {
+    const OpNode& n = node(v);
+    if (n.kind != OpKind::Broadcast || n.operands.size() != 1) return false;
+    const OpNode& c = node(n.operands[0]);
+    return c.kind == OpKind::Constant && std::fabs(c.attrs.value - val) <= 1e-6 * std::fabs(val);
+  };
+  // binary op of kind k with operands {x, y} in either order; calls pick(x, y)
+  auto bin = [&](int v, OpKind k, auto&& pick) {
+    const OpNode& n = node(v);
+    if (n.kind != k || n.operands.size() != 2) return false;
+    return pick(n.operands[0], n.operands[1]) || pick(n.operands[1], n.operands[0]);
+  };
+  // the pattern's single output: the vertex no other member reads
+  int out = -1;
+  for (int v : verts) {
+    bool read = false;
+    for (int w : verts)
+      for (int o : node(w).operands) read = read || o == v;
+    if (!read) {
+      if (out >= 0) return false;
+      out = v;
+    }
+  }
+  if (out < 0) return false;
+  int a = -1;
+  auto is_a = [&](int v) {
+    return bin(v, OpKind::Add, [&](int x, int y) {
+      const OpNode& b = node(y);
+      if (b.kind != OpKind::Broadcast || b.attrs.dims != std::vector<int>{1}) return false;
+      const OpNode& bias = node(b.operands[0]);
+      if (bias.kind != OpKind::Parameter || bias.shape.rank() != 1 || in.count(x)) return false;
+      if (a >= 0 && a != v) return false;
+      a = v, *G_out = x, *bias_out = bias.id;
+      return true;
+    });
+  };
+  const bool ok = bin(out, OpKind::Mul, [&](int ah, int th1) {
+    return bin(ah, OpKind::Mul, [&](int x, int c) { return is_a(x) && cbcast(c, 0.5); }) &&
+           bin(th1, OpKind::Add, [&](int th, int c) {
+             if (!cbcast(c, 1.0) || node(th).kind != OpKind::Tanh) return false;
+             return bin(node(th).operands[0], OpKind::Mul, [&](int inner, int c2) {
+               return cbcast(c2, 0.7978845608028654) && bin(inner, OpKind::Add, [&](int x, int a3s) {
+                        return x == a && bin(a3s, OpKind::Mul, [&](int a3, int c3) {
+                                 return cbcast(c3, 0.044715) && bin(a3, OpKind::Mul, [&](int a2, int y) {
+                                          return y == a && bin(a2, OpKind::Mul, [&](int p, int q) { return p == a && q == a; });
+                                        });
+                               });
+                      });
+             });
+           });
+  });
+  // every member is one of the recognised ops (nothing else computed here)
+  *out_v = out;
+  return ok && a >= 0 && in.count(a) && verts.size() <= 16;
+}
+}  // namespace
+
 // cuBLASLt state for the plan's GEMM units (model mode)
 struct Executor::GemmState {
   cublasLtHandle_t lt = nullptr;
@@ -442,6 +512,44 @@ PlanKernels generate_plan_kernels(const CompGraph& g_, const FusionPlan& plan,
   };
   std::map<std::string, KernelPlan> singles;
   int idx = 0;
+  // model mode: a GEMM whose output feeds only the plan's bias + GELU(tanh)
+  // pattern writes that pattern's output from its epilogue (one CUTLASS
+  // tcgen05 kernel instead of cuBLASLt + a stitched kernel; the [M,N] GEMM
+  // output never reaches HBM).  STITCH_GEMM_FUSE=0 keeps them separate; full
+  // f32 GEMMs (STITCH_GEMM_FP32=1) are never fused (the fused kernel is TF32)
+  const char* fz = std::getenv("STITCH_GEMM_FUSE");
+  const char* f32 = std::getenv("STITCH_GEMM_FP32");
+  const bool fuse_gemm_epilogue_ = !(fz && *fz == '0') && !(f32 && *f32 == '1');
+  size_t fused_units_ = 0;
+  auto fuse_into_gemm = [&](int G, int bias, int outv, const std::vector<int>& verts) {
+    if (g_.is_output(G)) return false;
+    const std::set<int> in(verts.begin(), verts.end());
+    for (int c : cons[static_cast<size_t>(G)])
+      if (!in.count(c)) return false;  // G read outside the pattern: it must exist
+    for (int v : verts)
+      if (v != outv) {
+        if (g_.is_output(v)) return false;
+        for (int c : cons[static_cast<size_t>(v)])
+          if (!in.count(c)) return false;  // an intermediate leaves the pattern
+      }
+    for (auto& k : specs_) {
+      if (!k.is_gemm || k.outputs.size() != 1 || k.outputs[0] != g_.node(G).name || !k.gemm_epilogue.empty()) continue;
+      const OpNode& b = g_.node(bias);
+      if (b.shape.dims[0] != k.gemm_n || b.shape.dtype != DType::F32 || g_.node(outv).shape.dtype != DType::F32) return false;
+      if (!gemm_bias_gelu_supported(static_cast<int>(k.gemm_m), static_cast<int>(k.gemm_n), static_cast<int>(k.gemm_k),
+                                    size_t(32) << 20))
+        return false;
+      k.gemm_epilogue = "bias_gelu";
+      k.tmpl = "gemm(cutlass tcgen05 tf32)+bias+gelu";
+      k.pattern_key += "+" + std::to_string(outv);
+      k.inputs.push_back(b.name);
+      k.outputs = {g_.node(outv).name};
+      k.alg_bytes = g_.node(g_.node(G).operands[0]).shape.byte_size() + g_.node(g_.node(G).operands[1]).shape.byte_size() +
+                    b.shape.byte_size() + g_.node(outv).shape.byte_size();
+      return true;
+    }
+    return false;
+  };
   auto add_pattern = [&](const std::vector<int>& verts, const std::string& key) {
     const std::string name = "k" + std::to_string(idx++) + "_" + sanitize(g_.node(verts.front()).name);
     KernelSpec spec;
@@ -544,6 +652,10 @@ PlanKernels generate_plan_kernels(const CompGraph& g_, const FusionPlan& plan,
                                                                    sanitize(g_.node(un.verts[0]).name),
                                               sm_count));
       opaque_vertex[specs_.size() - 1] = un.verts[0];
+    } else if (int G = -1, bias = -1, outv = -1; gemm_opaque && fuse_gemm_epilogue_ &&
+               match_bias_gelu(g_, un.verts, &G, &bias, &outv) && fuse_into_gemm(G, bias, outv, un.verts)) {
+      // the GEMM that produced G now writes this pattern's output itself
+      ++fused_units_;
     } else {
       add_pattern(un.verts, un.key);
       if (specs_.back().tmpl == "local" || specs_.back().tmpl == "regional") local_verts[specs_.size() - 1] = un.verts;
@@ -552,7 +664,7 @@ PlanKernels generate_plan_kernels(const CompGraph& g_, const FusionPlan& plan,
     for (int w : users[static_cast<size_t>(u)])
       if (--pending[static_cast<size_t>(w)] == 0) ready.insert({units[static_cast<size_t>(w)].fire, w});
   }
-  if (specs_.size() != units.size()) throw std::runtime_error("[exec] contracted plan graph has a cycle");
+  if (specs_.size() + fused_units_ != units.size()) throw std::runtime_error("[exec] contracted plan graph has a cycle");
   // Resident template (cg_resident.cpp): a row-shardable launch-bound plan
   // runs as one thread-block cluster, plan-kernel boundaries kept in shared
   // memory.  Default: tried for plans of >= 16 launch units (DIEN: 88 / 178;
@@ -786,6 +898,15 @@ void Executor::launch_kernel(size_t i, int set, cudaStream_t s, int after, const
       if (auto it = bind->find(t); it != bind->end()) return it->second;
     return tensors_.at(t).dptr[static_cast<size_t>(set)];
   };
+  if (k.is_gemm && k.gemm_epilogue == "bias_gelu") {
+    if (const int rc = gemm_bias_gelu_tf32(static_cast<const float*>(ptr_of(k.inputs[0])),
+                                           static_cast<const float*>(ptr_of(k.inputs[1])),
+                                           static_cast<const float*>(ptr_of(k.inputs[2])), static_cast<float*>(ptr_of(k.outputs[0])),
+                                           static_cast<int>(k.gemm_m), static_cast<int>(k.gemm_n), static_cast<int>(k.gemm_k),
+                                           gemm_->workspace, gemm_->ws_bytes, s))
+      throw std::runtime_error("[cutlass] fused GEMM " + k.name + " failed (" + std::to_string(rc) + ")");
+    return;
+  }
   if (k.is_gemm) {
     launch_gemm(i, ptr_of(k.inputs[0]), ptr_of(k.inputs[1]), ptr_of(k.outputs[0]), s);
     return;

@@ -281,7 +281,10 @@ def test_model_mode_gemm_bert_layer(monkeypatch, precision):
     g = stitch.Graph(text)
     ex = stitch.Executor(stitch.Plan(g, "b200"), gemm=True)
     kinds = [k["template"] for k in ex.describe()]
-    assert kinds.count("gemm(cublasLt)") == 2, kinds
+    if precision == "fp32":  # full-f32 GEMMs are never fused (the fused kernel is TF32)
+        assert kinds.count("gemm(cublasLt)") == 2, kinds
+    else:  # ffn1's GEMM absorbs the bias + GELU pattern (CUTLASS tcgen05 epilogue)
+        assert kinds.count("gemm(cublasLt)") == 1 and "gemm(cutlass tcgen05 tf32)+bias+gelu" in kinds, kinds
     inputs = stitch.random_inputs(g, 1)
     got = ex.run(inputs)
     og = no.parse_graph(text)
@@ -294,6 +297,36 @@ def test_model_mode_gemm_bert_layer(monkeypatch, precision):
     again = ex.run(inputs)
     for k in got:
         assert np.array_equal(again[k], got[k])
+
+
+def test_fused_gemm_bias_gelu_matches_unfused_model_mode(monkeypatch):
+    """model mode: the CUTLASS tcgen05 TF32 GEMM with the bias + GELU(tanh)
+    epilogue (csrc/kernels/gemm_sm100.cu) vs cuBLASLt TF32 + the stitched
+    bias+GELU kernel -- both against the f64-matmul oracle at the TF32 band,
+    and the GELU output itself compared directly (same TF32 operand rounding,
+    different accumulation order): abs <= 5e-3 OR rel <= 5e-3"""
+    stitch = _stitch()
+    text = config_graph("bert_layer").replace("output y", "output y\noutput gl")
+    g = stitch.Graph(text)
+    plan = stitch.Plan(g, "b200")
+    inputs = stitch.random_inputs(g, 2)
+    # gl (the pattern's output) is a graph output here: the fused GEMM writes
+    # it from its epilogue; an intermediate of the pattern as a graph output
+    # keeps the pattern separate (nothing the plan exposes is dropped)
+    kinds_a = [k["template"] for k in
+               stitch.Plan(stitch.Graph(text.replace("output gl", "output a")), "b200").codegen(gemm=True)[1]]
+    assert "gemm(cutlass tcgen05 tf32)+bias+gelu" not in kinds_a, kinds_a
+    ex_out = stitch.Executor(plan, gemm=True)
+    assert "gemm(cutlass tcgen05 tf32)+bias+gelu" in [k["template"] for k in ex_out.describe()]
+    fused = ex_out.run(inputs)
+    monkeypatch.setenv("STITCH_GEMM_FUSE", "0")
+    ref = stitch.Executor(plan, gemm=True).run(inputs)
+    rep = stitch.compare({"gl": fused["gl"]}, {"gl": ref["gl"]}, 5e-3, 5e-3)
+    assert rep["pass"], (rep["message"], rep["max_abs"], rep["max_rel"])
+    og = no.parse_graph(text)
+    want = no.eval_reference(og, {k: v.astype(np.float64) for k, v in inputs.items()}, opaque=no.matmul_opaque)
+    for k in ("y", "gl"):
+        assert stitch.compare({k: fused[k]}, {k: want[k]}, 3e-2, 3e-2)["pass"], k
 
 
 def test_async_compile_matches_sync():
