@@ -652,6 +652,12 @@ struct StageCfg {
   int stages = 3;
   int64_t tile_floats = 0;   // RPB * L
   int64_t bytes = 0;         // dynamic smem: barriers + stages * tensors * tile
+  // STITCH_STAGE=2: per-team rings -- every row team owns `stages` row
+  // buffers, each with its own mbarrier; the team's lead thread issues one
+  // bulk copy per tensor per row, and a buffer is refilled after a team-only
+  // sync (no CTA-wide barrier, no wait on other teams' rows)
+  bool team = false;
+  int64_t bar_bytes = 128;   // mbarrier region ahead of the buffers
 };
 
 // block = 0: the team's natural CTA (max(256, TPR)); else the kernel's CTA
@@ -773,7 +779,40 @@ void emit_row(Emitter& em, const CompGraph& g, const std::set<int>& pat, const B
     }
     if (hoist_mode == 2 && !srcs.empty()) em.line("__syncthreads();");
   }
-  if (st) {
+  if (st && st->team) {
+    for (int v : st->tensors)
+      if (!em.is_param(v)) em.ensure_wait();
+    const std::string S = std::to_string(st->stages), sROWS = std::to_string(ROWS);
+    const int64_t nt = static_cast<int64_t>(st->tensors.size());
+    const std::string ring = std::to_string(int64_t(st->stages) * nt * L);  // floats per team
+    em.line("// TMA per-team rings: " + S + " row buffers x " + std::to_string(nt) + " tensor(s) x " +
+            std::to_string(L * 4) + " B per team, one mbarrier per buffer");
+    em.line("unsigned long long* sbar_ = reinterpret_cast<unsigned long long*>(dsmem_) + team_ * " + S + ";");
+    em.line("float* sbuf_ = reinterpret_cast<float*>(dsmem_ + " + std::to_string(st->bar_bytes) + ") + (i64)team_ * " +
+            ring + ";");
+    em.line("if (tl_ == 0) { for (int s = 0; s < " + S + "; ++s) mbar_init(sbar_ + s, 1); mbar_fence_init(); }");
+    em.line("__syncthreads();");
+    std::string issue = "auto issue_ = [&](i64 rb, int s) { const i64 r = min(rb + team_, (i64)" +
+                        std::to_string(ROWS - 1) + "); mbar_expect_tx(sbar_ + s, " + std::to_string(L * 4 * nt) + "u); ";
+    for (int64_t k = 0; k < nt; ++k)
+      issue += "bulk_g2s(sbuf_ + (i64)(s * " + std::to_string(nt) + " + " + std::to_string(k) + ") * " + sL + ", " +
+               tensor_ident(g.node(st->tensors[static_cast<size_t>(k)]).name) + " + r * " + sL + ", " +
+               std::to_string(L * 4) + "u, sbar_ + s); ";
+    issue += "};";
+    em.line(issue);
+    const std::string step = "(i64)vgrid * " + sRPB;
+    em.line("if (tl_ == 0) for (int s = 0; s < " + S + "; ++s) { const i64 rb = (i64)vbid * " + sRPB + " + (i64)s * " +
+            step + "; if (rb < " + sROWS + ") issue_(rb, s); }");
+    em.open("for (i64 rb_ = (i64)vbid * " + sRPB + ", i_ = 0; rb_ < " + sROWS + "; rb_ += " + step + ", ++i_)");
+    em.line("const int s_ = (int)(i_ % " + S + ");");
+    em.line("mbar_wait(sbar_ + s_, (unsigned)((i_ / " + S + ") & 1));");
+    for (int64_t k = 0; k < nt; ++k) {
+      const std::string nm = em.fresh("stg");
+      em.line("const float* " + nm + " = sbuf_ + (i64)(s_ * " + std::to_string(nt) + " + " + std::to_string(k) + ") * " +
+              sL + ";");
+      em.staged_ptr[st->tensors[static_cast<size_t>(k)]] = nm;
+    }
+  } else if (st) {
     // TMA-staged inputs that a kernel produces must wait; graph parameters
     // are streamed before the wait (hoisted prologue)
     for (int v : st->tensors)
@@ -1014,7 +1053,17 @@ void emit_row(Emitter& em, const CompGraph& g, const std::set<int>& pat, const B
     for (int o : outs) store_val(em, g, o, c, em.value(o, c), "row_ok");
     em.close();
   }
-  if (st) {  // every thread is done with stage s_: refill it with tile t_ + stages
+  if (st && st->team) {  // the team is done with buffer s_: its lead refills it with the team's row S iterations on
+    if (rp.TPR > 32)
+      em.line("__syncthreads();  // team spans warps (the row loop is CTA-uniform)");
+    else if (rp.TPR == 32)
+      em.line("__syncwarp();");
+    else
+      em.line("__syncwarp(((1u << " + std::to_string(rp.TPR) + ") - 1u) << ((threadIdx.x & 31) / " +
+              std::to_string(rp.TPR) + " * " + std::to_string(rp.TPR) + "));");
+    em.line("if (tl_ == 0) { const i64 nb_ = rb_ + (i64)" + std::to_string(st->stages) + " * vgrid * " + sRPB +
+            "; if (nb_ < " + std::to_string(ROWS) + ") { fence_proxy_async(); issue_(nb_, s_); } }");
+  } else if (st) {  // every thread is done with stage s_: refill it with tile t_ + stages
     em.line("__syncthreads();");
     em.line("if (threadIdx.x == 0 && t_ + " + std::to_string(st->stages) + " < te_) { fence_proxy_async(); issue_(t_ + " +
             std::to_string(st->stages) + ", s_); }");
@@ -1527,12 +1576,15 @@ KernelSpec generate_pattern_kernel(const CompGraph& g, const std::vector<int>& v
           sc.tensors = hits;
           sc.stages = std::max(2, env_int("STITCH_STAGES", 3));
           sc.tile_floats = int64_t(rp.RPB) * L;
+          sc.team = env_int("STITCH_STAGE", 0) == 2;
+          auto bar_bytes = [&](int s) { return sc.team ? std::max<int64_t>(128, (int64_t(rp.RPB) * s * 8 + 127) / 128 * 128) : 128; };
           // keep >= 2 CTAs per SM: fewer stages when several tensors are staged
           const int64_t smem_cap = int64_t(env_int("STITCH_STAGE_SMEM_KB", 110)) * 1024;
-          while (sc.stages > 2 && 128 + int64_t(sc.stages) * static_cast<int64_t>(hits.size()) * sc.tile_floats * 4 >
+          while (sc.stages > 2 && bar_bytes(sc.stages) + int64_t(sc.stages) * static_cast<int64_t>(hits.size()) * sc.tile_floats * 4 >
                                       smem_cap)
             --sc.stages;
-          sc.bytes = 128 + int64_t(sc.stages) * static_cast<int64_t>(hits.size()) * sc.tile_floats * 4;
+          sc.bar_bytes = bar_bytes(sc.stages);
+          sc.bytes = sc.bar_bytes + int64_t(sc.stages) * static_cast<int64_t>(hits.size()) * sc.tile_floats * 4;
           if (sc.bytes <= 200 * 1024) {
             // (less the row-invariant operands hoisted into static smem, ~2 rows)
             const int64_t fit = std::clamp<int64_t>((int64_t(220 * 1024) - 2 * L * 4) / sc.bytes, 1, 2048 / rp.block);

@@ -565,13 +565,16 @@ def _variant_text(name):
     return EDGE_SHAPES[name] if name in EDGE_SHAPES else config_graph(name)
 
 
+@pytest.mark.parametrize("mode", ["1", "2"])
 @pytest.mark.parametrize("stages", ["2", "3"])
 @pytest.mark.parametrize("name", STAGE_CASES)
-def test_tma_staged_regional_matches_oracle(name, stages, monkeypatch):
+def test_tma_staged_regional_matches_oracle(name, stages, mode, monkeypatch):
     """STITCH_STAGE=1: regional rows streamed into shared memory by
     cp.async.bulk (TMA bulk copies completing on an mbarrier, multi-stage
     ring per CTA) instead of registers -- same bits as the register path,
     within tolerance of the oracle, over repeated launches (ring phases).
+    STITCH_STAGE=2: the same through per-team rings (one bulk copy per row
+    and tensor, one mbarrier per row buffer, team-only sync before a refill).
     2 stages: dynamic smem below 48 KB plus the hoisted row-invariant
     operands in static smem above it (the launch needs the opt-in)"""
     stitch = _stitch()
@@ -580,7 +583,7 @@ def test_tma_staged_regional_matches_oracle(name, stages, monkeypatch):
     plan = stitch.Plan(g, "b200")
     inputs = stitch.random_inputs(g, 4)
     ref = stitch.Executor(plan).run(inputs)
-    monkeypatch.setenv("STITCH_STAGE", "1")
+    monkeypatch.setenv("STITCH_STAGE", mode)
     monkeypatch.setenv("STITCH_STAGES", stages)
     ex = stitch.Executor(plan)
     kinds = [k["template"] for k in ex.describe()]
