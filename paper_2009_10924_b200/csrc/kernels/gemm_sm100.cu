@@ -60,8 +60,69 @@ typename Gemm::Arguments make_args(const float* A, const float* B, const float* 
   args.epilogue.thread.bias_ptr = bias;
   return args;
 }
+
+// Plain D = A . B for the GEMMs with no fused epilogue, on CUTLASS's stream-K
+// tile scheduler.  BERT's ffn2 ([4096,3072] x [3072,768]) has only 16 x 3 =
+// 48 output tiles of 256x256 for 74 SM pairs: a data-parallel grid leaves a
+// third of the pairs idle, stream-K splits the K loop of the remainder over
+// them (deterministic fix-up in the workspace).
+using SkFusion = cutlass::epilogue::fusion::LinearCombination<float, float, float, float>;
+using SkEpilogue = typename cutlass::epilogue::collective::CollectiveBuilder<
+    cutlass::arch::Sm100, cutlass::arch::OpClassTensorOp, MmaTile, Cluster, cutlass::epilogue::collective::EpilogueTileAuto,
+    float, float, float, Row, 4, float, Row, 4, cutlass::epilogue::collective::EpilogueScheduleAuto, SkFusion>::CollectiveOp;
+using SkMainloop = typename cutlass::gemm::collective::CollectiveBuilder<
+    cutlass::arch::Sm100, cutlass::arch::OpClassTensorOp, float, Row, 4, float, Row, 4, float, MmaTile, Cluster,
+    cutlass::gemm::collective::StageCountAutoCarveout<static_cast<int>(sizeof(typename SkEpilogue::SharedStorage))>,
+    cutlass::gemm::collective::KernelScheduleAuto>::CollectiveOp;
+using SkKernel =
+    cutlass::gemm::kernel::GemmUniversal<Shape<int, int, int, int>, SkMainloop, SkEpilogue, cutlass::gemm::StreamKScheduler>;
+using SkGemm = cutlass::gemm::device::GemmUniversalAdapter<SkKernel>;
+
+// splits > 1: split-K with that many splits; 0: CUTLASS's stream-K heuristic
+typename SkGemm::Arguments make_sk_args(const float* A, const float* B, float* D, int M, int N, int K, int splits) {
+  auto sA = cutlass::make_cute_packed_stride(typename SkKernel::StrideA{}, cute::make_shape(M, K, 1));
+  auto sB = cutlass::make_cute_packed_stride(typename SkKernel::StrideB{}, cute::make_shape(N, K, 1));
+  auto sC = cutlass::make_cute_packed_stride(typename SkKernel::StrideC{}, cute::make_shape(M, N, 1));
+  auto sD = cutlass::make_cute_packed_stride(typename SkKernel::StrideD{}, cute::make_shape(M, N, 1));
+  typename SkGemm::Arguments args{cutlass::gemm::GemmUniversalMode::kGemm, {M, N, K, 1}, {A, sA, B, sB},
+                                  {{}, nullptr, sC, D, sD}};
+  args.epilogue.thread.alpha = 1.f;
+  args.epilogue.thread.beta = 0.f;
+  if (splits > 1) args.scheduler.splits = splits;
+  return args;
+}
 }  // namespace
 #endif
+
+// D[M,N] = A[M,K] . B[K,N], row-major f32, TF32 tensor cores, stream-K
+// (splits > 1: split-K).  Same return codes as gemm_bias_gelu_tf32.  The
+// workspace must hold gemm_tf32_streamk_workspace() bytes and belong to this
+// GEMM alone (it carries the fix-up partials and their flags).
+int gemm_tf32_streamk(const float* A, const float* B, float* D, int M, int N, int K, int splits, void* workspace,
+                      size_t workspace_bytes, cudaStream_t stream) {
+#ifdef STC_HAVE_CUTLASS
+  auto args = make_sk_args(A, B, D, M, N, K, splits);
+  SkGemm gemm;
+  if (SkGemm::get_workspace_size(args) > workspace_bytes || gemm.can_implement(args) != cutlass::Status::kSuccess) return 1;
+  if (gemm.initialize(args, workspace, stream) != cutlass::Status::kSuccess) return 2;
+  return gemm.run(stream) == cutlass::Status::kSuccess ? 0 : 2;
+#else
+  (void)A, (void)B, (void)D, (void)M, (void)N, (void)K, (void)splits, (void)workspace, (void)workspace_bytes, (void)stream;
+  return 1;
+#endif
+}
+
+// workspace bytes the stream-K GEMM needs for this shape; -1 = not implementable
+long long gemm_tf32_streamk_workspace(int M, int N, int K, int splits) {
+#ifdef STC_HAVE_CUTLASS
+  auto args = make_sk_args(nullptr, nullptr, nullptr, M, N, K, splits);
+  if (SkGemm::can_implement(args) != cutlass::Status::kSuccess) return -1;
+  return static_cast<long long>(SkGemm::get_workspace_size(args));
+#else
+  (void)M, (void)N, (void)K, (void)splits;
+  return -1;
+#endif
+}
 
 // D[M,N] = GELU(A[M,K] . B[K,N] + bias[N]), all row-major f32, TF32 tensor
 // cores.  0 = launched on `stream`; 1 = unavailable (no CUTLASS / shape not

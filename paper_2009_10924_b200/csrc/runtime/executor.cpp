@@ -39,6 +39,9 @@ std::string json_escape(const std::string& s) {
 int gemm_bias_gelu_tf32(const float* A, const float* B, const float* bias, float* D, int M, int N, int K, void* workspace,
                         size_t workspace_bytes, cudaStream_t stream);
 bool gemm_bias_gelu_supported(int M, int N, int K, size_t workspace_bytes);
+int gemm_tf32_streamk(const float* A, const float* B, float* D, int M, int N, int K, int splits, void* workspace,
+                      size_t workspace_bytes, cudaStream_t stream);
+long long gemm_tf32_streamk_workspace(int M, int N, int K, int splits);
 
 namespace {
 // the plan's bias + GELU(tanh) pattern over one GEMM output (graphs/
@@ -114,6 +117,10 @@ struct Executor::GemmState {
     cublasLtMatmulDesc_t op = nullptr;
     cublasLtMatrixLayout_t a = nullptr, b = nullptr, c = nullptr;
     cublasLtMatmulAlgo_t algo{};
+    // CUTLASS stream-K kernel instead of cuBLASLt (timed faster at init);
+    // its fix-up workspace is the unit's per-set scratch
+    bool streamk = false;
+    int sk_splits = 0;
   };
   std::map<size_t, Unit> units;
   ~GemmState() {
@@ -252,7 +259,18 @@ void Executor::finish_init(const std::string& cubin) {
       if (hs != CUBLAS_STATUS_SUCCESS || found < 1)
         throw std::runtime_error("[cublasLt] no algorithm for GEMM " + k.name);
       int best = 0;
-      if (found > 1) {
+      // STITCH_GEMM_SK: the CUTLASS stream-K TF32 kernel as a candidate
+      // (auto: timed against cuBLASLt's pick, the faster kept; 1: always when
+      // implementable; 0: never).  STITCH_GEMM_SK_SPLITS=n > 1: split-K
+      const char* skv = std::getenv("STITCH_GEMM_SK");
+      const std::string sk_mode = skv && *skv ? skv : "auto";
+      const char* sksv = std::getenv("STITCH_GEMM_SK_SPLITS");
+      const int sk_splits = sksv && *sksv ? std::max(0, std::atoi(sksv)) : 0;
+      const long long sk_ws = ct == CUBLAS_COMPUTE_32F || sk_mode == "0"
+                                  ? -1
+                                  : gemm_tf32_streamk_workspace(static_cast<int>(M), static_cast<int>(N), static_cast<int>(K),
+                                                                sk_splits);
+      if (found > 1 || (sk_ws >= 0 && sk_mode == "auto")) {
         void *da = nullptr, *db = nullptr, *dc = nullptr;
         STC_RT(cudaMalloc(&da, M * K * sizeof(float)));
         STC_RT(cudaMalloc(&db, K * N * sizeof(float)));
@@ -281,6 +299,29 @@ void Executor::finish_init(const std::string& cubin) {
           }
           if (t > 0.f && (best_ms == 0.f || t < best_ms)) best_ms = t, best = c;
         }
+        if (sk_ws >= 0 && sk_mode == "auto") {
+          void* ws = nullptr;
+          STC_RT(cudaMalloc(&ws, static_cast<size_t>(std::max<long long>(sk_ws, 256))));
+          STC_RT(cudaMemset(ws, 0, static_cast<size_t>(std::max<long long>(sk_ws, 256))));
+          float t = -1.f;
+          for (int rep = 0; rep < 4; ++rep) {
+            STC_RT(cudaEventRecord(e0, stream_));
+            if (gemm_tf32_streamk(static_cast<const float*>(da), static_cast<const float*>(db), static_cast<float*>(dc),
+                                  static_cast<int>(M), static_cast<int>(N), static_cast<int>(K), sk_splits, ws,
+                                  static_cast<size_t>(std::max<long long>(sk_ws, 256)), stream_) != 0) {
+              t = -1.f;
+              break;
+            }
+            STC_RT(cudaEventRecord(e1, stream_));
+            STC_RT(cudaEventSynchronize(e1));
+            float ms = 0.f;
+            STC_RT(cudaEventElapsedTime(&ms, e0, e1));
+            if (rep > 0 && (t < 0.f || ms < t)) t = ms;
+          }
+          STC_RT(cudaDeviceSynchronize());
+          cudaFree(ws);
+          if (t > 0.f && (best_ms == 0.f || t < best_ms)) best_ms = t, u.streamk = true;
+        }
         cudaEventDestroy(e0);
         cudaEventDestroy(e1);
         cudaFree(da);
@@ -288,6 +329,13 @@ void Executor::finish_init(const std::string& cubin) {
         cudaFree(dc);
       }
       u.algo = res[static_cast<size_t>(best)].algo;
+      if (sk_ws >= 0 && sk_mode == "1") u.streamk = true;
+      if (u.streamk) {
+        u.sk_splits = sk_splits;
+        specs_[ki].scratch_bytes = std::max<long long>(sk_ws, 256);
+        specs_[ki].scratch_header = 0;
+        specs_[ki].tmpl = "gemm(cutlass tcgen05 tf32 stream-k)";
+      }
       gemm_->units[ki] = u;
       fns_.push_back(nullptr);
       continue;
@@ -905,6 +953,15 @@ void Executor::launch_kernel(size_t i, int set, cudaStream_t s, int after, const
                                            static_cast<int>(k.gemm_m), static_cast<int>(k.gemm_n), static_cast<int>(k.gemm_k),
                                            gemm_->workspace, gemm_->ws_bytes, s))
       throw std::runtime_error("[cutlass] fused GEMM " + k.name + " failed (" + std::to_string(rc) + ")");
+    return;
+  }
+  if (k.is_gemm && gemm_->units.at(i).streamk) {
+    if (const int rc = gemm_tf32_streamk(static_cast<const float*>(ptr_of(k.inputs[0])),
+                                         static_cast<const float*>(ptr_of(k.inputs[1])), static_cast<float*>(ptr_of(k.outputs[0])),
+                                         static_cast<int>(k.gemm_m), static_cast<int>(k.gemm_n), static_cast<int>(k.gemm_k),
+                                         gemm_->units.at(i).sk_splits, scratch_[static_cast<size_t>(set)][i],
+                                         static_cast<size_t>(k.scratch_bytes), s))
+      throw std::runtime_error("[cutlass] stream-K GEMM " + k.name + " failed (" + std::to_string(rc) + ")");
     return;
   }
   if (k.is_gemm) {

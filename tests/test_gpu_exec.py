@@ -283,8 +283,10 @@ def test_model_mode_gemm_bert_layer(monkeypatch, precision):
     kinds = [k["template"] for k in ex.describe()]
     if precision == "fp32":  # full-f32 GEMMs are never fused (the fused kernel is TF32)
         assert kinds.count("gemm(cublasLt)") == 2, kinds
-    else:  # ffn1's GEMM absorbs the bias + GELU pattern (CUTLASS tcgen05 epilogue)
-        assert kinds.count("gemm(cublasLt)") == 1 and "gemm(cutlass tcgen05 tf32)+bias+gelu" in kinds, kinds
+    else:  # ffn1's GEMM absorbs the bias + GELU pattern (CUTLASS tcgen05 epilogue);
+        # ffn2's runs on whichever of cuBLASLt / the CUTLASS stream-K kernel timed faster
+        assert kinds.count("gemm(cublasLt)") + kinds.count("gemm(cutlass tcgen05 tf32 stream-k)") == 1, kinds
+        assert "gemm(cutlass tcgen05 tf32)+bias+gelu" in kinds, kinds
     inputs = stitch.random_inputs(g, 1)
     got = ex.run(inputs)
     og = no.parse_graph(text)
@@ -327,6 +329,41 @@ def test_fused_gemm_bias_gelu_matches_unfused_model_mode(monkeypatch):
     want = no.eval_reference(og, {k: v.astype(np.float64) for k, v in inputs.items()}, opaque=no.matmul_opaque)
     for k in ("y", "gl"):
         assert stitch.compare({k: fused[k]}, {k: want[k]}, 3e-2, 3e-2)["pass"], k
+
+
+@pytest.mark.parametrize("splits", ["0", "3"])
+def test_streamk_gemm_matches_cublaslt_model_mode(monkeypatch, splits):
+    """model mode: ffn2's plain GEMM on the CUTLASS tcgen05 TF32 kernel with
+    the stream-K tile scheduler (splits 0: CUTLASS's stream-K heuristic; 3:
+    split-K) vs cuBLASLt TF32 -- the LayerNorm output y of both against each
+    other (TF32 operands, different K order and operand rounding: abs <=
+    1e-2 OR rel <= 1e-2 on the unit-variance LN output) and against the f64-matmul oracle at the TF32 band (3e-2);
+    the deterministic fix-up makes replays bitwise equal"""
+    stitch = _stitch()
+    text = config_graph("bert_layer")
+    g = stitch.Graph(text)
+    plan = stitch.Plan(g, "b200")
+    inputs = stitch.random_inputs(g, 3)
+    monkeypatch.setenv("STITCH_GEMM_SK", "1")
+    monkeypatch.setenv("STITCH_GEMM_SK_SPLITS", splits)
+    ex = stitch.Executor(plan, gemm=True)
+    kinds = [k["template"] for k in ex.describe()]
+    assert kinds.count("gemm(cutlass tcgen05 tf32 stream-k)") == 1, kinds
+    sk = ex.run(inputs)
+    for _ in range(2):
+        again = ex.run(inputs)
+        for k in sk:
+            assert np.array_equal(again[k], sk[k]), k
+    monkeypatch.setenv("STITCH_GEMM_SK", "0")
+    ex_lt = stitch.Executor(plan, gemm=True)
+    assert "gemm(cublasLt)" in [k["template"] for k in ex_lt.describe()]
+    lt = ex_lt.run(inputs)
+    rep = stitch.compare({"y": sk["y"]}, {"y": lt["y"]}, 1e-2, 1e-2)
+    assert rep["pass"], (rep["message"], rep["max_abs"], rep["max_rel"])
+    og = no.parse_graph(text)
+    want = no.eval_reference(og, {k: v.astype(np.float64) for k, v in inputs.items()}, opaque=no.matmul_opaque)
+    for k in want:
+        assert stitch.compare({k: sk[k]}, {k: want[k]}, 3e-2, 3e-2)["pass"], k
 
 
 def test_async_compile_matches_sync():
