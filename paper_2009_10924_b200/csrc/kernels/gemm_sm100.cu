@@ -47,18 +47,28 @@ using Mainloop = typename cutlass::gemm::collective::CollectiveBuilder<
     cutlass::gemm::collective::KernelScheduleAuto>::CollectiveOp;
 using Kernel = cutlass::gemm::kernel::GemmUniversal<Shape<int, int, int, int>, Mainloop, Epilogue>;
 using Gemm = cutlass::gemm::device::GemmUniversalAdapter<Kernel>;
+// the same fused kernel on the stream-K tile scheduler: ffn1 ([4096,768] x
+// [768,3072]) is 192 tiles of 256x256 for 74 SM pairs, 2.6 waves
+using KernelSk =
+    cutlass::gemm::kernel::GemmUniversal<Shape<int, int, int, int>, Mainloop, Epilogue, cutlass::gemm::StreamKScheduler>;
+using GemmSkFused = cutlass::gemm::device::GemmUniversalAdapter<KernelSk>;
 
-typename Gemm::Arguments make_args(const float* A, const float* B, const float* bias, float* D, int M, int N, int K) {
-  auto sA = cutlass::make_cute_packed_stride(typename Kernel::StrideA{}, cute::make_shape(M, K, 1));
-  auto sB = cutlass::make_cute_packed_stride(typename Kernel::StrideB{}, cute::make_shape(N, K, 1));
-  auto sC = cutlass::make_cute_packed_stride(typename Kernel::StrideC{}, cute::make_shape(M, N, 1));
-  auto sD = cutlass::make_cute_packed_stride(typename Kernel::StrideD{}, cute::make_shape(M, N, 1));
-  typename Gemm::Arguments args{cutlass::gemm::GemmUniversalMode::kGemm, {M, N, K, 1}, {A, sA, B, sB},
-                                {{}, nullptr, sC, D, sD}};
+template <class G>
+typename G::Arguments make_args_t(const float* A, const float* B, const float* bias, float* D, int M, int N, int K) {
+  using Kn = typename G::GemmKernel;
+  auto sA = cutlass::make_cute_packed_stride(typename Kn::StrideA{}, cute::make_shape(M, K, 1));
+  auto sB = cutlass::make_cute_packed_stride(typename Kn::StrideB{}, cute::make_shape(N, K, 1));
+  auto sC = cutlass::make_cute_packed_stride(typename Kn::StrideC{}, cute::make_shape(M, N, 1));
+  auto sD = cutlass::make_cute_packed_stride(typename Kn::StrideD{}, cute::make_shape(M, N, 1));
+  typename G::Arguments args{cutlass::gemm::GemmUniversalMode::kGemm, {M, N, K, 1}, {A, sA, B, sB},
+                             {{}, nullptr, sC, D, sD}};
   args.epilogue.thread.alpha = 1.f;
   args.epilogue.thread.beta = 0.f;
   args.epilogue.thread.bias_ptr = bias;
   return args;
+}
+typename Gemm::Arguments make_args(const float* A, const float* B, const float* bias, float* D, int M, int N, int K) {
+  return make_args_t<Gemm>(A, B, bias, D, M, N, K);
 }
 
 // Plain D = A . B for the GEMMs with no fused epilogue, on CUTLASS's stream-K
@@ -138,6 +148,34 @@ int gemm_bias_gelu_tf32(const float* A, const float* B, const float* bias, float
 #else
   (void)A, (void)B, (void)bias, (void)D, (void)M, (void)N, (void)K, (void)workspace, (void)workspace_bytes, (void)stream;
   return 1;
+#endif
+}
+
+// the fused GEMM on the stream-K scheduler; the workspace (fix-up partials)
+// belongs to this unit alone: gemm_bias_gelu_tf32_sk_workspace() bytes
+int gemm_bias_gelu_tf32_sk(const float* A, const float* B, const float* bias, float* D, int M, int N, int K,
+                           void* workspace, size_t workspace_bytes, cudaStream_t stream) {
+#ifdef STC_HAVE_CUTLASS
+  auto args = make_args_t<GemmSkFused>(A, B, bias, D, M, N, K);
+  GemmSkFused gemm;
+  if (GemmSkFused::get_workspace_size(args) > workspace_bytes || gemm.can_implement(args) != cutlass::Status::kSuccess)
+    return 1;
+  if (gemm.initialize(args, workspace, stream) != cutlass::Status::kSuccess) return 2;
+  return gemm.run(stream) == cutlass::Status::kSuccess ? 0 : 2;
+#else
+  (void)A, (void)B, (void)bias, (void)D, (void)M, (void)N, (void)K, (void)workspace, (void)workspace_bytes, (void)stream;
+  return 1;
+#endif
+}
+
+long long gemm_bias_gelu_tf32_sk_workspace(int M, int N, int K) {
+#ifdef STC_HAVE_CUTLASS
+  auto args = make_args_t<GemmSkFused>(nullptr, nullptr, nullptr, nullptr, M, N, K);
+  if (GemmSkFused::can_implement(args) != cutlass::Status::kSuccess) return -1;
+  return static_cast<long long>(GemmSkFused::get_workspace_size(args));
+#else
+  (void)M, (void)N, (void)K;
+  return -1;
 #endif
 }
 

@@ -42,6 +42,9 @@ bool gemm_bias_gelu_supported(int M, int N, int K, size_t workspace_bytes);
 int gemm_tf32_streamk(const float* A, const float* B, float* D, int M, int N, int K, int splits, void* workspace,
                       size_t workspace_bytes, cudaStream_t stream);
 long long gemm_tf32_streamk_workspace(int M, int N, int K, int splits);
+int gemm_bias_gelu_tf32_sk(const float* A, const float* B, const float* bias, float* D, int M, int N, int K,
+                           void* workspace, size_t workspace_bytes, cudaStream_t stream);
+long long gemm_bias_gelu_tf32_sk_workspace(int M, int N, int K);
 
 namespace {
 // the plan's bias + GELU(tanh) pattern over one GEMM output (graphs/
@@ -266,10 +269,11 @@ void Executor::finish_init(const std::string& cubin) {
       const std::string sk_mode = skv && *skv ? skv : "auto";
       const char* sksv = std::getenv("STITCH_GEMM_SK_SPLITS");
       const int sk_splits = sksv && *sksv ? std::max(0, std::atoi(sksv)) : 0;
-      const long long sk_ws = ct == CUBLAS_COMPUTE_32F || sk_mode == "0"
-                                  ? -1
-                                  : gemm_tf32_streamk_workspace(static_cast<int>(M), static_cast<int>(N), static_cast<int>(K),
-                                                                sk_splits);
+      const bool fused = k.gemm_epilogue == "bias_gelu";
+      const long long sk_ws =
+          ct == CUBLAS_COMPUTE_32F || sk_mode == "0" ? -1
+          : fused ? gemm_bias_gelu_tf32_sk_workspace(static_cast<int>(M), static_cast<int>(N), static_cast<int>(K))
+                  : gemm_tf32_streamk_workspace(static_cast<int>(M), static_cast<int>(N), static_cast<int>(K), sk_splits);
       if (found > 1 || (sk_ws >= 0 && sk_mode == "auto")) {
         void *da = nullptr, *db = nullptr, *dc = nullptr;
         STC_RT(cudaMalloc(&da, M * K * sizeof(float)));
@@ -282,12 +286,22 @@ void Executor::finish_init(const std::string& cubin) {
         STC_RT(cudaEventCreate(&e1));
         const float alpha = 1.f, beta = 0.f;
         float best_ms = 0.f;
+        void* dbias = nullptr;  // fused units: the bias operand (zeros)
+        if (fused) {
+          STC_RT(cudaMalloc(&dbias, N * sizeof(float)));
+          STC_RT(cudaMemset(dbias, 0, N * sizeof(float)));
+        }
         for (int c = 0; c < found; ++c) {
           float t = -1.f;
           for (int rep = 0; rep < 4; ++rep) {
             STC_RT(cudaEventRecord(e0, stream_));
-            if (cublasLtMatmul(gemm_->lt, u.op, &alpha, db, u.b, da, u.a, &beta, dc, u.c, dc, u.c, &res[c].algo,
-                               gemm_->workspace, gemm_->ws_bytes, stream_) != CUBLAS_STATUS_SUCCESS) {
+            // fused units: the data-parallel fused kernel is the baseline
+            if (fused ? gemm_bias_gelu_tf32(static_cast<const float*>(da), static_cast<const float*>(db),
+                                            static_cast<const float*>(dbias), static_cast<float*>(dc), static_cast<int>(M),
+                                            static_cast<int>(N), static_cast<int>(K), gemm_->workspace, gemm_->ws_bytes,
+                                            stream_) != 0
+                      : cublasLtMatmul(gemm_->lt, u.op, &alpha, db, u.b, da, u.a, &beta, dc, u.c, dc, u.c, &res[c].algo,
+                                       gemm_->workspace, gemm_->ws_bytes, stream_) != CUBLAS_STATUS_SUCCESS) {
               t = -1.f;
               break;
             }
@@ -306,9 +320,13 @@ void Executor::finish_init(const std::string& cubin) {
           float t = -1.f;
           for (int rep = 0; rep < 4; ++rep) {
             STC_RT(cudaEventRecord(e0, stream_));
-            if (gemm_tf32_streamk(static_cast<const float*>(da), static_cast<const float*>(db), static_cast<float*>(dc),
-                                  static_cast<int>(M), static_cast<int>(N), static_cast<int>(K), sk_splits, ws,
-                                  static_cast<size_t>(std::max<long long>(sk_ws, 256)), stream_) != 0) {
+            const size_t wsb = static_cast<size_t>(std::max<long long>(sk_ws, 256));
+            if ((fused ? gemm_bias_gelu_tf32_sk(static_cast<const float*>(da), static_cast<const float*>(db),
+                                                static_cast<const float*>(dbias), static_cast<float*>(dc),
+                                                static_cast<int>(M), static_cast<int>(N), static_cast<int>(K), ws, wsb, stream_)
+                       : gemm_tf32_streamk(static_cast<const float*>(da), static_cast<const float*>(db),
+                                           static_cast<float*>(dc), static_cast<int>(M), static_cast<int>(N),
+                                           static_cast<int>(K), sk_splits, ws, wsb, stream_)) != 0) {
               t = -1.f;
               break;
             }
@@ -322,6 +340,7 @@ void Executor::finish_init(const std::string& cubin) {
           cudaFree(ws);
           if (t > 0.f && (best_ms == 0.f || t < best_ms)) best_ms = t, u.streamk = true;
         }
+        if (dbias) cudaFree(dbias);
         cudaEventDestroy(e0);
         cudaEventDestroy(e1);
         cudaFree(da);
@@ -334,7 +353,7 @@ void Executor::finish_init(const std::string& cubin) {
         u.sk_splits = sk_splits;
         specs_[ki].scratch_bytes = std::max<long long>(sk_ws, 256);
         specs_[ki].scratch_header = 0;
-        specs_[ki].tmpl = "gemm(cutlass tcgen05 tf32 stream-k)";
+        specs_[ki].tmpl = fused ? "gemm(cutlass tcgen05 tf32 stream-k)+bias+gelu" : "gemm(cutlass tcgen05 tf32 stream-k)";
       }
       gemm_->units[ki] = u;
       fns_.push_back(nullptr);
@@ -946,6 +965,16 @@ void Executor::launch_kernel(size_t i, int set, cudaStream_t s, int after, const
       if (auto it = bind->find(t); it != bind->end()) return it->second;
     return tensors_.at(t).dptr[static_cast<size_t>(set)];
   };
+  if (k.is_gemm && k.gemm_epilogue == "bias_gelu" && gemm_->units.at(i).streamk) {
+    if (const int rc = gemm_bias_gelu_tf32_sk(static_cast<const float*>(ptr_of(k.inputs[0])),
+                                              static_cast<const float*>(ptr_of(k.inputs[1])),
+                                              static_cast<const float*>(ptr_of(k.inputs[2])),
+                                              static_cast<float*>(ptr_of(k.outputs[0])), static_cast<int>(k.gemm_m),
+                                              static_cast<int>(k.gemm_n), static_cast<int>(k.gemm_k),
+                                              scratch_[static_cast<size_t>(set)][i], static_cast<size_t>(k.scratch_bytes), s))
+      throw std::runtime_error("[cutlass] fused stream-K GEMM " + k.name + " failed (" + std::to_string(rc) + ")");
+    return;
+  }
   if (k.is_gemm && k.gemm_epilogue == "bias_gelu") {
     if (const int rc = gemm_bias_gelu_tf32(static_cast<const float*>(ptr_of(k.inputs[0])),
                                            static_cast<const float*>(ptr_of(k.inputs[1])),
