@@ -122,8 +122,11 @@ int gemm_tf32_streamk(const float* A, const float* B, float* D, int M, int N, in
 #endif
 }
 
-// workspace bytes the stream-K GEMM needs for this shape; -1 = not implementable
+// workspace bytes the stream-K GEMM needs for this shape; -1 = not
+// implementable.  Split-K (splits > 1) is refused: its launch could not be
+// captured into the plan's CUDA graph ("stream capture of the plan failed")
 long long gemm_tf32_streamk_workspace(int M, int N, int K, int splits) {
+  if (splits > 1) return -1;
 #ifdef STC_HAVE_CUTLASS
   auto args = make_sk_args(nullptr, nullptr, nullptr, M, N, K, splits);
   if (SkGemm::can_implement(args) != cutlass::Status::kSuccess) return -1;

@@ -262,11 +262,15 @@ void Executor::finish_init(const std::string& cubin) {
       if (hs != CUBLAS_STATUS_SUCCESS || found < 1)
         throw std::runtime_error("[cublasLt] no algorithm for GEMM " + k.name);
       int best = 0;
-      // STITCH_GEMM_SK: the CUTLASS stream-K TF32 kernel as a candidate
-      // (auto: timed against cuBLASLt's pick, the faster kept; 1: always when
-      // implementable; 0: never).  STITCH_GEMM_SK_SPLITS=n > 1: split-K
+      // STITCH_GEMM_SK: the CUTLASS stream-K TF32 kernels (plain, and the
+      // fused bias+GELU one) -- 0 (default): never; 1: always when
+      // implementable; auto: timed here against cuBLASLt's pick / the
+      // data-parallel fused kernel, the faster kept.  Measured slower on the
+      // BERT layer (ffn2 46.3 vs 40.0 us, fused ffn1 44.6 vs 42.4 us), and
+      // auto mis-picks (an isolated warm call favours stream-K; 89.0 vs
+      // 82.7 us per layer in the graph): profiles/r02/gemm/streamk.jsonl
       const char* skv = std::getenv("STITCH_GEMM_SK");
-      const std::string sk_mode = skv && *skv ? skv : "auto";
+      const std::string sk_mode = skv && *skv ? skv : "0";
       const char* sksv = std::getenv("STITCH_GEMM_SK_SPLITS");
       const int sk_splits = sksv && *sksv ? std::max(0, std::atoi(sksv)) : 0;
       const bool fused = k.gemm_epilogue == "bias_gelu";

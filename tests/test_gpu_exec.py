@@ -331,11 +331,10 @@ def test_fused_gemm_bias_gelu_matches_unfused_model_mode(monkeypatch):
         assert stitch.compare({k: fused[k]}, {k: want[k]}, 3e-2, 3e-2)["pass"], k
 
 
-@pytest.mark.parametrize("splits", ["0", "3"])
-def test_streamk_gemm_matches_cublaslt_model_mode(monkeypatch, splits):
-    """model mode: ffn2's plain GEMM on the CUTLASS tcgen05 TF32 kernel with
-    the stream-K tile scheduler (splits 0: CUTLASS's stream-K heuristic; 3:
-    split-K), and ffn1's fused bias+GELU GEMM on the same scheduler, vs
+def test_streamk_gemm_matches_cublaslt_model_mode(monkeypatch):
+    """model mode, opt-in STITCH_GEMM_SK=1: ffn2's plain GEMM on the CUTLASS
+    tcgen05 TF32 kernel with the stream-K tile scheduler (CUTLASS's stream-K
+    heuristic), and ffn1's fused bias+GELU GEMM on the same scheduler, vs
     cuBLASLt TF32 + the data-parallel fused kernel -- gl and the LayerNorm
     output y of both against each
     other (TF32 operands, different K order and operand rounding: abs <=
@@ -347,7 +346,6 @@ def test_streamk_gemm_matches_cublaslt_model_mode(monkeypatch, splits):
     plan = stitch.Plan(g, "b200")
     inputs = stitch.random_inputs(g, 3)
     monkeypatch.setenv("STITCH_GEMM_SK", "1")
-    monkeypatch.setenv("STITCH_GEMM_SK_SPLITS", splits)
     ex = stitch.Executor(plan, gemm=True)
     kinds = [k["template"] for k in ex.describe()]
     assert kinds.count("gemm(cutlass tcgen05 tf32 stream-k)") == 1, kinds
