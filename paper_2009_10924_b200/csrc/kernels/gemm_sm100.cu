@@ -8,6 +8,7 @@
 // entry point reports "unavailable" and the executor keeps cuBLASLt + the
 // stitched kernel.
 #include <cstddef>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 #if __has_include("cutlass/cutlass.h")
@@ -35,162 +36,129 @@ using namespace cute;
 // epilogue warps are few and the accurate tanh sequence long.  TF32 operand
 // rounding (~1e-3 relative) dominates the error either way.
 using Row = cutlass::layout::RowMajor;
-using MmaTile = Shape<_256, _256, _32>;
-using Cluster = Shape<_2, _1, _1>;
-using Fusion = cutlass::epilogue::fusion::LinCombPerColBiasEltAct<cutlass::epilogue::thread::GELU_taylor, float, float, float>;
-using Epilogue = typename cutlass::epilogue::collective::CollectiveBuilder<
-    cutlass::arch::Sm100, cutlass::arch::OpClassTensorOp, MmaTile, Cluster, cutlass::epilogue::collective::EpilogueTileAuto,
-    float, float, float, Row, 4, float, Row, 4, cutlass::epilogue::collective::EpilogueScheduleAuto, Fusion>::CollectiveOp;
-using Mainloop = typename cutlass::gemm::collective::CollectiveBuilder<
-    cutlass::arch::Sm100, cutlass::arch::OpClassTensorOp, float, Row, 4, float, Row, 4, float, MmaTile, Cluster,
-    cutlass::gemm::collective::StageCountAutoCarveout<static_cast<int>(sizeof(typename Epilogue::SharedStorage))>,
-    cutlass::gemm::collective::KernelScheduleAuto>::CollectiveOp;
-using Kernel = cutlass::gemm::kernel::GemmUniversal<Shape<int, int, int, int>, Mainloop, Epilogue>;
-using Gemm = cutlass::gemm::device::GemmUniversalAdapter<Kernel>;
-// the same fused kernel on the stream-K tile scheduler: ffn1 ([4096,768] x
-// [768,3072]) is 192 tiles of 256x256 for 74 SM pairs, 2.6 waves
-using KernelSk =
-    cutlass::gemm::kernel::GemmUniversal<Shape<int, int, int, int>, Mainloop, Epilogue, cutlass::gemm::StreamKScheduler>;
-using GemmSkFused = cutlass::gemm::device::GemmUniversalAdapter<KernelSk>;
+using GeluFusion =
+    cutlass::epilogue::fusion::LinCombPerColBiasEltAct<cutlass::epilogue::thread::GELU_taylor, float, float, float>;
+using PlainFusion = cutlass::epilogue::fusion::LinearCombination<float, float, float, float>;
 
-template <class G>
-typename G::Arguments make_args_t(const float* A, const float* B, const float* bias, float* D, int M, int N, int K) {
-  using Kn = typename G::GemmKernel;
-  auto sA = cutlass::make_cute_packed_stride(typename Kn::StrideA{}, cute::make_shape(M, K, 1));
-  auto sB = cutlass::make_cute_packed_stride(typename Kn::StrideB{}, cute::make_shape(N, K, 1));
-  auto sC = cutlass::make_cute_packed_stride(typename Kn::StrideC{}, cute::make_shape(M, N, 1));
-  auto sD = cutlass::make_cute_packed_stride(typename Kn::StrideD{}, cute::make_shape(M, N, 1));
-  typename G::Arguments args{cutlass::gemm::GemmUniversalMode::kGemm, {M, N, K, 1}, {A, sA, B, sB},
-                             {{}, nullptr, sC, D, sD}};
-  args.epilogue.thread.alpha = 1.f;
-  args.epilogue.thread.beta = 0.f;
-  args.epilogue.thread.bias_ptr = bias;
-  return args;
+// one TF32 tcgen05 GEMM configuration: MMA tile, cluster (2 along M = the
+// 2-SM cta_group::2 MMA), tile scheduler (void = data-parallel persistent),
+// epilogue fusion
+template <class MmaTile, class Cluster, class Sched, class Fusion>
+struct Cfg {
+  using Epilogue = typename cutlass::epilogue::collective::CollectiveBuilder<
+      cutlass::arch::Sm100, cutlass::arch::OpClassTensorOp, MmaTile, Cluster,
+      cutlass::epilogue::collective::EpilogueTileAuto, float, float, float, Row, 4, float, Row, 4,
+      cutlass::epilogue::collective::EpilogueScheduleAuto, Fusion>::CollectiveOp;
+  using Mainloop = typename cutlass::gemm::collective::CollectiveBuilder<
+      cutlass::arch::Sm100, cutlass::arch::OpClassTensorOp, float, Row, 4, float, Row, 4, float, MmaTile, Cluster,
+      cutlass::gemm::collective::StageCountAutoCarveout<static_cast<int>(sizeof(typename Epilogue::SharedStorage))>,
+      cutlass::gemm::collective::KernelScheduleAuto>::CollectiveOp;
+  using Kernel = cutlass::gemm::kernel::GemmUniversal<Shape<int, int, int, int>, Mainloop, Epilogue, Sched>;
+  using Gemm = cutlass::gemm::device::GemmUniversalAdapter<Kernel>;
+  static constexpr bool kFused = !std::is_same_v<Fusion, PlainFusion>;
+
+  static typename Gemm::Arguments args(const float* A, const float* B, const float* bias, float* D, int M, int N, int K) {
+    auto sA = cutlass::make_cute_packed_stride(typename Kernel::StrideA{}, cute::make_shape(M, K, 1));
+    auto sB = cutlass::make_cute_packed_stride(typename Kernel::StrideB{}, cute::make_shape(N, K, 1));
+    auto sC = cutlass::make_cute_packed_stride(typename Kernel::StrideC{}, cute::make_shape(M, N, 1));
+    auto sD = cutlass::make_cute_packed_stride(typename Kernel::StrideD{}, cute::make_shape(M, N, 1));
+    typename Gemm::Arguments a{cutlass::gemm::GemmUniversalMode::kGemm, {M, N, K, 1}, {A, sA, B, sB},
+                               {{}, nullptr, sC, D, sD}};
+    a.epilogue.thread.alpha = 1.f;
+    a.epilogue.thread.beta = 0.f;
+    if constexpr (kFused) a.epilogue.thread.bias_ptr = bias;
+    return a;
+  }
+  static long long workspace(int M, int N, int K) {
+    auto a = args(nullptr, nullptr, nullptr, nullptr, M, N, K);
+    if (Gemm::can_implement(a) != cutlass::Status::kSuccess) return -1;
+    return static_cast<long long>(Gemm::get_workspace_size(a));
+  }
+  static int run(const float* A, const float* B, const float* bias, float* D, int M, int N, int K, void* ws,
+                 size_t ws_bytes, cudaStream_t stream) {
+    auto a = args(A, B, bias, D, M, N, K);
+    Gemm gemm;
+    if (Gemm::get_workspace_size(a) > ws_bytes || gemm.can_implement(a) != cutlass::Status::kSuccess) return 1;
+    if (gemm.initialize(a, ws, stream) != cutlass::Status::kSuccess) return 2;
+    return gemm.run(stream) == cutlass::Status::kSuccess ? 0 : 2;
+  }
+};
+
+using T256x256 = Shape<_256, _256, _32>;
+using T256x192 = Shape<_256, _192, _32>;
+using T128x192 = Shape<_128, _192, _32>;
+using C2 = Shape<_2, _1, _1>;
+using C1 = Shape<_1, _1, _1>;
+using SK = cutlass::gemm::StreamKScheduler;
+
+// variants (ids are the STITCH_GEMM_PLAIN / STITCH_GEMM_FUSED values):
+//   0  2-SM 256x256 data-parallel (fused default; plain default is cuBLASLt)
+//   1  2-SM 256x256 stream-K: BERT's ffn2 ([4096,3072] x [3072,768]) has
+//      only 48 output tiles of 256x256 for 74 SM pairs
+//   2  1-SM 128x192 data-parallel: 128 ffn2 tiles for 148 SMs, one wave
+//   3  2-SM 256x192 data-parallel
+template <class Fusion>
+long long ws_of(int v, int M, int N, int K) {
+  switch (v) {
+    case 0: return Cfg<T256x256, C2, void, Fusion>::workspace(M, N, K);
+    case 1: return Cfg<T256x256, C2, SK, Fusion>::workspace(M, N, K);
+    case 2: return Cfg<T128x192, C1, void, Fusion>::workspace(M, N, K);
+    case 3: return Cfg<T256x192, C2, void, Fusion>::workspace(M, N, K);
+    default: return -1;
+  }
 }
-typename Gemm::Arguments make_args(const float* A, const float* B, const float* bias, float* D, int M, int N, int K) {
-  return make_args_t<Gemm>(A, B, bias, D, M, N, K);
-}
-
-// Plain D = A . B for the GEMMs with no fused epilogue, on CUTLASS's stream-K
-// tile scheduler.  BERT's ffn2 ([4096,3072] x [3072,768]) has only 16 x 3 =
-// 48 output tiles of 256x256 for 74 SM pairs: a data-parallel grid leaves a
-// third of the pairs idle, stream-K splits the K loop of the remainder over
-// them (deterministic fix-up in the workspace).
-using SkFusion = cutlass::epilogue::fusion::LinearCombination<float, float, float, float>;
-using SkEpilogue = typename cutlass::epilogue::collective::CollectiveBuilder<
-    cutlass::arch::Sm100, cutlass::arch::OpClassTensorOp, MmaTile, Cluster, cutlass::epilogue::collective::EpilogueTileAuto,
-    float, float, float, Row, 4, float, Row, 4, cutlass::epilogue::collective::EpilogueScheduleAuto, SkFusion>::CollectiveOp;
-using SkMainloop = typename cutlass::gemm::collective::CollectiveBuilder<
-    cutlass::arch::Sm100, cutlass::arch::OpClassTensorOp, float, Row, 4, float, Row, 4, float, MmaTile, Cluster,
-    cutlass::gemm::collective::StageCountAutoCarveout<static_cast<int>(sizeof(typename SkEpilogue::SharedStorage))>,
-    cutlass::gemm::collective::KernelScheduleAuto>::CollectiveOp;
-using SkKernel =
-    cutlass::gemm::kernel::GemmUniversal<Shape<int, int, int, int>, SkMainloop, SkEpilogue, cutlass::gemm::StreamKScheduler>;
-using SkGemm = cutlass::gemm::device::GemmUniversalAdapter<SkKernel>;
-
-// splits > 1: split-K with that many splits; 0: CUTLASS's stream-K heuristic
-typename SkGemm::Arguments make_sk_args(const float* A, const float* B, float* D, int M, int N, int K, int splits) {
-  auto sA = cutlass::make_cute_packed_stride(typename SkKernel::StrideA{}, cute::make_shape(M, K, 1));
-  auto sB = cutlass::make_cute_packed_stride(typename SkKernel::StrideB{}, cute::make_shape(N, K, 1));
-  auto sC = cutlass::make_cute_packed_stride(typename SkKernel::StrideC{}, cute::make_shape(M, N, 1));
-  auto sD = cutlass::make_cute_packed_stride(typename SkKernel::StrideD{}, cute::make_shape(M, N, 1));
-  typename SkGemm::Arguments args{cutlass::gemm::GemmUniversalMode::kGemm, {M, N, K, 1}, {A, sA, B, sB},
-                                  {{}, nullptr, sC, D, sD}};
-  args.epilogue.thread.alpha = 1.f;
-  args.epilogue.thread.beta = 0.f;
-  if (splits > 1) args.scheduler.splits = splits;
-  return args;
+template <class Fusion>
+int run_of(int v, const float* A, const float* B, const float* bias, float* D, int M, int N, int K, void* ws, size_t wsb,
+           cudaStream_t s) {
+  switch (v) {
+    case 0: return Cfg<T256x256, C2, void, Fusion>::run(A, B, bias, D, M, N, K, ws, wsb, s);
+    case 1: return Cfg<T256x256, C2, SK, Fusion>::run(A, B, bias, D, M, N, K, ws, wsb, s);
+    case 2: return Cfg<T128x192, C1, void, Fusion>::run(A, B, bias, D, M, N, K, ws, wsb, s);
+    case 3: return Cfg<T256x192, C2, void, Fusion>::run(A, B, bias, D, M, N, K, ws, wsb, s);
+    default: return 1;
+  }
 }
 }  // namespace
 #endif
 
-// D[M,N] = A[M,K] . B[K,N], row-major f32, TF32 tensor cores, stream-K
-// (splits > 1: split-K).  Same return codes as gemm_bias_gelu_tf32.  The
-// workspace must hold gemm_tf32_streamk_workspace() bytes and belong to this
-// GEMM alone (it carries the fix-up partials and their flags).
-int gemm_tf32_streamk(const float* A, const float* B, float* D, int M, int N, int K, int splits, void* workspace,
-                      size_t workspace_bytes, cudaStream_t stream) {
+// D[M,N] = A[M,K] . B[K,N] (+ per-column bias, then GELU(tanh), when `fused`),
+// row-major f32, TF32 tensor cores, CUTLASS configuration `variant` (above).
+// 0 = launched on `stream`; 1 = unavailable (no CUTLASS / shape not
+// implementable / unknown variant); 2 = launch error.  The workspace must
+// hold gemm_tf32_workspace() bytes and belong to this GEMM (stream-K keeps
+// its fix-up partials and flags there).
+int gemm_tf32(int variant, bool fused, const float* A, const float* B, const float* bias, float* D, int M, int N, int K,
+              void* workspace, size_t workspace_bytes, cudaStream_t stream) {
 #ifdef STC_HAVE_CUTLASS
-  auto args = make_sk_args(A, B, D, M, N, K, splits);
-  SkGemm gemm;
-  if (SkGemm::get_workspace_size(args) > workspace_bytes || gemm.can_implement(args) != cutlass::Status::kSuccess) return 1;
-  if (gemm.initialize(args, workspace, stream) != cutlass::Status::kSuccess) return 2;
-  return gemm.run(stream) == cutlass::Status::kSuccess ? 0 : 2;
+  return fused ? run_of<GeluFusion>(variant, A, B, bias, D, M, N, K, workspace, workspace_bytes, stream)
+               : run_of<PlainFusion>(variant, A, B, bias, D, M, N, K, workspace, workspace_bytes, stream);
 #else
-  (void)A, (void)B, (void)D, (void)M, (void)N, (void)K, (void)splits, (void)workspace, (void)workspace_bytes, (void)stream;
+  (void)variant, (void)fused, (void)A, (void)B, (void)bias, (void)D, (void)M, (void)N, (void)K, (void)workspace,
+      (void)workspace_bytes, (void)stream;
   return 1;
 #endif
 }
 
-// workspace bytes the stream-K GEMM needs for this shape; -1 = not
-// implementable.  Split-K (splits > 1) is refused: its launch could not be
-// captured into the plan's CUDA graph ("stream capture of the plan failed")
-long long gemm_tf32_streamk_workspace(int M, int N, int K, int splits) {
-  if (splits > 1) return -1;
+// workspace bytes of that configuration for this shape; -1 = not implementable
+long long gemm_tf32_workspace(int variant, bool fused, int M, int N, int K) {
 #ifdef STC_HAVE_CUTLASS
-  auto args = make_sk_args(nullptr, nullptr, nullptr, M, N, K, splits);
-  if (SkGemm::can_implement(args) != cutlass::Status::kSuccess) return -1;
-  return static_cast<long long>(SkGemm::get_workspace_size(args));
+  return fused ? ws_of<GeluFusion>(variant, M, N, K) : ws_of<PlainFusion>(variant, M, N, K);
 #else
-  (void)M, (void)N, (void)K, (void)splits;
+  (void)variant, (void)fused, (void)M, (void)N, (void)K;
   return -1;
 #endif
 }
 
-// D[M,N] = GELU(A[M,K] . B[K,N] + bias[N]), all row-major f32, TF32 tensor
-// cores.  0 = launched on `stream`; 1 = unavailable (no CUTLASS / shape not
-// implementable); 2 = launch error.
+// D[M,N] = GELU(A[M,K] . B[K,N] + bias[N]) on the default fused configuration
 int gemm_bias_gelu_tf32(const float* A, const float* B, const float* bias, float* D, int M, int N, int K, void* workspace,
                         size_t workspace_bytes, cudaStream_t stream) {
-#ifdef STC_HAVE_CUTLASS
-  auto args = make_args(A, B, bias, D, M, N, K);
-  Gemm gemm;
-  if (Gemm::get_workspace_size(args) > workspace_bytes || gemm.can_implement(args) != cutlass::Status::kSuccess) return 1;
-  if (gemm.initialize(args, workspace, stream) != cutlass::Status::kSuccess) return 2;
-  return gemm.run(stream) == cutlass::Status::kSuccess ? 0 : 2;
-#else
-  (void)A, (void)B, (void)bias, (void)D, (void)M, (void)N, (void)K, (void)workspace, (void)workspace_bytes, (void)stream;
-  return 1;
-#endif
-}
-
-// the fused GEMM on the stream-K scheduler; the workspace (fix-up partials)
-// belongs to this unit alone: gemm_bias_gelu_tf32_sk_workspace() bytes
-int gemm_bias_gelu_tf32_sk(const float* A, const float* B, const float* bias, float* D, int M, int N, int K,
-                           void* workspace, size_t workspace_bytes, cudaStream_t stream) {
-#ifdef STC_HAVE_CUTLASS
-  auto args = make_args_t<GemmSkFused>(A, B, bias, D, M, N, K);
-  GemmSkFused gemm;
-  if (GemmSkFused::get_workspace_size(args) > workspace_bytes || gemm.can_implement(args) != cutlass::Status::kSuccess)
-    return 1;
-  if (gemm.initialize(args, workspace, stream) != cutlass::Status::kSuccess) return 2;
-  return gemm.run(stream) == cutlass::Status::kSuccess ? 0 : 2;
-#else
-  (void)A, (void)B, (void)bias, (void)D, (void)M, (void)N, (void)K, (void)workspace, (void)workspace_bytes, (void)stream;
-  return 1;
-#endif
-}
-
-long long gemm_bias_gelu_tf32_sk_workspace(int M, int N, int K) {
-#ifdef STC_HAVE_CUTLASS
-  auto args = make_args_t<GemmSkFused>(nullptr, nullptr, nullptr, nullptr, M, N, K);
-  if (GemmSkFused::can_implement(args) != cutlass::Status::kSuccess) return -1;
-  return static_cast<long long>(GemmSkFused::get_workspace_size(args));
-#else
-  (void)M, (void)N, (void)K;
-  return -1;
-#endif
+  return gemm_tf32(0, true, A, B, bias, D, M, N, K, workspace, workspace_bytes, stream);
 }
 
 // whether the fused path can run this shape (host-side check, no launch)
 bool gemm_bias_gelu_supported(int M, int N, int K, size_t workspace_bytes) {
-#ifdef STC_HAVE_CUTLASS
-  auto args = make_args(nullptr, nullptr, nullptr, nullptr, M, N, K);
-  return Gemm::get_workspace_size(args) <= workspace_bytes && Gemm::can_implement(args) == cutlass::Status::kSuccess;
-#else
-  (void)M, (void)N, (void)K, (void)workspace_bytes;
-  return false;
-#endif
+  const long long ws = gemm_tf32_workspace(0, true, M, N, K);
+  return ws >= 0 && static_cast<size_t>(ws) <= workspace_bytes;
 }
 
 }  // namespace stitch::gpu

@@ -39,12 +39,9 @@ std::string json_escape(const std::string& s) {
 int gemm_bias_gelu_tf32(const float* A, const float* B, const float* bias, float* D, int M, int N, int K, void* workspace,
                         size_t workspace_bytes, cudaStream_t stream);
 bool gemm_bias_gelu_supported(int M, int N, int K, size_t workspace_bytes);
-int gemm_tf32_streamk(const float* A, const float* B, float* D, int M, int N, int K, int splits, void* workspace,
-                      size_t workspace_bytes, cudaStream_t stream);
-long long gemm_tf32_streamk_workspace(int M, int N, int K, int splits);
-int gemm_bias_gelu_tf32_sk(const float* A, const float* B, const float* bias, float* D, int M, int N, int K,
-                           void* workspace, size_t workspace_bytes, cudaStream_t stream);
-long long gemm_bias_gelu_tf32_sk_workspace(int M, int N, int K);
+int gemm_tf32(int variant, bool fused, const float* A, const float* B, const float* bias, float* D, int M, int N, int K,
+              void* workspace, size_t workspace_bytes, cudaStream_t stream);
+long long gemm_tf32_workspace(int variant, bool fused, int M, int N, int K);
 
 namespace {
 // the plan's bias + GELU(tanh) pattern over one GEMM output (graphs/
@@ -120,10 +117,9 @@ struct Executor::GemmState {
     cublasLtMatmulDesc_t op = nullptr;
     cublasLtMatrixLayout_t a = nullptr, b = nullptr, c = nullptr;
     cublasLtMatmulAlgo_t algo{};
-    // CUTLASS stream-K kernel instead of cuBLASLt (timed faster at init);
-    // its fix-up workspace is the unit's per-set scratch
-    bool streamk = false;
-    int sk_splits = 0;
+    // CUTLASS configuration (gemm_sm100.cu) instead of cuBLASLt; -1 =
+    // cuBLASLt.  Its workspace is the unit's per-set scratch
+    int variant = -1;
   };
   std::map<size_t, Unit> units;
   ~GemmState() {
@@ -262,23 +258,7 @@ void Executor::finish_init(const std::string& cubin) {
       if (hs != CUBLAS_STATUS_SUCCESS || found < 1)
         throw std::runtime_error("[cublasLt] no algorithm for GEMM " + k.name);
       int best = 0;
-      // STITCH_GEMM_SK: the CUTLASS stream-K TF32 kernels (plain, and the
-      // fused bias+GELU one) -- 0 (default): never; 1: always when
-      // implementable; auto: timed here against cuBLASLt's pick / the
-      // data-parallel fused kernel, the faster kept.  Measured slower on the
-      // BERT layer (ffn2 46.3 vs 40.0 us, fused ffn1 44.6 vs 42.4 us), and
-      // auto mis-picks (an isolated warm call favours stream-K; 89.0 vs
-      // 82.7 us per layer in the graph): profiles/r02/gemm/streamk.jsonl
-      const char* skv = std::getenv("STITCH_GEMM_SK");
-      const std::string sk_mode = skv && *skv ? skv : "0";
-      const char* sksv = std::getenv("STITCH_GEMM_SK_SPLITS");
-      const int sk_splits = sksv && *sksv ? std::max(0, std::atoi(sksv)) : 0;
-      const bool fused = k.gemm_epilogue == "bias_gelu";
-      const long long sk_ws =
-          ct == CUBLAS_COMPUTE_32F || sk_mode == "0" ? -1
-          : fused ? gemm_bias_gelu_tf32_sk_workspace(static_cast<int>(M), static_cast<int>(N), static_cast<int>(K))
-                  : gemm_tf32_streamk_workspace(static_cast<int>(M), static_cast<int>(N), static_cast<int>(K), sk_splits);
-      if (found > 1 || (sk_ws >= 0 && sk_mode == "auto")) {
+      if (found > 1) {
         void *da = nullptr, *db = nullptr, *dc = nullptr;
         STC_RT(cudaMalloc(&da, M * K * sizeof(float)));
         STC_RT(cudaMalloc(&db, K * N * sizeof(float)));
@@ -290,22 +270,12 @@ void Executor::finish_init(const std::string& cubin) {
         STC_RT(cudaEventCreate(&e1));
         const float alpha = 1.f, beta = 0.f;
         float best_ms = 0.f;
-        void* dbias = nullptr;  // fused units: the bias operand (zeros)
-        if (fused) {
-          STC_RT(cudaMalloc(&dbias, N * sizeof(float)));
-          STC_RT(cudaMemset(dbias, 0, N * sizeof(float)));
-        }
         for (int c = 0; c < found; ++c) {
           float t = -1.f;
           for (int rep = 0; rep < 4; ++rep) {
             STC_RT(cudaEventRecord(e0, stream_));
-            // fused units: the data-parallel fused kernel is the baseline
-            if (fused ? gemm_bias_gelu_tf32(static_cast<const float*>(da), static_cast<const float*>(db),
-                                            static_cast<const float*>(dbias), static_cast<float*>(dc), static_cast<int>(M),
-                                            static_cast<int>(N), static_cast<int>(K), gemm_->workspace, gemm_->ws_bytes,
-                                            stream_) != 0
-                      : cublasLtMatmul(gemm_->lt, u.op, &alpha, db, u.b, da, u.a, &beta, dc, u.c, dc, u.c, &res[c].algo,
-                                       gemm_->workspace, gemm_->ws_bytes, stream_) != CUBLAS_STATUS_SUCCESS) {
+            if (cublasLtMatmul(gemm_->lt, u.op, &alpha, db, u.b, da, u.a, &beta, dc, u.c, dc, u.c, &res[c].algo,
+                               gemm_->workspace, gemm_->ws_bytes, stream_) != CUBLAS_STATUS_SUCCESS) {
               t = -1.f;
               break;
             }
@@ -317,34 +287,6 @@ void Executor::finish_init(const std::string& cubin) {
           }
           if (t > 0.f && (best_ms == 0.f || t < best_ms)) best_ms = t, best = c;
         }
-        if (sk_ws >= 0 && sk_mode == "auto") {
-          void* ws = nullptr;
-          STC_RT(cudaMalloc(&ws, static_cast<size_t>(std::max<long long>(sk_ws, 256))));
-          STC_RT(cudaMemset(ws, 0, static_cast<size_t>(std::max<long long>(sk_ws, 256))));
-          float t = -1.f;
-          for (int rep = 0; rep < 4; ++rep) {
-            STC_RT(cudaEventRecord(e0, stream_));
-            const size_t wsb = static_cast<size_t>(std::max<long long>(sk_ws, 256));
-            if ((fused ? gemm_bias_gelu_tf32_sk(static_cast<const float*>(da), static_cast<const float*>(db),
-                                                static_cast<const float*>(dbias), static_cast<float*>(dc),
-                                                static_cast<int>(M), static_cast<int>(N), static_cast<int>(K), ws, wsb, stream_)
-                       : gemm_tf32_streamk(static_cast<const float*>(da), static_cast<const float*>(db),
-                                           static_cast<float*>(dc), static_cast<int>(M), static_cast<int>(N),
-                                           static_cast<int>(K), sk_splits, ws, wsb, stream_)) != 0) {
-              t = -1.f;
-              break;
-            }
-            STC_RT(cudaEventRecord(e1, stream_));
-            STC_RT(cudaEventSynchronize(e1));
-            float ms = 0.f;
-            STC_RT(cudaEventElapsedTime(&ms, e0, e1));
-            if (rep > 0 && (t < 0.f || ms < t)) t = ms;
-          }
-          STC_RT(cudaDeviceSynchronize());
-          cudaFree(ws);
-          if (t > 0.f && (best_ms == 0.f || t < best_ms)) best_ms = t, u.streamk = true;
-        }
-        if (dbias) cudaFree(dbias);
         cudaEventDestroy(e0);
         cudaEventDestroy(e1);
         cudaFree(da);
@@ -352,12 +294,34 @@ void Executor::finish_init(const std::string& cubin) {
         cudaFree(dc);
       }
       u.algo = res[static_cast<size_t>(best)].algo;
-      if (sk_ws >= 0 && sk_mode == "1") u.streamk = true;
-      if (u.streamk) {
-        u.sk_splits = sk_splits;
-        specs_[ki].scratch_bytes = std::max<long long>(sk_ws, 256);
+      // CUTLASS tcgen05 TF32 configuration (csrc/kernels/gemm_sm100.cu):
+      // STITCH_GEMM_FUSED for the GEMM + bias + GELU units (default 0, the
+      // 2-SM 256x256 kernel), STITCH_GEMM_PLAIN for the plain GEMMs (default
+      // cuBLASLt); STITCH_GEMM_SK=1 = stream-K (variant 1) for both.  The
+      // alternatives measured slower on the BERT layer
+      // (profiles/r02/gemm/streamk.jsonl, gemm_variants.jsonl)
+      const bool fused = k.gemm_epilogue == "bias_gelu";
+      auto env_variant = [](const char* name, int dflt) {
+        const char* v = std::getenv(name);
+        return v && *v ? std::atoi(v) : dflt;
+      };
+      const bool sk = env_variant("STITCH_GEMM_SK", 0) == 1;
+      int variant = fused ? env_variant("STITCH_GEMM_FUSED", sk ? 1 : 0) : env_variant("STITCH_GEMM_PLAIN", sk ? 1 : -1);
+      if (ct == CUBLAS_COMPUTE_32F && !fused) variant = -1;
+      long long ws = variant >= 0 ? gemm_tf32_workspace(variant, fused, static_cast<int>(M), static_cast<int>(N),
+                                                        static_cast<int>(K))
+                                  : -1;
+      if (fused && ws < 0) {  // an unimplementable choice: the default fused kernel (the plan matched it)
+        variant = 0;
+        ws = gemm_tf32_workspace(0, true, static_cast<int>(M), static_cast<int>(N), static_cast<int>(K));
+      }
+      if (ws < 0) variant = -1;
+      u.variant = variant;
+      if (variant >= 0) {
+        static const char* kDesc[] = {"", " stream-k", " 1sm 128x192", " 2sm 256x192"};
+        specs_[ki].scratch_bytes = std::max<long long>(ws, 256);
         specs_[ki].scratch_header = 0;
-        specs_[ki].tmpl = fused ? "gemm(cutlass tcgen05 tf32 stream-k)+bias+gelu" : "gemm(cutlass tcgen05 tf32 stream-k)";
+        specs_[ki].tmpl = std::string("gemm(cutlass tcgen05 tf32") + kDesc[variant] + ")" + (fused ? "+bias+gelu" : "");
       }
       gemm_->units[ki] = u;
       fns_.push_back(nullptr);
@@ -969,32 +933,15 @@ void Executor::launch_kernel(size_t i, int set, cudaStream_t s, int after, const
       if (auto it = bind->find(t); it != bind->end()) return it->second;
     return tensors_.at(t).dptr[static_cast<size_t>(set)];
   };
-  if (k.is_gemm && k.gemm_epilogue == "bias_gelu" && gemm_->units.at(i).streamk) {
-    if (const int rc = gemm_bias_gelu_tf32_sk(static_cast<const float*>(ptr_of(k.inputs[0])),
-                                              static_cast<const float*>(ptr_of(k.inputs[1])),
-                                              static_cast<const float*>(ptr_of(k.inputs[2])),
-                                              static_cast<float*>(ptr_of(k.outputs[0])), static_cast<int>(k.gemm_m),
-                                              static_cast<int>(k.gemm_n), static_cast<int>(k.gemm_k),
-                                              scratch_[static_cast<size_t>(set)][i], static_cast<size_t>(k.scratch_bytes), s))
-      throw std::runtime_error("[cutlass] fused stream-K GEMM " + k.name + " failed (" + std::to_string(rc) + ")");
-    return;
-  }
-  if (k.is_gemm && k.gemm_epilogue == "bias_gelu") {
-    if (const int rc = gemm_bias_gelu_tf32(static_cast<const float*>(ptr_of(k.inputs[0])),
-                                           static_cast<const float*>(ptr_of(k.inputs[1])),
-                                           static_cast<const float*>(ptr_of(k.inputs[2])), static_cast<float*>(ptr_of(k.outputs[0])),
-                                           static_cast<int>(k.gemm_m), static_cast<int>(k.gemm_n), static_cast<int>(k.gemm_k),
-                                           gemm_->workspace, gemm_->ws_bytes, s))
-      throw std::runtime_error("[cutlass] fused GEMM " + k.name + " failed (" + std::to_string(rc) + ")");
-    return;
-  }
-  if (k.is_gemm && gemm_->units.at(i).streamk) {
-    if (const int rc = gemm_tf32_streamk(static_cast<const float*>(ptr_of(k.inputs[0])),
-                                         static_cast<const float*>(ptr_of(k.inputs[1])), static_cast<float*>(ptr_of(k.outputs[0])),
-                                         static_cast<int>(k.gemm_m), static_cast<int>(k.gemm_n), static_cast<int>(k.gemm_k),
-                                         gemm_->units.at(i).sk_splits, scratch_[static_cast<size_t>(set)][i],
-                                         static_cast<size_t>(k.scratch_bytes), s))
-      throw std::runtime_error("[cutlass] stream-K GEMM " + k.name + " failed (" + std::to_string(rc) + ")");
+  if (k.is_gemm && gemm_->units.at(i).variant >= 0) {
+    const bool fused = k.gemm_epilogue == "bias_gelu";
+    if (const int rc = gemm_tf32(gemm_->units.at(i).variant, fused, static_cast<const float*>(ptr_of(k.inputs[0])),
+                                 static_cast<const float*>(ptr_of(k.inputs[1])),
+                                 fused ? static_cast<const float*>(ptr_of(k.inputs[2])) : nullptr,
+                                 static_cast<float*>(ptr_of(k.outputs[0])), static_cast<int>(k.gemm_m),
+                                 static_cast<int>(k.gemm_n), static_cast<int>(k.gemm_k), scratch_[static_cast<size_t>(set)][i],
+                                 static_cast<size_t>(k.scratch_bytes), s))
+      throw std::runtime_error("[cutlass] GEMM " + k.name + " failed (" + std::to_string(rc) + ")");
     return;
   }
   if (k.is_gemm) {

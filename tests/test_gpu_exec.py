@@ -331,42 +331,59 @@ def test_fused_gemm_bias_gelu_matches_unfused_model_mode(monkeypatch):
         assert stitch.compare({k: fused[k]}, {k: want[k]}, 3e-2, 3e-2)["pass"], k
 
 
-def test_streamk_gemm_matches_cublaslt_model_mode(monkeypatch):
-    """model mode, opt-in STITCH_GEMM_SK=1: ffn2's plain GEMM on the CUTLASS
-    tcgen05 TF32 kernel with the stream-K tile scheduler (CUTLASS's stream-K
-    heuristic), and ffn1's fused bias+GELU GEMM on the same scheduler, vs
-    cuBLASLt TF32 + the data-parallel fused kernel -- gl and the LayerNorm
-    output y of both against each
-    other (TF32 operands, different K order and operand rounding: abs <=
-    1e-2 OR rel <= 1e-2 on the unit-variance LN output) and against the f64-matmul oracle at the TF32 band (3e-2);
-    the deterministic fix-up makes replays bitwise equal"""
+GEMM_VARIANTS = {"1": " stream-k", "2": " 1sm 128x192", "3": " 2sm 256x192"}
+
+
+@pytest.mark.parametrize("variant", sorted(GEMM_VARIANTS))
+def test_cutlass_gemm_variants_match_default_model_mode(monkeypatch, variant):
+    """model mode, opt-in CUTLASS tcgen05 TF32 configurations
+    (csrc/kernels/gemm_sm100.cu; STITCH_GEMM_PLAIN / STITCH_GEMM_FUSED):
+    1 = 2-SM 256x256 on the stream-K tile scheduler, 2 = 1-SM 128x192,
+    3 = 2-SM 256x192 -- ffn2's plain GEMM and ffn1's fused bias+GELU GEMM on
+    that configuration vs the defaults (cuBLASLt TF32 + the 2-SM 256x256 fused
+    kernel): the LayerNorm output y of both against each other (TF32
+    operands, different K order and operand rounding: abs <= 1e-2 OR rel <=
+    1e-2 on the unit-variance LN output) and against the f64-matmul oracle
+    at the TF32 band (3e-2); replays bitwise equal (stream-K's fix-up is
+    deterministic)"""
     stitch = _stitch()
     text = config_graph("bert_layer")
     g = stitch.Graph(text)
     plan = stitch.Plan(g, "b200")
     inputs = stitch.random_inputs(g, 3)
-    monkeypatch.setenv("STITCH_GEMM_SK", "1")
+    monkeypatch.setenv("STITCH_GEMM_PLAIN", variant)
+    monkeypatch.setenv("STITCH_GEMM_FUSED", variant)
     ex = stitch.Executor(plan, gemm=True)
     kinds = [k["template"] for k in ex.describe()]
-    assert kinds.count("gemm(cutlass tcgen05 tf32 stream-k)") == 1, kinds
-    assert "gemm(cutlass tcgen05 tf32 stream-k)+bias+gelu" in kinds, kinds
-    sk = ex.run(inputs)
+    desc = GEMM_VARIANTS[variant]
+    assert kinds.count("gemm(cutlass tcgen05 tf32%s)" % desc) == 1, kinds
+    assert "gemm(cutlass tcgen05 tf32%s)+bias+gelu" % desc in kinds, kinds
+    got = ex.run(inputs)
     for _ in range(2):
         again = ex.run(inputs)
-        for k in sk:
-            assert np.array_equal(again[k], sk[k]), k
-    monkeypatch.setenv("STITCH_GEMM_SK", "0")
-    ex_lt = stitch.Executor(plan, gemm=True)
-    assert "gemm(cublasLt)" in [k["template"] for k in ex_lt.describe()]
-    assert "gemm(cutlass tcgen05 tf32)+bias+gelu" in [k["template"] for k in ex_lt.describe()]
-    lt = ex_lt.run(inputs)
-    for k in ("y",):
-        rep = stitch.compare({k: sk[k]}, {k: lt[k]}, 1e-2, 1e-2)
-        assert rep["pass"], (k, rep["message"], rep["max_abs"], rep["max_rel"])
+        for k in got:
+            assert np.array_equal(again[k], got[k]), k
+    monkeypatch.delenv("STITCH_GEMM_PLAIN")
+    monkeypatch.delenv("STITCH_GEMM_FUSED")
+    ex_d = stitch.Executor(plan, gemm=True)
+    kinds_d = [k["template"] for k in ex_d.describe()]
+    assert "gemm(cublasLt)" in kinds_d and "gemm(cutlass tcgen05 tf32)+bias+gelu" in kinds_d, kinds_d
+    ref = ex_d.run(inputs)
+    rep = stitch.compare({"y": got["y"]}, {"y": ref["y"]}, 1e-2, 1e-2)
+    assert rep["pass"], (rep["message"], rep["max_abs"], rep["max_rel"])
     og = no.parse_graph(text)
     want = no.eval_reference(og, {k: v.astype(np.float64) for k, v in inputs.items()}, opaque=no.matmul_opaque)
     for k in want:
-        assert stitch.compare({k: sk[k]}, {k: want[k]}, 3e-2, 3e-2)["pass"], k
+        assert stitch.compare({k: got[k]}, {k: want[k]}, 3e-2, 3e-2)["pass"], k
+
+
+def test_streamk_switch_model_mode(monkeypatch):
+    """STITCH_GEMM_SK=1 selects the stream-K configuration for both GEMMs"""
+    stitch = _stitch()
+    g = stitch.Graph(config_graph("bert_layer"))
+    monkeypatch.setenv("STITCH_GEMM_SK", "1")
+    kinds = [k["template"] for k in stitch.Executor(stitch.Plan(g, "b200"), gemm=True).describe()]
+    assert "gemm(cutlass tcgen05 tf32 stream-k)" in kinds and "gemm(cutlass tcgen05 tf32 stream-k)+bias+gelu" in kinds, kinds
 
 
 def test_async_compile_matches_sync():
