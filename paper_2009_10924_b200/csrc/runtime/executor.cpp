@@ -296,17 +296,27 @@ void Executor::finish_init(const std::string& cubin) {
       u.algo = res[static_cast<size_t>(best)].algo;
       // CUTLASS tcgen05 TF32 configuration (csrc/kernels/gemm_sm100.cu):
       // STITCH_GEMM_FUSED for the GEMM + bias + GELU units (default 0, the
-      // 2-SM 256x256 kernel), STITCH_GEMM_PLAIN for the plain GEMMs (default
-      // cuBLASLt); STITCH_GEMM_SK=1 = stream-K (variant 1) for both.  The
-      // alternatives measured slower on the BERT layer
+      // 2-SM 256x256 kernel), STITCH_GEMM_PLAIN for the plain GEMMs;
+      // STITCH_GEMM_SK=1 = stream-K (variant 1) for both.  Plain default:
+      // the 2-SM 256x192 kernel where its tiles fill the SM pairs' waves
+      // clearly better than 256x256 tiles would (BERT's ffn2, N = 768: 64
+      // tiles for 74 pairs instead of 48; 35.8 vs cuBLASLt's 39.9 us), else
+      // cuBLASLt.  Stream-K and the 1-SM 128x192 kernel measured slower
       // (profiles/r02/gemm/streamk.jsonl, gemm_variants.jsonl)
       const bool fused = k.gemm_epilogue == "bias_gelu";
       auto env_variant = [](const char* name, int dflt) {
         const char* v = std::getenv(name);
         return v && *v ? std::atoi(v) : dflt;
       };
+      auto wave_fill = [&](int64_t tm, int64_t tn) {
+        const int64_t tiles = ((static_cast<int64_t>(M) + tm - 1) / tm) * ((static_cast<int64_t>(N) + tn - 1) / tn);
+        const int64_t pairs = std::max(1, dev_->sm_count / 2), waves = (tiles + pairs - 1) / pairs;
+        return static_cast<double>(tiles) / static_cast<double>(waves * pairs);
+      };
+      const int plain_default = N % 192 == 0 && M % 256 == 0 && wave_fill(256, 192) > wave_fill(256, 256) + 0.05 ? 3 : -1;
       const bool sk = env_variant("STITCH_GEMM_SK", 0) == 1;
-      int variant = fused ? env_variant("STITCH_GEMM_FUSED", sk ? 1 : 0) : env_variant("STITCH_GEMM_PLAIN", sk ? 1 : -1);
+      int variant = fused ? env_variant("STITCH_GEMM_FUSED", sk ? 1 : 0)
+                          : env_variant("STITCH_GEMM_PLAIN", sk ? 1 : plain_default);
       if (ct == CUBLAS_COMPUTE_32F && !fused) variant = -1;
       long long ws = variant >= 0 ? gemm_tf32_workspace(variant, fused, static_cast<int>(M), static_cast<int>(N),
                                                         static_cast<int>(K))
