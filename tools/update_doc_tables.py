@@ -55,9 +55,12 @@ v = S["bert_layer"]
 rows.append("| C3 full BERT FFN layer (A.4, placeholders) | 8 plan kernels (6 + 2 opaque) in 6 launches | 333.5 MB | local + regional + "
             "grid opaque | %s (%s) | %s | %s / %s | — | %s |" % (f(v["us"]), f(v["frac_of_measured_peak"], 3), f(v["us_serial"]),
                                                               f(v["us_one_launch_per_step"]), f(v["us_one_call"]), cpu(v)))
-rows.append("| BERT FFN layer, model mode (§9) | 8 plan kernels in %d launches (cuBLASLt TF32 GEMM + CUTLASS tcgen05 GEMM with the "
-            "bias+GELU epilogue) | — | GEMM + local + regional | %s (%s refined, %d launches) | — | — | — | — |"
-            % (S["bert_layer_model_tf32"]["kernels"], f(S["bert_layer_model_tf32"]["us"], 1),
+rows.append("| BERT FFN layer, model mode (§9) | 8 plan kernels in %d launches (%s) | — | GEMM + local + regional | %s (%s refined, "
+            "%d launches) | — | — | — | — |"
+            % (S["bert_layer_model_tf32"]["kernels"],
+               " + ".join(t for t in S["bert_layer_model_tf32"].get("templates", []) if t.startswith("gemm")) or
+               "cuBLASLt TF32 GEMM + CUTLASS tcgen05 GEMM with the bias+GELU epilogue",
+               f(S["bert_layer_model_tf32"]["us"], 1),
                f(S["bert_layer_model_tf32_refined"]["us"], 1), S["bert_layer_model_tf32_refined"]["kernels"]))
 
 p = os.path.join(ROOT, "DESIGN.md")
