@@ -88,6 +88,7 @@ using T256x256 = Shape<_256, _256, _32>;
 using T256x192 = Shape<_256, _192, _32>;
 using T128x192 = Shape<_128, _192, _32>;
 using C2 = Shape<_2, _1, _1>;
+using C22 = Shape<_2, _2, _1>;  // 2 SM pairs along N: A tiles multicast by TMA
 using C1 = Shape<_1, _1, _1>;
 using SK = cutlass::gemm::StreamKScheduler;
 
@@ -97,6 +98,8 @@ using SK = cutlass::gemm::StreamKScheduler;
 //      only 48 output tiles of 256x256 for 74 SM pairs
 //   2  1-SM 128x192 data-parallel: 128 ffn2 tiles for 148 SMs, one wave
 //   3  2-SM 256x192 data-parallel
+//   4  2-SM 256x256, clusters of 2 pairs along N (A multicast)
+//   5  2-SM 256x192, clusters of 2 pairs along N (A multicast)
 template <class Fusion>
 long long ws_of(int v, int M, int N, int K) {
   switch (v) {
@@ -104,6 +107,8 @@ long long ws_of(int v, int M, int N, int K) {
     case 1: return Cfg<T256x256, C2, SK, Fusion>::workspace(M, N, K);
     case 2: return Cfg<T128x192, C1, void, Fusion>::workspace(M, N, K);
     case 3: return Cfg<T256x192, C2, void, Fusion>::workspace(M, N, K);
+    case 4: return Cfg<T256x256, C22, void, Fusion>::workspace(M, N, K);
+    case 5: return Cfg<T256x192, C22, void, Fusion>::workspace(M, N, K);
     default: return -1;
   }
 }
@@ -115,6 +120,8 @@ int run_of(int v, const float* A, const float* B, const float* bias, float* D, i
     case 1: return Cfg<T256x256, C2, SK, Fusion>::run(A, B, bias, D, M, N, K, ws, wsb, s);
     case 2: return Cfg<T128x192, C1, void, Fusion>::run(A, B, bias, D, M, N, K, ws, wsb, s);
     case 3: return Cfg<T256x192, C2, void, Fusion>::run(A, B, bias, D, M, N, K, ws, wsb, s);
+    case 4: return Cfg<T256x256, C22, void, Fusion>::run(A, B, bias, D, M, N, K, ws, wsb, s);
+    case 5: return Cfg<T256x192, C22, void, Fusion>::run(A, B, bias, D, M, N, K, ws, wsb, s);
     default: return 1;
   }
 }
