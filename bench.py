@@ -63,13 +63,15 @@ def read_graph(name):
         return f.read()
 
 
-def measured_peaks():
+def measured_peaks(tensor=False):
+    """(HBM GB/s, source); tensor=True: the dense bf16 matmul TFLOP/s burst
+    figure (fallback: the profiling recipe's 2250 nominal)"""
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             p = json.load(f)
-        return float(p["hbm_gbs"]), "measured"
+        return float(p["bf16_tflops"]) if tensor else (float(p["hbm_gbs"]), "measured")
     except Exception:
-        return 6650.0, "fallback"
+        return 2250.0 if tensor else (6650.0, "fallback")
 
 
 def ncu_traffic(graph):
@@ -304,6 +306,15 @@ def time_subgraph(stitch, name, gemm=False, refine=False):
            "dominant": {"name": desc[top]["name"], "template": desc[top]["template"],
                         "us_event": round(kus[top], 3), "bytes": desc[top]["bytes"],
                         "frac_event": round(desc[top]["bytes"] / kus[top] / 1e3 / peak, 4)}}
+    gemms = [(k, u) for k, u in zip(desc, kus) if "gemm_mnk" in k and u > 0]
+    if gemms:
+        # model mode: the GEMMs against the tensor roofline -- TF32 dense peak
+        # taken as half the measured bf16 matmul peak (the B200 TF32:BF16 rate)
+        tf32_peak = measured_peaks(tensor=True) / 2
+        out["gemms"] = [{"name": k["name"], "template": k["template"], "mnk": k["gemm_mnk"], "us_event": round(u, 3),
+                         "tflops": round(2 * math.prod(k["gemm_mnk"]) / u / 1e6, 1),
+                         "frac_of_tf32_peak": round(2 * math.prod(k["gemm_mnk"]) / u / 1e6 / tf32_peak, 3)}
+                        for k, u in gemms]
     del ex
     if len(desc) != plan_kernels and not refine:
         # the same plan as a launch graph: packed (default packing), and in

@@ -1434,7 +1434,9 @@ std::string describe_specs(const std::vector<KernelSpec>& specs) {
       << "\",\"pattern\":\"" << k.pattern_key << "\",\"grid\":" << k.grid << ",\"block\":" << k.block
       << ",\"smem\":" << k.smem << ",\"cooperative\":" << (k.cooperative ? "true" : "false")
       << ",\"cluster\":" << k.cluster
-      << ",\"bytes\":" << k.alg_bytes << ",\"inputs\":[";
+      << ",\"bytes\":" << k.alg_bytes;
+    if (k.is_gemm) o << ",\"gemm_mnk\":[" << k.gemm_m << "," << k.gemm_n << "," << k.gemm_k << "]";
+    o << ",\"inputs\":[";
     for (size_t j = 0; j < k.inputs.size(); ++j) o << (j ? "," : "") << "\"" << k.inputs[j] << "\"";
     o << "],\"outputs\":[";
     for (size_t j = 0; j < k.outputs.size(); ++j) o << (j ? "," : "") << "\"" << k.outputs[j] << "\"";
