@@ -87,8 +87,7 @@ struct Cfg {
 using T256x256 = Shape<_256, _256, _32>;
 using T256x192 = Shape<_256, _192, _32>;
 using T128x192 = Shape<_128, _192, _32>;
-using T256x256k64 = Shape<_256, _256, _64>;
-using T256x192k64 = Shape<_256, _192, _64>;
+
 using C2 = Shape<_2, _1, _1>;
 using C22 = Shape<_2, _2, _1>;  // 2 SM pairs along N: A tiles multicast by TMA
 using C1 = Shape<_1, _1, _1>;
@@ -102,8 +101,8 @@ using SK = cutlass::gemm::StreamKScheduler;
 //   3  2-SM 256x192 data-parallel
 //   4  2-SM 256x256, clusters of 2 pairs along N (A multicast)
 //   5  2-SM 256x192, clusters of 2 pairs along N (A multicast)
-//   6  2-SM 256x256 with 64-deep K tiles (two 128 B swizzle atoms per row)
-//   7  2-SM 256x192 with 64-deep K tiles
+// (64-deep K tiles, 2-SM 256x256 / 256x192, measured 13-45% slower: fewer
+// pipeline stages fit; profiles/r02/gemm/gemm_variants_k64.jsonl)
 template <class Fusion>
 long long ws_of(int v, int M, int N, int K) {
   switch (v) {
@@ -113,8 +112,6 @@ long long ws_of(int v, int M, int N, int K) {
     case 3: return Cfg<T256x192, C2, void, Fusion>::workspace(M, N, K);
     case 4: return Cfg<T256x256, C22, void, Fusion>::workspace(M, N, K);
     case 5: return Cfg<T256x192, C22, void, Fusion>::workspace(M, N, K);
-    case 6: return Cfg<T256x256k64, C2, void, Fusion>::workspace(M, N, K);
-    case 7: return Cfg<T256x192k64, C2, void, Fusion>::workspace(M, N, K);
     default: return -1;
   }
 }
@@ -128,8 +125,6 @@ int run_of(int v, const float* A, const float* B, const float* bias, float* D, i
     case 3: return Cfg<T256x192, C2, void, Fusion>::run(A, B, bias, D, M, N, K, ws, wsb, s);
     case 4: return Cfg<T256x256, C22, void, Fusion>::run(A, B, bias, D, M, N, K, ws, wsb, s);
     case 5: return Cfg<T256x192, C22, void, Fusion>::run(A, B, bias, D, M, N, K, ws, wsb, s);
-    case 6: return Cfg<T256x256k64, C2, void, Fusion>::run(A, B, bias, D, M, N, K, ws, wsb, s);
-    case 7: return Cfg<T256x192k64, C2, void, Fusion>::run(A, B, bias, D, M, N, K, ws, wsb, s);
     default: return 1;
   }
 }

@@ -328,8 +328,7 @@ void Executor::finish_init(const std::string& cubin) {
       if (ws < 0) variant = -1;
       u.variant = variant;
       if (variant >= 0) {
-        static const char* kDesc[] = {"",          " stream-k",    " 1sm 128x192",     " 2sm 256x192",
-                                      " 2x2 256x256", " 2x2 256x192", " 2sm 256x256x64", " 2sm 256x192x64"};
+        static const char* kDesc[] = {"", " stream-k", " 1sm 128x192", " 2sm 256x192", " 2x2 256x256", " 2x2 256x192"};
         specs_[ki].scratch_bytes = std::max<long long>(ws, 256);
         specs_[ki].scratch_header = 0;
         specs_[ki].tmpl = std::string("gemm(cutlass tcgen05 tf32") + kDesc[variant] + ")" + (fused ? "+bias+gelu" : "");
