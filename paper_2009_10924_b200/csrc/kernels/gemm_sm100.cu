@@ -43,14 +43,14 @@ using PlainFusion = cutlass::epilogue::fusion::LinearCombination<float, float, f
 // one TF32 tcgen05 GEMM configuration: MMA tile, cluster (2 along M = the
 // 2-SM cta_group::2 MMA), tile scheduler (void = data-parallel persistent),
 // epilogue fusion
-template <class MmaTile, class Cluster, class Sched, class Fusion>
+template <class MmaTile, class Cluster, class Sched, class Fusion, class LayoutB = Row>
 struct Cfg {
   using Epilogue = typename cutlass::epilogue::collective::CollectiveBuilder<
       cutlass::arch::Sm100, cutlass::arch::OpClassTensorOp, MmaTile, Cluster,
       cutlass::epilogue::collective::EpilogueTileAuto, float, float, float, Row, 4, float, Row, 4,
       cutlass::epilogue::collective::EpilogueScheduleAuto, Fusion>::CollectiveOp;
   using Mainloop = typename cutlass::gemm::collective::CollectiveBuilder<
-      cutlass::arch::Sm100, cutlass::arch::OpClassTensorOp, float, Row, 4, float, Row, 4, float, MmaTile, Cluster,
+      cutlass::arch::Sm100, cutlass::arch::OpClassTensorOp, float, Row, 4, float, LayoutB, 4, float, MmaTile, Cluster,
       cutlass::gemm::collective::StageCountAutoCarveout<static_cast<int>(sizeof(typename Epilogue::SharedStorage))>,
       cutlass::gemm::collective::KernelScheduleAuto>::CollectiveOp;
   using Kernel = cutlass::gemm::kernel::GemmUniversal<Shape<int, int, int, int>, Mainloop, Epilogue, Sched>;
@@ -92,6 +92,7 @@ using C2 = Shape<_2, _1, _1>;
 using C22 = Shape<_2, _2, _1>;  // 2 SM pairs along N: A tiles multicast by TMA
 using C1 = Shape<_1, _1, _1>;
 using SK = cutlass::gemm::StreamKScheduler;
+using Col = cutlass::layout::ColumnMajor;
 
 // variants (ids are the STITCH_GEMM_PLAIN / STITCH_GEMM_FUSED values):
 //   0  2-SM 256x256 data-parallel (fused default; plain default is cuBLASLt)
@@ -101,6 +102,10 @@ using SK = cutlass::gemm::StreamKScheduler;
 //   3  2-SM 256x192 data-parallel
 //   4  2-SM 256x256, clusters of 2 pairs along N (A multicast)
 //   5  2-SM 256x192, clusters of 2 pairs along N (A multicast)
+//   6  2-SM 256x192 with B column-major (K-major: B^T stored [N,K]) -- layout
+//      probe only (tools/gemm_layout_probe.py); the executor's weights are
+//      row-major [K,N] and it never selects 6 / 7
+//   7  2-SM 256x256 with B column-major (probe only)
 // (64-deep K tiles, 2-SM 256x256 / 256x192, measured 13-45% slower: fewer
 // pipeline stages fit; profiles/r02/gemm/gemm_variants_k64.jsonl)
 template <class Fusion>
@@ -112,6 +117,8 @@ long long ws_of(int v, int M, int N, int K) {
     case 3: return Cfg<T256x192, C2, void, Fusion>::workspace(M, N, K);
     case 4: return Cfg<T256x256, C22, void, Fusion>::workspace(M, N, K);
     case 5: return Cfg<T256x192, C22, void, Fusion>::workspace(M, N, K);
+    case 6: return Cfg<T256x192, C2, void, Fusion, Col>::workspace(M, N, K);
+    case 7: return Cfg<T256x256, C2, void, Fusion, Col>::workspace(M, N, K);
     default: return -1;
   }
 }
@@ -125,6 +132,8 @@ int run_of(int v, const float* A, const float* B, const float* bias, float* D, i
     case 3: return Cfg<T256x192, C2, void, Fusion>::run(A, B, bias, D, M, N, K, ws, wsb, s);
     case 4: return Cfg<T256x256, C22, void, Fusion>::run(A, B, bias, D, M, N, K, ws, wsb, s);
     case 5: return Cfg<T256x192, C22, void, Fusion>::run(A, B, bias, D, M, N, K, ws, wsb, s);
+    case 6: return Cfg<T256x192, C2, void, Fusion, Col>::run(A, B, bias, D, M, N, K, ws, wsb, s);
+    case 7: return Cfg<T256x256, C2, void, Fusion, Col>::run(A, B, bias, D, M, N, K, ws, wsb, s);
     default: return 1;
   }
 }

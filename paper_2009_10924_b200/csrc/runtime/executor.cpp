@@ -318,6 +318,7 @@ void Executor::finish_init(const std::string& cubin) {
       int variant = fused ? env_variant("STITCH_GEMM_FUSED", sk ? 1 : 0)
                           : env_variant("STITCH_GEMM_PLAIN", sk ? 1 : plain_default);
       if (ct == CUBLAS_COMPUTE_32F && !fused) variant = -1;
+      if (variant > 5) variant = fused ? 0 : -1;  // 6 / 7 take B column-major: layout probe only
       long long ws = variant >= 0 ? gemm_tf32_workspace(variant, fused, static_cast<int>(M), static_cast<int>(N),
                                                         static_cast<int>(K))
                                   : -1;
