@@ -143,6 +143,26 @@ def test_launch_units_packed_per_producer_set(monkeypatch):
     assert len({k["symbol"] for k in nodedup}) == 88
 
 
+@pytest.mark.parametrize("mode", ["1", "2"])
+def test_tma_staged_rows_codegen(monkeypatch, mode):
+    """TMA-staged regional rows compile for sm_100a without a device: mode 1
+    (one ring of row tiles per CTA, the whole tile on one mbarrier), mode 2
+    (per-team rings: one bulk copy per row and tensor, one mbarrier per row
+    buffer, a team-only sync before the refill -- __syncwarp for teams of at
+    most one warp, the CTA barrier for wider teams)"""
+    stitch = _stitch()
+    monkeypatch.setenv("STITCH_STAGE", mode)
+    for name in ("ln_4096x768", "bert_resln", "attn_softmax"):
+        src, kernels = stitch.Plan(stitch.Graph(config_graph(name)), "b200").codegen()
+        assert all(k["template"].endswith("+tma") for k in kernels), (name, kernels)
+        assert "bulk_g2s(" in src and "mbar_wait(" in src
+        if mode == "2":
+            assert "TMA per-team rings" in src and "__syncwarp" in src, name
+        else:
+            assert "TMA pipeline" in src, name
+        assert re.fullmatch(r"[0-9a-f]{32}", stitch.compile_cuda(src))
+
+
 def test_persistent_template_codegen(monkeypatch):
     """opt-in persistent template: a launch-bound plan becomes one cooperative
     kernel whose unit bodies are shared between textually identical units
