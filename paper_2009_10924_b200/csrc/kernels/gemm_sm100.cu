@@ -7,6 +7,12 @@
 // headers vendored in the image (flashinfer/data/cutlass); without them the
 // entry point reports "unavailable" and the executor keeps cuBLASLt + the
 // stitched kernel.
+// griddepcontrol in the CUTLASS kernels: the TMA load, bias load and tile
+// scheduler warps wait on the producer grid before touching global memory,
+// so the GEMM may be launched with programmatic dependent launch
+// (gemm_tf32_launch(pdl = true)); without this define those waits compile
+// to nothing and a PDL launch would race its producer
+#define CUTLASS_ENABLE_GDC_FOR_SM100 1
 #include <cstddef>
 #include <type_traits>
 #include <cuda_runtime.h>
@@ -75,12 +81,12 @@ struct Cfg {
     return static_cast<long long>(Gemm::get_workspace_size(a));
   }
   static int run(const float* A, const float* B, const float* bias, float* D, int M, int N, int K, void* ws,
-                 size_t ws_bytes, cudaStream_t stream) {
+                 size_t ws_bytes, cudaStream_t stream, bool pdl) {
     auto a = args(A, B, bias, D, M, N, K);
     Gemm gemm;
     if (Gemm::get_workspace_size(a) > ws_bytes || gemm.can_implement(a) != cutlass::Status::kSuccess) return 1;
     if (gemm.initialize(a, ws, stream) != cutlass::Status::kSuccess) return 2;
-    return gemm.run(stream) == cutlass::Status::kSuccess ? 0 : 2;
+    return gemm.run(stream, nullptr, pdl) == cutlass::Status::kSuccess ? 0 : 2;
   }
 };
 
@@ -124,16 +130,16 @@ long long ws_of(int v, int M, int N, int K) {
 }
 template <class Fusion>
 int run_of(int v, const float* A, const float* B, const float* bias, float* D, int M, int N, int K, void* ws, size_t wsb,
-           cudaStream_t s) {
+           cudaStream_t s, bool pdl) {
   switch (v) {
-    case 0: return Cfg<T256x256, C2, void, Fusion>::run(A, B, bias, D, M, N, K, ws, wsb, s);
-    case 1: return Cfg<T256x256, C2, SK, Fusion>::run(A, B, bias, D, M, N, K, ws, wsb, s);
-    case 2: return Cfg<T128x192, C1, void, Fusion>::run(A, B, bias, D, M, N, K, ws, wsb, s);
-    case 3: return Cfg<T256x192, C2, void, Fusion>::run(A, B, bias, D, M, N, K, ws, wsb, s);
-    case 4: return Cfg<T256x256, C22, void, Fusion>::run(A, B, bias, D, M, N, K, ws, wsb, s);
-    case 5: return Cfg<T256x192, C22, void, Fusion>::run(A, B, bias, D, M, N, K, ws, wsb, s);
-    case 6: return Cfg<T256x192, C2, void, Fusion, Col>::run(A, B, bias, D, M, N, K, ws, wsb, s);
-    case 7: return Cfg<T256x256, C2, void, Fusion, Col>::run(A, B, bias, D, M, N, K, ws, wsb, s);
+    case 0: return Cfg<T256x256, C2, void, Fusion>::run(A, B, bias, D, M, N, K, ws, wsb, s, pdl);
+    case 1: return Cfg<T256x256, C2, SK, Fusion>::run(A, B, bias, D, M, N, K, ws, wsb, s, pdl);
+    case 2: return Cfg<T128x192, C1, void, Fusion>::run(A, B, bias, D, M, N, K, ws, wsb, s, pdl);
+    case 3: return Cfg<T256x192, C2, void, Fusion>::run(A, B, bias, D, M, N, K, ws, wsb, s, pdl);
+    case 4: return Cfg<T256x256, C22, void, Fusion>::run(A, B, bias, D, M, N, K, ws, wsb, s, pdl);
+    case 5: return Cfg<T256x192, C22, void, Fusion>::run(A, B, bias, D, M, N, K, ws, wsb, s, pdl);
+    case 6: return Cfg<T256x192, C2, void, Fusion, Col>::run(A, B, bias, D, M, N, K, ws, wsb, s, pdl);
+    case 7: return Cfg<T256x256, C2, void, Fusion, Col>::run(A, B, bias, D, M, N, K, ws, wsb, s, pdl);
     default: return 1;
   }
 }
@@ -146,16 +152,23 @@ int run_of(int v, const float* A, const float* B, const float* bias, float* D, i
 // implementable / unknown variant); 2 = launch error.  The workspace must
 // hold gemm_tf32_workspace() bytes and belong to this GEMM (stream-K keeps
 // its fix-up partials and flags there).
-int gemm_tf32(int variant, bool fused, const float* A, const float* B, const float* bias, float* D, int M, int N, int K,
-              void* workspace, size_t workspace_bytes, cudaStream_t stream) {
+// pdl: launched with programmatic stream serialization (the kernel's
+// griddepcontrol.wait orders it after its producer)
+int gemm_tf32_launch(int variant, bool fused, bool pdl, const float* A, const float* B, const float* bias, float* D, int M,
+                     int N, int K, void* workspace, size_t workspace_bytes, cudaStream_t stream) {
 #ifdef STC_HAVE_CUTLASS
-  return fused ? run_of<GeluFusion>(variant, A, B, bias, D, M, N, K, workspace, workspace_bytes, stream)
-               : run_of<PlainFusion>(variant, A, B, bias, D, M, N, K, workspace, workspace_bytes, stream);
+  return fused ? run_of<GeluFusion>(variant, A, B, bias, D, M, N, K, workspace, workspace_bytes, stream, pdl)
+               : run_of<PlainFusion>(variant, A, B, bias, D, M, N, K, workspace, workspace_bytes, stream, pdl);
 #else
-  (void)variant, (void)fused, (void)A, (void)B, (void)bias, (void)D, (void)M, (void)N, (void)K, (void)workspace,
-      (void)workspace_bytes, (void)stream;
+  (void)variant, (void)fused, (void)pdl, (void)A, (void)B, (void)bias, (void)D, (void)M, (void)N, (void)K,
+      (void)workspace, (void)workspace_bytes, (void)stream;
   return 1;
 #endif
+}
+
+int gemm_tf32(int variant, bool fused, const float* A, const float* B, const float* bias, float* D, int M, int N, int K,
+              void* workspace, size_t workspace_bytes, cudaStream_t stream) {
+  return gemm_tf32_launch(variant, fused, false, A, B, bias, D, M, N, K, workspace, workspace_bytes, stream);
 }
 
 // workspace bytes of that configuration for this shape; -1 = not implementable

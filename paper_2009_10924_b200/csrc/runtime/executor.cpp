@@ -42,6 +42,8 @@ bool gemm_bias_gelu_supported(int M, int N, int K, size_t workspace_bytes);
 int gemm_tf32(int variant, bool fused, const float* A, const float* B, const float* bias, float* D, int M, int N, int K,
               void* workspace, size_t workspace_bytes, cudaStream_t stream);
 long long gemm_tf32_workspace(int variant, bool fused, int M, int N, int K);
+int gemm_tf32_launch(int variant, bool fused, bool pdl, const float* A, const float* B, const float* bias, float* D, int M,
+                     int N, int K, void* workspace, size_t workspace_bytes, cudaStream_t stream);
 
 namespace {
 // the plan's bias + GELU(tanh) pattern over one GEMM output (graphs/
@@ -946,7 +948,14 @@ void Executor::launch_kernel(size_t i, int set, cudaStream_t s, int after, const
   };
   if (k.is_gemm && gemm_->units.at(i).variant >= 0) {
     const bool fused = k.gemm_epilogue == "bias_gelu";
-    if (const int rc = gemm_tf32(gemm_->units.at(i).variant, fused, static_cast<const float*>(ptr_of(k.inputs[0])),
+    // STITCH_GEMM_PDL=1: the CUTLASS GEMM launches under programmatic
+    // dependent launch behind its stream predecessor (its setup -- barrier
+    // init, TMEM allocation, descriptor prefetch -- overlaps the producer's
+    // drain; its load warps griddepcontrol.wait before reading)
+    const char* gp = std::getenv("STITCH_GEMM_PDL");
+    const bool gemm_pdl = gp && *gp == '1';
+    const bool pdl = gemm_pdl && pdl_ && after >= 0 && !specs_[static_cast<size_t>(after)].cooperative;
+    if (const int rc = gemm_tf32_launch(gemm_->units.at(i).variant, fused, pdl, static_cast<const float*>(ptr_of(k.inputs[0])),
                                  static_cast<const float*>(ptr_of(k.inputs[1])),
                                  fused ? static_cast<const float*>(ptr_of(k.inputs[2])) : nullptr,
                                  static_cast<float*>(ptr_of(k.outputs[0])), static_cast<int>(k.gemm_m),

@@ -379,6 +379,32 @@ def test_cutlass_gemm_variants_match_default_model_mode(monkeypatch, variant):
         assert stitch.compare({k: got[k]}, {k: want[k]}, 3e-2, 3e-2)["pass"], k
 
 
+def test_gemm_pdl_matches_plain_launch_model_mode(monkeypatch):
+    """STITCH_GEMM_PDL=1: the CUTLASS GEMMs launch under programmatic
+    dependent launch (built with CUTLASS_ENABLE_GDC_FOR_SM100: their load
+    warps griddepcontrol.wait before reading).  ffn2's GEMM then starts while
+    ffn1's fused GEMM, its producer, drains -- the outputs must be bitwise
+    those of plain launches over repeated replays, and within the TF32 band
+    of the f64-matmul oracle"""
+    stitch = _stitch()
+    text = config_graph("bert_layer")
+    g = stitch.Graph(text)
+    plan = stitch.Plan(g, "b200")
+    inputs = stitch.random_inputs(g, 5)
+    monkeypatch.setenv("STITCH_GEMM_PDL", "0")
+    ref = stitch.Executor(plan, gemm=True).run(inputs)
+    monkeypatch.setenv("STITCH_GEMM_PDL", "1")
+    ex = stitch.Executor(plan, gemm=True)
+    for _ in range(4):
+        got = ex.run(inputs)
+        for k in ref:
+            assert np.array_equal(got[k], ref[k]), k
+    og = no.parse_graph(text)
+    want = no.eval_reference(og, {k: v.astype(np.float64) for k, v in inputs.items()}, opaque=no.matmul_opaque)
+    for k in want:
+        assert stitch.compare({k: got[k]}, {k: want[k]}, 3e-2, 3e-2)["pass"], k
+
+
 def test_streamk_switch_model_mode(monkeypatch):
     """STITCH_GEMM_SK=1 selects the stream-K configuration for both GEMMs"""
     stitch = _stitch()
