@@ -948,12 +948,13 @@ void Executor::launch_kernel(size_t i, int set, cudaStream_t s, int after, const
   };
   if (k.is_gemm && gemm_->units.at(i).variant >= 0) {
     const bool fused = k.gemm_epilogue == "bias_gelu";
-    // STITCH_GEMM_PDL=1: the CUTLASS GEMM launches under programmatic
-    // dependent launch behind its stream predecessor (its setup -- barrier
-    // init, TMEM allocation, descriptor prefetch -- overlaps the producer's
-    // drain; its load warps griddepcontrol.wait before reading)
+    // STITCH_GEMM_PDL (default 1): the CUTLASS GEMM launches under
+    // programmatic dependent launch behind its stream predecessor (its setup
+    // -- barrier init, TMEM allocation, descriptor prefetch -- overlaps the
+    // producer's drain; its load warps griddepcontrol.wait before reading).
+    // BERT layer 81.1 -> 79.1 us (profiles/r02/gemm/gemm_pdl.jsonl)
     const char* gp = std::getenv("STITCH_GEMM_PDL");
-    const bool gemm_pdl = gp && *gp == '1';
+    const bool gemm_pdl = !(gp && *gp == '0');
     const bool pdl = gemm_pdl && pdl_ && after >= 0 && !specs_[static_cast<size_t>(after)].cooperative;
     if (const int rc = gemm_tf32_launch(gemm_->units.at(i).variant, fused, pdl, static_cast<const float*>(ptr_of(k.inputs[0])),
                                  static_cast<const float*>(ptr_of(k.inputs[1])),
